@@ -1,0 +1,257 @@
+"""CPU oracle of the S3R-GS streamlined per-view splatting path (ctypes wrapper).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (paper_2503_08217_b200/) never imports it.  The C sources in this
+directory are the oracle; this file only marshals numpy arrays to them.
+
+``build()`` compiles liboracle.so with gcc -O2 -ffp-contract=off (see Makefile).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+from typing import Dict, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRCS = ["s3r_oracle_f32.c", "s3r_oracle_f64.c", "s3r_oracle_impl.inc", "s3r_oracle.h", "Makefile"]
+_lock = threading.Lock()
+_lib = None
+
+F_TEMPORAL, F_VISIBLE, F_SMALL, F_DROPPED, F_RENDERED, F_BADID = 1, 2, 4, 8, 16, 32
+TILE = 16
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so if missing or older than its sources."""
+    newest = max(os.path.getmtime(os.path.join(_HERE, s)) for s in _SRCS)
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
+        subprocess.run(["make", "-s", "-B", "liboracle.so"], cwd=_HERE, check=True)
+    return _SO
+
+
+class Scene(C.Structure):
+    _fields_ = [("n", C.c_int64), ("num_instances", C.c_int32),
+                ("means_opacity", C.c_void_p), ("scales", C.c_void_p),
+                ("rotations", C.c_void_p), ("colors", C.c_void_p),
+                ("instance_ids", C.c_void_p), ("visibility", C.c_void_p),
+                ("life", C.c_void_p)]
+
+
+class View(C.Structure):
+    _fields_ = [("t", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("near_plane", C.c_float), ("instance_w2c", C.c_void_p),
+                ("lod_r", C.c_float), ("lod_pmax", C.c_float), ("lod_D", C.c_float),
+                ("lod_seed", C.c_uint64)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("n_scene", "n_temporal", "n_visible", "n_lod_small",
+                                         "n_lod_dropped", "n_rendered", "n_pairs",
+                                         "n_bad_instance")]
+
+
+class Out(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("final_T", C.c_void_p),
+                ("visible", C.c_void_p), ("temporal_idx", C.c_void_p), ("keys", C.c_void_p),
+                ("flags", C.c_void_p), ("rect", C.c_void_p), ("pair_tile", C.c_void_p),
+                ("pair_gauss", C.c_void_p), ("pair_capacity", C.c_int64),
+                ("ranges", C.c_void_p), ("stats", Stats)]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_SO)
+            P = C.c_void_p
+            sig = {
+                "so_normalize_time": (C.c_double, [C.c_int64, C.c_int64]),
+                "so_exp_f32": (C.c_float, [C.c_float]),
+                "so_exp_f64": (C.c_double, [C.c_double]),
+                "so_splitmix64": (C.c_uint64, [C.c_uint64]),
+                "so_lod_uniform": (C.c_float, [C.c_uint64, C.c_int64]),
+                "so_compose_instance_cameras": (None, [P, P, C.c_int32, P]),
+                "so_temporal_filter_f32": (C.c_int64, [P, C.c_float, P]),
+                "so_temporal_filter_f64": (C.c_int64, [P, C.c_double, P]),
+                "so_project_f32": (C.c_int, [P, P, C.c_int64, P]),
+                "so_project_f64": (C.c_int, [P, P, C.c_int64, P]),
+                "so_drop_probability_f32": (C.c_float, [C.c_float, C.c_float, C.c_float]),
+                "so_drop_probability_f64": (C.c_double, [C.c_double, C.c_double, C.c_double]),
+                "so_render_view_f32": (C.c_int, [P, P, P]),
+                "so_render_view_f64": (C.c_int, [P, P, P]),
+                "so_blend_bruteforce_f32": (C.c_int, [P, P, P, P, P, P, P, P]),
+                "so_blend_bruteforce_f64": (C.c_int, [P, P, P, P, P, P, P, P]),
+                "so_update_life_f32": (None, [P, P, C.c_float]),
+                "so_commit_visibility": (None, [P, C.c_float]),
+                "so_reset_visibility": (None, [P]),
+            }
+            for name, (res, args) in sig.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class _SceneRef:
+    """Keeps contiguous numpy arrays alive behind a ctypes Scene struct."""
+
+    def __init__(self, scene, life: bool = True):
+        self.arrs = {k: np.ascontiguousarray(getattr(scene, k)) for k in
+                     ("means_opacity", "scales", "rotations", "colors", "instance_ids")}
+        # visibility / life are mutated in place: keep the caller's arrays if contiguous
+        self.visibility = scene.visibility
+        self.life = scene.life if life else None
+        assert self.visibility.flags.c_contiguous and self.visibility.dtype == np.float32
+        if self.life is not None:
+            assert self.life.flags.c_contiguous and self.life.dtype == np.float32
+        self.s = Scene(scene.n, scene.num_instances, _ptr(self.arrs["means_opacity"]),
+                       _ptr(self.arrs["scales"]), _ptr(self.arrs["rotations"]),
+                       _ptr(self.arrs["colors"]), _ptr(self.arrs["instance_ids"]),
+                       _ptr(self.visibility), _ptr(self.life))
+
+
+def compose(view) -> np.ndarray:
+    """Instance camera table (K+1, 12) f32 for a scenegen.View."""
+    K = view.i2g.shape[0]
+    w2c = np.ascontiguousarray(view.w2c, np.float32).reshape(12)
+    i2g = np.ascontiguousarray(view.i2g, np.float32).reshape(max(K, 0) * 12)
+    out = np.zeros((K + 1, 12), np.float32)
+    lib().so_compose_instance_cameras(_ptr(w2c), _ptr(i2g) if K else None, K, _ptr(out))
+    return out
+
+
+class _ViewRef:
+    def __init__(self, view, table: Optional[np.ndarray] = None):
+        self.table = np.ascontiguousarray(compose(view) if table is None else table, np.float32)
+        self.v = View(view.t, view.width, view.height, view.fx, view.fy, view.cx, view.cy,
+                      view.near, _ptr(self.table), view.lod_r, view.lod_pmax, view.lod_D,
+                      view.lod_seed & ((1 << 64) - 1))
+
+
+def render_view(scene, view, precision: str = "f32", table: Optional[np.ndarray] = None,
+                pairs: bool = True, image: bool = True) -> Dict[str, np.ndarray]:
+    """One streamlined render (O1-O6) of one view.  Returns numpy arrays:
+    rgb (H,W,3), depth (H,W), final_T (H,W), visible (N,) u8, temporal_idx,
+    keys (N,6) (NaN where not projected), flags (N,), rect (N,4),
+    pair_tile / pair_gauss (P,), ranges (tiles,2), stats (dict), rc."""
+    L = lib()
+    real = np.float32 if precision == "f32" else np.float64
+    sr, vr = _SceneRef(scene, life=False), _ViewRef(view, table)
+    N, W, H = scene.n, view.width, view.height
+    TX, TY = (W + TILE - 1) // TILE, (H + TILE - 1) // TILE
+    o = {
+        "visible": np.zeros(N, np.uint8), "temporal_idx": np.zeros(max(N, 1), np.int32),
+        "keys": np.zeros((N, 6), real), "flags": np.zeros(N, np.uint8),
+        "rect": np.zeros((N, 4), np.int16), "ranges": np.zeros((TX * TY, 2), np.int32),
+    }
+    if image:
+        o.update(rgb=np.zeros((H, W, 3), real), depth=np.zeros((H, W), real),
+                 final_T=np.zeros((H, W), real))
+    out = Out()
+    for k in ("rgb", "depth", "final_T", "visible", "temporal_idx", "keys", "flags", "rect",
+              "ranges"):
+        if k in o:
+            setattr(out, k, _ptr(o[k]))
+    fn = L.so_render_view_f32 if precision == "f32" else L.so_render_view_f64
+    rc = fn(C.byref(sr.s), C.byref(vr.v), C.byref(out))
+    if pairs:
+        P = out.stats.n_pairs
+        o["pair_tile"] = np.zeros(max(P, 1), np.int32)
+        o["pair_gauss"] = np.zeros(max(P, 1), np.int32)
+        out.pair_tile, out.pair_gauss = _ptr(o["pair_tile"]), _ptr(o["pair_gauss"])
+        out.pair_capacity = P
+        # a second, identical run fills the pair list (the oracle is deterministic)
+        out.rgb = out.depth = out.final_T = None
+        rc = fn(C.byref(sr.s), C.byref(vr.v), C.byref(out))
+        o["pair_tile"], o["pair_gauss"] = o["pair_tile"][:P], o["pair_gauss"][:P]
+    o["temporal_idx"] = o["temporal_idx"][: out.stats.n_temporal]
+    o["stats"] = {k: getattr(out.stats, k) for k, _ in Stats._fields_}
+    o["rc"] = rc
+    o["table"] = vr.table
+    return o
+
+
+def blend_bruteforce(scene, view, flags, keys, rect, precision="f32", table=None):
+    L = lib()
+    real = np.float32 if precision == "f32" else np.float64
+    sr, vr = _SceneRef(scene, life=False), _ViewRef(view, table)
+    H, W = view.height, view.width
+    rgb, depth, T = np.zeros((H, W, 3), real), np.zeros((H, W), real), np.zeros((H, W), real)
+    keys = np.ascontiguousarray(keys, real)
+    flags = np.ascontiguousarray(flags, np.uint8)
+    rect = np.ascontiguousarray(rect, np.int16)
+    fn = L.so_blend_bruteforce_f32 if precision == "f32" else L.so_blend_bruteforce_f64
+    fn(C.byref(sr.s), C.byref(vr.v), _ptr(flags), _ptr(keys), _ptr(rect), _ptr(rgb),
+       _ptr(depth), _ptr(T))
+    return rgb, depth, T
+
+
+def temporal_filter(scene, t, precision="f32") -> np.ndarray:
+    L = lib()
+    sr = _SceneRef(scene, life=False)
+    idx = np.zeros(max(scene.n, 1), np.int32)
+    fn = L.so_temporal_filter_f32 if precision == "f32" else L.so_temporal_filter_f64
+    m = fn(C.byref(sr.s), t, _ptr(idx))
+    return idx[:m]
+
+
+def project(scene, view, g, precision="f32", table=None):
+    """(status, keys[6]) for one Gaussian: status 0 ok, 1 behind near plane, 2 bad id."""
+    L = lib()
+    real = np.float32 if precision == "f32" else np.float64
+    sr, vr = _SceneRef(scene, life=False), _ViewRef(view, table)
+    k = np.zeros(6, real)
+    fn = L.so_project_f32 if precision == "f32" else L.so_project_f64
+    st = fn(C.byref(sr.s), C.byref(vr.v), int(g), _ptr(k))
+    return st, k
+
+
+def drop_probability(d, pmax, D, precision="f32"):
+    L = lib()
+    fn = L.so_drop_probability_f32 if precision == "f32" else L.so_drop_probability_f64
+    return fn(d, pmax, D)
+
+
+def exp32(x: float) -> float:
+    return lib().so_exp_f32(x)
+
+
+def splitmix64(x: int) -> int:
+    return lib().so_splitmix64(x & ((1 << 64) - 1))
+
+
+def lod_uniform(seed: int, g: int) -> float:
+    return lib().so_lod_uniform(seed & ((1 << 64) - 1), g)
+
+
+def normalize_time(frame: int, frames: int) -> float:
+    return lib().so_normalize_time(frame, frames)
+
+
+def update_life(scene, visible: np.ndarray, t: float) -> None:
+    sr = _SceneRef(scene, life=True)
+    vis = np.ascontiguousarray(visible, np.uint8)
+    lib().so_update_life_f32(C.byref(sr.s), _ptr(vis), t)
+
+
+def commit_visibility(scene, margin: float = 0.1) -> None:
+    sr = _SceneRef(scene, life=True)
+    lib().so_commit_visibility(C.byref(sr.s), margin)
+
+
+def reset_visibility(scene) -> None:
+    sr = _SceneRef(scene, life=True)
+    lib().so_reset_visibility(C.byref(sr.s))

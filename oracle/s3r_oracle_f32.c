@@ -1,0 +1,146 @@
+/*
+ * s3r_oracle_f32.c — fp32 CONTRACT instance of the CPU oracle, plus the
+ * precision-independent pieces (time normalisation, instance-camera
+ * composition, the LOD random generator, point-life update, commit, reset).
+ * TEST INFRASTRUCTURE ONLY (see s3r_oracle.h).  Build: gcc -O2
+ * -ffp-contract=off (no fast-math): every line is one IEEE-754 operation.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include "s3r_oracle.h"
+
+/* ------------------------------------------------------------------------
+ * s3r_exp (DESIGN.md R-ARITH): a Cephes-style single-precision exponential,
+ * written out so that any IEEE-754 machine evaluates it bit-identically.
+ * Used for exp(power) in Eq.2's alpha.  Called with x <= 0.
+ *   x < -30            -> 0
+ *   n = rint(x log2 e)  (ties to even)
+ *   r = x - n*C1 - n*C2 (C1 + C2 = ln 2; C1 = 0x3F318000 has 9 significant
+ *                        bits, so n*C1 is exact for |n| <= 44)
+ *   y = 1 + r + r^2 P(r)  with the Cephes expf minimax P
+ *   return y * 2^n      (exact: 2^-44 is normal)
+ * ---------------------------------------------------------------------- */
+float so_exp_f32(float x)
+{
+    if (!(x >= -30.0f)) return 0.0f;
+    float n = rintf(x * 1.44269504f);
+    float r = fmaf(-n, 0.693359375f, x);
+    r = fmaf(-n, -2.12194440e-4f, r);
+    float p = 1.9875691500e-4f;
+    p = fmaf(p, r, 1.3981999507e-3f);
+    p = fmaf(p, r, 8.3334519073e-3f);
+    p = fmaf(p, r, 4.1665795894e-2f);
+    p = fmaf(p, r, 1.6666665459e-1f);
+    p = fmaf(p, r, 5.0000001201e-1f);
+    float r2 = r * r;
+    float y = fmaf(p, r2, r);
+    y = y + 1.0f;
+    return ldexpf(y, (int)n);
+}
+
+/* SplitMix64 (reading R9): the counter-based generator behind the Bernoulli
+ * draw of Eq.7 row 2.  Keyed by (per-view seed, global Gaussian
+ * index) so the draw is independent of compaction, batching and GPU count. */
+uint64_t so_splitmix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+/* u = top 24 bits of splitmix64(seed ^ splitmix64(g)) times 2^-24: exact in
+ * fp32, uniform on {0, 2^-24, ..., 1 - 2^-24}. */
+float so_lod_uniform(uint64_t seed, int64_t g)
+{
+    uint64_t h = so_splitmix64(seed ^ so_splitmix64((uint64_t)g));
+    return (float)(uint32_t)(h >> 40) * 5.9604644775390625e-8f;
+}
+
+/* Time normalisation ("we first normalize the rendering time of the
+ * whole scene to [-1,1]"): frame i of F -> -1 + 2 i / (F - 1); F = 1 -> 0. */
+double so_normalize_time(int64_t frame, int64_t frame_count)
+{
+    if (frame_count <= 1) return 0.0;
+    return -1.0 + (2.0 * (double)frame) / (double)(frame_count - 1);
+}
+
+/* Instance cameras: W_{t,i} = W_t W_{t,i2g}; slot 0 = W_t
+ * (reading R17).  3x4 row-major [R|t] operands; computed in fp64 with the
+ * dot3 order of R-ARITH, then rounded once to fp32.
+ *   w2c: [12], i2g: [K][12], out: [(K+1)][12]. */
+void so_compose_instance_cameras(const float* w2c, const float* i2g, int32_t K, float* out)
+{
+    for (int k = 0; k < 12; ++k) out[k] = w2c[k];
+    for (int32_t i = 0; i < K; ++i) {
+        const float* B = i2g + 12 * (int64_t)i;
+        float* O = out + 12 * (int64_t)(i + 1);
+        for (int r = 0; r < 3; ++r) {
+            double a0 = w2c[4 * r + 0], a1 = w2c[4 * r + 1], a2 = w2c[4 * r + 2], a3 = w2c[4 * r + 3];
+            for (int c = 0; c < 3; ++c) {
+                double acc = a0 * (double)B[0 * 4 + c];
+                acc = fma(a1, (double)B[1 * 4 + c], acc);
+                acc = fma(a2, (double)B[2 * 4 + c], acc);
+                O[4 * r + c] = (float)acc;
+            }
+            double acc = fma(a0, (double)B[0 * 4 + 3], a3);
+            acc = fma(a1, (double)B[1 * 4 + 3], acc);
+            acc = fma(a2, (double)B[2 * 4 + 3], acc);
+            O[4 * r + 3] = (float)acc;
+        }
+    }
+}
+
+/* O7 point-life update (Eq.5): for M_t[i]: l_s = min(l_s, t),
+ * l_e = max(l_e, t).  t is canonicalised (-0 -> +0). */
+void so_update_life_f32(so_scene* s, const uint8_t* visible, float t)
+{
+    t = t + 0.0f;
+    for (int64_t g = 0; g < s->n; ++g) {
+        if (!visible[g]) continue;
+        if (t < s->life[2 * g + 0]) s->life[2 * g + 0] = t;
+        if (t > s->life[2 * g + 1]) s->life[2 * g + 1] = t;
+    }
+}
+
+/* O8 commit (Eq.6): t_s = l_s - 0.1, t_e = l_e + 0.1, clamped to
+ * [-1,1]; a never-observed Gaussian (l_s > l_e, the initial (1,-1)) becomes
+ * visible at all times (reading R18); life is reset to (1,-1). */
+void so_commit_visibility(so_scene* s, float margin)
+{
+    for (int64_t g = 0; g < s->n; ++g) {
+        float ls = s->life[2 * g + 0], le = s->life[2 * g + 1];
+        if (ls > le) {
+            s->visibility[2 * g + 0] = -1.0f;
+            s->visibility[2 * g + 1] = 1.0f;
+        } else {
+            s->visibility[2 * g + 0] = fmaxf(-1.0f, ls - margin);
+            s->visibility[2 * g + 1] = fminf(1.0f, le + margin);
+        }
+        s->life[2 * g + 0] = 1.0f;
+        s->life[2 * g + 1] = -1.0f;
+    }
+}
+
+/* P:183 "we periodically reset the temporal visibility ... to be visible". */
+void so_reset_visibility(so_scene* s)
+{
+    for (int64_t g = 0; g < s->n; ++g) {
+        s->visibility[2 * g + 0] = -1.0f;
+        s->visibility[2 * g + 1] = 1.0f;
+    }
+}
+
+#define REAL float
+#define SO(x) x##_f32
+#define R(x) x##f
+#define FMA fmaf
+#define SQRT sqrtf
+#define CEIL ceilf
+#define FLOOR floorf
+#define FMIN fminf
+#define FMAX fmaxf
+#define ISFIN isfinite
+#define EXPF so_exp_f32
+#include "s3r_oracle_impl.inc"
