@@ -1,0 +1,227 @@
+/*
+ * s3r.h — C ABI of the B200-native S3R-GS streamlined per-view splatting path.
+ *
+ * The library (paper_2503_08217_b200/libs3r.so, CUDA for sm_100a) renders
+ * batches of camera views of one Gaussian scene through the pipeline of
+ * PAPER.md §3.3 (arxiv 2503.08217, "Streamlined Reconstruction Stage",
+ * P:148-199; Fig.1b):
+ *
+ *   temporal-visibility filter          -> s3r_render_batch, stage K1
+ *   instance-specific projection (Eq.1)  -> stage K2
+ *   Adaptive-LOD cull (Eq.7 rows 1-3)    -> stage K2
+ *   tile binning + depth sort                       -> stages K3-K6
+ *   alpha-blended tile rasterization (Eq.2)  -> stage K7
+ *   point-life update with M_t (Eq.5)    -> stage K2 (atomics)
+ *   visibility commit / reset (Eq.6)     -> s3r_commit_visibility,
+ *                                                      s3r_reset_visibility
+ *
+ * "P:n" = line n of /root/reference/PAPER.md.  The arithmetic is the fp32
+ * contract "R-ARITH" of DESIGN.md; readings of the paper (R1-R19) are listed
+ * there.
+ *
+ * Conventions for every call:
+ *  - Plain C types only.  "device" pointers are CUDA device (or managed)
+ *    memory of the context's device; "host" pointers are CPU memory.
+ *  - All scene, view and output memory is CALLER-OWNED.  The context owns only
+ *    scratch, grown on demand and reused; no caller pointer is retained after a
+ *    call returns.
+ *  - Calls enqueue work on `stream` (a cudaStream_t, NULL = legacy default
+ *    stream) and return.  s3r_render / s3r_render_batch synchronise the stream
+ *    twice internally to size scratch (after K1 and after K2); s3r_check,
+ *    s3r_get_stage_times and s3r_render_batch_host synchronise it fully.
+ *  - Return value: S3R_OK (0) or a negative S3R_E* code; the message is in
+ *    s3r_last_error(ctx).  Nothing throws or aborts across the ABI.
+ *  - A context is bound to one device and must not be used from two threads
+ *    at once.
+ */
+#ifndef S3R_H
+#define S3R_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S3R_VERSION 10000 /* 1.0.0 */
+#define S3R_TILE 16       /* tile edge in pixels (reading R12) */
+
+enum {
+    S3R_OK = 0,
+    S3R_EINVAL = -1,    /* bad argument: NULL required pointer, misaligned
+                           pointer, n < 0, width/height outside [1,16384],
+                           fx/fy <= 0 or non-finite, t outside [-1,1] or NaN,
+                           num_instances < 1, non-finite LOD parameters,
+                           lod_pmax outside [0,1], lod_D <= 0, near_plane <= 0,
+                           n_views < 0                                        */
+    S3R_EINSTANCE = -2, /* a Gaussian carried an instance id outside
+                           [0, num_instances-1]; it was treated as invisible
+                           ("ID in Z"); reported by s3r_check          */
+    S3R_ENOMEM = -3,    /* scratch allocation failed                          */
+    S3R_ECUDA = -4,     /* a CUDA runtime error; see s3r_last_error           */
+    S3R_ESTATE = -5     /* call out of order (e.g. dump without a render, or
+                           debug data requested without s3r_set_debug)        */
+};
+
+typedef struct s3r_ctx s3r_ctx;
+
+/* The Gaussian scene ("each Gaussian is assigned a 3D position mu, a 3D
+ * covariance Sigma, an opacity alpha, a temporal visibility v and a point life
+ * l ... dynamic Gaussian is associated with an instance ID").  Structure of
+ * arrays, one element per Gaussian, all DEVICE pointers, 16-byte aligned.   */
+typedef struct {
+    int64_t n;                   /* number of Gaussians, 0 <= n < 2^31          */
+    int32_t num_instances;       /* K+1: id 0 = static background, 1..K objects */
+    const float* means_opacity;  /* float4[n]: mu (x,y,z) in the local frame of
+                                    its instance (world frame for id 0), opacity
+                                    in (0,1)                                    */
+    const float* scales;         /* float4[n]: sigma_x, sigma_y, sigma_z (> 0,
+                                    linear metres; activation is the caller's),
+                                    .w ignored                                  */
+    const float* rotations;      /* float4[n]: quaternion (w,x,y,z), non-zero,
+                                    normalised inside the kernel                */
+    const float* colors;         /* float4[n]: r,g,b (constant per Gaussian,
+                                    reading R16), .w ignored                    */
+    const int32_t* instance_ids; /* int32[n]                                    */
+    float* visibility;           /* float2[n]: (v_s, v_e) temporal visibility;
+                                    read by render, written by commit/reset     */
+    float* life;                 /* float2[n]: (l_s, l_e) point life; updated by
+                                    render with atomics (Eq.5); NULL = no update */
+} s3r_scene;
+
+/* One camera view at time t ("at each time t rendering").            */
+typedef struct {
+    float t;                     /* normalised time in [-1,1]; -0 is
+                                    treated as +0                               */
+    int32_t width, height;       /* image size in pixels, [1, 16384]            */
+    float fx, fy, cx, cy;        /* pinhole intrinsics K_t (pixels)             */
+    float near_plane;            /* camera-z near plane, > 0 (0.01 m, R5)       */
+    const float* instance_w2c;   /* DEVICE float[num_instances][12]: row-major
+                                    3x4 [R|t] local->camera, slot 0 = W_t, slot
+                                    i = W_t W_{t,i2g}.  Build it with
+                                    s3r_compose_instance_cameras.               */
+    float lod_r;                 /* LOD threshold r in pixels ("such as 4
+                                    pixels"); <= 0 disables LOD                 */
+    float lod_pmax;              /* p_max in [0,1] (Eq.7)                       */
+    float lod_D;                 /* D > 0 in metres (Eq.7)                      */
+    uint64_t lod_seed;           /* per-view seed of the Bernoulli draw (R9)    */
+} s3r_view;
+
+/* Per-view outputs, DEVICE pointers, caller-allocated.  rgb is required.    */
+typedef struct {
+    float* rgb;                  /* float[height][width][3], Eq.2 colour       */
+    float* depth;                /* float[height][width] sum_i w_i z_i, or NULL */
+    float* final_T;              /* float[height][width] final transmittance,
+                                    or NULL                                     */
+    uint8_t* visible;            /* uint8[n] M_t (1 = in the view frustum after
+                                    projection, before LOD; reading R2), or NULL */
+} s3r_outputs;
+
+/* Per-view counts (rendered <= visible <= temporal <= scene).               */
+typedef struct {
+    int64_t n_scene;             /* N                                           */
+    int64_t n_temporal;          /* passed the temporal filter (projected)      */
+    int64_t n_visible;           /* |M_t|                                       */
+    int64_t n_lod_small;         /* 2D scale <= r                               */
+    int64_t n_lod_dropped;       /* culled by the Bernoulli draw                */
+    int64_t n_rendered;          /* blended                                     */
+    int64_t n_pairs;             /* (tile, Gaussian) pairs                      */
+    int64_t n_bad_instance;      /* ids outside [0,K]                           */
+} s3r_stats;
+
+/* Debug dump of one view's intermediates (DEVICE pointers, caller-allocated
+ * with the sizes of s3r_get_stats; any may be NULL).  keys/flags/rect need
+ * s3r_set_debug(ctx, 1) before the render.                                 */
+typedef struct {
+    int32_t* temporal_idx;       /* [n_temporal] ascending Gaussian indices     */
+    float* keys;                 /* [n_temporal][6] mx,my,z,a,b,c (fp32 keys)   */
+    uint8_t* flags;              /* [n_temporal] bit 1 visible, 2 small,
+                                    3 dropped, 4 rendered, 5 bad id (bit 0 set)  */
+    int16_t* rect;               /* [n_temporal][4] tile rect tx0,tx1,ty0,ty1   */
+    int32_t* depth_order;        /* [n_rendered] Gaussian indices by (z, index) */
+    int32_t* pair_tile;          /* [n_pairs] sorted pairs: tile id (row-major) */
+    int32_t* pair_gauss;         /* [n_pairs] sorted pairs: Gaussian index      */
+    int32_t* ranges;             /* [tiles][2] [start,end) per tile             */
+} s3r_debug;
+
+/* Stage timers (milliseconds, summed over renders since the last reset).    */
+enum {
+    S3R_STAGE_FILTER = 0,        /* K1 temporal filter + compaction            */
+    S3R_STAGE_PROJECT,           /* K2 projection + LOD + life update          */
+    S3R_STAGE_DEPTH_SORT,        /* K5a depth radix sort                        */
+    S3R_STAGE_EMIT,              /* K3/K4 permute + scan + key emission         */
+    S3R_STAGE_PAIR_SORT,         /* K5b tile radix sort                         */
+    S3R_STAGE_RANGES,            /* K6 tile ranges                              */
+    S3R_STAGE_RASTER,            /* K7 alpha-blend rasterizer                   */
+    S3R_NUM_STAGES
+};
+
+int s3r_version(void);
+
+/* Create a context on CUDA device `device`.  *out receives the handle.      */
+int s3r_create(int device, s3r_ctx** out);
+void s3r_destroy(s3r_ctx* ctx);
+/* Message of the last failed call (never NULL; empty when none).            */
+const char* s3r_last_error(const s3r_ctx* ctx);
+
+/* Enable (1) / disable (0) the per-Gaussian debug intermediates
+ * (keys/flags/rect) of s3r_dump_intermediates.  Costs one extra write of
+ * 34 B per projected Gaussian when on.                                      */
+int s3r_set_debug(s3r_ctx* ctx, int enable);
+/* Enable (1) / disable (0) CUDA-event stage timers; resets the sums.        */
+int s3r_set_timing(s3r_ctx* ctx, int enable);
+/* out_ms[S3R_NUM_STAGES]: summed stage times; out_count: renders timed.
+ * Synchronises the context's last stream.                                   */
+int s3r_get_stage_times(s3r_ctx* ctx, double* out_ms, int64_t* out_count);
+
+/* Instance-specific cameras: for each view v, out[v][0] = w2c[v]
+ * and out[v][i] = w2c[v] * i2g[v][i-1] (3x4 [R|t] as 4x4 homogeneous), i in
+ * 1..K, computed in fp64 and rounded once to fp32 (R-ARITH).
+ *   w2c: DEVICE float[n_views][12]; i2g: DEVICE float[n_views][K][12] (NULL if
+ *   K == 0); out: DEVICE float[n_views][K+1][12].                           */
+int s3r_compose_instance_cameras(s3r_ctx* ctx, const float* w2c, const float* i2g,
+                                 int32_t n_views, int32_t K, float* out, void* stream);
+
+/* Render one view: s3r_render_batch with n_views = 1.                       */
+int s3r_render(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* view,
+               const s3r_outputs* out, void* stream);
+
+/* Render n_views views of one scene (views/outs: HOST arrays of structs whose
+ * pointer members are DEVICE pointers).  Views sharing a time t share one
+ * temporal compaction.  If scene->life is non-NULL it is updated with every
+ * view's M_t (Eq.5; order-independent, so the result does not depend on the
+ * batch split).  Returns S3R_EINSTANCE (after completing the render) if a
+ * Gaussian had an out-of-range instance id.                                 */
+int s3r_render_batch(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* views,
+                     int32_t n_views, const s3r_outputs* outs, void* stream);
+
+/* Same as s3r_render_batch, but every pointer of scene, views (including
+ * instance_w2c) and outs is a HOST pointer (page-locked memory recommended).
+ * The library copies the inputs to device scratch, renders, copies the
+ * outputs (and the updated life) back and synchronises the stream.         */
+int s3r_render_batch_host(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* views,
+                          int32_t n_views, const s3r_outputs* outs, void* stream);
+
+/* Counts of view `view_index` of the last render (host struct).            */
+int s3r_get_stats(const s3r_ctx* ctx, int32_t view_index, s3r_stats* out);
+
+/* Copy intermediates of view `view_index` of the last render into `dbg`.   */
+int s3r_dump_intermediates(s3r_ctx* ctx, int32_t view_index, const s3r_debug* dbg,
+                           void* stream);
+
+/* Visibility commit after a sweep (Eq.6): for every Gaussian,
+ * l_s > l_e (never observed) -> v = (-1, 1); else v = (max(-1, l_s - margin),
+ * min(1, l_e + margin)); then l = (1, -1).  margin = 0.1 in the paper.      */
+int s3r_commit_visibility(s3r_ctx* ctx, const s3r_scene* scene, float margin, void* stream);
+
+/* Periodic reset: v = (-1, 1) for every Gaussian.                   */
+int s3r_reset_visibility(s3r_ctx* ctx, const s3r_scene* scene, void* stream);
+
+/* Synchronise `stream` and return the device error state accumulated since
+ * the last check: S3R_EINSTANCE, S3R_ECUDA or S3R_OK.                      */
+int s3r_check(s3r_ctx* ctx, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S3R_H */

@@ -1,0 +1,156 @@
+// k_filter.cu — K1: temporal-visibility filter + ordered stream compaction.
+//
+// PAPER.md P:171-172 (§3.3 "Temporal separation"): "we directly select the
+// visible Gaussians G' whose visibility intervals encompass t, denoted as
+// t_s <= t <= t_e".  Reading R1: t_s == v_s, t_e == v_e, inclusive; NaN -> out.
+//
+// One launch serves up to MAX_TSLOTS distinct view times: each CTA reads its
+// 4096-Gaussian slice of v = (v_s, v_e) ONCE (16-byte vector loads, 8 per
+// thread) and produces, for every time slot, the ascending list of kept
+// indices.  Within a CTA the order is fixed by warp ballots + popc (per
+// (round, warp) counts, one warp scan per slot); across CTAs by a decoupled
+// look-back per slot (CTA order from an atomic ticket, so a CTA only waits on
+// CTAs that are already resident).  Algorithmic bytes: 8 N read + 4 sum_s N_t(s)
+// written.
+#include "s3r_internal.cuh"
+
+namespace s3r {
+
+namespace {
+constexpr int FT = 256;          // threads
+constexpr int FV = 8;            // float4 (2 Gaussians) per thread
+constexpr int FTILE = FT * FV * 2;
+constexpr int FGROUPS = FV * (FT / 32);   // (round, warp) groups = 64
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p)
+{
+    return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v)
+{
+    *reinterpret_cast<volatile uint32_t*>(p) = v;
+}
+
+__global__ void __launch_bounds__(FT) k_filter(const float2* __restrict__ vis, long long n,
+                                               const float* __restrict__ times, int T,
+                                               int32_t* __restrict__ idx_out, long long stride,
+                                               unsigned long long* __restrict__ counts,
+                                               uint32_t* __restrict__ lookback,
+                                               int* __restrict__ ticket, int ntiles)
+{
+    __shared__ int s_tile;
+    __shared__ float s_t[MAX_TSLOTS];
+    __shared__ uint16_t s_cnt[MAX_TSLOTS][FGROUPS];
+    __shared__ uint32_t s_agg[MAX_TSLOTS];
+    __shared__ uint32_t s_base[MAX_TSLOTS];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1);
+    if (tid < T) s_t[tid] = times[tid];
+    __syncthreads();
+    const int tile = s_tile;
+    const long long g0 = (long long)tile * FTILE;
+
+    // v for Gaussians g0 + 2*(k*FT + tid) + {0,1}
+    float4 v[FV];
+    const float4* vis4 = reinterpret_cast<const float4*>(vis);
+#pragma unroll
+    for (int k = 0; k < FV; ++k) {
+        long long g = g0 + 2ll * (k * FT + tid);
+        if (g + 1 < n) {
+            v[k] = __ldg(vis4 + (g >> 1));
+        } else if (g < n) {
+            float2 a = __ldg(vis + g);
+            v[k] = make_float4(a.x, a.y, __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+        } else {
+            v[k] = make_float4(__int_as_float(0x7fc00000), 0.f, __int_as_float(0x7fc00000), 0.f);
+        }
+    }
+
+    // per (slot, round, warp) counts
+    for (int s = 0; s < T; ++s) {
+        const float t = s_t[s];
+#pragma unroll
+        for (int k = 0; k < FV; ++k) {
+            bool f0 = (v[k].x <= t) && (t <= v[k].y);
+            bool f1 = (v[k].z <= t) && (t <= v[k].w);
+            unsigned b0 = __ballot_sync(0xffffffffu, f0);
+            unsigned b1 = __ballot_sync(0xffffffffu, f1);
+            if (lane == 0) s_cnt[s][k * (FT / 32) + warp] = (uint16_t)(__popc(b0) + __popc(b1));
+        }
+    }
+    __syncthreads();
+
+    // exclusive scan of the 64 groups of each slot (one warp per slot)
+    for (int s = warp; s < T; s += FT / 32) {
+        uint32_t c0 = s_cnt[s][2 * lane], c1 = s_cnt[s][2 * lane + 1];
+        uint32_t x = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        uint32_t ex = x - (c0 + c1);
+        s_cnt[s][2 * lane] = (uint16_t)ex;
+        s_cnt[s][2 * lane + 1] = (uint16_t)(ex + c0);
+        if (lane == 31) s_agg[s] = x;
+    }
+    __syncthreads();
+
+    // decoupled look-back, one thread per slot
+    if (tid < T) {
+        uint32_t agg = s_agg[tid];
+        uint32_t* lb = lookback + (long long)tid * ntiles;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st_volatile(lb, LB_PRE | agg);
+        } else {
+            st_volatile(lb + tile, LB_AGG | agg);
+            int j = tile - 1;
+            while (true) {
+                uint32_t w = ld_volatile(lb + j);
+                if ((w >> 30) == 0) continue;
+                excl += w & LB_MASK;
+                if (w & LB_PRE) break;
+                --j;
+            }
+            st_volatile(lb + tile, LB_PRE | (excl + agg));
+        }
+        s_base[tid] = excl;
+        if (tile == ntiles - 1) counts[tid] = (unsigned long long)(excl + agg);
+    }
+    __syncthreads();
+
+    const unsigned lt = (1u << lane) - 1u;
+    for (int s = 0; s < T; ++s) {
+        const float t = s_t[s];
+        const uint32_t base = s_base[s];
+        int32_t* out = idx_out + (long long)s * stride;
+#pragma unroll
+        for (int k = 0; k < FV; ++k) {
+            bool f0 = (v[k].x <= t) && (t <= v[k].y);
+            bool f1 = (v[k].z <= t) && (t <= v[k].w);
+            unsigned b0 = __ballot_sync(0xffffffffu, f0);
+            unsigned b1 = __ballot_sync(0xffffffffu, f1);
+            uint32_t o = base + s_cnt[s][k * (FT / 32) + warp] + __popc(b0 & lt) + __popc(b1 & lt);
+            long long g = g0 + 2ll * (k * FT + tid);
+            if (f0) out[o] = (int32_t)g;
+            if (f1) out[o + (f0 ? 1 : 0)] = (int32_t)(g + 1);
+        }
+    }
+}
+}  // namespace
+
+void launch_filter(const float2* vis, long long n, const float* d_times, int T, int32_t* idx_out,
+                   long long idx_stride, unsigned long long* counts, uint32_t* lookback,
+                   int* ticket, cudaStream_t st)
+{
+    int ntiles = (int)((n + FTILE - 1) / FTILE);
+    if (ntiles == 0) return;
+    k_filter<<<ntiles, FT, 0, st>>>(vis, n, d_times, T, idx_out, idx_stride, counts, lookback,
+                                    ticket, ntiles);
+}
+
+int filter_tile() { return FTILE; }
+
+}  // namespace s3r

@@ -1,0 +1,451 @@
+// k_project.cu — K2: instance-specific projection + EWA covariance + frustum
+// mask M_t + Adaptive-LOD cull + point-life update, with ordered compaction of
+// the rendered splats of every view; plus the instance-camera composition.
+//
+// PAPER.md P:158-159 (instance-specific projection: W_{t,i} = W_t W_{t,i2g},
+// "we simply select the corresponding cameras based on the Gaussian's instance
+// ID"), Eq.1 P:107-112 (mu' = K W mu, Sigma' = J W Sigma W^T J^T)
+// (frustum mask M_t), Eq.7 rows 1-3 P:189-193 (LOD: p = p_max + (p_max - 1e-2)
+// min(0,(d-D)/D), M_LOD = Bernoulli(p) <= 0), Eq.5 P:173-178 (l_s = min(l_s,t),
+// l_e = max(l_e,t) where M_t).  Readings R2-R9 of DESIGN.md.
+//
+// Arithmetic: the fp32 R-ARITH contract of DESIGN.md, op for op (this file is
+// compiled with -fmad=false; FMAs are the explicit __fmaf_rn below).
+//
+// Layout: one CTA = 512 consecutive entries of one view's temporal index list
+// (2 per thread, coalesced 4-byte index loads, then 16-byte gathers of the
+// SoA float4 streams).  The view's (K+1) x 3x4 camera table is staged in
+// shared memory.  Rendered splats are compacted in index order (ballot/popc
+// within the CTA, decoupled look-back across the view's CTAs) into 48-byte
+// records {mx,my,z,o}{A,B,C,rect.x}{r,g,b,rect.y} plus a 4-byte depth key.
+#include "s3r_internal.cuh"
+
+namespace s3r {
+
+namespace {
+constexpr int PT = 256;
+constexpr int PITEMS = 2;
+constexpr int PTILE = PT * PITEMS;
+constexpr int PGROUPS = PITEMS * (PT / 32);   // 16
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p)
+{
+    return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v)
+{
+    *reinterpret_cast<volatile uint32_t*>(p) = v;
+}
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// Exact float min / max through integer atomics (valid for non-NaN values;
+// times are canonicalised so -0 never occurs).
+__device__ __forceinline__ void atomic_min_f(float* addr, float v)
+{
+    if (v >= 0.f) atomicMin(reinterpret_cast<int*>(addr), __float_as_int(v));
+    else atomicMax(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
+}
+__device__ __forceinline__ void atomic_max_f(float* addr, float v)
+{
+    if (v >= 0.f) atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+    else atomicMin(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
+}
+
+struct Splat {
+    float k[6];          // mx, my, z, a, b, c
+    float A, B, C;
+    int tx0, tx1, ty0, ty1;
+    uint8_t flags;
+};
+
+// O2 + O3 + O4 of DESIGN.md for Gaussian g in view V; M = the 12 floats of
+// its instance camera.  Returns flags.
+__device__ __forceinline__ void project_one(const float* __restrict__ M, float4 mo, float4 sc,
+                                            float4 q, const DevView& V, float lox, float hix,
+                                            float loy, float hiy, long long g, Splat& s)
+{
+    s.flags = F_TEMPORAL;
+    const float x = mo.x, y = mo.y, z = mo.z;
+    float p[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        float acc = __fmaf_rn(M[4 * r + 0], x, M[4 * r + 3]);
+        acc = __fmaf_rn(M[4 * r + 1], y, acc);
+        acc = __fmaf_rn(M[4 * r + 2], z, acc);
+        p[r] = acc;
+    }
+    const float pz = p[2];
+    if (!(pz > V.near_plane)) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) s.k[j] = __int_as_float(0x7fc00000);
+        return;
+    }
+    float n2 = q.x * q.x;
+    n2 = __fmaf_rn(q.y, q.y, n2);
+    n2 = __fmaf_rn(q.z, q.z, n2);
+    n2 = __fmaf_rn(q.w, q.w, n2);
+    const float nrm = sqrtf(n2);
+    const float w = q.x / nrm, a1 = q.y / nrm, a2 = q.z / nrm, a3 = q.w / nrm;
+    const float xx = a1 * a1, yy = a2 * a2, zz = a3 * a3;
+    const float xy = a1 * a2, xz = a1 * a3, yz = a2 * a3;
+    const float wx = w * a1, wy = w * a2, wz = w * a3;
+    float Rq[9];
+    Rq[0] = 1.0f - 2.0f * (yy + zz);
+    Rq[1] = 2.0f * (xy - wz);
+    Rq[2] = 2.0f * (xz + wy);
+    Rq[3] = 2.0f * (xy + wz);
+    Rq[4] = 1.0f - 2.0f * (xx + zz);
+    Rq[5] = 2.0f * (yz - wx);
+    Rq[6] = 2.0f * (xz - wy);
+    Rq[7] = 2.0f * (yz + wx);
+    Rq[8] = 1.0f - 2.0f * (xx + yy);
+    const float sg[3] = {sc.x, sc.y, sc.z};
+    float T[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float acc = M[4 * r + 0] * Rq[c];
+            acc = __fmaf_rn(M[4 * r + 1], Rq[3 + c], acc);
+            acc = __fmaf_rn(M[4 * r + 2], Rq[6 + c], acc);
+            T[3 * r + c] = acc * sg[c];
+        }
+    }
+    const float u = p[0] / pz;
+    const float vv = p[1] / pz;
+    const float uc = fminf(fmaxf(u, lox), hix);
+    const float vc = fminf(fmaxf(vv, loy), hiy);
+    const float j00 = V.fx / pz;
+    const float j02 = -((V.fx * uc) / pz);
+    const float j11 = V.fy / pz;
+    const float j12 = -((V.fy * vc) / pz);
+    float U0[3], U1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        U0[c] = __fmaf_rn(j02, T[6 + c], j00 * T[c]);
+        U1[c] = __fmaf_rn(j12, T[6 + c], j11 * T[3 + c]);
+    }
+    float ka = U0[0] * U0[0];
+    ka = __fmaf_rn(U0[1], U0[1], ka);
+    ka = __fmaf_rn(U0[2], U0[2], ka);
+    float kb = U0[0] * U1[0];
+    kb = __fmaf_rn(U0[1], U1[1], kb);
+    kb = __fmaf_rn(U0[2], U1[2], kb);
+    float kc = U1[0] * U1[0];
+    kc = __fmaf_rn(U1[1], U1[1], kc);
+    kc = __fmaf_rn(U1[2], U1[2], kc);
+    const float mx = __fmaf_rn(V.fx, u, V.cx);
+    const float my = __fmaf_rn(V.fy, vv, V.cy);
+    s.k[0] = mx; s.k[1] = my; s.k[2] = pz; s.k[3] = ka; s.k[4] = kb; s.k[5] = kc;
+
+    // ---- O3 decisions ----
+    if (!(isfinite(mx) && isfinite(my) && isfinite(pz) && isfinite(ka) && isfinite(kb) &&
+          isfinite(kc)))
+        return;
+    const float ad = ka + 0.3f;
+    const float cd = kc + 0.3f;
+    const float d1 = ad * cd;
+    const float d2 = kb * kb;
+    const float det = d1 - d2;
+    if (!(det > 0.0f)) return;
+    s.A = cd / det;
+    s.B = (-kb) / det;
+    s.C = ad / det;
+    const float h = 0.5f * (ka - kc);
+    const float e1 = h * h;
+    const float e2 = kb * kb;
+    const float disc = sqrtf(e1 + e2);
+    const float lamd = (0.5f * (ad + cd)) + disc;
+    const float rf = ceilf(3.0f * sqrtf(lamd));
+    if (!isfinite(rf)) return;
+    const float xlo = ceilf(mx - rf), xhi = floorf(mx + rf);
+    const float ylo = ceilf(my - rf), yhi = floorf(my + rf);
+    const float Wm1 = (float)(V.W - 1), Hm1 = (float)(V.H - 1);
+    if (!(xlo <= Wm1 && xhi >= 0.0f && ylo <= Hm1 && yhi >= 0.0f)) return;
+    const int x0 = (int)fmaxf(xlo, 0.0f), x1 = (int)fminf(xhi, Wm1);
+    const int y0 = (int)fmaxf(ylo, 0.0f), y1 = (int)fminf(yhi, Hm1);
+    s.tx0 = x0 >> 4; s.tx1 = x1 >> 4; s.ty0 = y0 >> 4; s.ty1 = y1 >> 4;
+    s.flags |= F_VISIBLE;
+
+    // ---- O4 adaptive LOD ----
+    const float lam = (0.5f * (ka + kc)) + disc;
+    const float sc2 = 3.0f * sqrtf(fmaxf(lam, 0.0f));
+    if (V.lod_r > 0.0f && sc2 <= V.lod_r) {
+        s.flags |= F_SMALL;
+        const float m = fminf(0.0f, (pz - V.lod_D) / V.lod_D);
+        float pd = __fmaf_rn(V.lod_pmax - 0.01f, m, V.lod_pmax);
+        pd = fminf(fmaxf(pd, 0.0f), 1.0f);
+        const unsigned long long hsh = splitmix64(V.seed ^ splitmix64((unsigned long long)g));
+        const float uu = (float)(uint32_t)(hsh >> 40) * 5.9604644775390625e-8f;
+        if (uu < pd) {
+            s.flags |= F_DROPPED;
+            return;
+        }
+    }
+    s.flags |= F_RENDERED;
+}
+
+__global__ void __launch_bounds__(PT) k_project(ProjectArgs a)
+{
+    extern __shared__ float s_tab[];          // [K1][12]
+    __shared__ int s_gtile, s_view;
+    __shared__ float s_bounds[4];
+    __shared__ uint32_t s_grp[PGROUPS];
+    __shared__ uint32_t s_base;
+    __shared__ unsigned long long s_red[5][PT / 32];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        int gt = atomicAdd(a.ticket, 1);
+        // view = last v with view_tile0[v] <= gt
+        int lo = 0, hi = a.n_views - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (a.view_tile0[mid] <= gt) lo = mid; else hi = mid - 1;
+        }
+        s_gtile = gt;
+        s_view = lo;
+    }
+    __syncthreads();
+    const int gtile = s_gtile, vi = s_view;
+    const DevView V = a.views[vi];
+    const int ltile = gtile - a.view_tile0[vi];
+    const int K1 = a.num_instances;
+    for (int i = tid; i < K1 * 12; i += PT) s_tab[i] = V.table[i];
+    if (tid == 0) {
+        // tangent-plane clamp bounds (reading R5), per view, in R-ARITH order
+        const float Wf = (float)V.W, Hf = (float)V.H;
+        s_bounds[0] = (-(0.15f * Wf) - V.cx) / V.fx;
+        s_bounds[1] = ((1.15f * Wf) - V.cx) / V.fx;
+        s_bounds[2] = (-(0.15f * Hf) - V.cy) / V.fy;
+        s_bounds[3] = ((1.15f * Hf) - V.cy) / V.fy;
+    }
+    __syncthreads();
+    const float lox = s_bounds[0], hix = s_bounds[1], loy = s_bounds[2], hiy = s_bounds[3];
+    const int32_t* tl = a.tidx + (long long)V.tslot * a.idx_stride;
+
+    Splat sp[PITEMS];
+    long long gg[PITEMS];
+    float4 col[PITEMS];
+    unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0;
+#pragma unroll
+    for (int k = 0; k < PITEMS; ++k) {
+        const long long i = (long long)ltile * PTILE + k * PT + tid;
+        sp[k].flags = 0;
+        gg[k] = -1;
+        if (i < V.n_temporal) {
+            const long long g = tl[i];
+            gg[k] = g;
+            const int id = __ldg(a.ids + g);
+            if (id < 0 || id >= K1) {
+                sp[k].flags = F_TEMPORAL | F_BADID;
+#pragma unroll
+                for (int j = 0; j < 6; ++j) sp[k].k[j] = __int_as_float(0x7fc00000);
+                c_bad++;
+            } else {
+                const float4 mo = __ldg(a.means_opacity + g);
+                const float4 sc = __ldg(a.scales + g);
+                const float4 q = __ldg(a.rotations + g);
+                project_one(s_tab + 12 * id, mo, sc, q, V, lox, hix, loy, hiy, g, sp[k]);
+                if (sp[k].flags & F_VISIBLE) {
+                    c_vis++;
+                    if (V.visible) V.visible[g] = 1;
+                    if (a.life) {
+                        float2 l = a.life[g];
+                        float* lp = reinterpret_cast<float*>(a.life + g);
+                        if (V.t < l.x) atomic_min_f(lp, V.t);
+                        if (V.t > l.y) atomic_max_f(lp + 1, V.t);
+                    }
+                }
+                if (sp[k].flags & F_SMALL) c_small++;
+                if (sp[k].flags & F_DROPPED) c_drop++;
+                if (sp[k].flags & F_RENDERED) {
+                    col[k] = __ldg(a.colors + g);
+                    c_pairs += (unsigned long long)(sp[k].tx1 - sp[k].tx0 + 1) *
+                               (unsigned long long)(sp[k].ty1 - sp[k].ty0 + 1);
+                    col[k].w = mo.w;   // opacity travels in the record
+                }
+            }
+            if (a.dbg_flags) {
+                const long long di = V.dbg_off + i;
+                a.dbg_flags[di] = sp[k].flags;
+#pragma unroll
+                for (int j = 0; j < 6; ++j) a.dbg_keys[6 * di + j] = sp[k].k[j];
+                const bool vis = sp[k].flags & F_VISIBLE;
+                a.dbg_rect[4 * di + 0] = (int16_t)(vis ? sp[k].tx0 : 0);
+                a.dbg_rect[4 * di + 1] = (int16_t)(vis ? sp[k].tx1 : 0);
+                a.dbg_rect[4 * di + 2] = (int16_t)(vis ? sp[k].ty0 : 0);
+                a.dbg_rect[4 * di + 3] = (int16_t)(vis ? sp[k].ty1 : 0);
+            }
+        }
+    }
+
+    // ---- ordered compaction of rendered splats ----
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned bal[PITEMS];
+#pragma unroll
+    for (int k = 0; k < PITEMS; ++k) {
+        bal[k] = __ballot_sync(0xffffffffu, (sp[k].flags & F_RENDERED) != 0);
+        if (lane == 0) s_grp[k * (PT / 32) + warp] = __popc(bal[k]);
+    }
+    // counters: warp reduce
+    unsigned long long cv[5] = {c_vis, c_small, c_drop, c_pairs, c_bad};
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        unsigned long long x = cv[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) s_red[j][warp] = x;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t c = lane < PGROUPS ? s_grp[lane] : 0;
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane < PGROUPS) s_grp[lane] = x - c;
+        const uint32_t agg = __shfl_sync(0xffffffffu, x, 31);
+        if (lane == 0) {
+            uint32_t* lb = a.lookback;
+            uint32_t excl = 0;
+            if (ltile == 0) {
+                st_volatile(lb + gtile, LB_PRE | agg);
+            } else {
+                st_volatile(lb + gtile, LB_AGG | agg);
+                int j = gtile - 1;
+                while (true) {
+                    uint32_t w = ld_volatile(lb + j);
+                    if ((w >> 30) == 0) continue;
+                    excl += w & LB_MASK;
+                    if (w & LB_PRE) break;
+                    --j;
+                }
+                st_volatile(lb + gtile, LB_PRE | (excl + agg));
+            }
+            s_base = excl;
+            ViewCounters* ctr = a.counters + vi;
+            unsigned long long t5[5] = {0, 0, 0, 0, 0};
+            for (int w = 0; w < PT / 32; ++w)
+                for (int j = 0; j < 5; ++j) t5[j] += s_red[j][w];
+            if (t5[0]) atomicAdd(&ctr->n_visible, t5[0]);
+            if (t5[1]) atomicAdd(&ctr->n_small, t5[1]);
+            if (t5[2]) atomicAdd(&ctr->n_dropped, t5[2]);
+            if (t5[3]) atomicAdd(&ctr->n_pairs, t5[3]);
+            if (t5[4]) { atomicAdd(&ctr->n_bad, t5[4]); atomicOr(a.err, ERR_BADID); }
+            if (agg) atomicAdd(&ctr->n_rendered, (unsigned long long)agg);
+        }
+    }
+    __syncthreads();
+    const long long base = V.cap_off + s_base;
+#pragma unroll
+    for (int k = 0; k < PITEMS; ++k) {
+        if (sp[k].flags & F_RENDERED) {
+            const long long o = base + s_grp[k * (PT / 32) + warp] + __popc(bal[k] & lt);
+            const uint32_t rx = (uint32_t)sp[k].tx0 | ((uint32_t)sp[k].tx1 << 16);
+            const uint32_t ry = (uint32_t)sp[k].ty0 | ((uint32_t)sp[k].ty1 << 16);
+            float4* r = a.rec + 3 * o;
+            r[0] = make_float4(sp[k].k[0], sp[k].k[1], sp[k].k[2], col[k].w);
+            r[1] = make_float4(sp[k].A, sp[k].B, sp[k].C, __uint_as_float(rx));
+            r[2] = make_float4(col[k].x, col[k].y, col[k].z, __uint_as_float(ry));
+            a.dkey[o] = __float_as_uint(sp[k].k[2]);
+            if (a.gidx) a.gidx[o] = (int32_t)gg[k];
+        }
+    }
+}
+
+// W_{t,i} = W_t W_{t,i2g} in fp64 (R-ARITH dot3 order), rounded once.
+__global__ void k_compose(const float* __restrict__ w2c, const float* __restrict__ i2g,
+                          int n_views, int K, float* __restrict__ out)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int K1 = K + 1;
+    if (idx >= n_views * K1) return;
+    const int v = idx / K1, i = idx % K1;
+    const float* A = w2c + 12ll * v;
+    float* O = out + 12ll * idx;
+    if (i == 0) {
+        for (int k = 0; k < 12; ++k) O[k] = A[k];
+        return;
+    }
+    const float* B = i2g + 12ll * ((long long)v * K + (i - 1));
+    for (int r = 0; r < 3; ++r) {
+        const double a0 = A[4 * r + 0], a1 = A[4 * r + 1], a2 = A[4 * r + 2], a3 = A[4 * r + 3];
+        for (int c = 0; c < 3; ++c) {
+            double acc = a0 * (double)B[c];
+            acc = __fma_rn(a1, (double)B[4 + c], acc);
+            acc = __fma_rn(a2, (double)B[8 + c], acc);
+            O[4 * r + c] = (float)acc;
+        }
+        double acc = __fma_rn(a0, (double)B[3], a3);
+        acc = __fma_rn(a1, (double)B[7], acc);
+        acc = __fma_rn(a2, (double)B[11], acc);
+        O[4 * r + 3] = (float)acc;
+    }
+}
+
+// K9: Eq.6 commit and P:183 reset.
+__global__ void k_commit(float2* __restrict__ vis, float2* __restrict__ life, long long n,
+                         float margin)
+{
+    const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const float2 l = life[g];
+    float2 v;
+    if (l.x > l.y) {
+        v = make_float2(-1.0f, 1.0f);
+    } else {
+        v = make_float2(fmaxf(-1.0f, l.x - margin), fminf(1.0f, l.y + margin));
+    }
+    vis[g] = v;
+    life[g] = make_float2(1.0f, -1.0f);
+}
+
+__global__ void k_reset(float2* __restrict__ vis, long long n)
+{
+    const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (g < n) vis[g] = make_float2(-1.0f, 1.0f);
+}
+}  // namespace
+
+void launch_project(const ProjectArgs& a, cudaStream_t st)
+{
+    if (a.total_tiles == 0) return;
+    const size_t smem = (size_t)a.num_instances * 12 * sizeof(float);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_project<<<a.total_tiles, PT, smem, st>>>(a);
+}
+
+int project_tile() { return PTILE; }
+
+void launch_compose(const float* w2c, const float* i2g, int n_views, int K, float* out,
+                    cudaStream_t st)
+{
+    const int total = n_views * (K + 1);
+    if (total == 0) return;
+    k_compose<<<(total + 127) / 128, 128, 0, st>>>(w2c, i2g, n_views, K, out);
+}
+
+void launch_commit(float2* vis, float2* life, long long n, float margin, cudaStream_t st)
+{
+    if (n == 0) return;
+    k_commit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vis, life, n, margin);
+}
+
+void launch_reset(float2* vis, long long n, cudaStream_t st)
+{
+    if (n == 0) return;
+    k_reset<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vis, n);
+}
+
+}  // namespace s3r

@@ -1,0 +1,863 @@
+// s3r_api.cu — the C ABI of include/s3r.h: validation, scratch management and
+// the launch sequence of one batch (K1 -> K2 -> depth sort -> emit -> tile
+// sort -> ranges -> raster).  Host code only orchestrates; every step of the
+// path runs in the kernels of k_*.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/s3r.h"
+#include "s3r_internal.cuh"
+
+using namespace s3r;
+
+namespace s3r {
+int filter_tile();
+int project_tile();
+}
+
+namespace {
+
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+struct StageEvent {
+    int stage;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct s3r_ctx {
+    int device = 0;
+    std::string err;
+    bool debug = false, timing = false;
+    bool last_debug = false;
+    // pinned staging
+    char* h_stage = nullptr;
+    size_t h_stage_cap = 0;
+    size_t h_stage_top = 0;
+    cudaEvent_t staging_free = nullptr;
+    bool staging_recorded = false;
+    cudaStream_t last_stream = nullptr;
+    // device scratch
+    Buf d_views, d_times, d_tidx, d_counts, d_lb, d_ticket, d_tile0, d_ctr, d_rec, d_dkey,
+        d_gidx, d_sortk[2], d_sortv[2], d_recs, d_pairs[2], d_hist, d_dsegs, d_dtile0, d_etile0,
+        d_psegs, d_ptile0, d_ranges, d_range_off, d_vpo, d_err, d_dbg_keys, d_dbg_flags,
+        d_dbg_rect;
+    int ticket_slot = 0;
+    // mirrors for s3r_render_batch_host
+    Buf m_scene[7];
+    std::vector<Buf> m_tab, m_rgb, m_depth, m_T, m_vis;
+    // last batch
+    std::vector<DevView> hv;
+    std::vector<s3r_stats> stats;
+    std::vector<int> range_off;
+    long long N_last = 0;
+    int final_order = 1, final_pairs = 0;
+    bool have_render = false;
+    // timers
+    std::vector<StageEvent> ev;
+    double stage_ms[S3R_NUM_STAGES] = {0};
+    long long timed_renders = 0;
+};
+
+namespace {
+
+int fail(s3r_ctx* c, int code, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+#define CU(x)                                                                               \
+    do {                                                                                    \
+        cudaError_t e_ = (x);                                                               \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(c, S3R_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x,              \
+                        cudaGetErrorString(e_));                                            \
+    } while (0)
+
+int ensure(s3r_ctx* c, Buf& b, size_t bytes)
+{
+    if (bytes <= b.cap && b.p) return S3R_OK;
+    if (b.p) {
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        if (cudaMalloc(&b.p, std::max<size_t>(bytes, 256)) != cudaSuccess) {
+            cudaGetLastError();
+            b.p = nullptr;
+            return fail(c, S3R_ENOMEM, "cudaMalloc of %zu bytes failed", bytes);
+        }
+        want = std::max<size_t>(bytes, 256);
+    }
+    b.cap = want;
+    return S3R_OK;
+}
+
+template <typename T>
+T* P(const Buf& b) { return reinterpret_cast<T*>(b.p); }
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+// pinned staging: a bump allocator reset at the start of each batch
+int stage_reserve(s3r_ctx* c, size_t bytes)
+{
+    if (bytes <= c->h_stage_cap) return S3R_OK;
+    if (c->h_stage) {
+        cudaDeviceSynchronize();
+        cudaFreeHost(c->h_stage);
+        c->h_stage = nullptr;
+    }
+    size_t want = std::max<size_t>(bytes * 2, 1 << 16);
+    if (cudaHostAlloc((void**)&c->h_stage, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        c->h_stage = nullptr;
+        c->h_stage_cap = 0;
+        return fail(c, S3R_ENOMEM, "cudaHostAlloc of %zu bytes failed", want);
+    }
+    c->h_stage_cap = want;
+    return S3R_OK;
+}
+
+void* stage_alloc(s3r_ctx* c, size_t bytes)
+{
+    size_t off = (c->h_stage_top + 255) & ~size_t(255);
+    c->h_stage_top = off + bytes;
+    return c->h_stage + off;
+}
+
+int* next_ticket(s3r_ctx* c) { return P<int>(c->d_ticket) + (c->ticket_slot++); }
+
+void ev_begin(s3r_ctx* c, int stage, cudaStream_t st, StageEvent& e)
+{
+    e.stage = -1;
+    if (!c->timing) return;
+    if (c->ev.size() > 200000) return;
+    e.stage = stage;
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    cudaEventRecord(e.a, st);
+}
+void ev_end(s3r_ctx* c, cudaStream_t st, StageEvent& e)
+{
+    if (e.stage < 0) return;
+    cudaEventRecord(e.b, st);
+    c->ev.push_back(e);
+}
+
+int validate(s3r_ctx* c, const s3r_scene* s, const s3r_view* views, int nv,
+             const s3r_outputs* outs)
+{
+    if (!s) return fail(c, S3R_EINVAL, "scene is NULL");
+    if (s->n < 0 || s->n >= (1ll << 30)) return fail(c, S3R_EINVAL, "n = %lld out of [0, 2^30)", (long long)s->n);
+    if (s->num_instances < 1 || s->num_instances > 4096)
+        return fail(c, S3R_EINVAL, "num_instances = %d out of [1, 4096]", s->num_instances);
+    if (s->n > 0) {
+        const void* req[] = {s->means_opacity, s->scales, s->rotations, s->colors, s->visibility};
+        const char* nm[] = {"means_opacity", "scales", "rotations", "colors", "visibility"};
+        for (int i = 0; i < 5; ++i) {
+            if (!req[i]) return fail(c, S3R_EINVAL, "scene.%s is NULL", nm[i]);
+            if (!aligned(req[i], 16)) return fail(c, S3R_EINVAL, "scene.%s is not 16-byte aligned", nm[i]);
+        }
+        if (!s->instance_ids || !aligned(s->instance_ids, 4))
+            return fail(c, S3R_EINVAL, "scene.instance_ids is NULL or misaligned");
+        if (s->life && !aligned(s->life, 8)) return fail(c, S3R_EINVAL, "scene.life is not 8-byte aligned");
+    }
+    if (nv < 0) return fail(c, S3R_EINVAL, "n_views < 0");
+    if (nv > 0 && (!views || !outs)) return fail(c, S3R_EINVAL, "views/outs is NULL");
+    for (int v = 0; v < nv; ++v) {
+        const s3r_view& V = views[v];
+        if (V.width < 1 || V.width > 16384 || V.height < 1 || V.height > 16384)
+            return fail(c, S3R_EINVAL, "view %d: size %dx%d out of [1,16384]", v, V.width, V.height);
+        if (!(std::isfinite(V.fx) && V.fx > 0 && std::isfinite(V.fy) && V.fy > 0))
+            return fail(c, S3R_EINVAL, "view %d: fx/fy must be finite and > 0", v);
+        if (!(std::isfinite(V.cx) && std::isfinite(V.cy)))
+            return fail(c, S3R_EINVAL, "view %d: cx/cy must be finite", v);
+        if (!(V.t >= -1.0f && V.t <= 1.0f)) return fail(c, S3R_EINVAL, "view %d: t outside [-1,1]", v);
+        if (!(std::isfinite(V.near_plane) && V.near_plane > 0))
+            return fail(c, S3R_EINVAL, "view %d: near_plane must be finite and > 0", v);
+        if (!V.instance_w2c || !aligned(V.instance_w2c, 4))
+            return fail(c, S3R_EINVAL, "view %d: instance_w2c is NULL or misaligned", v);
+        if (!std::isfinite(V.lod_r)) return fail(c, S3R_EINVAL, "view %d: lod_r not finite", v);
+        if (!(V.lod_pmax >= 0.0f && V.lod_pmax <= 1.0f))
+            return fail(c, S3R_EINVAL, "view %d: lod_pmax outside [0,1]", v);
+        if (!(std::isfinite(V.lod_D) && V.lod_D > 0))
+            return fail(c, S3R_EINVAL, "view %d: lod_D must be finite and > 0", v);
+        const s3r_outputs& O = outs[v];
+        if (!O.rgb || !aligned(O.rgb, 4)) return fail(c, S3R_EINVAL, "outs[%d].rgb is NULL or misaligned", v);
+        if (O.depth && !aligned(O.depth, 4)) return fail(c, S3R_EINVAL, "outs[%d].depth misaligned", v);
+        if (O.final_T && !aligned(O.final_T, 4)) return fail(c, S3R_EINVAL, "outs[%d].final_T misaligned", v);
+    }
+    return S3R_OK;
+}
+
+int bits_for(long long x)   // bits needed to hold values in [0, x)
+{
+    int b = 0;
+    while ((1ll << b) < x) ++b;
+    return std::max(b, 1);
+}
+
+int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
+                const s3r_outputs* outs, cudaStream_t st)
+{
+    int rc = validate(c, sc, views, nv, outs);
+    if (rc) return rc;
+    CU(cudaSetDevice(c->device));
+    c->last_stream = st;
+    c->have_render = false;
+    if (c->staging_recorded) CU(cudaEventSynchronize(c->staging_free));
+    const long long N = sc->n;
+    c->N_last = N;
+    c->ticket_slot = 0;
+    c->last_debug = c->debug;
+
+    // ---- distinct times (views sharing t share K1's compaction)
+    std::vector<float> tk;
+    std::vector<int> slot(nv);
+    for (int v = 0; v < nv; ++v) {
+        const float t = views[v].t + 0.0f;
+        int s = -1;
+        for (size_t i = 0; i < tk.size(); ++i)
+            if (tk[i] == t) { s = (int)i; break; }
+        if (s < 0) { s = (int)tk.size(); tk.push_back(t); }
+        slot[v] = s;
+    }
+    const int T = (int)tk.size();
+
+    c->hv.assign(nv, DevView{});
+    for (int v = 0; v < nv; ++v) {
+        const s3r_view& V = views[v];
+        DevView& d = c->hv[v];
+        d.t = V.t + 0.0f;
+        d.W = V.width; d.H = V.height;
+        d.fx = V.fx; d.fy = V.fy; d.cx = V.cx; d.cy = V.cy; d.near_plane = V.near_plane;
+        d.table = V.instance_w2c;
+        d.lod_r = V.lod_r; d.lod_pmax = V.lod_pmax; d.lod_D = V.lod_D;
+        d.seed = (unsigned long long)V.lod_seed;
+        d.tslot = slot[v];
+        d.TX = (V.width + TILE - 1) / TILE;
+        d.TY = (V.height + TILE - 1) / TILE;
+        d.ntiles = d.TX * d.TY;
+        d.rgb = outs[v].rgb; d.depth = outs[v].depth; d.finalT = outs[v].final_T;
+        d.visible = outs[v].visible;
+    }
+
+    // staging layout for this batch
+    const size_t stage_bytes = 8192 + (size_t)T * 16 + (size_t)nv * (3 * sizeof(DevView) + 256) +
+                               (size_t)(nv + 1) * 64;
+    if ((rc = stage_reserve(c, stage_bytes))) return rc;
+    c->h_stage_top = 0;
+    if ((rc = ensure(c, c->d_ticket, 256 * sizeof(int)))) return rc;
+    if ((rc = ensure(c, c->d_err, sizeof(uint32_t)))) return rc;
+    CU(cudaMemsetAsync(c->d_ticket.p, 0, 256 * sizeof(int), st));
+
+    // ================= K1: temporal filter + compaction
+    const long long Ns = std::max<long long>(N, 1);
+    if ((rc = ensure(c, c->d_tidx, (size_t)std::max(T, 1) * Ns * sizeof(int32_t)))) return rc;
+    if ((rc = ensure(c, c->d_counts, (size_t)std::max(T, 1) * sizeof(unsigned long long)))) return rc;
+    if ((rc = ensure(c, c->d_times, (size_t)std::max(T, 1) * sizeof(float)))) return rc;
+    CU(cudaMemsetAsync(c->d_counts.p, 0, (size_t)std::max(T, 1) * sizeof(unsigned long long), st));
+    float* h_times = (float*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(float));
+    for (int i = 0; i < T; ++i) h_times[i] = tk[i];
+    if (T) CU(cudaMemcpyAsync(c->d_times.p, h_times, T * sizeof(float), cudaMemcpyHostToDevice, st));
+    {
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_FILTER, st, e);
+        const long long ntf = (N + filter_tile() - 1) / filter_tile();
+        for (int c0 = 0; c0 < T && N > 0; c0 += MAX_TSLOTS) {
+            const int Tc = std::min(MAX_TSLOTS, T - c0);
+            if ((rc = ensure(c, c->d_lb, (size_t)Tc * ntf * sizeof(uint32_t)))) return rc;
+            CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)Tc * ntf * sizeof(uint32_t), st));
+            launch_filter(reinterpret_cast<const float2*>(sc->visibility), N,
+                          P<float>(c->d_times) + c0, Tc, P<int32_t>(c->d_tidx) + (long long)c0 * Ns,
+                          Ns, P<unsigned long long>(c->d_counts) + c0, P<uint32_t>(c->d_lb),
+                          next_ticket(c), st);
+        }
+        ev_end(c, st, e);
+    }
+    CU(cudaGetLastError());
+    unsigned long long* h_counts =
+        (unsigned long long*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(unsigned long long));
+    if (T) CU(cudaMemcpyAsync(h_counts, c->d_counts.p, T * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+
+    // ================= K2: projection + LOD + life + compaction
+    long long cap = 0;
+    std::vector<int> vtile0(nv + 1, 0);
+    for (int v = 0; v < nv; ++v) {
+        DevView& d = c->hv[v];
+        d.n_temporal = (long long)h_counts[d.tslot];
+        d.cap_off = cap;
+        d.dbg_off = cap;
+        cap += d.n_temporal;
+        vtile0[v + 1] = vtile0[v] + (int)((d.n_temporal + project_tile() - 1) / project_tile());
+    }
+    const long long capS = std::max<long long>(cap, 1);
+    const int k2_tiles = vtile0[nv];
+    if ((rc = ensure(c, c->d_rec, (size_t)capS * 48))) return rc;
+    if ((rc = ensure(c, c->d_dkey, (size_t)capS * 4))) return rc;
+    if (c->debug) {
+        if ((rc = ensure(c, c->d_gidx, (size_t)capS * 4))) return rc;
+        if ((rc = ensure(c, c->d_dbg_keys, (size_t)capS * 24))) return rc;
+        if ((rc = ensure(c, c->d_dbg_flags, (size_t)capS))) return rc;
+        if ((rc = ensure(c, c->d_dbg_rect, (size_t)capS * 8))) return rc;
+    }
+    if ((rc = ensure(c, c->d_views, (size_t)std::max(nv, 1) * sizeof(DevView)))) return rc;
+    if ((rc = ensure(c, c->d_tile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
+    if ((rc = ensure(c, c->d_ctr, (size_t)std::max(nv, 1) * sizeof(ViewCounters)))) return rc;
+    DevView* h_views = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
+    std::memcpy(h_views, c->hv.data(), (size_t)nv * sizeof(DevView));
+    int* h_t0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
+    std::memcpy(h_t0, vtile0.data(), (size_t)(nv + 1) * sizeof(int));
+    if (nv) {
+        CU(cudaMemcpyAsync(c->d_views.p, h_views, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_tile0.p, h_t0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(c->d_ctr.p, 0, nv * sizeof(ViewCounters), st));
+    }
+    if ((rc = ensure(c, c->d_lb, (size_t)std::max(k2_tiles, 1) * sizeof(uint32_t)))) return rc;
+    CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)std::max(k2_tiles, 1) * sizeof(uint32_t), st));
+    for (int v = 0; v < nv; ++v)
+        if (outs[v].visible && N > 0) CU(cudaMemsetAsync(outs[v].visible, 0, (size_t)N, st));
+    {
+        ProjectArgs a{};
+        a.means_opacity = reinterpret_cast<const float4*>(sc->means_opacity);
+        a.scales = reinterpret_cast<const float4*>(sc->scales);
+        a.rotations = reinterpret_cast<const float4*>(sc->rotations);
+        a.colors = reinterpret_cast<const float4*>(sc->colors);
+        a.ids = sc->instance_ids;
+        a.life = reinterpret_cast<float2*>(sc->life);
+        a.num_instances = sc->num_instances;
+        a.n = N;
+        a.views = P<DevView>(c->d_views);
+        a.n_views = nv;
+        a.tidx = P<int32_t>(c->d_tidx);
+        a.idx_stride = Ns;
+        a.view_tile0 = P<int>(c->d_tile0);
+        a.total_tiles = k2_tiles;
+        a.rec = P<float4>(c->d_rec);
+        a.dkey = P<uint32_t>(c->d_dkey);
+        a.gidx = c->debug ? P<int32_t>(c->d_gidx) : nullptr;
+        a.counters = P<ViewCounters>(c->d_ctr);
+        a.lookback = P<uint32_t>(c->d_lb);
+        a.ticket = next_ticket(c);
+        a.err = P<uint32_t>(c->d_err);
+        a.dbg_keys = c->debug ? P<float>(c->d_dbg_keys) : nullptr;
+        a.dbg_flags = c->debug ? P<uint8_t>(c->d_dbg_flags) : nullptr;
+        a.dbg_rect = c->debug ? P<int16_t>(c->d_dbg_rect) : nullptr;
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_PROJECT, st, e);
+        launch_project(a, st);
+        ev_end(c, st, e);
+    }
+    CU(cudaGetLastError());
+    ViewCounters* h_ctr = (ViewCounters*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(ViewCounters));
+    if (nv) CU(cudaMemcpyAsync(h_ctr, c->d_ctr.p, nv * sizeof(ViewCounters), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+
+    // ================= sizes of the sort / emit / raster phase
+    c->stats.assign(nv, s3r_stats{});
+    std::vector<long long> vpo(nv + 1, 0);
+    std::vector<int> dt0(nv + 1, 0), et0(nv + 1, 0), pt0(nv + 1, 0);
+    c->range_off.assign(nv + 1, 0);
+    int max_tiles = 0;
+    bool bad = false;
+    const int stile = onesweep32_tile();
+    for (int v = 0; v < nv; ++v) {
+        DevView& d = c->hv[v];
+        const ViewCounters& k = h_ctr[v];
+        d.n_rendered = (long long)k.n_rendered;
+        d.n_pairs = (long long)k.n_pairs;
+        if (d.n_pairs >= (1ll << 30))
+            return fail(c, S3R_EINVAL, "view %d: %lld tile pairs exceed 2^30", v, d.n_pairs);
+        d.pair_off = vpo[v];
+        vpo[v + 1] = vpo[v] + d.n_pairs;
+        dt0[v + 1] = dt0[v] + (int)((d.n_rendered + stile - 1) / stile);
+        et0[v + 1] = et0[v] + (int)((d.n_rendered + emit_tile() - 1) / emit_tile());
+        pt0[v + 1] = pt0[v] + (int)((d.n_pairs + onesweep64_tile() - 1) / onesweep64_tile());
+        c->range_off[v + 1] = c->range_off[v] + d.ntiles;
+        max_tiles = std::max(max_tiles, d.ntiles);
+        s3r_stats& s = c->stats[v];
+        s.n_scene = N;
+        s.n_temporal = d.n_temporal;
+        s.n_visible = (long long)k.n_visible;
+        s.n_lod_small = (long long)k.n_small;
+        s.n_lod_dropped = (long long)k.n_dropped;
+        s.n_rendered = d.n_rendered;
+        s.n_pairs = d.n_pairs;
+        s.n_bad_instance = (long long)k.n_bad;
+        if (k.n_bad) bad = true;
+    }
+    const long long total_pairs = vpo[nv];
+    const int dtiles = dt0[nv], etiles = et0[nv], ptiles = pt0[nv];
+    const int tilebits = bits_for(std::max(max_tiles, 1));
+    const int ppasses = (tilebits + RADIX_BITS - 1) / RADIX_BITS;
+
+    // device-side metadata for the rest of the batch
+    Seg* h_dsegs = (Seg*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(Seg));
+    Seg* h_psegs = (Seg*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(Seg));
+    int* h_dt0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
+    int* h_et0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
+    int* h_pt0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
+    int* h_ro = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
+    long long* h_vpo = (long long*)stage_alloc(c, (size_t)(nv + 1) * sizeof(long long));
+    DevView* h_views2 = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
+    for (int v = 0; v < nv; ++v) {
+        const DevView& d = c->hv[v];
+        h_dsegs[v] = Seg{d.cap_off, d.n_rendered, dt0[v], dt0[v + 1] - dt0[v]};
+        h_psegs[v] = Seg{d.pair_off, d.n_pairs, pt0[v], pt0[v + 1] - pt0[v]};
+    }
+    std::memcpy(h_dt0, dt0.data(), (nv + 1) * sizeof(int));
+    std::memcpy(h_et0, et0.data(), (nv + 1) * sizeof(int));
+    std::memcpy(h_pt0, pt0.data(), (nv + 1) * sizeof(int));
+    std::memcpy(h_ro, c->range_off.data(), (nv + 1) * sizeof(int));
+    std::memcpy(h_vpo, vpo.data(), (nv + 1) * sizeof(long long));
+    std::memcpy(h_views2, c->hv.data(), (size_t)nv * sizeof(DevView));
+
+    if ((rc = ensure(c, c->d_dsegs, (size_t)std::max(nv, 1) * sizeof(Seg)))) return rc;
+    if ((rc = ensure(c, c->d_psegs, (size_t)std::max(nv, 1) * sizeof(Seg)))) return rc;
+    if ((rc = ensure(c, c->d_dtile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
+    if ((rc = ensure(c, c->d_etile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
+    if ((rc = ensure(c, c->d_ptile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
+    if ((rc = ensure(c, c->d_range_off, (size_t)(nv + 1) * sizeof(int)))) return rc;
+    if ((rc = ensure(c, c->d_vpo, (size_t)(nv + 1) * sizeof(long long)))) return rc;
+    if (nv) {
+        CU(cudaMemcpyAsync(c->d_dsegs.p, h_dsegs, nv * sizeof(Seg), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_psegs.p, h_psegs, nv * sizeof(Seg), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_dtile0.p, h_dt0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_etile0.p, h_et0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_ptile0.p, h_pt0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_range_off.p, h_ro, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_vpo.p, h_vpo, (nv + 1) * sizeof(long long), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(c->d_views.p, h_views2, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
+    }
+    for (int i = 0; i < 2; ++i) {
+        if ((rc = ensure(c, c->d_sortk[i], (size_t)capS * 4))) return rc;
+        if ((rc = ensure(c, c->d_sortv[i], (size_t)capS * 4))) return rc;
+        if ((rc = ensure(c, c->d_pairs[i], (size_t)std::max<long long>(total_pairs, 1) * 8))) return rc;
+    }
+    if ((rc = ensure(c, c->d_recs, (size_t)capS * 48))) return rc;
+    const int hpasses = std::max(4, ppasses);
+    if ((rc = ensure(c, c->d_hist, (size_t)std::max(nv, 1) * hpasses * RADIX * 4))) return rc;
+    if ((rc = ensure(c, c->d_ranges, (size_t)std::max(c->range_off[nv], 1) * sizeof(int2)))) return rc;
+    const size_t lb_need = (size_t)std::max({(long long)dtiles * RADIX, (long long)ptiles * RADIX,
+                                             (long long)etiles, 1ll}) * sizeof(uint32_t);
+    if ((rc = ensure(c, c->d_lb, lb_need))) return rc;
+
+    // ================= K5a: depth sort (4 x 8-bit passes over bits(z), values j)
+    {
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_DEPTH_SORT, st, e);
+        CU(cudaMemsetAsync(c->d_hist.p, 0, (size_t)std::max(nv, 1) * 4 * RADIX * 4, st));
+        launch_hist32(P<uint32_t>(c->d_dkey), P<Seg>(c->d_dsegs), nv, P<int>(c->d_dtile0), dtiles,
+                      4, P<uint32_t>(c->d_hist), st);
+        launch_hist_scan(P<uint32_t>(c->d_hist), nv, 4, st);
+        const uint32_t* kin = P<uint32_t>(c->d_dkey);
+        const uint32_t* vin = nullptr;
+        for (int pass = 0; pass < 4; ++pass) {
+            const int o = pass & 1;
+            if (dtiles) CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)dtiles * RADIX * 4, st));
+            launch_onesweep32(kin, vin, P<uint32_t>(c->d_sortk[o]), P<uint32_t>(c->d_sortv[o]),
+                              P<Seg>(c->d_dsegs), nv, P<int>(c->d_dtile0), dtiles,
+                              P<uint32_t>(c->d_hist), pass, 4, P<uint32_t>(c->d_lb),
+                              next_ticket(c), 8 * pass, st);
+            kin = P<uint32_t>(c->d_sortk[o]);
+            vin = P<uint32_t>(c->d_sortv[o]);
+        }
+        c->final_order = 1;   // pass 3 wrote buffer 1
+        ev_end(c, st, e);
+    }
+    CU(cudaGetLastError());
+
+    // ================= K3/K4: permute to depth order, scan tile counts, emit pairs
+    {
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_EMIT, st, e);
+        if (etiles) CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)etiles * 4, st));
+        EmitArgs a{};
+        a.views = P<DevView>(c->d_views);
+        a.segs = P<Seg>(c->d_dsegs);
+        a.nsegs = nv;
+        a.seg_tile0 = P<int>(c->d_etile0);
+        a.total_tiles = etiles;
+        a.order = P<uint32_t>(c->d_sortv[c->final_order]);
+        a.rec = P<float4>(c->d_rec);
+        a.rec_sorted = P<float4>(c->d_recs);
+        a.pairs = P<unsigned long long>(c->d_pairs[0]);
+        a.lookback = P<uint32_t>(c->d_lb);
+        a.ticket = next_ticket(c);
+        launch_emit(a, st);
+        ev_end(c, st, e);
+    }
+    CU(cudaGetLastError());
+
+    // ================= K5b: stable tile sort of the pair words
+    {
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_PAIR_SORT, st, e);
+        CU(cudaMemsetAsync(c->d_hist.p, 0, (size_t)std::max(nv, 1) * ppasses * RADIX * 4, st));
+        launch_hist64(P<unsigned long long>(c->d_pairs[0]), P<Seg>(c->d_psegs), nv,
+                      P<int>(c->d_ptile0), ptiles, 32, ppasses, P<uint32_t>(c->d_hist), st);
+        launch_hist_scan(P<uint32_t>(c->d_hist), nv, ppasses, st);
+        for (int pass = 0; pass < ppasses; ++pass) {
+            if (ptiles) CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)ptiles * RADIX * 4, st));
+            launch_onesweep64(P<unsigned long long>(c->d_pairs[pass & 1]),
+                              P<unsigned long long>(c->d_pairs[(pass + 1) & 1]), P<Seg>(c->d_psegs),
+                              nv, P<int>(c->d_ptile0), ptiles, P<uint32_t>(c->d_hist), pass,
+                              ppasses, P<uint32_t>(c->d_lb), next_ticket(c), 32 + 8 * pass, st);
+        }
+        c->final_pairs = ppasses & 1;
+        ev_end(c, st, e);
+    }
+    CU(cudaGetLastError());
+
+    // ================= K6: tile ranges
+    {
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_RANGES, st, e);
+        CU(cudaMemsetAsync(c->d_ranges.p, 0, (size_t)std::max(c->range_off[nv], 1) * sizeof(int2), st));
+        launch_ranges(P<unsigned long long>(c->d_pairs[c->final_pairs]), total_pairs,
+                      P<DevView>(c->d_views), nv, P<long long>(c->d_vpo), P<int>(c->d_range_off),
+                      P<int2>(c->d_ranges), st);
+        ev_end(c, st, e);
+    }
+    CU(cudaGetLastError());
+
+    // ================= K7: rasterizer
+    {
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_RASTER, st, e);
+        RasterArgs a{};
+        a.views = P<DevView>(c->d_views);
+        a.n_views = nv;
+        a.max_tiles = max_tiles;
+        a.ranges = P<int2>(c->d_ranges);
+        a.range_off = P<int>(c->d_range_off);
+        a.pairs = P<unsigned long long>(c->d_pairs[c->final_pairs]);
+        a.rec_sorted = P<float4>(c->d_recs);
+        launch_raster(a, st);
+        ev_end(c, st, e);
+    }
+    CU(cudaGetLastError());
+    if (c->timing) c->timed_renders++;
+    CU(cudaEventRecord(c->staging_free, st));
+    c->staging_recorded = true;
+    c->have_render = true;
+    if (bad) return fail(c, S3R_EINSTANCE, "a Gaussian had an instance id outside [0, %d]",
+                         sc->num_instances - 1);
+    c->err.clear();
+    return S3R_OK;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+int s3r_version(void) { return S3R_VERSION; }
+
+int s3r_create(int device, s3r_ctx** out)
+{
+    if (!out) return S3R_EINVAL;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return S3R_ECUDA;
+    }
+    s3r_ctx* c = new (std::nothrow) s3r_ctx();
+    if (!c) return S3R_ENOMEM;
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return S3R_ECUDA;
+    }
+    if (ensure(c, c->d_err, sizeof(uint32_t)) || cudaMemset(c->d_err.p, 0, sizeof(uint32_t)) != cudaSuccess) {
+        delete c;
+        return S3R_ECUDA;
+    }
+    *out = c;
+    return S3R_OK;
+}
+
+void s3r_destroy(s3r_ctx* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    Buf* bufs[] = {&c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
+                   &c->d_tile0, &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0],
+                   &c->d_sortk[1], &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_pairs[0],
+                   &c->d_pairs[1], &c->d_hist, &c->d_dsegs, &c->d_dtile0, &c->d_etile0,
+                   &c->d_psegs, &c->d_ptile0, &c->d_ranges, &c->d_range_off, &c->d_vpo, &c->d_err,
+                   &c->d_dbg_keys, &c->d_dbg_flags, &c->d_dbg_rect};
+    for (Buf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    for (auto& b : c->m_scene)
+        if (b.p) cudaFree(b.p);
+    for (auto* vec : {&c->m_tab, &c->m_rgb, &c->m_depth, &c->m_T, &c->m_vis})
+        for (auto& b : *vec)
+            if (b.p) cudaFree(b.p);
+    for (auto& e : c->ev) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->staging_free) cudaEventDestroy(c->staging_free);
+    delete c;
+}
+
+const char* s3r_last_error(const s3r_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int s3r_set_debug(s3r_ctx* c, int enable)
+{
+    if (!c) return S3R_EINVAL;
+    c->debug = enable != 0;
+    return S3R_OK;
+}
+
+int s3r_set_timing(s3r_ctx* c, int enable)
+{
+    if (!c) return S3R_EINVAL;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& e : c->ev) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    c->ev.clear();
+    for (double& m : c->stage_ms) m = 0;
+    c->timed_renders = 0;
+    c->timing = enable != 0;
+    return S3R_OK;
+}
+
+int s3r_get_stage_times(s3r_ctx* c, double* out_ms, int64_t* out_count)
+{
+    if (!c) return S3R_EINVAL;
+    CU(cudaSetDevice(c->device));
+    for (auto& e : c->ev) {
+        CU(cudaEventSynchronize(e.b));
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, e.a, e.b));
+        c->stage_ms[e.stage] += ms;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    c->ev.clear();
+    if (out_ms)
+        for (int i = 0; i < S3R_NUM_STAGES; ++i) out_ms[i] = c->stage_ms[i];
+    if (out_count) *out_count = c->timed_renders;
+    return S3R_OK;
+}
+
+int s3r_compose_instance_cameras(s3r_ctx* c, const float* w2c, const float* i2g, int32_t n_views,
+                                 int32_t K, float* out, void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    if (n_views < 0 || K < 0 || K > 4095 || (n_views > 0 && (!w2c || !out)) ||
+        (n_views > 0 && K > 0 && !i2g))
+        return fail(c, S3R_EINVAL, "compose: bad arguments");
+    CU(cudaSetDevice(c->device));
+    launch_compose(w2c, i2g, n_views, K, out, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return S3R_OK;
+}
+
+int s3r_render_batch(s3r_ctx* c, const s3r_scene* scene, const s3r_view* views, int32_t n_views,
+                     const s3r_outputs* outs, void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    return render_impl(c, scene, views, n_views, outs, (cudaStream_t)stream);
+}
+
+int s3r_render(s3r_ctx* c, const s3r_scene* scene, const s3r_view* view, const s3r_outputs* out,
+               void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    return render_impl(c, scene, view, 1, out, (cudaStream_t)stream);
+}
+
+int s3r_render_batch_host(s3r_ctx* c, const s3r_scene* hs, const s3r_view* hviews,
+                          int32_t nv, const s3r_outputs* houts, void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    if (!hs || nv < 0 || (nv > 0 && (!hviews || !houts)))
+        return fail(c, S3R_EINVAL, "render_batch_host: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(c->device));
+    const long long N = hs->n;
+    if (N < 0 || N >= (1ll << 30)) return fail(c, S3R_EINVAL, "n out of range");
+    int rc;
+    const size_t sz[7] = {16, 16, 16, 16, 4, 8, 8};
+    const void* src[7] = {hs->means_opacity, hs->scales, hs->rotations, hs->colors,
+                          hs->instance_ids, hs->visibility, hs->life};
+    s3r_scene ds = *hs;
+    void* dst[7];
+    for (int i = 0; i < 7; ++i) {
+        dst[i] = nullptr;
+        if (!src[i] || N == 0) continue;
+        if ((rc = ensure(c, c->m_scene[i], (size_t)N * sz[i]))) return rc;
+        dst[i] = c->m_scene[i].p;
+        CU(cudaMemcpyAsync(dst[i], src[i], (size_t)N * sz[i], cudaMemcpyHostToDevice, st));
+    }
+    ds.means_opacity = (const float*)dst[0];
+    ds.scales = (const float*)dst[1];
+    ds.rotations = (const float*)dst[2];
+    ds.colors = (const float*)dst[3];
+    ds.instance_ids = (const int32_t*)dst[4];
+    ds.visibility = (float*)dst[5];
+    ds.life = (float*)dst[6];
+    c->m_tab.resize(std::max<size_t>(c->m_tab.size(), nv));
+    c->m_rgb.resize(std::max<size_t>(c->m_rgb.size(), nv));
+    c->m_depth.resize(std::max<size_t>(c->m_depth.size(), nv));
+    c->m_T.resize(std::max<size_t>(c->m_T.size(), nv));
+    c->m_vis.resize(std::max<size_t>(c->m_vis.size(), nv));
+    std::vector<s3r_view> dv(hviews, hviews + nv);
+    std::vector<s3r_outputs> dout(nv);
+    for (int v = 0; v < nv; ++v) {
+        const size_t tb = (size_t)hs->num_instances * 12 * sizeof(float);
+        if (!hviews[v].instance_w2c || !houts[v].rgb)
+            return fail(c, S3R_EINVAL, "render_batch_host: view %d has NULL table/rgb", v);
+        if ((rc = ensure(c, c->m_tab[v], tb))) return rc;
+        CU(cudaMemcpyAsync(c->m_tab[v].p, hviews[v].instance_w2c, tb, cudaMemcpyHostToDevice, st));
+        dv[v].instance_w2c = P<float>(c->m_tab[v]);
+        const size_t px = (size_t)std::max(hviews[v].width, 1) * std::max(hviews[v].height, 1);
+        if ((rc = ensure(c, c->m_rgb[v], px * 12))) return rc;
+        dout[v].rgb = P<float>(c->m_rgb[v]);
+        if (houts[v].depth) {
+            if ((rc = ensure(c, c->m_depth[v], px * 4))) return rc;
+            dout[v].depth = P<float>(c->m_depth[v]);
+        }
+        if (houts[v].final_T) {
+            if ((rc = ensure(c, c->m_T[v], px * 4))) return rc;
+            dout[v].final_T = P<float>(c->m_T[v]);
+        }
+        if (houts[v].visible && N > 0) {
+            if ((rc = ensure(c, c->m_vis[v], (size_t)N))) return rc;
+            dout[v].visible = P<uint8_t>(c->m_vis[v]);
+        }
+    }
+    rc = render_impl(c, &ds, dv.data(), nv, dout.data(), st);
+    if (rc != S3R_OK && rc != S3R_EINSTANCE) return rc;
+    for (int v = 0; v < nv; ++v) {
+        const size_t px = (size_t)hviews[v].width * hviews[v].height;
+        CU(cudaMemcpyAsync(houts[v].rgb, dout[v].rgb, px * 12, cudaMemcpyDeviceToHost, st));
+        if (houts[v].depth)
+            CU(cudaMemcpyAsync(houts[v].depth, dout[v].depth, px * 4, cudaMemcpyDeviceToHost, st));
+        if (houts[v].final_T)
+            CU(cudaMemcpyAsync(houts[v].final_T, dout[v].final_T, px * 4, cudaMemcpyDeviceToHost, st));
+        if (houts[v].visible && N > 0)
+            CU(cudaMemcpyAsync(houts[v].visible, dout[v].visible, (size_t)N, cudaMemcpyDeviceToHost, st));
+    }
+    if (hs->life && N > 0)
+        CU(cudaMemcpyAsync(hs->life, ds.life, (size_t)N * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return rc;
+}
+
+int s3r_get_stats(const s3r_ctx* c, int32_t view_index, s3r_stats* out)
+{
+    if (!c || !out) return S3R_EINVAL;
+    if (!c->have_render || view_index < 0 || view_index >= (int)c->stats.size())
+        return S3R_ESTATE;
+    *out = c->stats[view_index];
+    return S3R_OK;
+}
+
+int s3r_dump_intermediates(s3r_ctx* c, int32_t vi, const s3r_debug* dbg, void* stream)
+{
+    if (!c || !dbg) return S3R_EINVAL;
+    if (!c->have_render || vi < 0 || vi >= (int)c->hv.size())
+        return fail(c, S3R_ESTATE, "dump: no render or view index out of range");
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(c->device));
+    const DevView& d = c->hv[vi];
+    const long long Ns = std::max<long long>(c->N_last, 1);
+    if (dbg->temporal_idx && d.n_temporal)
+        CU(cudaMemcpyAsync(dbg->temporal_idx, P<int32_t>(c->d_tidx) + (long long)d.tslot * Ns,
+                           d.n_temporal * 4, cudaMemcpyDeviceToDevice, st));
+    const bool need_dbg = dbg->keys || dbg->flags || dbg->rect || dbg->depth_order || dbg->pair_gauss;
+    if (need_dbg && !c->last_debug)
+        return fail(c, S3R_ESTATE, "dump: keys/flags/rect/depth_order/pair_gauss need s3r_set_debug(1) before the render");
+    if (dbg->keys && d.n_temporal)
+        CU(cudaMemcpyAsync(dbg->keys, P<float>(c->d_dbg_keys) + 6 * d.dbg_off, d.n_temporal * 24,
+                           cudaMemcpyDeviceToDevice, st));
+    if (dbg->flags && d.n_temporal)
+        CU(cudaMemcpyAsync(dbg->flags, P<uint8_t>(c->d_dbg_flags) + d.dbg_off, d.n_temporal,
+                           cudaMemcpyDeviceToDevice, st));
+    if (dbg->rect && d.n_temporal)
+        CU(cudaMemcpyAsync(dbg->rect, P<int16_t>(c->d_dbg_rect) + 4 * d.dbg_off, d.n_temporal * 8,
+                           cudaMemcpyDeviceToDevice, st));
+    const uint32_t* order = P<uint32_t>(c->d_sortv[c->final_order]);
+    if (dbg->depth_order)
+        launch_dump_order(order, P<int32_t>(c->d_gidx), d.cap_off, d.n_rendered, dbg->depth_order, st);
+    if (dbg->pair_tile || dbg->pair_gauss)
+        launch_dump_pairs(P<unsigned long long>(c->d_pairs[c->final_pairs]) + d.pair_off, d.n_pairs,
+                          order, c->last_debug ? P<int32_t>(c->d_gidx) : nullptr, d.cap_off,
+                          dbg->pair_tile, dbg->pair_gauss, st);
+    if (dbg->ranges)
+        CU(cudaMemcpyAsync(dbg->ranges, P<int2>(c->d_ranges) + c->range_off[vi],
+                           (size_t)d.ntiles * sizeof(int2), cudaMemcpyDeviceToDevice, st));
+    CU(cudaGetLastError());
+    return S3R_OK;
+}
+
+int s3r_commit_visibility(s3r_ctx* c, const s3r_scene* s, float margin, void* stream)
+{
+    if (!c || !s) return S3R_EINVAL;
+    if (s->n < 0 || (s->n > 0 && (!s->visibility || !s->life)) || !std::isfinite(margin))
+        return fail(c, S3R_EINVAL, "commit: bad arguments (visibility and life required)");
+    CU(cudaSetDevice(c->device));
+    launch_commit(reinterpret_cast<float2*>(s->visibility), reinterpret_cast<float2*>(s->life),
+                  s->n, margin, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return S3R_OK;
+}
+
+int s3r_reset_visibility(s3r_ctx* c, const s3r_scene* s, void* stream)
+{
+    if (!c || !s) return S3R_EINVAL;
+    if (s->n < 0 || (s->n > 0 && !s->visibility))
+        return fail(c, S3R_EINVAL, "reset: bad arguments");
+    CU(cudaSetDevice(c->device));
+    launch_reset(reinterpret_cast<float2*>(s->visibility), s->n, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return S3R_OK;
+}
+
+int s3r_check(s3r_ctx* c, void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    CU(cudaSetDevice(c->device));
+    CU(cudaStreamSynchronize((cudaStream_t)stream));
+    uint32_t e = 0;
+    CU(cudaMemcpy(&e, c->d_err.p, sizeof e, cudaMemcpyDeviceToHost));
+    CU(cudaMemset(c->d_err.p, 0, sizeof e));
+    if (e & ERR_BADID) return fail(c, S3R_EINSTANCE, "a Gaussian had an out-of-range instance id");
+    return S3R_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// s3r_internal.cuh — device-side types and launch declarations of libs3r.
+//
+// sm_100a only.  Compiled with -fmad=false: every multiply-add that the
+// R-ARITH contract writes as an FMA is an explicit __fmaf_rn; no
+// other contraction happens, so the fp32 keys are reproducible bit for bit.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef __CUDACC__
+#error "s3r kernels need nvcc"
+#endif
+
+namespace s3r {
+
+constexpr int TILE = 16;                 // tile edge (reading R12)
+constexpr int MAX_TSLOTS = 64;           // distinct times per K1 launch
+constexpr int RADIX_BITS = 8;
+constexpr int RADIX = 1 << RADIX_BITS;   // 256 bins per onesweep pass
+
+// Decoupled look-back word: 2 flag bits + 30-bit count.
+constexpr uint32_t LB_AGG = 1u << 30;
+constexpr uint32_t LB_PRE = 2u << 30;
+constexpr uint32_t LB_MASK = (1u << 30) - 1;
+
+// Per-Gaussian flag bits (debug dump; same meaning as the header)
+constexpr uint8_t F_TEMPORAL = 1, F_VISIBLE = 2, F_SMALL = 4, F_DROPPED = 8,
+                  F_RENDERED = 16, F_BADID = 32;
+
+// Device error bits
+constexpr uint32_t ERR_BADID = 1;
+
+// Per-view descriptor in device memory (one per view of a batch).
+struct DevView {
+    float t;
+    int W, H;
+    float fx, fy, cx, cy, near_plane;
+    const float* table;      // [K1][12]
+    float lod_r, lod_pmax, lod_D;
+    unsigned long long seed;
+    int tslot;               // index of the view's distinct time
+    int TX, TY, ntiles;
+    float* rgb;
+    float* depth;
+    float* finalT;
+    uint8_t* visible;
+    // filled per phase by the host
+    long long cap_off;       // offset of the view's segment in per-rendered arrays
+    long long n_temporal;
+    long long pair_off;      // offset of the view's pairs
+    long long n_rendered;
+    long long n_pairs;
+    long long dbg_off;       // offset in the debug arrays (keys/flags/rect)
+};
+
+// Per-view counters written by K2 (device, zeroed per batch)
+struct ViewCounters {
+    unsigned long long n_visible, n_small, n_dropped, n_rendered, n_pairs, n_bad;
+};
+
+// Segment of a segmented onesweep sort / scan (one per view)
+struct Seg {
+    long long base;          // element offset of the segment
+    long long count;         // elements
+    int tile0;               // first global tile of the segment
+    int ntiles;              // tiles of the segment
+};
+
+// ---------------- launchers (each enqueues on `st`) ----------------------
+
+// K1: temporal filter + ordered compaction for up to MAX_TSLOTS distinct times.
+void launch_filter(const float2* vis, long long n, const float* d_times, int T,
+                   int32_t* idx_out, long long idx_stride, unsigned long long* counts,
+                   uint32_t* lookback, int* ticket, cudaStream_t st);
+
+// Compose instance cameras (fp64, rounded once).
+void launch_compose(const float* w2c, const float* i2g, int n_views, int K, float* out,
+                    cudaStream_t st);
+
+// K2: instance-specific projection + EWA + decisions + LOD + life update,
+// ordered compaction of rendered splats per view.
+struct ProjectArgs {
+    const float4* means_opacity;
+    const float4* scales;
+    const float4* rotations;
+    const float4* colors;
+    const int32_t* ids;
+    float2* life;
+    int num_instances;
+    long long n;
+    const DevView* views;
+    int n_views;
+    const int32_t* tidx;         // [T][idx_stride]
+    long long idx_stride;
+    const int* view_tile0;       // [n_views+1] first K2 tile per view
+    int total_tiles;
+    // outputs
+    float4* rec;                 // [cap][3] splat records (unsorted, compacted)
+    uint32_t* dkey;              // [cap] depth bits
+    int32_t* gidx;               // [cap] Gaussian index (debug) or NULL
+    ViewCounters* counters;      // [n_views]
+    uint32_t* lookback;          // [total_tiles]
+    int* ticket;
+    uint32_t* err;
+    // debug (NULL when off)
+    float* dbg_keys;
+    uint8_t* dbg_flags;
+    int16_t* dbg_rect;
+};
+void launch_project(const ProjectArgs& a, cudaStream_t st);
+
+// Segmented LSD radix sort helpers (onesweep with decoupled look-back).
+// keys: u32 (depth) or u64 (pair words).  digit = (key >> shift) & 255.
+void launch_hist32(const uint32_t* keys, const Seg* segs, int nsegs, const int* seg_tile0,
+                   int total_tiles, int npasses, uint32_t* hist, cudaStream_t st);
+void launch_hist64(const unsigned long long* keys, const Seg* segs, int nsegs,
+                   const int* seg_tile0, int total_tiles, int shift0, int npasses,
+                   uint32_t* hist, cudaStream_t st);
+void launch_hist_scan(uint32_t* hist, int nsegs, int npasses, cudaStream_t st);
+void launch_onesweep32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
+                       uint32_t* vout, const Seg* segs, int nsegs, const int* seg_tile0,
+                       int total_tiles, const uint32_t* digit_base, int pass, int npasses,
+                       uint32_t* lookback, int* ticket, int shift, cudaStream_t st);
+void launch_onesweep64(const unsigned long long* kin, unsigned long long* kout,
+                       const Seg* segs, int nsegs, const int* seg_tile0, int total_tiles,
+                       const uint32_t* digit_base, int pass, int npasses, uint32_t* lookback,
+                       int* ticket, int shift, cudaStream_t st);
+int onesweep32_tile();
+int onesweep64_tile();
+int hist_tile();
+
+// K3/K4: depth-ordered permute + tile-count scan + key emission.
+struct EmitArgs {
+    const DevView* views;
+    const Seg* segs;             // per view: rendered segment (base = cap_off)
+    int nsegs;
+    const int* seg_tile0;
+    int total_tiles;
+    const uint32_t* order;       // [cap] depth-sorted local index j
+    const float4* rec;           // [cap][3] unsorted records
+    float4* rec_sorted;          // [cap][3]
+    unsigned long long* pairs;   // [total pairs] (tile << 32) | rank
+    uint32_t* lookback;
+    int* ticket;
+};
+void launch_emit(const EmitArgs& a, cudaStream_t st);
+int emit_tile();
+
+// K6: tile ranges from sorted pair words.
+void launch_ranges(const unsigned long long* pairs, long long total_pairs,
+                   const DevView* views, int n_views, const long long* view_pair_off,
+                   const int* range_off, int2* ranges, cudaStream_t st);
+
+// K7: rasterizer.
+struct RasterArgs {
+    const DevView* views;
+    int n_views;
+    int max_tiles;
+    const int2* ranges;          // per view at range_off[v]
+    const int* range_off;
+    const unsigned long long* pairs;
+    const float4* rec_sorted;
+};
+void launch_raster(const RasterArgs& a, cudaStream_t st);
+
+// K9: commit / reset.
+void launch_commit(float2* vis, float2* life, long long n, float margin, cudaStream_t st);
+void launch_reset(float2* vis, long long n, cudaStream_t st);
+
+// Debug helpers.
+void launch_dump_order(const uint32_t* order, const int32_t* gidx, long long base,
+                       long long count, int32_t* out, cudaStream_t st);
+void launch_dump_pairs(const unsigned long long* pairs, long long count, const uint32_t* order,
+                       const int32_t* gidx, long long base, int32_t* tile_out,
+                       int32_t* gauss_out, cudaStream_t st);
+
+}  // namespace s3r

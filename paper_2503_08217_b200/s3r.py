@@ -1,0 +1,313 @@
+"""Thin Python binding of libs3r.so (include/s3r.h) — argument marshalling only.
+
+Every step of the path runs in the CUDA kernels behind the C ABI; this module
+turns torch tensors into pointers and the header's structs into ctypes
+structs.  PyTorch provides device memory and streams.  There is no fallback:
+if libs3r.so is missing and cannot be built, or no CUDA device is present,
+the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libs3r.so")
+_lock = threading.Lock()
+_lib = None
+
+S3R_OK, S3R_EINVAL, S3R_EINSTANCE, S3R_ENOMEM, S3R_ECUDA, S3R_ESTATE = 0, -1, -2, -3, -4, -5
+STAGES = ["filter", "project", "depth_sort", "emit", "pair_sort", "ranges", "raster"]
+TILE = 16
+# every symbol include/s3r.h declares
+EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_set_debug",
+           "s3r_set_timing", "s3r_get_stage_times", "s3r_compose_instance_cameras", "s3r_render",
+           "s3r_render_batch", "s3r_render_batch_host", "s3r_get_stats",
+           "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
+           "s3r_check"]
+
+
+class S3RError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"s3r error {code}: {msg}")
+        self.code = code
+
+
+class Scene_(C.Structure):
+    _fields_ = [("n", C.c_int64), ("num_instances", C.c_int32),
+                ("means_opacity", C.c_void_p), ("scales", C.c_void_p),
+                ("rotations", C.c_void_p), ("colors", C.c_void_p),
+                ("instance_ids", C.c_void_p), ("visibility", C.c_void_p), ("life", C.c_void_p)]
+
+
+class View_(C.Structure):
+    _fields_ = [("t", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("near_plane", C.c_float), ("instance_w2c", C.c_void_p),
+                ("lod_r", C.c_float), ("lod_pmax", C.c_float), ("lod_D", C.c_float),
+                ("lod_seed", C.c_uint64)]
+
+
+class Outputs_(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("final_T", C.c_void_p),
+                ("visible", C.c_void_p)]
+
+
+class Stats_(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("n_scene", "n_temporal", "n_visible", "n_lod_small",
+                                         "n_lod_dropped", "n_rendered", "n_pairs",
+                                         "n_bad_instance")]
+
+
+class Debug_(C.Structure):
+    _fields_ = [("temporal_idx", C.c_void_p), ("keys", C.c_void_p), ("flags", C.c_void_p),
+                ("rect", C.c_void_p), ("depth_order", C.c_void_p), ("pair_tile", C.c_void_p),
+                ("pair_gauss", C.c_void_p), ("ranges", C.c_void_p)]
+
+
+def lib_path() -> str:
+    return _SO
+
+
+def lib():
+    """Load libs3r.so (building it in-tree with nvcc if absent)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_SO):
+                from . import build as _b
+                _b.build()
+            L = C.CDLL(_SO)
+            P, I, I64 = C.c_void_p, C.c_int, C.c_int64
+            sig = {
+                "s3r_version": (I, []),
+                "s3r_create": (I, [I, C.POINTER(C.c_void_p)]),
+                "s3r_destroy": (None, [P]),
+                "s3r_last_error": (C.c_char_p, [P]),
+                "s3r_set_debug": (I, [P, I]),
+                "s3r_set_timing": (I, [P, I]),
+                "s3r_get_stage_times": (I, [P, P, P]),
+                "s3r_compose_instance_cameras": (I, [P, P, P, C.c_int32, C.c_int32, P, P]),
+                "s3r_render": (I, [P, P, P, P, P]),
+                "s3r_render_batch": (I, [P, P, P, C.c_int32, P, P]),
+                "s3r_render_batch_host": (I, [P, P, P, C.c_int32, P, P]),
+                "s3r_get_stats": (I, [P, C.c_int32, P]),
+                "s3r_dump_intermediates": (I, [P, C.c_int32, P, P]),
+                "s3r_commit_visibility": (I, [P, P, C.c_float, P]),
+                "s3r_reset_visibility": (I, [P, P, P]),
+                "s3r_check": (I, [P, P]),
+            }
+            for name, (res, args) in sig.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class DeviceScene:
+    """Scene tensors on one CUDA device (SoA, 16-byte rows)."""
+    means_opacity: torch.Tensor   # (N,4) f32
+    scales: torch.Tensor          # (N,4) f32
+    rotations: torch.Tensor       # (N,4) f32
+    colors: torch.Tensor          # (N,4) f32
+    instance_ids: torch.Tensor    # (N,) i32
+    visibility: torch.Tensor      # (N,2) f32
+    life: Optional[torch.Tensor]  # (N,2) f32 or None
+    num_instances: int
+
+    @property
+    def n(self) -> int:
+        return int(self.means_opacity.shape[0])
+
+    @staticmethod
+    def from_numpy(scene, device="cuda", life: bool = True) -> "DeviceScene":
+        f = lambda a, dt=torch.float32: torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+        return DeviceScene(f(scene.means_opacity), f(scene.scales), f(scene.rotations),
+                           f(scene.colors), f(scene.instance_ids, torch.int32),
+                           f(scene.visibility), f(scene.life) if life else None,
+                           int(scene.num_instances))
+
+    def struct(self) -> Scene_:
+        for t in (self.means_opacity, self.scales, self.rotations, self.colors,
+                  self.instance_ids, self.visibility):
+            assert t.is_cuda and t.is_contiguous()
+        return Scene_(self.n, self.num_instances, _ptr(self.means_opacity), _ptr(self.scales),
+                      _ptr(self.rotations), _ptr(self.colors), _ptr(self.instance_ids),
+                      _ptr(self.visibility), _ptr(self.life))
+
+
+def view_struct(v, table: torch.Tensor) -> View_:
+    """scenegen.View (or any object with the same fields) + its device table."""
+    return View_(float(v.t), int(v.width), int(v.height), float(v.fx), float(v.fy), float(v.cx),
+                 float(v.cy), float(getattr(v, "near", 0.01)), _ptr(table), float(v.lod_r),
+                 float(v.lod_pmax), float(v.lod_D), int(v.lod_seed) & ((1 << 64) - 1))
+
+
+class Context:
+    """One s3r_ctx on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("s3r needs a CUDA device (no CPU fallback)")
+        self.L = lib()
+        self.device = device
+        h = C.c_void_p()
+        rc = self.L.s3r_create(device, C.byref(h))
+        if rc != S3R_OK:
+            raise S3RError(rc, "s3r_create failed")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.s3r_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, allow=(S3R_OK,)):
+        if rc not in allow:
+            raise S3RError(rc, self.L.s3r_last_error(self.h).decode())
+        return rc
+
+    # -- configuration
+    def set_debug(self, on: bool):
+        self._check(self.L.s3r_set_debug(self.h, int(on)))
+
+    def set_timing(self, on: bool):
+        self._check(self.L.s3r_set_timing(self.h, int(on)))
+
+    def stage_times(self) -> Dict[str, float]:
+        ms = (C.c_double * len(STAGES))()
+        cnt = C.c_int64()
+        self._check(self.L.s3r_get_stage_times(self.h, ms, C.byref(cnt)))
+        out = {k: ms[i] for i, k in enumerate(STAGES)}
+        out["renders"] = cnt.value
+        return out
+
+    # -- path
+    def compose(self, w2c: torch.Tensor, i2g: Optional[torch.Tensor], stream=None) -> torch.Tensor:
+        """(V,3,4) world->camera and (V,K,3,4) object->world -> (V,K+1,12) tables."""
+        w2c = w2c.contiguous()
+        V = w2c.shape[0]
+        K = 0 if i2g is None else int(i2g.shape[1])
+        out = torch.empty((V, K + 1, 12), dtype=torch.float32, device=w2c.device)
+        i2g_c = None if (i2g is None or K == 0) else i2g.contiguous()
+        self._check(self.L.s3r_compose_instance_cameras(self.h, _ptr(w2c), _ptr(i2g_c), V, K,
+                                                        _ptr(out), _stream(stream)))
+        return out
+
+    def render_batch(self, scene: DeviceScene, views: Sequence, tables: Sequence[torch.Tensor],
+                     outs: Sequence[Dict[str, torch.Tensor]], stream=None) -> int:
+        n = len(views)
+        vs = (View_ * max(n, 1))(*[view_struct(v, t) for v, t in zip(views, tables)])
+        os_ = (Outputs_ * max(n, 1))(*[Outputs_(_ptr(o["rgb"]), _ptr(o.get("depth")),
+                                                _ptr(o.get("final_T")), _ptr(o.get("visible")))
+                                       for o in outs])
+        sc = scene.struct()
+        return self._check(self.L.s3r_render_batch(self.h, C.byref(sc), vs, n, os_,
+                                                   _stream(stream)),
+                           allow=(S3R_OK, S3R_EINSTANCE))
+
+    def render_batch_host(self, scene, views: Sequence, tables: Sequence[np.ndarray],
+                          outs: Sequence[Dict[str, np.ndarray]], stream=None) -> int:
+        """All buffers in host memory (numpy, ideally pinned); copies inside the call."""
+        def hp(a):
+            return None if a is None else C.c_void_p(a.ctypes.data)
+        n = len(views)
+        vs = (View_ * max(n, 1))(*[View_(float(v.t), v.width, v.height, v.fx, v.fy, v.cx, v.cy,
+                                         float(getattr(v, "near", 0.01)), hp(t), v.lod_r,
+                                         v.lod_pmax, v.lod_D, int(v.lod_seed) & ((1 << 64) - 1))
+                                   for v, t in zip(views, tables)])
+        os_ = (Outputs_ * max(n, 1))(*[Outputs_(hp(o["rgb"]), hp(o.get("depth")),
+                                                hp(o.get("final_T")), hp(o.get("visible")))
+                                       for o in outs])
+        sc = Scene_(scene.n, scene.num_instances, hp(scene.means_opacity), hp(scene.scales),
+                    hp(scene.rotations), hp(scene.colors), hp(scene.instance_ids),
+                    hp(scene.visibility), hp(scene.life))
+        return self._check(self.L.s3r_render_batch_host(self.h, C.byref(sc), vs, n, os_,
+                                                        _stream(stream)),
+                           allow=(S3R_OK, S3R_EINSTANCE))
+
+    def stats(self, view_index: int) -> Dict[str, int]:
+        s = Stats_()
+        self._check(self.L.s3r_get_stats(self.h, view_index, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in Stats_._fields_}
+
+    def dump(self, view_index: int, width: int, height: int, keys: bool = True,
+             stream=None) -> Dict[str, torch.Tensor]:
+        st = self.stats(view_index)
+        dev = torch.device("cuda", self.device)
+        nt, nr, npairs = st["n_temporal"], st["n_rendered"], st["n_pairs"]
+        ntiles = ((width + TILE - 1) // TILE) * ((height + TILE - 1) // TILE)
+        d = {"temporal_idx": torch.empty(nt, dtype=torch.int32, device=dev),
+             "pair_tile": torch.empty(npairs, dtype=torch.int32, device=dev),
+             "ranges": torch.empty((ntiles, 2), dtype=torch.int32, device=dev)}
+        if keys:
+            d.update(keys=torch.empty((nt, 6), dtype=torch.float32, device=dev),
+                     flags=torch.empty(nt, dtype=torch.uint8, device=dev),
+                     rect=torch.empty((nt, 4), dtype=torch.int16, device=dev),
+                     depth_order=torch.empty(nr, dtype=torch.int32, device=dev),
+                     pair_gauss=torch.empty(npairs, dtype=torch.int32, device=dev))
+        dbg = Debug_(*[_ptr(d.get(k)) if (k in d and d[k].numel()) else None
+                       for k, _ in Debug_._fields_])
+        self._check(self.L.s3r_dump_intermediates(self.h, view_index, C.byref(dbg),
+                                                  _stream(stream)))
+        return d
+
+    def commit_visibility(self, scene: DeviceScene, margin: float = 0.1, stream=None):
+        sc = scene.struct()
+        self._check(self.L.s3r_commit_visibility(self.h, C.byref(sc), margin, _stream(stream)))
+
+    def reset_visibility(self, scene: DeviceScene, stream=None):
+        sc = scene.struct()
+        self._check(self.L.s3r_reset_visibility(self.h, C.byref(sc), _stream(stream)))
+
+    def check(self, stream=None) -> int:
+        return self._check(self.L.s3r_check(self.h, _stream(stream)), allow=(S3R_OK, S3R_EINSTANCE))
+
+
+def alloc_outputs(views: Sequence, device="cuda", depth=True, final_T=True, n_visible: int = 0
+                  ) -> List[Dict[str, torch.Tensor]]:
+    outs = []
+    for v in views:
+        o = {"rgb": torch.empty((v.height, v.width, 3), dtype=torch.float32, device=device)}
+        if depth:
+            o["depth"] = torch.empty((v.height, v.width), dtype=torch.float32, device=device)
+        if final_T:
+            o["final_T"] = torch.empty((v.height, v.width), dtype=torch.float32, device=device)
+        if n_visible:
+            o["visible"] = torch.empty(n_visible, dtype=torch.uint8, device=device)
+        outs.append(o)
+    return outs
+
+
+def view_tables(ctx: Context, views: Sequence, device="cuda", stream=None) -> torch.Tensor:
+    """Instance camera tables for scenegen views, composed on the device."""
+    w2c = torch.from_numpy(np.stack([np.asarray(v.w2c, np.float32) for v in views])).to(device)
+    K = views[0].i2g.shape[0] if len(views) else 0
+    i2g = torch.from_numpy(np.stack([np.asarray(v.i2g, np.float32).reshape(K, 3, 4)
+                                     for v in views])).to(device) if K else None
+    return ctx.compose(w2c, i2g, stream)

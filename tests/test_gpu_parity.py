@@ -1,0 +1,226 @@
+"""CUDA path (libs3r.so through the C ABI) vs the CPU oracle, on the same seeded inputs.
+
+Contract (BASELINE.json north_star): integer / indexing outputs bit-exact —
+temporal list, visible set (M_t), LOD set, tile rectangles, pair counts, sorted
+pair order, tile ranges, life update; RGB and depth within 1e-4 max abs.  Under
+the R-ARITH contract the fp32 keys and images are in fact
+bit-identical, which is asserted separately.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from helpers import make_scene, make_view
+from paper_2503_08217_b200 import s3r
+from paper_2503_08217_b200 import scenegen as sg
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = s3r.Context(0)
+    c.set_debug(True)
+    yield c
+    c.close()
+
+
+def gpu_render(ctx, scene, views, life=True, visible=True):
+    ds = s3r.DeviceScene.from_numpy(scene, life=life)
+    tabs = s3r.view_tables(ctx, views)
+    outs = s3r.alloc_outputs(views, n_visible=scene.n if visible else 0)
+    rc = ctx.render_batch(ds, views, list(tabs), outs)
+    torch.cuda.synchronize()
+    return ds, tabs, outs, rc
+
+
+def check_view(ctx, scene, view, table, out, vi, exact=True):
+    """Compare view `vi` of the last GPU render with the oracle (f32 contract)."""
+    o = oracle.render_view(scene, view, "f32", table=table.cpu().numpy())
+    st = ctx.stats(vi)
+    d = {k: v.cpu().numpy() for k, v in ctx.dump(vi, view.width, view.height).items()}
+    # counts
+    for k in ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped", "n_rendered", "n_pairs",
+              "n_bad_instance"):
+        assert st[k] == o["stats"][k], (k, st[k], o["stats"][k])
+    # K1: ascending temporal list, bit-exact
+    assert np.array_equal(d["temporal_idx"], o["temporal_idx"])
+    ti = o["temporal_idx"]
+    # K2: fp32 keys (bit-identical under R-ARITH), decisions bit-exact
+    ok = o["keys"][ti]
+    assert np.array_equal(d["keys"], ok, equal_nan=True), \
+        np.nanmax(np.abs(d["keys"] - ok))
+    assert np.array_equal(d["flags"], o["flags"][ti])
+    assert np.array_equal(d["rect"], o["rect"][ti])
+    if "visible" in out:
+        assert np.array_equal(out["visible"].cpu().numpy(), o["visible"])
+    # depth order of rendered Gaussians: (z, index)
+    rend = np.nonzero(o["flags"] & oracle.F_RENDERED)[0]
+    want_order = rend[np.lexsort((rend, o["keys"][rend, 2]))]
+    assert np.array_equal(d["depth_order"], want_order)
+    # K3-K6: pair list and ranges
+    assert np.array_equal(d["pair_tile"], o["pair_tile"])
+    assert np.array_equal(d["pair_gauss"], o["pair_gauss"])
+    assert np.array_equal(d["ranges"], o["ranges"])
+    # K7: images
+    rgb, dep, T = (out[k].cpu().numpy() for k in ("rgb", "depth", "final_T"))
+    assert np.abs(rgb - o["rgb"]).max() <= IMG_TOL
+    assert np.abs(dep - o["depth"]).max() <= IMG_TOL
+    assert np.abs(T - o["final_T"]).max() <= IMG_TOL
+    if exact:
+        assert np.array_equal(rgb, o["rgb"]) and np.array_equal(dep, o["depth"])
+        assert np.array_equal(T, o["final_T"])
+    return o
+
+
+def test_compose_matches_oracle(ctx):
+    scene, views = sg.make_random_dynamic(3, 10, 5, 2, 64, 64, 6)
+    tabs = s3r.view_tables(ctx, views).cpu().numpy()
+    for v, t in zip(views, tabs):
+        assert np.array_equal(t, oracle.compose(v))
+
+
+def test_c1_toy(ctx):
+    scene, views = sg.make_toy()
+    _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    assert rc == 0
+    o = check_view(ctx, scene, views[0], tabs[0], outs[0], 0)
+    assert o["stats"]["n_lod_dropped"] > 0
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_dynamic_batch(ctx, seed):
+    """Batched views of a scene with moving objects, random temporal intervals,
+    LOD on, ragged image sizes (not multiples of 16)."""
+    scene, views = sg.make_random_dynamic(seed, 3000, 4, 300, 203, 141, 5, lod=(3.0, 0.6, 12.0))
+    views[2].t = views[1].t          # two views share a time: shared K1 compaction
+    _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    assert rc == 0
+    for vi, v in enumerate(views):
+        check_view(ctx, scene, v, tabs[vi], outs[vi], vi)
+
+
+def test_street_scaled(ctx):
+    """C2 geometry at 10 % of the Gaussians, 4 views at full 960x640."""
+    scene, views = sg.make_config("street", scale=0.1, n_views=4)
+    _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    for vi, v in enumerate(views):
+        check_view(ctx, scene, v, tabs[vi], outs[vi], vi)
+
+
+def test_life_update_and_commit(ctx):
+    scene, views = sg.make_random_dynamic(9, 2000, 3, 100, 96, 80, 6, fresh=False)
+    ds, tabs, outs, rc = gpu_render(ctx, scene, views)
+    ref = scene.copy()
+    for vi, v in enumerate(views):
+        o = oracle.render_view(ref, v, "f32", table=tabs[vi].cpu().numpy(), pairs=False,
+                               image=False)
+        oracle.update_life(ref, o["visible"], v.t)
+    assert np.array_equal(ds.life.cpu().numpy(), ref.life)
+    ctx.commit_visibility(ds, 0.1)
+    oracle.commit_visibility(ref, 0.1)
+    torch.cuda.synchronize()
+    assert np.array_equal(ds.visibility.cpu().numpy(), ref.visibility)
+    assert np.array_equal(ds.life.cpu().numpy(), ref.life)
+    ctx.reset_visibility(ds)
+    oracle.reset_visibility(ref)
+    torch.cuda.synchronize()
+    assert np.array_equal(ds.visibility.cpu().numpy(), ref.visibility)
+
+
+def test_batch_split_invariance(ctx):
+    """Images and life do not depend on how views are batched."""
+    scene, views = sg.make_random_dynamic(12, 4000, 2, 500, 130, 97, 6, lod=(2.0, 0.5, 10.0))
+    dsa, tabs, outs_a, _ = gpu_render(ctx, scene, views)
+    dsb = s3r.DeviceScene.from_numpy(scene)
+    outs_b = s3r.alloc_outputs(views)
+    for i in range(len(views)):
+        ctx.render_batch(dsb, [views[i]], [tabs[i]], [outs_b[i]])
+    torch.cuda.synchronize()
+    for a, b in zip(outs_a, outs_b):
+        for k in ("rgb", "depth", "final_T"):
+            assert torch.equal(a[k], b[k])
+    assert torch.equal(dsa.life, dsb.life)
+
+
+def test_host_entry_point_matches_device(ctx):
+    scene, views = sg.make_random_dynamic(13, 2000, 2, 100, 77, 45, 3)
+    ds, tabs, outs, _ = gpu_render(ctx, scene, views, visible=True)
+    host_scene = scene.copy()
+    htabs = [t.cpu().numpy() for t in tabs]
+    houts = [{"rgb": np.zeros((v.height, v.width, 3), np.float32),
+              "depth": np.zeros((v.height, v.width), np.float32),
+              "final_T": np.zeros((v.height, v.width), np.float32),
+              "visible": np.zeros(scene.n, np.uint8)} for v in views]
+    ctx.render_batch_host(host_scene, views, htabs, houts)
+    for o, h in zip(outs, houts):
+        for k in ("rgb", "depth", "final_T", "visible"):
+            assert np.array_equal(o[k].cpu().numpy(), h[k])
+    assert np.array_equal(host_scene.life, ds.life.cpu().numpy())
+
+
+def test_edge_cases(ctx):
+    # empty scene
+    s0 = make_scene(np.zeros((0, 3)), 0.1)
+    v = make_view(64.0, 32.0, 40, 33)
+    _, tabs, outs, rc = gpu_render(ctx, s0, [v], visible=False)
+    assert rc == 0 and torch.all(outs[0]["rgb"] == 0) and torch.all(outs[0]["final_T"] == 1)
+    # every Gaussian filtered out by time; one view of 1x1 pixels; t = -0.0
+    s1 = make_scene([[0, 0, 3.0], [0.1, 0, 4.0]], 0.2, vis=[[0.5, 0.6], [0.7, 0.9]])
+    v1 = make_view(64.0, 0.0, 1, 1, t=-0.0)
+    _, tabs, outs, rc = gpu_render(ctx, s1, [v1])
+    check_view(ctx, s1, v1, tabs[0], outs[0], 0)
+    # bad instance id, near-plane splat covering every tile, behind-camera point
+    s2 = make_scene([[0, 0, 3.0], [0, 0, 3.0], [0, 0, 0.02], [0, 0, -1.0]], 0.1,
+                    ids=[0, 7, 0, 0], num_instances=1)
+    v2 = make_view(64.0, 32.0, 67, 50)
+    _, tabs, outs, rc = gpu_render(ctx, s2, [v2])
+    assert rc == s3r.S3R_EINSTANCE
+    assert ctx.check() == s3r.S3R_EINSTANCE
+    assert ctx.check() == 0
+    check_view(ctx, s2, v2, tabs[0], outs[0], 0)
+    # views of different sizes in one batch
+    scene, views = sg.make_random_dynamic(21, 500, 1, 50, 48, 48, 3)
+    views[1].width, views[1].height = 100, 17
+    views[2].width, views[2].height = 16, 160
+    _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    for vi, vv in enumerate(views):
+        check_view(ctx, scene, vv, tabs[vi], outs[vi], vi)
+
+
+def test_invalid_arguments(ctx):
+    scene, views = sg.make_toy()
+    ds = s3r.DeviceScene.from_numpy(scene)
+    tabs = s3r.view_tables(ctx, views)
+    outs = s3r.alloc_outputs(views)
+    bad = sg.View(**{**views[0].__dict__, "t": 1.5})
+    with pytest.raises(s3r.S3RError) as e:
+        ctx.render_batch(ds, [bad], [tabs[0]], outs)
+    assert e.value.code == s3r.S3R_EINVAL
+    bad = sg.View(**{**views[0].__dict__, "lod_pmax": 2.0})
+    with pytest.raises(s3r.S3RError):
+        ctx.render_batch(ds, [bad], [tabs[0]], outs)
+    bad = sg.View(**{**views[0].__dict__, "width": 0})
+    with pytest.raises(s3r.S3RError):
+        ctx.render_batch(ds, [bad], [tabs[0]], outs)
+
+
+@pytest.mark.slow
+def test_full_size_av2_sampled(ctx):
+    """C3 at its full size (2M Gaussians, 30 objects, 1550x2048), in the batch
+    launch configuration bench.py times (64 views in one s3r_render_batch);
+    the oracle checks two sampled views element by element and all views'
+    per-view counts through M_t."""
+    scene, views = sg.make_config("av2")
+    ds, tabs, outs, rc = gpu_render(ctx, scene, views, visible=False)
+    assert rc == 0
+    rng = np.random.default_rng(0)
+    for vi in sorted(rng.choice(len(views), 2, replace=False)):
+        check_view(ctx, scene, views[vi], tabs[vi], outs[vi], int(vi))
