@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the S3R-GS streamlined per-view splatting path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config av2] [--impl s3r|reference]
+
+One step = one s3r_render_batch of this rank's views (default 64) of the
+config's scene: temporal filter -> instance projection + LOD + life update ->
+depth sort -> key emission -> tile sort -> ranges -> alpha blend (every row of
+SURVEY.md §8(a)).  Inputs are resident in HBM before the timed region (scene
+168 MB at C3, larger than the 126 MB L2; each step also writes ~4 GB of
+images), so no L2 flush is needed between steps.  Under torchrun each rank
+renders its own 64 views (weak scaling, views sharded, Gaussians replicated, no
+data-path collective: views are independent).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, single-threaded C) on host
+cores: one view of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_2503_08217_b200 import scenegen as sg  # noqa: E402
+
+METRIC = "rendered views/sec and Gaussians/sec at 1/2/4/8 B200; % HBM/FP32 roofline"
+UNIT = "views/s"
+# FP32 operations per blend evaluation of the R-ARITH step (FMA = 2):
+# dx,dy 2; t1..t3 3; quadratic form 3; power 4; s3r_exp 21; alpha 2; w 1;
+# colour + depth 8; transmittance 2; termination test 1.
+FLOPS_PER_EVAL = 47
+SM_COUNT_B200 = 148
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons, util = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+                util.append(float(f[6]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s, u in zip(sm, util) if u > 50] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
+    """Algorithmic bytes per stage for one batch (DESIGN.md §Roofline)."""
+    Nt = sum(s["n_temporal"] for s in stats)
+    Nv = sum(s["n_visible"] for s in stats)
+    Nr = sum(s["n_rendered"] for s in stats)
+    P = sum(s["n_pairs"] for s in stats)
+    px = sum(v.width * v.height for v in views)
+    tiles = sum(((v.width + 15) // 16) * ((v.height + 15) // 16) for v in views)
+    # K1 writes each distinct time's list once
+    nt_distinct = sum({v.t: s["n_temporal"] for v, s in zip(views, stats)}.values())
+    return {
+        "filter": 8 * n_scene * math.ceil(max(n_distinct_t, 1) / 64) + 4 * nt_distinct,
+        "project": 56 * Nt + 8 * Nv + (16 + 48 + 4) * Nr,
+        "depth_sort": 4 * Nr + 4 * 16 * Nr,
+        "emit": (4 + 48 + 48) * Nr + 8 * P,
+        "pair_sort": 8 * P + pair_passes * 16 * P,
+        "ranges": 8 * P + 8 * tiles,
+        "raster": 8 * P + 48 * Nr + 20 * px,
+    }
+
+
+def run_reference(args, rank):
+    """The oracle as it stands, on host cores, one view per step."""
+    if rank != 0:
+        return
+    import oracle
+    cfg_name = args.config
+    scene, views = sg.make_config(cfg_name, n_views=max(args.views, 1))
+    W = args.warmup
+    K = args.steps
+    for i in range(W):
+        oracle.render_view(scene, views[i % len(views)], "f32", pairs=False)
+    t0 = time.perf_counter()
+    for i in range(K):
+        oracle.render_view(scene, views[(W + i) % len(views)], "f32", pairs=False)
+    dt = time.perf_counter() - t0
+    v = K / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg_name, "n_gaussians": scene.n,
+                   "image": f"{views[0].width}x{views[0].height}", "views_per_step": 1},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"1 view of {cfg_name} per step, single-threaded C oracle"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg_name, budget_s=12.0):
+    import oracle
+    scene, views = sg.make_config(cfg_name, n_views=8)
+    t0 = time.perf_counter()
+    n = 0
+    while n < len(views):
+        oracle.render_view(scene, views[n], "f32", pairs=False)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} view(s) of {cfg_name} ({scene.n} Gaussians, {views[0].width}x"
+                      f"{views[0].height}), single-threaded C oracle, {dt:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="s3r", choices=["s3r", "reference"])
+    ap.add_argument("--config", default="av2", choices=["toy", "street", "av2", "drive"])
+    ap.add_argument("--views", type=int, default=None, help="views per GPU per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pool", type=int, default=4, help="distinct view batches cycled per step")
+    args = ap.parse_args()
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    args.warmup = max(args.warmup, 3)
+    if args.views is None:
+        args.views = 1 if args.config == "toy" else sg.CONFIGS[args.config].n_views if \
+            args.config in ("street",) else 64
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2503_08217_b200 import s3r
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    # ---------------- workload (identical scene on every rank; views sharded)
+    if args.config == "toy":
+        scene, base_views = sg.make_toy()
+        pools = [base_views * args.views]
+    else:
+        cfg = sg.CONFIGS[args.config]
+        scene, traj = sg.make_street_scene(cfg)
+        pools = []
+        for p in range(args.pool):
+            allv = sg.make_views(cfg, traj, n_views=args.views * world, seed=cfg.seed + 101 * p)
+            pools.append(allv[rank * args.views:(rank + 1) * args.views])
+    ctx = s3r.Context(local)
+    ds = s3r.DeviceScene.from_numpy(scene, device=dev)
+    tables = [list(s3r.view_tables(ctx, vs, device=dev)) for vs in pools]
+    outs = s3r.alloc_outputs(pools[0], device=dev)
+    torch.cuda.synchronize()
+
+    def step(i):
+        p = i % len(pools)
+        ctx.render_batch(ds, pools[p], tables[p], outs)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.set_timing(True)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    st_times = ctx.stage_times()
+    ctx.set_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    views_per_step = len(pools[0])
+    value = views_per_step * world * args.steps / (ms / 1e3)
+
+    # ---------------- workload statistics + roofline (untimed render with counters)
+    ctx.set_counters(True)
+    ctx.render_batch(ds, pools[0], tables[0], outs)
+    torch.cuda.synchronize()
+    stats = [ctx.stats(i) for i in range(views_per_step)]
+    ctx.set_counters(False)
+    n_t = len({v.t for v in pools[0]})
+    max_tiles = max(((v.width + 15) // 16) * ((v.height + 15) // 16) for v in pools[0])
+    pair_passes = max(1, math.ceil(max(1, (max_tiles - 1).bit_length()) / 8))
+    bytes_ = stage_bytes(stats, pools[0], scene.n, n_t, pair_passes)
+    renders = max(st_times["renders"], 1)
+    stage_ms = {k: st_times[k] / renders for k in s3r.STAGES}
+    E_alg = sum(s["n_blend_evals"] for s in stats)
+    E_exec = sum(s["n_blend_exec"] for s in stats)
+    peaks, peak_src = load_peaks()
+    sm_max = float(clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = SM_COUNT_B200 * 128 * 2 * sm_max * 1e6 / 1e12   # TFLOP/s
+    hbm_peak = float(peaks["hbm_gbs"])
+    stages = {}
+    for k in s3r.STAGES:
+        t_s = stage_ms[k] / 1e3
+        stages[k] = {"ms": stage_ms[k], "alg_bytes": bytes_[k],
+                     "GBps": bytes_[k] / t_s / 1e9 if t_s > 0 else None}
+    stages["raster"]["TFLOPs"] = FLOPS_PER_EVAL * E_alg / (stage_ms["raster"] / 1e3) / 1e12 \
+        if stage_ms["raster"] > 0 else None
+    dom = max(s3r.STAGES, key=lambda k: stage_ms[k])
+    if dom == "raster":
+        ach = stages["raster"]["TFLOPs"]
+        roof = {"kernel": "k_raster", "bound": "alu", "achieved": ach, "peak": alu_peak,
+                "unit": "TFLOP/s", "frac": ach / alu_peak,
+                "peak_source": f"148 SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (B200_PROFILING.md unit counts)",
+                "alg_flops_per_launch": FLOPS_PER_EVAL * E_alg, "traffic": None}
+    else:
+        ach = stages[dom]["GBps"]
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                "alg_bytes_per_launch": bytes_[dom], "traffic": None}
+
+    # ---------------- e2e through the host-buffer C-ABI entry point
+    e2e = None
+    if not args.no_e2e:
+        hs = scene.copy()
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+        for k in ("means_opacity", "scales", "rotations", "colors", "instance_ids", "visibility",
+                  "life"):
+            setattr(hs, k, pin(np.ascontiguousarray(getattr(hs, k))))
+        htabs = [[t.cpu().pin_memory().numpy() for t in tb] for tb in tables]
+        hout = [{"rgb": torch.empty((v.height, v.width, 3), dtype=torch.float32,
+                                    pin_memory=True).numpy()} for v in pools[0]]
+        def estep(i):
+            p = i % len(pools)
+            ctx.render_batch_host(hs, pools[p], htabs[p], hout)
+        for i in range(2):
+            estep(i)
+        if world > 1:
+            dist.barrier()
+        k_e2e = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for i in range(k_e2e):
+            estep(i)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = sum(getattr(hs, k).nbytes for k in ("means_opacity", "scales", "rotations", "colors",
+                                                   "instance_ids", "visibility", "life"))
+        h2d += sum(t.nbytes for t in htabs[0])
+        d2h = sum(o["rgb"].nbytes for o in hout) + hs.life.nbytes
+        e2e = {"value": views_per_step * world * k_e2e / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": k_e2e, "api": "s3r_render_batch_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "toy":
+        cpu = cpu_baseline(args.config)
+    if rank == 0:
+        n_scene = scene.n
+        launches_per_step = 2 + math.ceil(max(n_t, 1) / 64) - 1 + 2 + 4 + 1 + 2 + pair_passes + 1 + 1
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "n_gaussians": n_scene,
+                       "instances": scene.num_instances - 1,
+                       "image": f"{pools[0][0].width}x{pools[0][0].height}",
+                       "views_per_gpu_per_step": views_per_step, "global_views_per_step":
+                       views_per_step * world, "parallelism": f"views sharded x{world}, Gaussians replicated",
+                       "l2": "inputs larger than L2 (scene > 126 MB; ~4 GB of images written per step)"},
+            "gaussians_per_s": n_scene * value,
+            "processed_gaussians_per_s": sum(s["n_temporal"] for s in stats) * world * value / views_per_step,
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof,
+            "stages": stages,
+            "workload_per_view": {k: sum(s[k] for s in stats) / views_per_step for k in
+                                  ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped",
+                                   "n_rendered", "n_pairs", "n_blend_evals", "n_blend_exec")},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -127,6 +127,11 @@ typedef struct {
     int64_t n_rendered;          /* blended                                     */
     int64_t n_pairs;             /* (tile, Gaussian) pairs                      */
     int64_t n_bad_instance;      /* ids outside [0,K]                           */
+    int64_t n_blend_evals;       /* E_alg: sum over pixels of the splats the
+                                    pixel examines up to and including its
+                                    terminating one (0 unless counters are on) */
+    int64_t n_blend_exec;        /* E_exec: 256 x splats each tile CTA walked
+                                    (0 unless counters are on)                  */
 } s3r_stats;
 
 /* Debug dump of one view's intermediates (DEVICE pointers, caller-allocated
@@ -168,6 +173,9 @@ const char* s3r_last_error(const s3r_ctx* ctx);
  * (keys/flags/rect) of s3r_dump_intermediates.  Costs one extra write of
  * 34 B per projected Gaussian when on.                                      */
 int s3r_set_debug(s3r_ctx* ctx, int enable);
+/* Enable (1) / disable (0) the rasterizer work counters n_blend_evals /
+ * n_blend_exec of s3r_stats (one block reduction + atomic per tile CTA).   */
+int s3r_set_counters(s3r_ctx* ctx, int enable);
 /* Enable (1) / disable (0) CUDA-event stage timers; resets the sums.        */
 int s3r_set_timing(s3r_ctx* ctx, int enable);
 /* out_ms[S3R_NUM_STAGES]: summed stage times; out_count: renders timed.

@@ -211,8 +211,10 @@ __global__ void __launch_bounds__(256) k_raster(RasterArgs a)
 
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, dp = 0.0f;
     bool done = !inside;
+    uint32_t n_eval = 0, n_exec = 0;    // work counters (only stored when a.evals)
     for (int b = rg.x; b < rg.y; b += 256) {
         if (__syncthreads_count(done) == 256) break;
+        n_exec += min(256, rg.y - b);
         const int i = b + tid;
         if (i < rg.y) {
             const uint32_t r = (uint32_t)pw[i];
@@ -224,7 +226,8 @@ __global__ void __launch_bounds__(256) k_raster(RasterArgs a)
         __syncthreads();
         const int nb = min(256, rg.y - b);
         if (!done) {
-            for (int j = 0; j < nb; ++j) {
+            int j = 0;
+            for (; j < nb; ++j) {
                 const float4 q0 = s0[j];
                 const float4 q1 = s1[j];
                 const float dx = q0.x - fpx;
@@ -246,10 +249,20 @@ __global__ void __launch_bounds__(256) k_raster(RasterArgs a)
                 T = T * (1.0f - alpha);
                 if (T < 1e-4f) {
                     done = true;
+                    ++j;
                     break;
                 }
             }
+            n_eval += j;
         }
+    }
+    if (a.evals) {
+        // E_alg = sum of per-pixel examined splats; E_exec = 256 x splats walked
+        unsigned long long e = n_eval;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
+        if ((tid & 31) == 0) atomicAdd(a.evals + 2 * v, e);
+        if (tid == 0) atomicAdd(a.evals + 2 * v + 1, 256ull * n_exec);
     }
     if (inside) {
         const long long pix = (long long)py * V.W + px;

@@ -39,7 +39,9 @@ struct StageEvent {
 struct s3r_ctx {
     int device = 0;
     std::string err;
-    bool debug = false, timing = false;
+    bool debug = false, timing = false, counters = false;
+    bool last_counters = false, evals_fetched = false;
+    Buf d_evals;
     bool last_debug = false;
     // pinned staging
     char* h_stage = nullptr;
@@ -555,8 +557,16 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.range_off = P<int>(c->d_range_off);
         a.pairs = P<unsigned long long>(c->d_pairs[c->final_pairs]);
         a.rec_sorted = P<float4>(c->d_recs);
+        a.evals = nullptr;
+        if (c->counters && nv) {
+            if ((rc = ensure(c, c->d_evals, (size_t)nv * 16))) return rc;
+            CU(cudaMemsetAsync(c->d_evals.p, 0, (size_t)nv * 16, st));
+            a.evals = P<unsigned long long>(c->d_evals);
+        }
         launch_raster(a, st);
         ev_end(c, st, e);
+        c->last_counters = a.evals != nullptr;
+        c->evals_fetched = false;
     }
     CU(cudaGetLastError());
     if (c->timing) c->timed_renders++;
@@ -612,7 +622,7 @@ void s3r_destroy(s3r_ctx* c)
                    &c->d_sortk[1], &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_pairs[0],
                    &c->d_pairs[1], &c->d_hist, &c->d_dsegs, &c->d_dtile0, &c->d_etile0,
                    &c->d_psegs, &c->d_ptile0, &c->d_ranges, &c->d_range_off, &c->d_vpo, &c->d_err,
-                   &c->d_dbg_keys, &c->d_dbg_flags, &c->d_dbg_rect};
+                   &c->d_dbg_keys, &c->d_dbg_flags, &c->d_dbg_rect, &c->d_evals};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& b : c->m_scene)
@@ -635,6 +645,13 @@ int s3r_set_debug(s3r_ctx* c, int enable)
 {
     if (!c) return S3R_EINVAL;
     c->debug = enable != 0;
+    return S3R_OK;
+}
+
+int s3r_set_counters(s3r_ctx* c, int enable)
+{
+    if (!c) return S3R_EINVAL;
+    c->counters = enable != 0;
     return S3R_OK;
 }
 
@@ -783,6 +800,20 @@ int s3r_get_stats(const s3r_ctx* c, int32_t view_index, s3r_stats* out)
     if (!c || !out) return S3R_EINVAL;
     if (!c->have_render || view_index < 0 || view_index >= (int)c->stats.size())
         return S3R_ESTATE;
+    s3r_ctx* m = const_cast<s3r_ctx*>(c);
+    if (m->last_counters && !m->evals_fetched) {
+        // E_alg / E_exec are produced by the rasterizer: fetch them once
+        const size_t nv = m->stats.size();
+        std::vector<unsigned long long> ev(2 * nv);
+        cudaSetDevice(m->device);
+        if (cudaMemcpy(ev.data(), m->d_evals.p, nv * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(m, S3R_ECUDA, "get_stats: fetching counters failed");
+        for (size_t v = 0; v < nv; ++v) {
+            m->stats[v].n_blend_evals = (int64_t)ev[2 * v];
+            m->stats[v].n_blend_exec = (int64_t)ev[2 * v + 1];
+        }
+        m->evals_fetched = true;
+    }
     *out = c->stats[view_index];
     return S3R_OK;
 }

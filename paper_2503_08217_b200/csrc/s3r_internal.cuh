@@ -160,6 +160,7 @@ struct RasterArgs {
     const int* range_off;
     const unsigned long long* pairs;
     const float4* rec_sorted;
+    unsigned long long* evals;   // [n_views][2] (E_alg, E_exec) or NULL
 };
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 

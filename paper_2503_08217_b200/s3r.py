@@ -27,7 +27,7 @@ STAGES = ["filter", "project", "depth_sort", "emit", "pair_sort", "ranges", "ras
 TILE = 16
 # every symbol include/s3r.h declares
 EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_set_debug",
-           "s3r_set_timing", "s3r_get_stage_times", "s3r_compose_instance_cameras", "s3r_render",
+           "s3r_set_counters", "s3r_set_timing", "s3r_get_stage_times", "s3r_compose_instance_cameras", "s3r_render",
            "s3r_render_batch", "s3r_render_batch_host", "s3r_get_stats",
            "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
            "s3r_check"]
@@ -62,7 +62,8 @@ class Outputs_(C.Structure):
 class Stats_(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("n_scene", "n_temporal", "n_visible", "n_lod_small",
                                          "n_lod_dropped", "n_rendered", "n_pairs",
-                                         "n_bad_instance")]
+                                         "n_bad_instance", "n_blend_evals",
+                                         "n_blend_exec")]
 
 
 class Debug_(C.Structure):
@@ -91,6 +92,7 @@ def lib():
                 "s3r_destroy": (None, [P]),
                 "s3r_last_error": (C.c_char_p, [P]),
                 "s3r_set_debug": (I, [P, I]),
+                "s3r_set_counters": (I, [P, I]),
                 "s3r_set_timing": (I, [P, I]),
                 "s3r_get_stage_times": (I, [P, P, P]),
                 "s3r_compose_instance_cameras": (I, [P, P, P, C.c_int32, C.c_int32, P, P]),
@@ -195,6 +197,9 @@ class Context:
     # -- configuration
     def set_debug(self, on: bool):
         self._check(self.L.s3r_set_debug(self.h, int(on)))
+
+    def set_counters(self, on: bool):
+        self._check(self.L.s3r_set_counters(self.h, int(on)))
 
     def set_timing(self, on: bool):
         self._check(self.L.s3r_set_timing(self.h, int(on)))

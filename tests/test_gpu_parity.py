@@ -68,7 +68,13 @@ def check_view(ctx, scene, view, table, out, vi, exact=True):
     # K3-K6: pair list and ranges
     assert np.array_equal(d["pair_tile"], o["pair_tile"])
     assert np.array_equal(d["pair_gauss"], o["pair_gauss"])
-    assert np.array_equal(d["ranges"], o["ranges"])
+    # tile ranges: [start, end) is unique for a non-empty tile; an empty tile
+    # only has to be empty (the oracle writes (k, k), the kernel (0, 0))
+    cnt_g = d["ranges"][:, 1] - d["ranges"][:, 0]
+    cnt_o = o["ranges"][:, 1] - o["ranges"][:, 0]
+    assert np.array_equal(cnt_g, cnt_o)
+    ne = cnt_o > 0
+    assert np.array_equal(d["ranges"][ne], o["ranges"][ne])
     # K7: images
     rgb, dep, T = (out[k].cpu().numpy() for k in ("rgb", "depth", "final_T"))
     assert np.abs(rgb - o["rgb"]).max() <= IMG_TOL
