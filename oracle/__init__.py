@@ -74,7 +74,7 @@ def lib():
             P = C.c_void_p
             sig = {
                 "so_normalize_time": (C.c_double, [C.c_int64, C.c_int64]),
-                "so_exp_f32": (C.c_float, [C.c_float]),
+                "so_exp2_f32": (C.c_float, [C.c_float]),
                 "so_exp_f64": (C.c_double, [C.c_double]),
                 "so_splitmix64": (C.c_uint64, [C.c_uint64]),
                 "so_lod_uniform": (C.c_float, [C.c_uint64, C.c_int64]),
@@ -225,8 +225,9 @@ def drop_probability(d, pmax, D, precision="f32"):
     return fn(d, pmax, D)
 
 
-def exp32(x: float) -> float:
-    return lib().so_exp_f32(x)
+def exp2_32(x: float) -> float:
+    """The contract's s3r_exp2 (DESIGN.md R-ARITH)."""
+    return lib().so_exp2_f32(x)
 
 
 def splitmix64(x: int) -> int:

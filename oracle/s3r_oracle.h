@@ -94,7 +94,7 @@ SO_DECLARE_OUT(f64, double)
 
 /* ---- f32 contract ---------------------------------------------------- */
 double   so_normalize_time(int64_t frame, int64_t frame_count);
-float    so_exp_f32(float x);
+float    so_exp2_f32(float x);
 uint64_t so_splitmix64(uint64_t x);
 float    so_lod_uniform(uint64_t seed, int64_t g);
 void     so_compose_instance_cameras(const float* w2c, const float* i2g,

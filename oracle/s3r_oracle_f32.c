@@ -11,31 +11,27 @@
 #include "s3r_oracle.h"
 
 /* ------------------------------------------------------------------------
- * s3r_exp (DESIGN.md R-ARITH): a Cephes-style single-precision exponential,
- * written out so that any IEEE-754 machine evaluates it bit-identically.
- * Used for exp(power) in Eq.2's alpha.  Called with x <= 0.
- *   x < -30            -> 0
- *   n = rint(x log2 e)  (ties to even)
- *   r = x - n*C1 - n*C2 (C1 + C2 = ln 2; C1 = 0x3F318000 has 9 significant
- *                        bits, so n*C1 is exact for |n| <= 44)
- *   y = 1 + r + r^2 P(r)  with the Cephes expf minimax P
+ * s3r_exp2 (DESIGN.md R-ARITH, exp2 form of Eq.2's exponential): 2^x for
+ * x <= 0, written so that any IEEE-754 machine evaluates it bit-identically.
+ *   x < -44             -> 0        (2^-44 = 5.7e-14; the result is flushed)
+ *   t = x + 1.5*2^23;  n = t - 1.5*2^23   (exact rint, ties to even)
+ *   r = x - n           (exact, |r| <= 1/2)
+ *   y = 1 + r P(r)      Cephes exp2f minimax P (degree 5), Horner with fma
  *   return y * 2^n      (exact: 2^-44 is normal)
  * ---------------------------------------------------------------------- */
-float so_exp_f32(float x)
+float so_exp2_f32(float x)
 {
-    if (!(x >= -30.0f)) return 0.0f;
-    float n = rintf(x * 1.44269504f);
-    float r = fmaf(-n, 0.693359375f, x);
-    r = fmaf(-n, -2.12194440e-4f, r);
-    float p = 1.9875691500e-4f;
-    p = fmaf(p, r, 1.3981999507e-3f);
-    p = fmaf(p, r, 8.3334519073e-3f);
-    p = fmaf(p, r, 4.1665795894e-2f);
-    p = fmaf(p, r, 1.6666665459e-1f);
-    p = fmaf(p, r, 5.0000001201e-1f);
-    float r2 = r * r;
-    float y = fmaf(p, r2, r);
-    y = y + 1.0f;
+    if (!(x >= -44.0f)) return 0.0f;
+    float t = x + 12582912.0f;
+    float n = t - 12582912.0f;
+    float r = x - n;
+    float p = 1.535336188319500e-4f;
+    p = fmaf(p, r, 1.339887440266574e-3f);
+    p = fmaf(p, r, 9.618437357674640e-3f);
+    p = fmaf(p, r, 5.550332471162809e-2f);
+    p = fmaf(p, r, 2.402264791363012e-1f);
+    p = fmaf(p, r, 6.931472028550421e-1f);
+    float y = fmaf(p, r, 1.0f);
     return ldexpf(y, (int)n);
 }
 
@@ -142,5 +138,6 @@ void so_reset_visibility(so_scene* s)
 #define FMIN fminf
 #define FMAX fmaxf
 #define ISFIN isfinite
-#define EXPF so_exp_f32
+#define EXPF so_exp2_f32   /* unused: SO_CONTRACT_EXP2 selects the exp2 form */
+#define SO_CONTRACT_EXP2 1
 #include "s3r_oracle_impl.inc"

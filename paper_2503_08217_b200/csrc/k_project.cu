@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(PT) k_project(ProjectArgs a)
             const uint32_t ry = (uint32_t)sp[k].ty0 | ((uint32_t)sp[k].ty1 << 16);
             float4* r = a.rec + 3 * o;
             r[0] = make_float4(sp[k].k[0], sp[k].k[1], sp[k].k[2], col[k].w);
-            r[1] = make_float4(sp[k].A, sp[k].B, sp[k].C, __uint_as_float(rx));
+            // exp2-form blend coefficients (R-ARITH): qa = A (-log2e/2), qb = B (-log2e),
+            // qc = C (-log2e/2)
+            r[1] = make_float4(sp[k].A * -0x1.715476p-1f, sp[k].B * -0x1.715476p+0f,
+                               sp[k].C * -0x1.715476p-1f, __uint_as_float(rx));
             r[2] = make_float4(col[k].x, col[k].y, col[k].z, __uint_as_float(ry));
             a.dkey[o] = __float_as_uint(sp[k].k[2]);
             if (a.gidx) a.gidx[o] = (int32_t)gg[k];

@@ -8,11 +8,13 @@
 // include-then-stop at T < 1e-4, black background, depth = sum w z.  exp is the
 // s3r_exp of R-ARITH (bit-identical to the oracle's).
 //
-// K7 layout: one CTA per (view, tile), one pixel per thread.  The tile's
-// sorted pair list is consumed in batches of 256: each thread fetches one
-// 48-byte splat record (3 x 16-byte loads from the depth-sorted record array)
-// into shared memory; every pixel then walks the batch.  A pixel stops at its
-// termination; the CTA stops when all 256 pixels have (__syncthreads_count).
+// K7 layout: one 64-thread CTA per (view, tile); each thread owns 4 pixels of
+// one column (rows ly, ly+4, ly+8, ly+12), so the per-splat dx terms and the
+// shared-memory record loads are amortised over 4 pixel evaluations.  The
+// tile's sorted pair list is consumed in batches of 256 records (48 B each,
+// 16-byte loads from the depth-sorted record array) staged in shared memory.
+// A pixel stops at its termination; the CTA stops when all its pixels have
+// (__syncthreads_count).
 #include "s3r_internal.cuh"
 
 namespace s3r {
@@ -174,104 +176,153 @@ __global__ void k_ranges(const unsigned long long* __restrict__ pairs, long long
 }
 
 // ------------------------------------------------------------------ K7
-__device__ __forceinline__ float s3r_exp(float x)
+// R-ARITH s3r_exp2 for -44 <= x <= 0 (the caller handles x < -44 -> 0):
+// n = rint(x) by the 1.5*2^23 shifter (all full-rate FADDs, no F2I/FRND),
+// r = x - n exact, 2^r by the Cephes exp2f polynomial, times 2^n built from
+// the shifter's bits: bits(t) = 0x4B400000 + n, so (bits(t) << 23) +
+// 0x3F800000 = bits(2^n).
+__device__ __forceinline__ float s3r_exp2(float x)
 {
-    // R-ARITH software exponential (Cephes expf), x <= 0
-    if (!(x >= -30.0f)) return 0.0f;
-    const float n = rintf(x * 1.44269504f);
-    float r = __fmaf_rn(-n, 0.693359375f, x);
-    r = __fmaf_rn(-n, -2.12194440e-4f, r);
-    float p = 1.9875691500e-4f;
-    p = __fmaf_rn(p, r, 1.3981999507e-3f);
-    p = __fmaf_rn(p, r, 8.3334519073e-3f);
-    p = __fmaf_rn(p, r, 4.1665795894e-2f);
-    p = __fmaf_rn(p, r, 1.6666665459e-1f);
-    p = __fmaf_rn(p, r, 5.0000001201e-1f);
-    const float r2 = r * r;
-    float y = __fmaf_rn(p, r2, r);
-    y = y + 1.0f;
-    return y * __int_as_float((127 + (int)n) << 23);
+    const float t = x + 12582912.0f;
+    const float n = t - 12582912.0f;
+    const float r = x - n;
+    float p = 1.535336188319500e-4f;
+    p = __fmaf_rn(p, r, 1.339887440266574e-3f);
+    p = __fmaf_rn(p, r, 9.618437357674640e-3f);
+    p = __fmaf_rn(p, r, 5.550332471162809e-2f);
+    p = __fmaf_rn(p, r, 2.402264791363012e-1f);
+    p = __fmaf_rn(p, r, 6.931472028550421e-1f);
+    const float y = __fmaf_rn(p, r, 1.0f);
+    return y * __uint_as_float((__float_as_uint(t) << 23) + 0x3F800000u);
 }
 
-__global__ void __launch_bounds__(256) k_raster(RasterArgs a)
+constexpr int RT = 64;      // threads per tile CTA: 16 columns x 4 row groups
+constexpr int RPIX = 4;     // pixels per thread: rows ly, ly+4, ly+8, ly+12 of one column
+constexpr int RB = 256;     // splat records staged in shared memory per batch
+
+template <bool COUNT>
+__global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
 {
-    __shared__ float4 s0[256], s1[256], s2[256];
+    __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
     const int v = blockIdx.y;
     const DevView& V = a.views[v];
     const int tile = blockIdx.x;
     if (tile >= V.ntiles) return;
     const int tid = threadIdx.x;
     const int tx = tile % V.TX, ty = tile / V.TX;
-    const int px = tx * TILE + (tid & 15), py = ty * TILE + (tid >> 4);
-    const bool inside = px < V.W && py < V.H;
-    const float fpx = (float)px, fpy = (float)py;
+    const int px = tx * TILE + (tid & 15);
+    const int py0 = ty * TILE + (tid >> 4);
+    const float fpx = (float)px;
+    float fpy[RPIX], T[RPIX], cr[RPIX], cg[RPIX], cb[RPIX], dp[RPIX];
+    int stop[RPIX];
+    int nlive = 0;                     // pixels of this thread still blending
+    unsigned inside = 0;
+#pragma unroll
+    for (int k = 0; k < RPIX; ++k) {
+        const int py = py0 + 4 * k;
+        fpy[k] = (float)py;
+        cr[k] = cg[k] = cb[k] = dp[k] = 0.0f;
+        stop[k] = -1;
+        const bool in = px < V.W && py < V.H;
+        // a pixel outside the image starts "terminated" (T = 0 is never written)
+        T[k] = in ? 1.0f : 0.0f;
+        inside |= (in ? 1u : 0u) << k;
+        nlive += in ? 1 : 0;
+    }
     const int2 rg = a.ranges[a.range_off[v] + tile];
     const unsigned long long* pw = a.pairs + V.pair_off;
     const float4* recs = a.rec_sorted + 3 * V.cap_off;
+    // first Horner coefficient of s3r_exp2, read once from shared memory so it
+    // stays in a register (as an immediate it would be re-materialised per use)
+    __shared__ float s_c0;
+    if (tid == 0) s_c0 = 1.535336188319500e-4f;
+    __syncthreads();
+    const float c0 = s_c0;
 
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, dp = 0.0f;
-    bool done = !inside;
-    uint32_t n_eval = 0, n_exec = 0;    // work counters (only stored when a.evals)
-    for (int b = rg.x; b < rg.y; b += 256) {
-        if (__syncthreads_count(done) == 256) break;
-        n_exec += min(256, rg.y - b);
-        const int i = b + tid;
-        if (i < rg.y) {
-            const uint32_t r = (uint32_t)pw[i];
+    uint32_t n_exec = 0;
+    for (int b = rg.x; b < rg.y; b += RB) {
+        if (__syncthreads_count(nlive) == 0) break;
+        const int nb = min(RB, rg.y - b);
+        n_exec += nb;
+        for (int i = tid; i < nb; i += RT) {
+            const uint32_t r = (uint32_t)pw[b + i];
             const float4* src = recs + 3ll * r;
-            s0[tid] = src[0];
-            s1[tid] = src[1];
-            s2[tid] = src[2];
+            s_rec[3 * i + 0] = src[0];
+            s_rec[3 * i + 1] = src[1];
+            s_rec[3 * i + 2] = src[2];
         }
         __syncthreads();
-        const int nb = min(256, rg.y - b);
-        if (!done) {
-            int j = 0;
-            for (; j < nb; ++j) {
-                const float4 q0 = s0[j];
-                const float4 q1 = s1[j];
+        if (nlive) {
+            for (int j = 0; j < nb; ++j) {
+                const float4* sr = s_rec + 3 * j;
+                const float4 q0 = sr[0];   // mx, my, z, o
+                const float4 q1 = sr[1];   // qa, qb, qc, rect
+                const float4 q2 = sr[2];   // r, g, b, rect
+                // e2 = log2(e) * power = qa dx^2 + qb dx dy + qc dy^2 (R-ARITH exp2
+                // form); the dx terms are shared by the thread's 4 pixels
                 const float dx = q0.x - fpx;
-                const float dy = q0.y - fpy;
-                const float t1 = dx * dx;
-                const float t2 = dy * dy;
-                const float t3 = dx * dy;
-                const float sq = __fmaf_rn(q1.x, t1, q1.z * t2);
-                const float power = fminf(0.0f, __fmaf_rn(-0.5f, sq, -(q1.y * t3)));
-                // exp(power) == 0 below -30: alpha = 0 leaves C, D and T bit-identical
-                if (!(power >= -30.0f)) continue;
-                const float alpha = fminf(0.99f, q0.w * s3r_exp(power));
-                const float w = alpha * T;
-                const float4 q2 = s2[j];
-                cr = __fmaf_rn(q2.x, w, cr);
-                cg = __fmaf_rn(q2.y, w, cg);
-                cb = __fmaf_rn(q2.z, w, cb);
-                dp = __fmaf_rn(q0.z, w, dp);
-                T = T * (1.0f - alpha);
-                if (T < 1e-4f) {
-                    done = true;
-                    ++j;
+                const float a1 = q1.x * dx;
+                const float a2 = a1 * dx;
+                const float b1 = q1.y * dx;
+#pragma unroll
+                for (int k = 0; k < RPIX; ++k) {
+                    const float dy = q0.y - fpy[k];
+                    const float c1 = __fmaf_rn(q1.z, dy, b1);
+                    const float e2 = fminf(0.0f, __fmaf_rn(dy, c1, a2));
+                    // live pixel (T >= 1e-4) and a non-zero exp2 (s3r_exp2 flushes
+                    // below -44: alpha = 0 would leave C, D and T bit-identical)
+                    if (e2 >= -44.0f && T[k] >= 1e-4f) {
+                        const float tt = e2 + 12582912.0f;
+                        const float nn = tt - 12582912.0f;
+                        const float rr = e2 - nn;
+                        float pp = __fmaf_rn(c0, rr, 1.339887440266574e-3f);
+                        pp = __fmaf_rn(pp, rr, 9.618437357674640e-3f);
+                        pp = __fmaf_rn(pp, rr, 5.550332471162809e-2f);
+                        pp = __fmaf_rn(pp, rr, 2.402264791363012e-1f);
+                        pp = __fmaf_rn(pp, rr, 6.931472028550421e-1f);
+                        const float yy = __fmaf_rn(pp, rr, 1.0f);
+                        const float ex = yy * __uint_as_float((__float_as_uint(tt) << 23) + 0x3F800000u);
+                        const float alpha = fminf(0.99f, q0.w * ex);
+                        const float w = alpha * T[k];
+                        cr[k] = __fmaf_rn(q2.x, w, cr[k]);
+                        cg[k] = __fmaf_rn(q2.y, w, cg[k]);
+                        cb[k] = __fmaf_rn(q2.z, w, cb[k]);
+                        dp[k] = __fmaf_rn(q0.z, w, dp[k]);
+                        T[k] = T[k] - w;
+                        // include-then-stop (R14): the pixel is dead once T < 1e-4
+                        if (COUNT && T[k] < 1e-4f) stop[k] = b + j + 1;
+                    }
+                }
+                const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
+                if (tmax < 1e-4f) {
+                    nlive = 0;
                     break;
                 }
             }
-            n_eval += j;
         }
     }
-    if (a.evals) {
-        // E_alg = sum of per-pixel examined splats; E_exec = 256 x splats walked
-        unsigned long long e = n_eval;
+    if (COUNT) {
+        // E_alg = sum over pixels of the splats examined up to and including the
+        // terminating one; E_exec = 256 x splats the CTA walked
+        unsigned long long e = 0;
+#pragma unroll
+        for (int k = 0; k < RPIX; ++k)
+            if (inside & (1u << k)) e += (unsigned long long)((stop[k] >= 0 ? stop[k] : rg.y) - rg.x);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
         if ((tid & 31) == 0) atomicAdd(a.evals + 2 * v, e);
         if (tid == 0) atomicAdd(a.evals + 2 * v + 1, 256ull * n_exec);
     }
-    if (inside) {
-        const long long pix = (long long)py * V.W + px;
+#pragma unroll
+    for (int k = 0; k < RPIX; ++k) {
+        if (!(inside & (1u << k))) continue;
+        const long long pix = (long long)(py0 + 4 * k) * V.W + px;
         float* o = V.rgb + 3 * pix;
-        o[0] = cr;
-        o[1] = cg;
-        o[2] = cb;
-        if (V.depth) V.depth[pix] = dp;
-        if (V.finalT) V.finalT[pix] = T;
+        o[0] = cr[k];
+        o[1] = cg[k];
+        o[2] = cb[k];
+        if (V.depth) V.depth[pix] = dp[k];
+        if (V.finalT) V.finalT[pix] = T[k];
     }
 }
 
@@ -319,7 +370,8 @@ void launch_raster(const RasterArgs& a, cudaStream_t st)
 {
     if (a.max_tiles == 0 || a.n_views == 0) return;
     dim3 grid(a.max_tiles, a.n_views);
-    k_raster<<<grid, 256, 0, st>>>(a);
+    if (a.evals) k_raster<true><<<grid, RT, 0, st>>>(a);
+    else k_raster<false><<<grid, RT, 0, st>>>(a);
 }
 
 void launch_dump_order(const uint32_t* order, const int32_t* gidx, long long base,
