@@ -37,10 +37,10 @@ from paper_2503_08217_b200 import scenegen as sg  # noqa: E402
 
 METRIC = "rendered views/sec and Gaussians/sec at 1/2/4/8 B200; % HBM/FP32 roofline"
 UNIT = "views/s"
-# FP32 operations per blend evaluation of the R-ARITH step (FMA = 2):
-# dx,dy 2; t1..t3 3; quadratic form 3; power 4; s3r_exp 21; alpha 2; w 1;
-# colour + depth 8; transmittance 2; termination test 1.
-FLOPS_PER_EVAL = 47
+# FP32 operations per blend evaluation of the R-ARITH exp2-form step (FMA = 2,
+# min / compare = 1): dx, dy 2; a1, a2, b1 3; c1, e2 4; clamp 1; s3r_exp2 16
+# (3 add, 6 fma, scale); alpha 2; w 1; colour + depth 8; T 1; termination 1.
+FLOPS_PER_EVAL = 39
 SM_COUNT_B200 = 148
 
 
@@ -61,58 +61,66 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    """SM clock + clock-event (throttle) reasons sampled through NVML every
+    50 ms during the timed region (the same counters nvidia-smi reports)."""
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self.stop_ev = threading.Event()
+        self.err = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = self.index
+            if vis:
+                ids = [x for x in vis.split(",") if x.strip()]
+                if idx < len(ids) and ids[idx].strip().isdigit():
+                    idx = int(ids[idx])
+            self.h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.smax = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception as e:           # noqa: BLE001
+            self.err = f"nvml unavailable: {e}"
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N = self.N
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap,
+                "hw_power_brake_slowdown": N.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        while not self.stop_ev.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                util = N.nvmlDeviceGetUtilizationRates(self.h).gpu
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, util))
+                for k, b in bits.items():
+                    if r & b:
+                        self.reasons.add(k)
+            except Exception as e:       # noqa: BLE001
+                self.err = str(e)
+                break
+            time.sleep(0.05)
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons, util = [], [], set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                smax.append(float(f[1]))
-                util.append(float(f[6]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        loaded = [s for s, u in zip(sm, util) if u > 50] or sm
+        if self.err and not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        sm = [s for s, _ in self.samples]
+        loaded = [s for s, u in self.samples if u > 50] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "sm_max_mhz": float(self.smax), "reasons": sorted(self.reasons),
+                "samples": len(sm), "source": "NVML, 50 ms period"}
 
 
 def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):

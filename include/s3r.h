@@ -225,6 +225,12 @@ int s3r_commit_visibility(s3r_ctx* ctx, const s3r_scene* scene, float margin, vo
 /* Periodic reset: v = (-1, 1) for every Gaussian.                   */
 int s3r_reset_visibility(s3r_ctx* ctx, const s3r_scene* scene, void* stream);
 
+/* Multi-GPU point-life merge helper (Eq.5 is a min/max, so replicas merge
+ * exactly): negates l_s of every Gaussian in place (an involution).  Between
+ * two calls an all-reduce MAX over the float[2n] life array (NCCL) yields
+ * (min l_s, max l_e) over ranks.  life: DEVICE float2[n].                  */
+int s3r_life_flip(s3r_ctx* ctx, float* life, int64_t n, void* stream);
+
 /* Synchronise `stream` and return the device error state accumulated since
  * the last check: S3R_EINSTANCE, S3R_ECUDA or S3R_OK.                      */
 int s3r_check(s3r_ctx* ctx, void* stream);

@@ -418,6 +418,13 @@ __global__ void k_reset(float2* __restrict__ vis, long long n)
     const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (g < n) vis[g] = make_float2(-1.0f, 1.0f);
 }
+
+// l_s -> -l_s (exact) so that one all-reduce MAX merges (min l_s, max l_e).
+__global__ void k_life_flip(float2* __restrict__ life, long long n)
+{
+    const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (g < n) life[g].x = -life[g].x;
+}
 }  // namespace
 
 void launch_project(const ProjectArgs& a, cudaStream_t st)
@@ -449,6 +456,12 @@ void launch_reset(float2* vis, long long n, cudaStream_t st)
 {
     if (n == 0) return;
     k_reset<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vis, n);
+}
+
+void launch_life_flip(float2* life, long long n, cudaStream_t st)
+{
+    if (n == 0) return;
+    k_life_flip<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(life, n);
 }
 
 }  // namespace s3r

@@ -879,6 +879,17 @@ int s3r_reset_visibility(s3r_ctx* c, const s3r_scene* s, void* stream)
     return S3R_OK;
 }
 
+int s3r_life_flip(s3r_ctx* c, float* life, int64_t n, void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    if (n < 0 || (n > 0 && (!life || !aligned(life, 8))))
+        return fail(c, S3R_EINVAL, "life_flip: bad arguments");
+    CU(cudaSetDevice(c->device));
+    launch_life_flip(reinterpret_cast<float2*>(life), n, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return S3R_OK;
+}
+
 int s3r_check(s3r_ctx* c, void* stream)
 {
     if (!c) return S3R_EINVAL;

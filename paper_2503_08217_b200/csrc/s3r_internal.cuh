@@ -167,6 +167,7 @@ void launch_raster(const RasterArgs& a, cudaStream_t st);
 // K9: commit / reset.
 void launch_commit(float2* vis, float2* life, long long n, float margin, cudaStream_t st);
 void launch_reset(float2* vis, long long n, cudaStream_t st);
+void launch_life_flip(float2* life, long long n, cudaStream_t st);
 
 // Debug helpers.
 void launch_dump_order(const uint32_t* order, const int32_t* gidx, long long base,

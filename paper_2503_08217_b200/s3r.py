@@ -30,7 +30,7 @@ EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_se
            "s3r_set_counters", "s3r_set_timing", "s3r_get_stage_times", "s3r_compose_instance_cameras", "s3r_render",
            "s3r_render_batch", "s3r_render_batch_host", "s3r_get_stats",
            "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
-           "s3r_check"]
+           "s3r_life_flip", "s3r_check"]
 
 
 class S3RError(RuntimeError):
@@ -103,6 +103,7 @@ def lib():
                 "s3r_dump_intermediates": (I, [P, C.c_int32, P, P]),
                 "s3r_commit_visibility": (I, [P, P, C.c_float, P]),
                 "s3r_reset_visibility": (I, [P, P, P]),
+                "s3r_life_flip": (I, [P, P, I64, P]),
                 "s3r_check": (I, [P, P]),
             }
             for name, (res, args) in sig.items():
@@ -289,6 +290,12 @@ class Context:
     def reset_visibility(self, scene: DeviceScene, stream=None):
         sc = scene.struct()
         self._check(self.L.s3r_reset_visibility(self.h, C.byref(sc), _stream(stream)))
+
+    def life_flip(self, life: torch.Tensor, stream=None):
+        """Negate l_s in place (see s3r_life_flip): brackets an all-reduce MAX."""
+        assert life.is_cuda and life.is_contiguous() and life.dtype == torch.float32
+        self._check(self.L.s3r_life_flip(self.h, _ptr(life), int(life.shape[0]),
+                                         _stream(stream)))
 
     def check(self, stream=None) -> int:
         return self._check(self.L.s3r_check(self.h, _stream(stream)), allow=(S3R_OK, S3R_EINSTANCE))

@@ -141,6 +141,17 @@ def test_life_update_and_commit(ctx):
     assert np.array_equal(ds.visibility.cpu().numpy(), ref.visibility)
 
 
+def test_life_flip_kernel(ctx):
+    life = torch.tensor([[0.25, 0.5], [1.0, -1.0], [-0.75, 0.0]], device="cuda")
+    ref = life.clone()
+    ctx.life_flip(life)
+    torch.cuda.synchronize()
+    assert torch.equal(life[:, 0], -ref[:, 0]) and torch.equal(life[:, 1], ref[:, 1])
+    ctx.life_flip(life)
+    torch.cuda.synchronize()
+    assert torch.equal(life, ref)
+
+
 def test_batch_split_invariance(ctx):
     """Images and life do not depend on how views are batched."""
     scene, views = sg.make_random_dynamic(12, 4000, 2, 500, 130, 97, 6, lod=(2.0, 0.5, 10.0))

@@ -1,0 +1,88 @@
+"""The N>1 host path on CPU: world_size 2 over gloo (127.0.0.1).
+
+Views are sharded across ranks (contiguous blocks); each rank applies its
+views' M_t to a private copy of the point life; one all-reduce MAX bracketed by
+l_s negation merges them (parallel.merge_life).  The merged life, and the
+committed visibility, must equal a single process applying every view
+(Eq.5 is order-independent, so equality is bit-exact).  The per-rank masks come
+from the CPU oracle here (no GPU in this suite); the CUDA flip kernel is
+covered by the gpu tests.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2503_08217_b200 import parallel
+from paper_2503_08217_b200 import scenegen as sg
+
+
+def _scene():
+    scene, views = sg.make_random_dynamic(41, 1500, 3, 80, 96, 64, 7, fresh=True)
+    for i, v in enumerate(views):
+        v.t = float(np.float32(-1.0 + 2.0 * i / (len(views) - 1)))
+    return scene, views
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        scene, views = _scene()
+        mine = parallel.shard_views(views, rank, world)
+        for v in mine:
+            o = oracle.render_view(scene, v, pairs=False, image=False)
+            oracle.update_life(scene, o["visible"], v.t)
+        life = torch.from_numpy(scene.life)
+
+        def flip(t):
+            t[:, 0].neg_()
+
+        parallel.merge_life(life, flip)
+        np.save(os.path.join(out_dir, f"life_{rank}.npy"), life.numpy().copy())
+        oracle.commit_visibility(scene, 0.1)
+        np.save(os.path.join(out_dir, f"vis_{rank}.npy"), scene.visibility)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_bounds_partition():
+    for n in (0, 1, 7, 64, 65):
+        for w in (1, 2, 3, 8):
+            seen = []
+            for r in range(w):
+                lo, hi = parallel.shard_bounds(n, r, w)
+                seen.extend(range(lo, hi))
+                assert hi - lo in (n // w, n // w + 1)
+            assert seen == list(range(n))
+
+
+def test_world2_life_merge_matches_single_process(tmp_path):
+    world = 2
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    scene, views = _scene()
+    for v in views:
+        o = oracle.render_view(scene, v, pairs=False, image=False)
+        oracle.update_life(scene, o["visible"], v.t)
+    want_life = scene.life.copy()
+    oracle.commit_visibility(scene, 0.1)
+    for r in range(world):
+        got = np.load(tmp_path / f"life_{r}.npy")
+        assert np.array_equal(got, want_life)
+        assert np.array_equal(np.load(tmp_path / f"vis_{r}.npy"), scene.visibility)
+    assert (want_life[:, 0] <= want_life[:, 1]).sum() > 100     # observed Gaussians exist
