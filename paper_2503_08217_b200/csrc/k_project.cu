@@ -24,7 +24,7 @@ namespace s3r {
 
 namespace {
 constexpr int PT = 256;
-constexpr int PITEMS = 2;
+constexpr int PITEMS = 1;
 constexpr int PTILE = PT * PITEMS;
 constexpr int PGROUPS = PITEMS * (PT / 32);   // 16
 
@@ -192,7 +192,7 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
     s.flags |= F_RENDERED;
 }
 
-__global__ void __launch_bounds__(PT) k_project(ProjectArgs a)
+__global__ void __launch_bounds__(PT, 4) k_project(ProjectArgs a)
 {
     extern __shared__ float s_tab[];          // [K1][12]
     __shared__ int s_gtile, s_view;

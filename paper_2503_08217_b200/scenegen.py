@@ -214,6 +214,11 @@ def make_street_scene(cfg: Config, scale: float = 1.0, seed: Optional[int] = Non
     fpm = (F - 1) / L
     v_lo, v_hi = _interval_to_t((xg - cfg.window_front) * fpm, (xg + cfg.window_back) * fpm, F)
     ids = np.zeros(n_static, np.int32)
+    # storage order of the static Gaussians: along the street (the order in
+    # which LiDAR-initialised points are acquired along the trajectory), so the
+    # Gaussians one time t keeps are a few contiguous runs of memory
+    order = np.argsort(xg, kind="stable")
+    mu, sig, quat, v_lo, v_hi = mu[order], sig[order], quat[order], v_lo[order], v_hi[order]
 
     # dynamic objects: car boxes 4.5 x 1.9 x 1.6 m in lanes y = +-3.5
     x0 = rng.uniform(-20.0, L + 20.0, K)
