@@ -22,14 +22,6 @@ constexpr int FV = 8;            // float4 (2 Gaussians) per thread
 constexpr int FTILE = FT * FV * 2;
 constexpr int FGROUPS = FV * (FT / 32);   // (round, warp) groups = 64
 
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p)
-{
-    return *reinterpret_cast<const volatile uint32_t*>(p);
-}
-__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v)
-{
-    *reinterpret_cast<volatile uint32_t*>(p) = v;
-}
 
 __global__ void __launch_bounds__(FT) k_filter(const float2* __restrict__ vis, long long n,
                                                const float* __restrict__ times, int T,
@@ -97,27 +89,19 @@ __global__ void __launch_bounds__(FT) k_filter(const float2* __restrict__ vis, l
     }
     __syncthreads();
 
-    // decoupled look-back, one thread per slot
-    if (tid < T) {
-        uint32_t agg = s_agg[tid];
-        uint32_t* lb = lookback + (long long)tid * ntiles;
-        uint32_t excl = 0;
-        if (tile == 0) {
-            st_volatile(lb, LB_PRE | agg);
-        } else {
-            st_volatile(lb + tile, LB_AGG | agg);
-            int j = tile - 1;
-            while (true) {
-                uint32_t w = ld_volatile(lb + j);
-                if ((w >> 30) == 0) continue;
-                excl += w & LB_MASK;
-                if (w & LB_PRE) break;
-                --j;
-            }
-            st_volatile(lb + tile, LB_PRE | (excl + agg));
+    // decoupled look-back per slot: publish every slot's aggregate first, then
+    // one warp per slot walks its chain 32 predecessors at a time
+    if (tid < T) lb_publish(lookback + (long long)tid * ntiles + tile,
+                            (tile == 0 ? LB_PRE : LB_AGG) | s_agg[tid]);
+    for (int s = warp; s < T; s += FT / 32) {
+        uint32_t* lb = lookback + (long long)s * ntiles;
+        const uint32_t agg = s_agg[s];
+        const uint32_t excl = (tile == 0) ? 0u : warp_lookback(lb, 1, tile, 0);
+        if (lane == 0) {
+            if (tile != 0) lb_publish(lb + tile, LB_PRE | (excl + agg));
+            s_base[s] = excl;
+            if (tile == ntiles - 1) counts[s] = (unsigned long long)(excl + agg);
         }
-        s_base[tid] = excl;
-        if (tile == ntiles - 1) counts[tid] = (unsigned long long)(excl + agg);
     }
     __syncthreads();
 

@@ -28,14 +28,6 @@ constexpr int PITEMS = 1;
 constexpr int PTILE = PT * PITEMS;
 constexpr int PGROUPS = PITEMS * (PT / 32);   // 16
 
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p)
-{
-    return *reinterpret_cast<const volatile uint32_t*>(p);
-}
-__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v)
-{
-    *reinterpret_cast<volatile uint32_t*>(p) = v;
-}
 
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x)
 {
@@ -192,7 +184,7 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
     s.flags |= F_RENDERED;
 }
 
-__global__ void __launch_bounds__(PT, 4) k_project(ProjectArgs a)
+__global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
 {
     extern __shared__ float s_tab[];          // [K1][12]
     __shared__ int s_gtile, s_view;
@@ -315,24 +307,16 @@ __global__ void __launch_bounds__(PT, 4) k_project(ProjectArgs a)
         }
         if (lane < PGROUPS) s_grp[lane] = x - c;
         const uint32_t agg = __shfl_sync(0xffffffffu, x, 31);
+        // decoupled look-back over the view's preceding CTAs (warp-cooperative)
+        uint32_t* lb = a.lookback;
+        const int first = gtile - ltile;
+        if (lane == 0) lb_publish(lb + gtile, (ltile == 0 ? LB_PRE : LB_AGG) | agg);
+        const uint32_t excl = (ltile == 0) ? 0u : warp_lookback(lb, 1, gtile, first);
         if (lane == 0) {
-            uint32_t* lb = a.lookback;
-            uint32_t excl = 0;
-            if (ltile == 0) {
-                st_volatile(lb + gtile, LB_PRE | agg);
-            } else {
-                st_volatile(lb + gtile, LB_AGG | agg);
-                int j = gtile - 1;
-                while (true) {
-                    uint32_t w = ld_volatile(lb + j);
-                    if ((w >> 30) == 0) continue;
-                    excl += w & LB_MASK;
-                    if (w & LB_PRE) break;
-                    --j;
-                }
-                st_volatile(lb + gtile, LB_PRE | (excl + agg));
-            }
+            if (ltile != 0) lb_publish(lb + gtile, LB_PRE | (excl + agg));
             s_base = excl;
+        }
+        if (lane == 1) {
             ViewCounters* ctr = a.counters + vi;
             unsigned long long t5[5] = {0, 0, 0, 0, 0};
             for (int w = 0; w < PT / 32; ++w)

@@ -24,14 +24,6 @@ constexpr int ET = 256;
 constexpr int EITEMS = 4;
 constexpr int ETILE = ET * EITEMS;
 
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p)
-{
-    return *reinterpret_cast<const volatile uint32_t*>(p);
-}
-__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v)
-{
-    *reinterpret_cast<volatile uint32_t*>(p) = v;
-}
 
 __device__ __forceinline__ int find_seg(const int* seg_tile0, int nsegs, int gt)
 {
@@ -105,23 +97,12 @@ __global__ void __launch_bounds__(ET) k_emit(EmitArgs a)
         }
         if (lane < ET / 32) s_warp[lane] = ww - w;
         const uint32_t agg = __shfl_sync(0xffffffffu, ww, ET / 32 - 1);
+        // decoupled look-back over the view's preceding CTAs (warp-cooperative)
+        uint32_t* lb = a.lookback;
+        if (lane == 0) lb_publish(lb + gt, (ltile == 0 ? LB_PRE : LB_AGG) | agg);
+        const uint32_t excl = (ltile == 0) ? 0u : warp_lookback(lb, 1, gt, gt - ltile);
         if (lane == 0) {
-            uint32_t excl = 0;
-            uint32_t* lb = a.lookback;
-            if (ltile == 0) {
-                st_volatile(lb + gt, LB_PRE | agg);
-            } else {
-                st_volatile(lb + gt, LB_AGG | agg);
-                int j = gt - 1;
-                while (true) {
-                    const uint32_t w2 = ld_volatile(lb + j);
-                    if ((w2 >> 30) == 0) continue;
-                    excl += w2 & LB_MASK;
-                    if (w2 & LB_PRE) break;
-                    --j;
-                }
-                st_volatile(lb + gt, LB_PRE | (excl + agg));
-            }
+            if (ltile != 0) lb_publish(lb + gt, LB_PRE | (excl + agg));
             s_base = excl;
             s_off[ETILE] = agg;
         }
@@ -181,13 +162,13 @@ __global__ void k_ranges(const unsigned long long* __restrict__ pairs, long long
 // r = x - n exact, 2^r by the Cephes exp2f polynomial, times 2^n built from
 // the shifter's bits: bits(t) = 0x4B400000 + n, so (bits(t) << 23) +
 // 0x3F800000 = bits(2^n).
-__device__ __forceinline__ float s3r_exp2(float x)
+// c0 = 1.535336188319500e-4f is passed in a register (see k_raster).
+__device__ __forceinline__ float s3r_exp2(float x, float c0)
 {
     const float t = x + 12582912.0f;
     const float n = t - 12582912.0f;
     const float r = x - n;
-    float p = 1.535336188319500e-4f;
-    p = __fmaf_rn(p, r, 1.339887440266574e-3f);
+    float p = __fmaf_rn(c0, r, 1.339887440266574e-3f);
     p = __fmaf_rn(p, r, 9.618437357674640e-3f);
     p = __fmaf_rn(p, r, 5.550332471162809e-2f);
     p = __fmaf_rn(p, r, 2.402264791363012e-1f);
@@ -232,12 +213,9 @@ __global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
     const int2 rg = a.ranges[a.range_off[v] + tile];
     const unsigned long long* pw = a.pairs + V.pair_off;
     const float4* recs = a.rec_sorted + 3 * V.cap_off;
-    // first Horner coefficient of s3r_exp2, read once from shared memory so it
-    // stays in a register (as an immediate it would be re-materialised per use)
-    __shared__ float s_c0;
-    if (tid == 0) s_c0 = 1.535336188319500e-4f;
-    __syncthreads();
-    const float c0 = s_c0;
+    // first Horner coefficient of s3r_exp2 (1.535336188319500e-4f), a kernel
+    // argument so it stays in a register (an immediate is re-materialised per use)
+    const float c0 = a.exp2_c0;
 
     uint32_t n_exec = 0;
     for (int b = rg.x; b < rg.y; b += RB) {
@@ -272,17 +250,7 @@ __global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
                     // live pixel (T >= 1e-4) and a non-zero exp2 (s3r_exp2 flushes
                     // below -44: alpha = 0 would leave C, D and T bit-identical)
                     if (e2 >= -44.0f && T[k] >= 1e-4f) {
-                        const float tt = e2 + 12582912.0f;
-                        const float nn = tt - 12582912.0f;
-                        const float rr = e2 - nn;
-                        float pp = __fmaf_rn(c0, rr, 1.339887440266574e-3f);
-                        pp = __fmaf_rn(pp, rr, 9.618437357674640e-3f);
-                        pp = __fmaf_rn(pp, rr, 5.550332471162809e-2f);
-                        pp = __fmaf_rn(pp, rr, 2.402264791363012e-1f);
-                        pp = __fmaf_rn(pp, rr, 6.931472028550421e-1f);
-                        const float yy = __fmaf_rn(pp, rr, 1.0f);
-                        const float ex = yy * __uint_as_float((__float_as_uint(tt) << 23) + 0x3F800000u);
-                        const float alpha = fminf(0.99f, q0.w * ex);
+                        const float alpha = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
                         const float w = alpha * T[k];
                         cr[k] = __fmaf_rn(q2.x, w, cr[k]);
                         cg[k] = __fmaf_rn(q2.y, w, cg[k]);
@@ -366,9 +334,11 @@ void launch_ranges(const unsigned long long* pairs, long long total_pairs, const
                                                                      range_off, ranges);
 }
 
-void launch_raster(const RasterArgs& a, cudaStream_t st)
+void launch_raster(const RasterArgs& args, cudaStream_t st)
 {
-    if (a.max_tiles == 0 || a.n_views == 0) return;
+    if (args.max_tiles == 0 || args.n_views == 0) return;
+    RasterArgs a = args;
+    a.exp2_c0 = 1.535336188319500e-4f;
     dim3 grid(a.max_tiles, a.n_views);
     if (a.evals) k_raster<true><<<grid, RT, 0, st>>>(a);
     else k_raster<false><<<grid, RT, 0, st>>>(a);

@@ -23,6 +23,43 @@ constexpr uint32_t LB_AGG = 1u << 30;
 constexpr uint32_t LB_PRE = 2u << 30;
 constexpr uint32_t LB_MASK = (1u << 30) - 1;
 
+__device__ __forceinline__ void lb_publish(uint32_t* p, uint32_t w)
+{
+    *reinterpret_cast<volatile uint32_t*>(p) = w;
+}
+
+// Warp-cooperative decoupled look-back (all 32 lanes of one warp call it).
+// Tiles [first, tile) precede `tile` in its chain; tile j's flag word is at
+// lb[j * stride].  Each step inspects 32 predecessors at once and stops at the
+// nearest inclusive prefix (LB_PRE); tiles before `first` count as a prefix of
+// 0.  Returns the exclusive prefix of `tile` (identical in every lane).
+__device__ __forceinline__ uint32_t warp_lookback(const uint32_t* lb, long long stride, int tile,
+                                                  int first)
+{
+    const int lane = threadIdx.x & 31;
+    uint32_t excl = 0;
+    int j = tile - 1;
+    while (j >= first) {
+        const int jj = j - lane;
+        uint32_t w = LB_PRE;
+        if (jj >= first) {
+            const volatile uint32_t* p = lb + (long long)jj * stride;
+            do {
+                w = *p;
+            } while ((w >> 30) == 0);
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (w & LB_PRE) != 0);
+        const int last = pre ? (__ffs(pre) - 1) : 31;
+        uint32_t c = (lane <= last) ? (w & LB_MASK) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        excl += c;
+        if (pre) break;
+        j -= 32;
+    }
+    return excl;
+}
+
 // Per-Gaussian flag bits (debug dump; same meaning as the header)
 constexpr uint8_t F_TEMPORAL = 1, F_VISIBLE = 2, F_SMALL = 4, F_DROPPED = 8,
                   F_RENDERED = 16, F_BADID = 32;
@@ -161,6 +198,7 @@ struct RasterArgs {
     const unsigned long long* pairs;
     const float4* rec_sorted;
     unsigned long long* evals;   // [n_views][2] (E_alg, E_exec) or NULL
+    float exp2_c0;               // 1.535336188319500e-4f (set by launch_raster)
 };
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 
