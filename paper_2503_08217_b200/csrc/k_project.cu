@@ -1,6 +1,7 @@
 // k_project.cu — K2: instance-specific projection + EWA covariance + frustum
-// mask M_t + Adaptive-LOD cull + point-life update, with ordered compaction of
-// the rendered splats of every view; plus the instance-camera composition.
+// mask M_t + Adaptive-LOD cull + point-life update, with compaction of the
+// rendered splats of every view; plus the instance-camera composition, the
+// depth-tie fix-up of K5a and the K9 commit / reset / life-flip kernels.
 //
 // PAPER.md P:158-159 (instance-specific projection: W_{t,i} = W_t W_{t,i2g},
 // "we simply select the corresponding cameras based on the Gaussian's instance
@@ -12,22 +13,23 @@
 // Arithmetic: the fp32 R-ARITH contract of DESIGN.md, op for op (this file is
 // compiled with -fmad=false; FMAs are the explicit __fmaf_rn below).
 //
-// Layout: one CTA = 512 consecutive entries of one view's temporal index list
-// (2 per thread, coalesced 4-byte index loads, then 16-byte gathers of the
-// SoA float4 streams).  The view's (K+1) x 3x4 camera table is staged in
-// shared memory.  Rendered splats are compacted in index order (ballot/popc
-// within the CTA, decoupled look-back across the view's CTAs) into 48-byte
-// records {mx,my,z,o}{A,B,C,rect.x}{r,g,b,rect.y} plus a 4-byte depth key.
+// Layout: grid (CTA, view); one CTA walks 4 x 256 consecutive entries of its
+// view's temporal index list (coalesced 4-byte index loads, then 16-byte
+// gathers of the SoA float4 streams).  The view's (K+1) x 3x4 camera table is
+// staged in shared memory once per CTA.  Rendered splats are compacted with
+// ballot/popc inside the CTA and ONE atomic per CTA-round on the view's
+// counter, into 48-byte records {mx,my,z,o}{qa,qb,qc,rect.x}{r,g,b,rect.y}, a
+// 4-byte depth key and the 4-byte Gaussian index.  The record order is
+// therefore not deterministic; the depth sort (K5a) plus k_depth_ties restore
+// the unique (depth, index) order, so everything downstream is deterministic.
 #include "s3r_internal.cuh"
 
 namespace s3r {
 
 namespace {
 constexpr int PT = 256;
-constexpr int PITEMS = 1;
-constexpr int PTILE = PT * PITEMS;
-constexpr int PGROUPS = PITEMS * (PT / 32);   // 16
-
+constexpr int PR = 4;                 // rounds of PT entries per CTA
+constexpr int PTILE = PT * PR;
 
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x)
 {
@@ -58,7 +60,7 @@ struct Splat {
 };
 
 // O2 + O3 + O4 of DESIGN.md for Gaussian g in view V; M = the 12 floats of
-// its instance camera.  Returns flags.
+// its instance camera.  Sets s.flags.
 __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 mo, float4 sc,
                                             float4 q, const DevView& V, float lox, float hix,
                                             float loy, float hiy, long long g, Splat& s)
@@ -187,28 +189,17 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
 __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
 {
     extern __shared__ float s_tab[];          // [K1][12]
-    __shared__ int s_gtile, s_view;
     __shared__ float s_bounds[4];
-    __shared__ uint32_t s_grp[PGROUPS];
+    __shared__ uint32_t s_wcnt[PT / 32];
     __shared__ uint32_t s_base;
     __shared__ unsigned long long s_red[5][PT / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        int gt = atomicAdd(a.ticket, 1);
-        // view = last v with view_tile0[v] <= gt
-        int lo = 0, hi = a.n_views - 1;
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (a.view_tile0[mid] <= gt) lo = mid; else hi = mid - 1;
-        }
-        s_gtile = gt;
-        s_view = lo;
-    }
-    __syncthreads();
-    const int gtile = s_gtile, vi = s_view;
-    const DevView V = a.views[vi];
-    const int ltile = gtile - a.view_tile0[vi];
+    const int vi = blockIdx.y;
+    const DevView& V = a.views[vi];
+    const long long n_t = V.n_temporal;
+    const long long i0 = (long long)blockIdx.x * PTILE;
+    if (i0 >= n_t) return;                    // uniform for the CTA
     const int K1 = a.num_instances;
     for (int i = tid; i < K1 * 12; i += PT) s_tab[i] = V.table[i];
     if (tid == 0) {
@@ -222,72 +213,98 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
     __syncthreads();
     const float lox = s_bounds[0], hix = s_bounds[1], loy = s_bounds[2], hiy = s_bounds[3];
     const int32_t* tl = a.tidx + (long long)V.tslot * a.idx_stride;
+    const long long cap_off = V.cap_off;
+    const float t = V.t;
+    uint8_t* vis_out = V.visible;
+    ViewCounters* ctr = a.counters + vi;
+    const unsigned lt = (1u << lane) - 1u;
 
-    Splat sp[PITEMS];
-    long long gg[PITEMS];
-    float4 col[PITEMS];
     unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0;
-#pragma unroll
-    for (int k = 0; k < PITEMS; ++k) {
-        const long long i = (long long)ltile * PTILE + k * PT + tid;
-        sp[k].flags = 0;
-        gg[k] = -1;
-        if (i < V.n_temporal) {
-            const long long g = tl[i];
-            gg[k] = g;
+    for (int rd = 0; rd < PR; ++rd) {
+        const long long i = i0 + rd * PT + tid;
+        Splat sp;
+        sp.flags = 0;
+        long long g = -1;
+        float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < n_t) {
+            g = tl[i];
             const int id = __ldg(a.ids + g);
             if (id < 0 || id >= K1) {
-                sp[k].flags = F_TEMPORAL | F_BADID;
+                sp.flags = F_TEMPORAL | F_BADID;
 #pragma unroll
-                for (int j = 0; j < 6; ++j) sp[k].k[j] = __int_as_float(0x7fc00000);
+                for (int j = 0; j < 6; ++j) sp.k[j] = __int_as_float(0x7fc00000);
                 c_bad++;
             } else {
                 const float4 mo = __ldg(a.means_opacity + g);
                 const float4 sc = __ldg(a.scales + g);
                 const float4 q = __ldg(a.rotations + g);
-                project_one(s_tab + 12 * id, mo, sc, q, V, lox, hix, loy, hiy, g, sp[k]);
-                if (sp[k].flags & F_VISIBLE) {
+                project_one(s_tab + 12 * id, mo, sc, q, V, lox, hix, loy, hiy, g, sp);
+                if (sp.flags & F_VISIBLE) {
                     c_vis++;
-                    if (V.visible) V.visible[g] = 1;
+                    if (vis_out) vis_out[g] = 1;
                     if (a.life) {
-                        float2 l = a.life[g];
+                        const float2 l = a.life[g];
                         float* lp = reinterpret_cast<float*>(a.life + g);
-                        if (V.t < l.x) atomic_min_f(lp, V.t);
-                        if (V.t > l.y) atomic_max_f(lp + 1, V.t);
+                        if (t < l.x) atomic_min_f(lp, t);
+                        if (t > l.y) atomic_max_f(lp + 1, t);
                     }
                 }
-                if (sp[k].flags & F_SMALL) c_small++;
-                if (sp[k].flags & F_DROPPED) c_drop++;
-                if (sp[k].flags & F_RENDERED) {
-                    col[k] = __ldg(a.colors + g);
-                    c_pairs += (unsigned long long)(sp[k].tx1 - sp[k].tx0 + 1) *
-                               (unsigned long long)(sp[k].ty1 - sp[k].ty0 + 1);
-                    col[k].w = mo.w;   // opacity travels in the record
+                if (sp.flags & F_SMALL) c_small++;
+                if (sp.flags & F_DROPPED) c_drop++;
+                if (sp.flags & F_RENDERED) {
+                    col = __ldg(a.colors + g);
+                    col.w = mo.w;    // opacity travels in the record
+                    c_pairs += (unsigned long long)(sp.tx1 - sp.tx0 + 1) *
+                               (unsigned long long)(sp.ty1 - sp.ty0 + 1);
                 }
             }
             if (a.dbg_flags) {
                 const long long di = V.dbg_off + i;
-                a.dbg_flags[di] = sp[k].flags;
+                a.dbg_flags[di] = sp.flags;
 #pragma unroll
-                for (int j = 0; j < 6; ++j) a.dbg_keys[6 * di + j] = sp[k].k[j];
-                const bool vis = sp[k].flags & F_VISIBLE;
-                a.dbg_rect[4 * di + 0] = (int16_t)(vis ? sp[k].tx0 : 0);
-                a.dbg_rect[4 * di + 1] = (int16_t)(vis ? sp[k].tx1 : 0);
-                a.dbg_rect[4 * di + 2] = (int16_t)(vis ? sp[k].ty0 : 0);
-                a.dbg_rect[4 * di + 3] = (int16_t)(vis ? sp[k].ty1 : 0);
+                for (int j = 0; j < 6; ++j) a.dbg_keys[6 * di + j] = sp.k[j];
+                const bool vis = sp.flags & F_VISIBLE;
+                a.dbg_rect[4 * di + 0] = (int16_t)(vis ? sp.tx0 : 0);
+                a.dbg_rect[4 * di + 1] = (int16_t)(vis ? sp.tx1 : 0);
+                a.dbg_rect[4 * di + 2] = (int16_t)(vis ? sp.ty0 : 0);
+                a.dbg_rect[4 * di + 3] = (int16_t)(vis ? sp.ty1 : 0);
             }
         }
-    }
-
-    // ---- ordered compaction of rendered splats ----
-    const unsigned lt = (1u << lane) - 1u;
-    unsigned bal[PITEMS];
+        // ---- compaction: ballot/popc in the CTA, one atomic per CTA-round ----
+        const bool rend = (sp.flags & F_RENDERED) != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, rend);
+        if (lane == 0) s_wcnt[warp] = __popc(bal);
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t c = lane < PT / 32 ? s_wcnt[lane] : 0u;
+            uint32_t x = c;
 #pragma unroll
-    for (int k = 0; k < PITEMS; ++k) {
-        bal[k] = __ballot_sync(0xffffffffu, (sp[k].flags & F_RENDERED) != 0);
-        if (lane == 0) s_grp[k * (PT / 32) + warp] = __popc(bal[k]);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane < PT / 32) s_wcnt[lane] = x - c;
+            const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+            if (lane == 0)
+                s_base = tot ? (uint32_t)atomicAdd(&ctr->n_rendered, (unsigned long long)tot) : 0u;
+        }
+        __syncthreads();
+        if (rend) {
+            const long long o = cap_off + s_base + s_wcnt[warp] + __popc(bal & lt);
+            const uint32_t rx = (uint32_t)sp.tx0 | ((uint32_t)sp.tx1 << 16);
+            const uint32_t ry = (uint32_t)sp.ty0 | ((uint32_t)sp.ty1 << 16);
+            float4* r = a.rec + 3 * o;
+            r[0] = make_float4(sp.k[0], sp.k[1], sp.k[2], col.w);
+            // exp2-form blend coefficients (R-ARITH): qa = A (-log2e/2), qb = B (-log2e),
+            // qc = C (-log2e/2)
+            r[1] = make_float4(sp.A * -0x1.715476p-1f, sp.B * -0x1.715476p+0f,
+                               sp.C * -0x1.715476p-1f, __uint_as_float(rx));
+            r[2] = make_float4(col.x, col.y, col.z, __uint_as_float(ry));
+            a.dkey[o] = __float_as_uint(sp.k[2]);
+            a.gidx[o] = (int32_t)g;
+        }
     }
-    // counters: warp reduce
+    // ---- per-view counters: one set of atomics per CTA ----
     unsigned long long cv[5] = {c_vis, c_small, c_drop, c_pairs, c_bad};
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
@@ -297,56 +314,47 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
         if (lane == 0) s_red[j][warp] = x;
     }
     __syncthreads();
-    if (warp == 0) {
-        uint32_t c = lane < PGROUPS ? s_grp[lane] : 0;
-        uint32_t x = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane < PGROUPS) s_grp[lane] = x - c;
-        const uint32_t agg = __shfl_sync(0xffffffffu, x, 31);
-        // decoupled look-back over the view's preceding CTAs (warp-cooperative)
-        uint32_t* lb = a.lookback;
-        const int first = gtile - ltile;
-        if (lane == 0) lb_publish(lb + gtile, (ltile == 0 ? LB_PRE : LB_AGG) | agg);
-        const uint32_t excl = (ltile == 0) ? 0u : warp_lookback(lb, 1, gtile, first);
-        if (lane == 0) {
-            if (ltile != 0) lb_publish(lb + gtile, LB_PRE | (excl + agg));
-            s_base = excl;
-        }
-        if (lane == 1) {
-            ViewCounters* ctr = a.counters + vi;
-            unsigned long long t5[5] = {0, 0, 0, 0, 0};
-            for (int w = 0; w < PT / 32; ++w)
-                for (int j = 0; j < 5; ++j) t5[j] += s_red[j][w];
-            if (t5[0]) atomicAdd(&ctr->n_visible, t5[0]);
-            if (t5[1]) atomicAdd(&ctr->n_small, t5[1]);
-            if (t5[2]) atomicAdd(&ctr->n_dropped, t5[2]);
-            if (t5[3]) atomicAdd(&ctr->n_pairs, t5[3]);
-            if (t5[4]) { atomicAdd(&ctr->n_bad, t5[4]); atomicOr(a.err, ERR_BADID); }
-            if (agg) atomicAdd(&ctr->n_rendered, (unsigned long long)agg);
+    if (tid == 0) {
+        unsigned long long t5[5] = {0, 0, 0, 0, 0};
+        for (int w = 0; w < PT / 32; ++w)
+            for (int j = 0; j < 5; ++j) t5[j] += s_red[j][w];
+        if (t5[0]) atomicAdd(&ctr->n_visible, t5[0]);
+        if (t5[1]) atomicAdd(&ctr->n_small, t5[1]);
+        if (t5[2]) atomicAdd(&ctr->n_dropped, t5[2]);
+        if (t5[3]) atomicAdd(&ctr->n_pairs, t5[3]);
+        if (t5[4]) {
+            atomicAdd(&ctr->n_bad, t5[4]);
+            atomicOr(a.err, ERR_BADID);
         }
     }
-    __syncthreads();
-    const long long base = V.cap_off + s_base;
-#pragma unroll
-    for (int k = 0; k < PITEMS; ++k) {
-        if (sp[k].flags & F_RENDERED) {
-            const long long o = base + s_grp[k * (PT / 32) + warp] + __popc(bal[k] & lt);
-            const uint32_t rx = (uint32_t)sp[k].tx0 | ((uint32_t)sp[k].tx1 << 16);
-            const uint32_t ry = (uint32_t)sp[k].ty0 | ((uint32_t)sp[k].ty1 << 16);
-            float4* r = a.rec + 3 * o;
-            r[0] = make_float4(sp[k].k[0], sp[k].k[1], sp[k].k[2], col[k].w);
-            // exp2-form blend coefficients (R-ARITH): qa = A (-log2e/2), qb = B (-log2e),
-            // qc = C (-log2e/2)
-            r[1] = make_float4(sp[k].A * -0x1.715476p-1f, sp[k].B * -0x1.715476p+0f,
-                               sp[k].C * -0x1.715476p-1f, __uint_as_float(rx));
-            r[2] = make_float4(col[k].x, col[k].y, col[k].z, __uint_as_float(ry));
-            a.dkey[o] = __float_as_uint(sp[k].k[2]);
-            if (a.gidx) a.gidx[o] = (int32_t)gg[k];
+}
+
+// After K5a (stable LSD on depth bits) the splats of one view are ordered by
+// depth, but equal depths keep K2's non-deterministic compaction order.  The
+// head of every run of equal keys sorts the run by Gaussian index (insertion
+// sort; runs are rare and short), giving the unique (depth, index) order of
+// reading R11.  Grid: (CTA over positions, view).
+__global__ void k_depth_ties(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                             const int32_t* __restrict__ gidx, const Seg* __restrict__ segs)
+{
+    const Seg S = segs[blockIdx.y];
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r + 1 >= S.count) return;
+    const uint32_t k = keys[S.base + r];
+    if (keys[S.base + r + 1] != k) return;
+    if (r > 0 && keys[S.base + r - 1] == k) return;       // not the head of the run
+    long long e = r + 2;
+    while (e < S.count && keys[S.base + e] == k) ++e;
+    uint32_t* v = vals + S.base;
+    for (long long x = r + 1; x < e; ++x) {
+        const uint32_t cur = v[x];
+        const int32_t gc = gidx[S.base + cur];
+        long long y = x - 1;
+        while (y >= r && gidx[S.base + v[y]] > gc) {
+            v[y + 1] = v[y];
+            --y;
         }
+        v[y + 1] = cur;
     }
 }
 
@@ -413,14 +421,23 @@ __global__ void k_life_flip(float2* __restrict__ life, long long n)
 
 void launch_project(const ProjectArgs& a, cudaStream_t st)
 {
-    if (a.total_tiles == 0) return;
+    if (a.max_tiles == 0 || a.n_views == 0) return;
     const size_t smem = (size_t)a.num_instances * 12 * sizeof(float);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_project<<<a.total_tiles, PT, smem, st>>>(a);
+    dim3 grid(a.max_tiles, a.n_views);
+    k_project<<<grid, PT, smem, st>>>(a);
 }
 
 int project_tile() { return PTILE; }
+
+void launch_depth_ties(const uint32_t* keys, uint32_t* vals, const int32_t* gidx, const Seg* segs,
+                       int nsegs, long long max_count, cudaStream_t st)
+{
+    if (nsegs == 0 || max_count < 2) return;
+    dim3 grid((unsigned)((max_count + 255) / 256), nsegs);
+    k_depth_ties<<<grid, 256, 0, st>>>(keys, vals, gidx, segs);
+}
 
 void launch_compose(const float* w2c, const float* i2g, int n_views, int K, float* out,
                     cudaStream_t st)

@@ -306,39 +306,32 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
 
     // ================= K2: projection + LOD + life + compaction
     long long cap = 0;
-    std::vector<int> vtile0(nv + 1, 0);
+    int k2_tiles = 0;          // grid.x of K2 (grid.y = views)
     for (int v = 0; v < nv; ++v) {
         DevView& d = c->hv[v];
         d.n_temporal = (long long)h_counts[d.tslot];
         d.cap_off = cap;
         d.dbg_off = cap;
         cap += d.n_temporal;
-        vtile0[v + 1] = vtile0[v] + (int)((d.n_temporal + project_tile() - 1) / project_tile());
+        k2_tiles = std::max(k2_tiles, (int)((d.n_temporal + project_tile() - 1) / project_tile()));
     }
     const long long capS = std::max<long long>(cap, 1);
-    const int k2_tiles = vtile0[nv];
     if ((rc = ensure(c, c->d_rec, (size_t)capS * 48))) return rc;
     if ((rc = ensure(c, c->d_dkey, (size_t)capS * 4))) return rc;
+    if ((rc = ensure(c, c->d_gidx, (size_t)capS * 4))) return rc;
     if (c->debug) {
-        if ((rc = ensure(c, c->d_gidx, (size_t)capS * 4))) return rc;
         if ((rc = ensure(c, c->d_dbg_keys, (size_t)capS * 24))) return rc;
         if ((rc = ensure(c, c->d_dbg_flags, (size_t)capS))) return rc;
         if ((rc = ensure(c, c->d_dbg_rect, (size_t)capS * 8))) return rc;
     }
     if ((rc = ensure(c, c->d_views, (size_t)std::max(nv, 1) * sizeof(DevView)))) return rc;
-    if ((rc = ensure(c, c->d_tile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
     if ((rc = ensure(c, c->d_ctr, (size_t)std::max(nv, 1) * sizeof(ViewCounters)))) return rc;
     DevView* h_views = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
     std::memcpy(h_views, c->hv.data(), (size_t)nv * sizeof(DevView));
-    int* h_t0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
-    std::memcpy(h_t0, vtile0.data(), (size_t)(nv + 1) * sizeof(int));
     if (nv) {
         CU(cudaMemcpyAsync(c->d_views.p, h_views, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_tile0.p, h_t0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
         CU(cudaMemsetAsync(c->d_ctr.p, 0, nv * sizeof(ViewCounters), st));
     }
-    if ((rc = ensure(c, c->d_lb, (size_t)std::max(k2_tiles, 1) * sizeof(uint32_t)))) return rc;
-    CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)std::max(k2_tiles, 1) * sizeof(uint32_t), st));
     for (int v = 0; v < nv; ++v)
         if (outs[v].visible && N > 0) CU(cudaMemsetAsync(outs[v].visible, 0, (size_t)N, st));
     {
@@ -355,14 +348,11 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.n_views = nv;
         a.tidx = P<int32_t>(c->d_tidx);
         a.idx_stride = Ns;
-        a.view_tile0 = P<int>(c->d_tile0);
-        a.total_tiles = k2_tiles;
+        a.max_tiles = k2_tiles;
         a.rec = P<float4>(c->d_rec);
         a.dkey = P<uint32_t>(c->d_dkey);
-        a.gidx = c->debug ? P<int32_t>(c->d_gidx) : nullptr;
+        a.gidx = P<int32_t>(c->d_gidx);
         a.counters = P<ViewCounters>(c->d_ctr);
-        a.lookback = P<uint32_t>(c->d_lb);
-        a.ticket = next_ticket(c);
         a.err = P<uint32_t>(c->d_err);
         a.dbg_keys = c->debug ? P<float>(c->d_dbg_keys) : nullptr;
         a.dbg_flags = c->debug ? P<uint8_t>(c->d_dbg_flags) : nullptr;
@@ -487,6 +477,11 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
             vin = P<uint32_t>(c->d_sortv[o]);
         }
         c->final_order = 1;   // pass 3 wrote buffer 1
+        // equal depths: restore ascending Gaussian index inside each run
+        long long max_r = 0;
+        for (int v = 0; v < nv; ++v) max_r = std::max(max_r, c->hv[v].n_rendered);
+        launch_depth_ties(P<uint32_t>(c->d_sortk[1]), P<uint32_t>(c->d_sortv[1]),
+                          P<int32_t>(c->d_gidx), P<Seg>(c->d_dsegs), nv, max_r, st);
         ev_end(c, st, e);
     }
     CU(cudaGetLastError());

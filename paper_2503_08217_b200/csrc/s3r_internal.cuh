@@ -129,15 +129,12 @@ struct ProjectArgs {
     int n_views;
     const int32_t* tidx;         // [T][idx_stride]
     long long idx_stride;
-    const int* view_tile0;       // [n_views+1] first K2 tile per view
-    int total_tiles;
+    int max_tiles;               // grid.x: max over views of ceil(n_temporal / project_tile)
     // outputs
-    float4* rec;                 // [cap][3] splat records (unsorted, compacted)
+    float4* rec;                 // [cap][3] splat records (compacted, unordered)
     uint32_t* dkey;              // [cap] depth bits
-    int32_t* gidx;               // [cap] Gaussian index (debug) or NULL
-    ViewCounters* counters;      // [n_views]
-    uint32_t* lookback;          // [total_tiles]
-    int* ticket;
+    int32_t* gidx;               // [cap] Gaussian index
+    ViewCounters* counters;      // [n_views]; n_rendered is the compaction cursor
     uint32_t* err;
     // debug (NULL when off)
     float* dbg_keys;
@@ -145,6 +142,10 @@ struct ProjectArgs {
     int16_t* dbg_rect;
 };
 void launch_project(const ProjectArgs& a, cudaStream_t st);
+int project_tile();
+// Restore (depth, Gaussian index) order inside runs of equal depth keys.
+void launch_depth_ties(const uint32_t* keys, uint32_t* vals, const int32_t* gidx, const Seg* segs,
+                       int nsegs, long long max_count, cudaStream_t st);
 
 // Segmented LSD radix sort helpers (onesweep with decoupled look-back).
 // keys: u32 (depth) or u64 (pair words).  digit = (key >> shift) & 255.

@@ -141,6 +141,21 @@ def test_life_update_and_commit(ctx):
     assert np.array_equal(ds.visibility.cpu().numpy(), ref.visibility)
 
 
+def test_equal_depth_ties(ctx):
+    """Many Gaussians at exactly the same camera depth (a fronto-parallel plane
+    seen by an identity camera): the order must still be (depth, index)."""
+    rng = np.random.default_rng(5)
+    n = 6000
+    pts = np.stack([rng.uniform(-3, 3, n), rng.uniform(-2, 2, n), np.full(n, 5.0)], 1)
+    pts[::3, 2] = 7.0
+    s = make_scene(pts, np.exp(rng.uniform(-4, -1.5, (n, 3))), opacity=rng.uniform(0.05, 0.9, n),
+                   rgb=rng.random((n, 3)))
+    v = make_view(200.0, 100.0, 203, 150)
+    _, tabs, outs, rc = gpu_render(ctx, s, [v])
+    o = check_view(ctx, s, v, tabs[0], outs[0], 0)
+    assert o["stats"]["n_rendered"] > 3000
+
+
 def test_life_flip_kernel(ctx):
     life = torch.tensor([[0.25, 0.5], [1.0, -1.0], [-0.75, 0.0]], device="cuda")
     ref = life.clone()
