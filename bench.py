@@ -124,6 +124,8 @@ class ClockSampler:
 
 
 def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
+    # depth sort passes over (depth bits << gbits | index): 32 + bits(N) key bits
+    depth_passes = math.ceil((32 + max(1, (max(n_scene, 2) - 1).bit_length())) / 8)
     """Algorithmic bytes per stage for one batch (DESIGN.md §Roofline)."""
     Nt = sum(s["n_temporal"] for s in stats)
     Nv = sum(s["n_visible"] for s in stats)
@@ -135,8 +137,8 @@ def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
     nt_distinct = sum({v.t: s["n_temporal"] for v, s in zip(views, stats)}.values())
     return {
         "filter": 8 * n_scene * math.ceil(max(n_distinct_t, 1) / 64) + 4 * nt_distinct,
-        "project": 56 * Nt + 8 * Nv + (16 + 48 + 4) * Nr,
-        "depth_sort": 4 * Nr + 4 * 16 * Nr,
+        "project": 56 * Nt + 8 * Nv + (16 + 48 + 8) * Nr,
+        "depth_sort": 8 * Nr + depth_passes * 24 * Nr,
         "emit": (4 + 48 + 48) * Nr + 8 * P,
         "pair_sort": 8 * P + pair_passes * 16 * P,
         "ranges": 8 * P + 8 * tiles,

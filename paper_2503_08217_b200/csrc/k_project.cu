@@ -1,7 +1,7 @@
 // k_project.cu — K2: instance-specific projection + EWA covariance + frustum
 // mask M_t + Adaptive-LOD cull + point-life update, with compaction of the
-// rendered splats of every view; plus the instance-camera composition, the
-// depth-tie fix-up of K5a and the K9 commit / reset / life-flip kernels.
+// rendered splats of every view; plus the instance-camera composition and the
+// K9 commit / reset / life-flip kernels.
 //
 // PAPER.md P:158-159 (instance-specific projection: W_{t,i} = W_t W_{t,i2g},
 // "we simply select the corresponding cameras based on the Gaussian's instance
@@ -19,8 +19,8 @@
 // staged in shared memory once per CTA.  Rendered splats are compacted with
 // ballot/popc inside the CTA and ONE atomic per CTA-round on the view's
 // counter, into 48-byte records {mx,my,z,o}{qa,qb,qc,rect.x}{r,g,b,rect.y}, a
-// 4-byte depth key and the 4-byte Gaussian index.  The record order is
-// therefore not deterministic; the depth sort (K5a) plus k_depth_ties restore
+// 64-bit depth key (depth bits << gbits | Gaussian index).  The record order
+// is therefore not deterministic; the depth sort (K5a) on those keys restores
 // the unique (depth, index) order, so everything downstream is deterministic.
 #include "s3r_internal.cuh"
 
@@ -300,8 +300,11 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
             r[1] = make_float4(sp.A * -0x1.715476p-1f, sp.B * -0x1.715476p+0f,
                                sp.C * -0x1.715476p-1f, __uint_as_float(rx));
             r[2] = make_float4(col.x, col.y, col.z, __uint_as_float(ry));
-            a.dkey[o] = __float_as_uint(sp.k[2]);
-            a.gidx[o] = (int32_t)g;
+            // depth-sort key (reading R11): depth bits above the Gaussian index,
+            // so the order is (depth, index) whatever the compaction order was
+            a.dkey[o] = ((unsigned long long)__float_as_uint(sp.k[2]) << a.gbits) |
+                        (unsigned long long)g;
+            if (a.gidx) a.gidx[o] = (int32_t)g;
         }
     }
     // ---- per-view counters: one set of atomics per CTA ----
@@ -326,35 +329,6 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
             atomicAdd(&ctr->n_bad, t5[4]);
             atomicOr(a.err, ERR_BADID);
         }
-    }
-}
-
-// After K5a (stable LSD on depth bits) the splats of one view are ordered by
-// depth, but equal depths keep K2's non-deterministic compaction order.  The
-// head of every run of equal keys sorts the run by Gaussian index (insertion
-// sort; runs are rare and short), giving the unique (depth, index) order of
-// reading R11.  Grid: (CTA over positions, view).
-__global__ void k_depth_ties(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             const int32_t* __restrict__ gidx, const Seg* __restrict__ segs)
-{
-    const Seg S = segs[blockIdx.y];
-    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r + 1 >= S.count) return;
-    const uint32_t k = keys[S.base + r];
-    if (keys[S.base + r + 1] != k) return;
-    if (r > 0 && keys[S.base + r - 1] == k) return;       // not the head of the run
-    long long e = r + 2;
-    while (e < S.count && keys[S.base + e] == k) ++e;
-    uint32_t* v = vals + S.base;
-    for (long long x = r + 1; x < e; ++x) {
-        const uint32_t cur = v[x];
-        const int32_t gc = gidx[S.base + cur];
-        long long y = x - 1;
-        while (y >= r && gidx[S.base + v[y]] > gc) {
-            v[y + 1] = v[y];
-            --y;
-        }
-        v[y + 1] = cur;
     }
 }
 
@@ -430,14 +404,6 @@ void launch_project(const ProjectArgs& a, cudaStream_t st)
 }
 
 int project_tile() { return PTILE; }
-
-void launch_depth_ties(const uint32_t* keys, uint32_t* vals, const int32_t* gidx, const Seg* segs,
-                       int nsegs, long long max_count, cudaStream_t st)
-{
-    if (nsegs == 0 || max_count < 2) return;
-    dim3 grid((unsigned)((max_count + 255) / 256), nsegs);
-    k_depth_ties<<<grid, 256, 0, st>>>(keys, vals, gidx, segs);
-}
 
 void launch_compose(const float* w2c, const float* i2g, int n_views, int K, float* out,
                     cudaStream_t st)

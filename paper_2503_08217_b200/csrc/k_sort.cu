@@ -258,6 +258,18 @@ void launch_onesweep32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
         shift);
 }
 
+void launch_onesweep64kv(const unsigned long long* kin, const uint32_t* vin,
+                         unsigned long long* kout, uint32_t* vout, const Seg* segs, int nsegs,
+                         const int* seg_tile0, int total_tiles, const uint32_t* digit_base,
+                         int pass, int npasses, uint32_t* lookback, int* ticket, int shift,
+                         cudaStream_t st)
+{
+    if (total_tiles == 0) return;
+    k_onesweep<unsigned long long, true, ITEMS64><<<total_tiles, ST, 0, st>>>(
+        kin, vin, kout, vout, segs, nsegs, seg_tile0, digit_base, pass, npasses, lookback, ticket,
+        shift);
+}
+
 void launch_onesweep64(const unsigned long long* kin, unsigned long long* kout, const Seg* segs,
                        int nsegs, const int* seg_tile0, int total_tiles,
                        const uint32_t* digit_base, int pass, int npasses, uint32_t* lookback,

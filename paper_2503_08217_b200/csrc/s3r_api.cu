@@ -56,6 +56,7 @@ struct s3r_ctx {
         d_psegs, d_ptile0, d_ranges, d_range_off, d_vpo, d_err, d_dbg_keys, d_dbg_flags,
         d_dbg_rect;
     int ticket_slot = 0;
+    int gbits = 1;
     // mirrors for s3r_render_batch_host
     Buf m_scene[7];
     std::vector<Buf> m_tab, m_rgb, m_depth, m_T, m_vis;
@@ -232,6 +233,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->N_last = N;
     c->ticket_slot = 0;
     c->last_debug = c->debug;
+    c->gbits = bits_for(std::max<long long>(N, 2));   // Gaussian-index bits of the depth key
 
     // ---- distinct times (views sharing t share K1's compaction)
     std::vector<float> tk;
@@ -317,8 +319,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     }
     const long long capS = std::max<long long>(cap, 1);
     if ((rc = ensure(c, c->d_rec, (size_t)capS * 48))) return rc;
-    if ((rc = ensure(c, c->d_dkey, (size_t)capS * 4))) return rc;
-    if ((rc = ensure(c, c->d_gidx, (size_t)capS * 4))) return rc;
+    if ((rc = ensure(c, c->d_dkey, (size_t)capS * 8))) return rc;
+    if (c->debug && (rc = ensure(c, c->d_gidx, (size_t)capS * 4))) return rc;
     if (c->debug) {
         if ((rc = ensure(c, c->d_dbg_keys, (size_t)capS * 24))) return rc;
         if ((rc = ensure(c, c->d_dbg_flags, (size_t)capS))) return rc;
@@ -350,8 +352,9 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.idx_stride = Ns;
         a.max_tiles = k2_tiles;
         a.rec = P<float4>(c->d_rec);
-        a.dkey = P<uint32_t>(c->d_dkey);
-        a.gidx = P<int32_t>(c->d_gidx);
+        a.dkey = P<unsigned long long>(c->d_dkey);
+        a.gbits = c->gbits;
+        a.gidx = c->debug ? P<int32_t>(c->d_gidx) : nullptr;
         a.counters = P<ViewCounters>(c->d_ctr);
         a.err = P<uint32_t>(c->d_err);
         a.dbg_keys = c->debug ? P<float>(c->d_dbg_keys) : nullptr;
@@ -374,7 +377,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->range_off.assign(nv + 1, 0);
     int max_tiles = 0;
     bool bad = false;
-    const int stile = onesweep32_tile();
+    const int stile = onesweep64_tile();
     for (int v = 0; v < nv; ++v) {
         DevView& d = c->hv[v];
         const ViewCounters& k = h_ctr[v];
@@ -444,44 +447,41 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         CU(cudaMemcpyAsync(c->d_views.p, h_views2, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
     }
     for (int i = 0; i < 2; ++i) {
-        if ((rc = ensure(c, c->d_sortk[i], (size_t)capS * 4))) return rc;
+        if ((rc = ensure(c, c->d_sortk[i], (size_t)capS * 8))) return rc;
         if ((rc = ensure(c, c->d_sortv[i], (size_t)capS * 4))) return rc;
         if ((rc = ensure(c, c->d_pairs[i], (size_t)std::max<long long>(total_pairs, 1) * 8))) return rc;
     }
     if ((rc = ensure(c, c->d_recs, (size_t)capS * 48))) return rc;
-    const int hpasses = std::max(4, ppasses);
+    const int dpasses = (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS;
+    const int hpasses = std::max(dpasses, ppasses);
     if ((rc = ensure(c, c->d_hist, (size_t)std::max(nv, 1) * hpasses * RADIX * 4))) return rc;
     if ((rc = ensure(c, c->d_ranges, (size_t)std::max(c->range_off[nv], 1) * sizeof(int2)))) return rc;
     const size_t lb_need = (size_t)std::max({(long long)dtiles * RADIX, (long long)ptiles * RADIX,
                                              (long long)etiles, 1ll}) * sizeof(uint32_t);
     if ((rc = ensure(c, c->d_lb, lb_need))) return rc;
 
-    // ================= K5a: depth sort (4 x 8-bit passes over bits(z), values j)
+    // ================= K5a: depth sort: 8-bit LSD passes over (depth << gbits | index),
+    // values = compacted slot j; gives the unique (depth, index) order (R11)
     {
         StageEvent e;
         ev_begin(c, S3R_STAGE_DEPTH_SORT, st, e);
-        CU(cudaMemsetAsync(c->d_hist.p, 0, (size_t)std::max(nv, 1) * 4 * RADIX * 4, st));
-        launch_hist32(P<uint32_t>(c->d_dkey), P<Seg>(c->d_dsegs), nv, P<int>(c->d_dtile0), dtiles,
-                      4, P<uint32_t>(c->d_hist), st);
-        launch_hist_scan(P<uint32_t>(c->d_hist), nv, 4, st);
-        const uint32_t* kin = P<uint32_t>(c->d_dkey);
+        CU(cudaMemsetAsync(c->d_hist.p, 0, (size_t)std::max(nv, 1) * dpasses * RADIX * 4, st));
+        launch_hist64(P<unsigned long long>(c->d_dkey), P<Seg>(c->d_dsegs), nv,
+                      P<int>(c->d_dtile0), dtiles, 0, dpasses, P<uint32_t>(c->d_hist), st);
+        launch_hist_scan(P<uint32_t>(c->d_hist), nv, dpasses, st);
+        const unsigned long long* kin = P<unsigned long long>(c->d_dkey);
         const uint32_t* vin = nullptr;
-        for (int pass = 0; pass < 4; ++pass) {
+        for (int pass = 0; pass < dpasses; ++pass) {
             const int o = pass & 1;
             if (dtiles) CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)dtiles * RADIX * 4, st));
-            launch_onesweep32(kin, vin, P<uint32_t>(c->d_sortk[o]), P<uint32_t>(c->d_sortv[o]),
-                              P<Seg>(c->d_dsegs), nv, P<int>(c->d_dtile0), dtiles,
-                              P<uint32_t>(c->d_hist), pass, 4, P<uint32_t>(c->d_lb),
-                              next_ticket(c), 8 * pass, st);
-            kin = P<uint32_t>(c->d_sortk[o]);
+            launch_onesweep64kv(kin, vin, P<unsigned long long>(c->d_sortk[o]),
+                                P<uint32_t>(c->d_sortv[o]), P<Seg>(c->d_dsegs), nv,
+                                P<int>(c->d_dtile0), dtiles, P<uint32_t>(c->d_hist), pass,
+                                dpasses, P<uint32_t>(c->d_lb), next_ticket(c), 8 * pass, st);
+            kin = P<unsigned long long>(c->d_sortk[o]);
             vin = P<uint32_t>(c->d_sortv[o]);
         }
-        c->final_order = 1;   // pass 3 wrote buffer 1
-        // equal depths: restore ascending Gaussian index inside each run
-        long long max_r = 0;
-        for (int v = 0; v < nv; ++v) max_r = std::max(max_r, c->hv[v].n_rendered);
-        launch_depth_ties(P<uint32_t>(c->d_sortk[1]), P<uint32_t>(c->d_sortv[1]),
-                          P<int32_t>(c->d_gidx), P<Seg>(c->d_dsegs), nv, max_r, st);
+        c->final_order = (dpasses - 1) & 1;
         ev_end(c, st, e);
     }
     CU(cudaGetLastError());

@@ -132,8 +132,9 @@ struct ProjectArgs {
     int max_tiles;               // grid.x: max over views of ceil(n_temporal / project_tile)
     // outputs
     float4* rec;                 // [cap][3] splat records (compacted, unordered)
-    uint32_t* dkey;              // [cap] depth bits
-    int32_t* gidx;               // [cap] Gaussian index
+    unsigned long long* dkey;    // [cap] (depth bits << gbits) | Gaussian index
+    int gbits;                   // bits of the Gaussian index in dkey
+    int32_t* gidx;               // [cap] Gaussian index (debug dumps) or NULL
     ViewCounters* counters;      // [n_views]; n_rendered is the compaction cursor
     uint32_t* err;
     // debug (NULL when off)
@@ -143,9 +144,6 @@ struct ProjectArgs {
 };
 void launch_project(const ProjectArgs& a, cudaStream_t st);
 int project_tile();
-// Restore (depth, Gaussian index) order inside runs of equal depth keys.
-void launch_depth_ties(const uint32_t* keys, uint32_t* vals, const int32_t* gidx, const Seg* segs,
-                       int nsegs, long long max_count, cudaStream_t st);
 
 // Segmented LSD radix sort helpers (onesweep with decoupled look-back).
 // keys: u32 (depth) or u64 (pair words).  digit = (key >> shift) & 255.
@@ -159,6 +157,12 @@ void launch_onesweep32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
                        uint32_t* vout, const Seg* segs, int nsegs, const int* seg_tile0,
                        int total_tiles, const uint32_t* digit_base, int pass, int npasses,
                        uint32_t* lookback, int* ticket, int shift, cudaStream_t st);
+// 64-bit keys with 32-bit values (vin == NULL: value = index in the segment).
+void launch_onesweep64kv(const unsigned long long* kin, const uint32_t* vin,
+                         unsigned long long* kout, uint32_t* vout, const Seg* segs, int nsegs,
+                         const int* seg_tile0, int total_tiles, const uint32_t* digit_base,
+                         int pass, int npasses, uint32_t* lookback, int* ticket, int shift,
+                         cudaStream_t st);
 void launch_onesweep64(const unsigned long long* kin, unsigned long long* kout,
                        const Seg* segs, int nsegs, const int* seg_tile0, int total_tiles,
                        const uint32_t* digit_base, int pass, int npasses, uint32_t* lookback,
