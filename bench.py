@@ -130,7 +130,7 @@ def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
     Nt = sum(s["n_temporal"] for s in stats)
     Nv = sum(s["n_visible"] for s in stats)
     Nr = sum(s["n_rendered"] for s in stats)
-    P = sum(s["n_pairs"] for s in stats)
+    Ps = sum(s["n_bin_pairs"] for s in stats)
     px = sum(v.width * v.height for v in views)
     tiles = sum(((v.width + 15) // 16) * ((v.height + 15) // 16) for v in views)
     # K1 writes each distinct time's list once
@@ -139,10 +139,10 @@ def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
         "filter": 8 * n_scene * math.ceil(max(n_distinct_t, 1) / 64) + 4 * nt_distinct,
         "project": 56 * Nt + 8 * Nv + (16 + 48 + 8) * Nr,
         "depth_sort": 8 * Nr + depth_passes * 24 * Nr,
-        "emit": (4 + 48 + 48) * Nr + 8 * P,
-        "pair_sort": 8 * P + pair_passes * 16 * P,
-        "ranges": 8 * P + 8 * tiles,
-        "raster": 8 * P + 48 * Nr + 20 * px,
+        # permute (order + record in/out + rectangle) + count + scatter (rect + 4 B/pair)
+        "bin": (4 + 48 + 48 + 8) * Nr + 8 * Nr + 8 * Nr + 4 * Ps,
+        # one read of the supertile lists (rank + rectangle), unique records, images
+        "raster": 12 * Ps + 48 * Nr + 20 * px,
     }
 
 
@@ -347,7 +347,9 @@ def main():
         cpu = cpu_baseline(args.config)
     if rank == 0:
         n_scene = scene.n
-        launches_per_step = 2 + math.ceil(max(n_t, 1) / 64) - 1 + 2 + 4 + 1 + 2 + pair_passes + 1 + 1
+        # K1 chunks + K2 + (hist, scan, depth passes) + (permute, count, scan, scatter) + raster
+        depth_passes = math.ceil((32 + max(1, (max(n_scene, 2) - 1).bit_length())) / 8)
+        launches_per_step = math.ceil(max(n_t, 1) / 64) + 1 + 2 + depth_passes + 4 + 1
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -366,7 +368,8 @@ def main():
             "stages": stages,
             "workload_per_view": {k: sum(s[k] for s in stats) / views_per_step for k in
                                   ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped",
-                                   "n_rendered", "n_pairs", "n_blend_evals", "n_blend_exec")},
+                                   "n_rendered", "n_pairs", "n_bin_pairs", "n_blend_evals",
+                                   "n_blend_exec")},
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

@@ -127,6 +127,7 @@ typedef struct {
     int64_t n_rendered;          /* blended                                     */
     int64_t n_pairs;             /* (tile, Gaussian) pairs                      */
     int64_t n_bad_instance;      /* ids outside [0,K]                           */
+    int64_t n_bin_pairs;         /* (supertile, Gaussian) pairs of the binning  */
     int64_t n_blend_evals;       /* E_alg: sum over pixels of the splats the
                                     pixel examines up to and including its
                                     terminating one (0 unless counters are on) */
@@ -153,11 +154,11 @@ typedef struct {
 enum {
     S3R_STAGE_FILTER = 0,        /* K1 temporal filter + compaction            */
     S3R_STAGE_PROJECT,           /* K2 projection + LOD + life update          */
-    S3R_STAGE_DEPTH_SORT,        /* K5a depth radix sort                        */
-    S3R_STAGE_EMIT,              /* K3/K4 permute + scan + key emission         */
-    S3R_STAGE_PAIR_SORT,         /* K5b tile radix sort                         */
-    S3R_STAGE_RANGES,            /* K6 tile ranges                              */
-    S3R_STAGE_RASTER,            /* K7 alpha-blend rasterizer                   */
+    S3R_STAGE_DEPTH_SORT,        /* K5 (depth, index) radix sort                */
+    S3R_STAGE_BIN,               /* K3 depth-order permute + K4 supertile
+                                    counting sort (count, scan, scatter) with
+                                    supertile ranges                            */
+    S3R_STAGE_RASTER,            /* K7 tile filter + alpha-blend rasterizer     */
     S3R_NUM_STAGES
 };
 

@@ -1,0 +1,292 @@
+// k_bin.cu — a4 tile binning: depth-ordered permute (K3) and a stable
+// counting sort of (supertile, depth rank) pairs (K4 count / scan / scatter),
+// plus the debug expansion of supertile lists into per-tile lists.
+//
+// Reading R11/R12: every pixel of a 16x16 tile blends, in (depth,
+// index) order, the rendered Gaussians whose tile rectangle contains the tile.
+// After the depth sort (K5a) the splats of a view sit in rank order r.  Instead
+// of materialising one (tile, r) pair per covered tile and radix-sorting them
+// (3DGS practice; ~28 pairs per splat here), the splats are binned by SUPERTILE
+// (S x S tiles, S = 4 unless the image needs more): each splat emits one pair
+// per supertile its rectangle touches (~5x fewer pairs), written directly to its
+// final position by a stable counting sort whose single digit is the supertile
+// id (one pass: count per (chunk, bin), exclusive scan in (bin, chunk) order,
+// scatter in rank order).  The rasterizer (K7) walks its supertile's list in
+// order and keeps the entries whose rectangle contains its tile, which yields
+// exactly the per-tile list of R11/R12 — the debug dump below materialises it.
+#include "s3r_internal.cuh"
+
+namespace s3r {
+
+namespace {
+
+constexpr int KT = 256;          // threads of the bin kernels
+constexpr int KCHUNK = 1024;     // splats (ranks) per chunk / CTA
+constexpr int KWARPS = KT / 32;
+constexpr int KWCHUNK = KCHUNK / KWARPS;   // 128 ranks per warp in the scatter
+
+__device__ __forceinline__ void rect_of(uint2 rr, int& tx0, int& tx1, int& ty0, int& ty1)
+{
+    tx0 = rr.x & 0xffff; tx1 = rr.x >> 16; ty0 = rr.y & 0xffff; ty1 = rr.y >> 16;
+}
+
+// ------------------------------------------------------------------ K3 permute
+// rec_sorted[r] = rec[order[r]] and rect_sorted[r] = its tile rectangle.
+__global__ void __launch_bounds__(256) k_permute(const DevView* __restrict__ views,
+                                                 const uint32_t* __restrict__ order,
+                                                 const float4* __restrict__ rec,
+                                                 float4* __restrict__ rec_sorted,
+                                                 uint2* __restrict__ rect_sorted)
+{
+    const DevView& V = views[blockIdx.y];
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= V.n_rendered) return;
+    const long long base = V.cap_off;
+    const uint32_t j = order[base + r];
+    const float4* src = rec + 3 * (base + j);
+    const float4 q0 = src[0], q1 = src[1], q2 = src[2];
+    float4* dst = rec_sorted + 3 * (base + r);
+    dst[0] = q0;
+    dst[1] = q1;
+    dst[2] = q2;
+    rect_sorted[base + r] = make_uint2(__float_as_uint(q1.w), __float_as_uint(q2.w));
+}
+
+// ------------------------------------------------------------------ K4 count
+// cnt[view][bin][chunk] = number of (bin, r) pairs of chunk `chunk`.
+__global__ void __launch_bounds__(KT) k_bin_count(const DevView* __restrict__ views,
+                                                  const uint2* __restrict__ rect_sorted,
+                                                  uint32_t* __restrict__ cnt)
+{
+    extern __shared__ uint32_t s_cnt[];        // [nbins]
+    const DevView& V = views[blockIdx.y];
+    const int c = blockIdx.x;
+    const long long r0 = (long long)c * KCHUNK;
+    if (r0 >= V.n_rendered || V.nbins == 0) return;
+    const int nb = V.nbins, sh = V.sshift, sx = V.STX;
+    for (int b = threadIdx.x; b < nb; b += KT) s_cnt[b] = 0;
+    __syncthreads();
+    const long long r1 = min((long long)KCHUNK, V.n_rendered - r0);
+    for (int i = threadIdx.x; i < r1; i += KT) {
+        int tx0, tx1, ty0, ty1;
+        rect_of(rect_sorted[V.cap_off + r0 + i], tx0, tx1, ty0, ty1);
+        for (int by = ty0 >> sh; by <= (ty1 >> sh); ++by)
+            for (int bx = tx0 >> sh; bx <= (tx1 >> sh); ++bx) atomicAdd(&s_cnt[by * sx + bx], 1u);
+    }
+    __syncthreads();
+    uint32_t* out = cnt + V.cnt_off;
+    for (int b = threadIdx.x; b < nb; b += KT) out[(long long)b * V.nchunks + c] = s_cnt[b];
+}
+
+// ------------------------------------------------------------------ K4 scan
+// One CTA per view: exclusive scan of cnt in (bin, chunk) order; bin ranges.
+__global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ views,
+                                                   uint32_t* __restrict__ cnt,
+                                                   int2* __restrict__ ranges)
+{
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    const DevView& V = views[blockIdx.x];
+    const long long n = (long long)V.nbins * V.nchunks;
+    uint32_t* a = cnt + V.cnt_off;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (long long base = 0; base < n; base += 1024) {
+        const long long i = base + tid;
+        const uint32_t x = i < n ? a[i] : 0u;
+        uint32_t v = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane == 31) s_warp[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t w = s_warp[lane];
+            uint32_t ww = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, ww, o);
+                if (lane >= o) ww += y;
+            }
+            s_warp[lane] = ww - w;
+        }
+        __syncthreads();
+        const uint32_t carry = s_carry;
+        const uint32_t ex = carry + s_warp[warp] + v - x;
+        if (i < n) a[i] = ex;
+        __syncthreads();
+        if (tid == 1023) s_carry = ex + x;
+        __syncthreads();
+    }
+    // bin ranges: [first of bin b, first of bin b+1)
+    const uint32_t total = s_carry;
+    int2* R = ranges + V.range_off;
+    for (int b = tid; b < V.nbins; b += 1024) {
+        const uint32_t s = a[(long long)b * V.nchunks];
+        const uint32_t e = (b + 1 < V.nbins) ? a[(long long)(b + 1) * V.nchunks] : total;
+        R[b] = make_int2((int)s, (int)e);
+    }
+}
+
+// ------------------------------------------------------------------ K4 scatter
+// Writes every (bin, r) pair's rank r at its final position.  Stability: a
+// chunk's pairs for one bin follow the chunk's scanned base; inside the chunk
+// warp w's pairs follow warps < w (per-warp counts, scanned in shared memory);
+// inside a warp the splats are taken one at a time in rank order.
+__global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ views,
+                                                    const uint2* __restrict__ rect_sorted,
+                                                    const uint32_t* __restrict__ cnt,
+                                                    uint32_t* __restrict__ lists)
+{
+    extern __shared__ uint32_t s_dyn[];
+    const DevView& V = views[blockIdx.y];
+    const int c = blockIdx.x;
+    const long long r0 = (long long)c * KCHUNK;
+    if (r0 >= V.n_rendered || V.nbins == 0) return;
+    const int nb = V.nbins, sh = V.sshift, sx = V.STX;
+    uint32_t* s_base = s_dyn;                                    // [nb] chunk base per bin
+    uint32_t* s_w = s_dyn + nb;                                  // [KWARPS][nb]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < KWARPS * nb; i += KT) s_w[i] = 0;
+    for (int b = tid; b < nb; b += KT) s_base[b] = cnt[V.cnt_off + (long long)b * V.nchunks + c];
+    __syncthreads();
+    const long long n_r = V.n_rendered;
+    const long long wr0 = r0 + (long long)warp * KWCHUNK;
+    const int wn = (int)max(0ll, min((long long)KWCHUNK, n_r - wr0));
+    // per-warp counts
+    uint32_t* mine = s_w + warp * nb;
+    for (int i = lane; i < wn; i += 32) {
+        int tx0, tx1, ty0, ty1;
+        rect_of(rect_sorted[V.cap_off + wr0 + i], tx0, tx1, ty0, ty1);
+        for (int by = ty0 >> sh; by <= (ty1 >> sh); ++by)
+            for (int bx = tx0 >> sh; bx <= (tx1 >> sh); ++bx)
+                atomicAdd(&mine[by * sx + bx], 1u);
+    }
+    __syncthreads();
+    // exclusive scan across warps, per bin
+    for (int b = tid; b < nb; b += KT) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < KWARPS; ++w) {
+            const uint32_t t = s_w[w * nb + b];
+            s_w[w * nb + b] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    // scatter: the warp walks its splats in rank order
+    uint32_t* out = lists + V.pair_off;
+    for (int i = 0; i < wn; ++i) {
+        const long long r = wr0 + i;
+        int tx0, tx1, ty0, ty1;
+        rect_of(rect_sorted[V.cap_off + r], tx0, tx1, ty0, ty1);
+        const int bx0 = tx0 >> sh, by0 = ty0 >> sh;
+        const int bw = (tx1 >> sh) - bx0 + 1;
+        const int nbb = bw * ((ty1 >> sh) - by0 + 1);
+        for (int k = lane; k < nbb; k += 32) {
+            const int b = (by0 + k / bw) * sx + bx0 + k % bw;
+            const uint32_t pos = s_base[b] + mine[b];
+            mine[b] = mine[b] + 1;
+            out[pos] = (uint32_t)r;
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ debug
+// Per-tile list of view V: entries of the tile's supertile list whose tile
+// rectangle contains the tile, in list order (== (tile, depth, index) order).
+__global__ void k_dbg_tile_count(const DevView* __restrict__ views, int vi,
+                                 const uint2* __restrict__ rect_sorted,
+                                 const uint32_t* __restrict__ lists, const int2* __restrict__ ranges,
+                                 uint32_t* __restrict__ tcount)
+{
+    const DevView& V = views[vi];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= V.ntiles) return;
+    const int tx = t % V.TX, ty = t / V.TX;
+    const int b = (ty >> V.sshift) * V.STX + (tx >> V.sshift);
+    const int2 rg = ranges[V.range_off + b];
+    uint32_t n = 0;
+    for (int i = rg.x; i < rg.y; ++i) {
+        int tx0, tx1, ty0, ty1;
+        rect_of(rect_sorted[V.cap_off + lists[V.pair_off + i]], tx0, tx1, ty0, ty1);
+        n += (tx >= tx0 && tx <= tx1 && ty >= ty0 && ty <= ty1) ? 1u : 0u;
+    }
+    tcount[t] = n;
+}
+
+__global__ void k_dbg_tile_write(const DevView* __restrict__ views, int vi,
+                                 const uint2* __restrict__ rect_sorted,
+                                 const uint32_t* __restrict__ lists, const int2* __restrict__ ranges,
+                                 const uint32_t* __restrict__ toff, const uint32_t* __restrict__ order,
+                                 const int32_t* __restrict__ gidx, int32_t* __restrict__ tile_out,
+                                 int32_t* __restrict__ gauss_out, int32_t* __restrict__ tranges)
+{
+    const DevView& V = views[vi];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= V.ntiles) return;
+    const int tx = t % V.TX, ty = t / V.TX;
+    const int b = (ty >> V.sshift) * V.STX + (tx >> V.sshift);
+    const int2 rg = ranges[V.range_off + b];
+    uint32_t o = toff[t];
+    if (tranges) tranges[2 * t] = (int32_t)o;
+    for (int i = rg.x; i < rg.y; ++i) {
+        const uint32_t r = lists[V.pair_off + i];
+        int tx0, tx1, ty0, ty1;
+        rect_of(rect_sorted[V.cap_off + r], tx0, tx1, ty0, ty1);
+        if (tx >= tx0 && tx <= tx1 && ty >= ty0 && ty <= ty1) {
+            if (tile_out) tile_out[o] = t;
+            if (gauss_out) gauss_out[o] = gidx[V.cap_off + order[V.cap_off + r]];
+            ++o;
+        }
+    }
+    if (tranges) tranges[2 * t + 1] = (int32_t)o;
+}
+
+}  // namespace
+
+int bin_chunk() { return KCHUNK; }
+
+void launch_permute(const DevView* views, int n_views, long long max_rendered,
+                    const uint32_t* order, const float4* rec, float4* rec_sorted,
+                    uint2* rect_sorted, cudaStream_t st)
+{
+    if (n_views == 0 || max_rendered == 0) return;
+    dim3 grid((unsigned)((max_rendered + 255) / 256), n_views);
+    k_permute<<<grid, 256, 0, st>>>(views, order, rec, rec_sorted, rect_sorted);
+}
+
+void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
+                const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
+                cudaStream_t st)
+{
+    if (n_views == 0 || max_chunks == 0) return;
+    dim3 grid(max_chunks, n_views);
+    k_bin_count<<<grid, KT, (size_t)max_bins * 4, st>>>(views, rect_sorted, cnt);
+    k_bin_scan<<<n_views, 1024, 0, st>>>(views, cnt, ranges);
+    const size_t smem = (size_t)max_bins * 4 * (1 + KWARPS);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_bin_scatter<<<grid, KT, smem, st>>>(views, rect_sorted, cnt, lists);
+}
+
+void launch_dbg_tile_lists(const DevView* views, int vi, int ntiles, const uint2* rect_sorted,
+                           const uint32_t* lists, const int2* ranges, uint32_t* tcount,
+                           const uint32_t* toff, const uint32_t* order, const int32_t* gidx,
+                           int32_t* tile_out, int32_t* gauss_out, int32_t* tranges, bool count,
+                           cudaStream_t st)
+{
+    if (ntiles == 0) return;
+    const unsigned g = (unsigned)((ntiles + 127) / 128);
+    if (count)
+        k_dbg_tile_count<<<g, 128, 0, st>>>(views, vi, rect_sorted, lists, ranges, tcount);
+    else
+        k_dbg_tile_write<<<g, 128, 0, st>>>(views, vi, rect_sorted, lists, ranges, toff, order,
+                                            gidx, tile_out, gauss_out, tranges);
+}
+
+}  // namespace s3r

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
     __shared__ float s_bounds[4];
     __shared__ uint32_t s_wcnt[PT / 32];
     __shared__ uint32_t s_base;
-    __shared__ unsigned long long s_red[5][PT / 32];
+    __shared__ unsigned long long s_red[6][PT / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int vi = blockIdx.y;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
     ViewCounters* ctr = a.counters + vi;
     const unsigned lt = (1u << lane) - 1u;
 
-    unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0;
+    unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0, c_spairs = 0;
     for (int rd = 0; rd < PR; ++rd) {
         const long long i = i0 + rd * PT + tid;
         Splat sp;
@@ -256,6 +256,9 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
                     col.w = mo.w;    // opacity travels in the record
                     c_pairs += (unsigned long long)(sp.tx1 - sp.tx0 + 1) *
                                (unsigned long long)(sp.ty1 - sp.ty0 + 1);
+                    const int sh = V.sshift;
+                    c_spairs += (unsigned long long)((sp.tx1 >> sh) - (sp.tx0 >> sh) + 1) *
+                                (unsigned long long)((sp.ty1 >> sh) - (sp.ty0 >> sh) + 1);
                 }
             }
             if (a.dbg_flags) {
@@ -308,9 +311,9 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
         }
     }
     // ---- per-view counters: one set of atomics per CTA ----
-    unsigned long long cv[5] = {c_vis, c_small, c_drop, c_pairs, c_bad};
+    unsigned long long cv[6] = {c_vis, c_small, c_drop, c_pairs, c_bad, c_spairs};
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
+    for (int j = 0; j < 6; ++j) {
         unsigned long long x = cv[j];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
@@ -318,9 +321,10 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
     }
     __syncthreads();
     if (tid == 0) {
-        unsigned long long t5[5] = {0, 0, 0, 0, 0};
+        unsigned long long t5[6] = {0, 0, 0, 0, 0, 0};
         for (int w = 0; w < PT / 32; ++w)
-            for (int j = 0; j < 5; ++j) t5[j] += s_red[j][w];
+            for (int j = 0; j < 6; ++j) t5[j] += s_red[j][w];
+        if (t5[5]) atomicAdd(&ctr->n_spairs, t5[5]);
         if (t5[0]) atomicAdd(&ctr->n_visible, t5[0]);
         if (t5[1]) atomicAdd(&ctr->n_small, t5[1]);
         if (t5[2]) atomicAdd(&ctr->n_dropped, t5[2]);

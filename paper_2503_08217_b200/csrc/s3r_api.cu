@@ -51,10 +51,9 @@ struct s3r_ctx {
     bool staging_recorded = false;
     cudaStream_t last_stream = nullptr;
     // device scratch
-    Buf d_views, d_times, d_tidx, d_counts, d_lb, d_ticket, d_tile0, d_ctr, d_rec, d_dkey,
-        d_gidx, d_sortk[2], d_sortv[2], d_recs, d_pairs[2], d_hist, d_dsegs, d_dtile0, d_etile0,
-        d_psegs, d_ptile0, d_ranges, d_range_off, d_vpo, d_err, d_dbg_keys, d_dbg_flags,
-        d_dbg_rect;
+    Buf d_views, d_times, d_tidx, d_counts, d_lb, d_ticket, d_ctr, d_rec, d_dkey, d_gidx,
+        d_sortk[2], d_sortv[2], d_recs, d_rects, d_lists, d_cnt, d_hist, d_dsegs, d_dtile0,
+        d_ranges, d_err, d_dbg_keys, d_dbg_flags, d_dbg_rect, d_dbg_tcnt;
     int ticket_slot = 0;
     int gbits = 1;
     // mirrors for s3r_render_batch_host
@@ -63,9 +62,8 @@ struct s3r_ctx {
     // last batch
     std::vector<DevView> hv;
     std::vector<s3r_stats> stats;
-    std::vector<int> range_off;
     long long N_last = 0;
-    int final_order = 1, final_pairs = 0;
+    int final_order = 1;
     bool have_render = false;
     // timers
     std::vector<StageEvent> ev;
@@ -262,6 +260,14 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         d.TX = (V.width + TILE - 1) / TILE;
         d.TY = (V.height + TILE - 1) / TILE;
         d.ntiles = d.TX * d.TY;
+        // supertile edge S = 2^sshift tiles: the smallest S >= 4 with <= MAX_BINS bins
+        d.sshift = 2;
+        while (((d.TX + (1 << d.sshift) - 1) >> d.sshift) *
+                   ((d.TY + (1 << d.sshift) - 1) >> d.sshift) > MAX_BINS)
+            ++d.sshift;
+        d.STX = (d.TX + (1 << d.sshift) - 1) >> d.sshift;
+        d.STY = (d.TY + (1 << d.sshift) - 1) >> d.sshift;
+        d.nbins = d.STX * d.STY;
         d.rgb = outs[v].rgb; d.depth = outs[v].depth; d.finalT = outs[v].final_T;
         d.visible = outs[v].visible;
     }
@@ -372,9 +378,9 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
 
     // ================= sizes of the sort / emit / raster phase
     c->stats.assign(nv, s3r_stats{});
-    std::vector<long long> vpo(nv + 1, 0);
-    std::vector<int> dt0(nv + 1, 0), et0(nv + 1, 0), pt0(nv + 1, 0);
-    c->range_off.assign(nv + 1, 0);
+    std::vector<int> dt0(nv + 1, 0);
+    long long total_pairs = 0, total_cnt = 0, max_r = 0;
+    int total_bins = 0, max_chunks = 0, max_bins = 0;
     int max_tiles = 0;
     bool bad = false;
     const int stile = onesweep64_tile();
@@ -383,14 +389,19 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         const ViewCounters& k = h_ctr[v];
         d.n_rendered = (long long)k.n_rendered;
         d.n_pairs = (long long)k.n_pairs;
-        if (d.n_pairs >= (1ll << 30))
-            return fail(c, S3R_EINVAL, "view %d: %lld tile pairs exceed 2^30", v, d.n_pairs);
-        d.pair_off = vpo[v];
-        vpo[v + 1] = vpo[v] + d.n_pairs;
+        if (d.n_pairs >= (1ll << 31))
+            return fail(c, S3R_EINVAL, "view %d: %lld tile pairs exceed 2^31", v, d.n_pairs);
+        d.nchunks = (int)((d.n_rendered + bin_chunk() - 1) / bin_chunk());
+        d.range_off = total_bins;
+        d.cnt_off = total_cnt;
+        d.pair_off = total_pairs;
+        total_bins += d.nbins;
+        total_cnt += (long long)d.nbins * d.nchunks;
+        total_pairs += (long long)k.n_spairs;
+        max_chunks = std::max(max_chunks, d.nchunks);
+        max_bins = std::max(max_bins, d.nbins);
+        max_r = std::max(max_r, d.n_rendered);
         dt0[v + 1] = dt0[v] + (int)((d.n_rendered + stile - 1) / stile);
-        et0[v + 1] = et0[v] + (int)((d.n_rendered + emit_tile() - 1) / emit_tile());
-        pt0[v + 1] = pt0[v] + (int)((d.n_pairs + onesweep64_tile() - 1) / onesweep64_tile());
-        c->range_off[v + 1] = c->range_off[v] + d.ntiles;
         max_tiles = std::max(max_tiles, d.ntiles);
         s3r_stats& s = c->stats[v];
         s.n_scene = N;
@@ -400,65 +411,42 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         s.n_lod_dropped = (long long)k.n_dropped;
         s.n_rendered = d.n_rendered;
         s.n_pairs = d.n_pairs;
+        s.n_bin_pairs = (long long)k.n_spairs;
         s.n_bad_instance = (long long)k.n_bad;
         if (k.n_bad) bad = true;
     }
-    const long long total_pairs = vpo[nv];
-    const int dtiles = dt0[nv], etiles = et0[nv], ptiles = pt0[nv];
-    const int tilebits = bits_for(std::max(max_tiles, 1));
-    const int ppasses = (tilebits + RADIX_BITS - 1) / RADIX_BITS;
+    const int dtiles = dt0[nv];
 
     // device-side metadata for the rest of the batch
     Seg* h_dsegs = (Seg*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(Seg));
-    Seg* h_psegs = (Seg*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(Seg));
     int* h_dt0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
-    int* h_et0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
-    int* h_pt0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
-    int* h_ro = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
-    long long* h_vpo = (long long*)stage_alloc(c, (size_t)(nv + 1) * sizeof(long long));
     DevView* h_views2 = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
     for (int v = 0; v < nv; ++v) {
         const DevView& d = c->hv[v];
         h_dsegs[v] = Seg{d.cap_off, d.n_rendered, dt0[v], dt0[v + 1] - dt0[v]};
-        h_psegs[v] = Seg{d.pair_off, d.n_pairs, pt0[v], pt0[v + 1] - pt0[v]};
     }
     std::memcpy(h_dt0, dt0.data(), (nv + 1) * sizeof(int));
-    std::memcpy(h_et0, et0.data(), (nv + 1) * sizeof(int));
-    std::memcpy(h_pt0, pt0.data(), (nv + 1) * sizeof(int));
-    std::memcpy(h_ro, c->range_off.data(), (nv + 1) * sizeof(int));
-    std::memcpy(h_vpo, vpo.data(), (nv + 1) * sizeof(long long));
     std::memcpy(h_views2, c->hv.data(), (size_t)nv * sizeof(DevView));
 
     if ((rc = ensure(c, c->d_dsegs, (size_t)std::max(nv, 1) * sizeof(Seg)))) return rc;
-    if ((rc = ensure(c, c->d_psegs, (size_t)std::max(nv, 1) * sizeof(Seg)))) return rc;
     if ((rc = ensure(c, c->d_dtile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
-    if ((rc = ensure(c, c->d_etile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
-    if ((rc = ensure(c, c->d_ptile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
-    if ((rc = ensure(c, c->d_range_off, (size_t)(nv + 1) * sizeof(int)))) return rc;
-    if ((rc = ensure(c, c->d_vpo, (size_t)(nv + 1) * sizeof(long long)))) return rc;
     if (nv) {
         CU(cudaMemcpyAsync(c->d_dsegs.p, h_dsegs, nv * sizeof(Seg), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_psegs.p, h_psegs, nv * sizeof(Seg), cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(c->d_dtile0.p, h_dt0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_etile0.p, h_et0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_ptile0.p, h_pt0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_range_off.p, h_ro, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_vpo.p, h_vpo, (nv + 1) * sizeof(long long), cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(c->d_views.p, h_views2, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
     }
     for (int i = 0; i < 2; ++i) {
         if ((rc = ensure(c, c->d_sortk[i], (size_t)capS * 8))) return rc;
         if ((rc = ensure(c, c->d_sortv[i], (size_t)capS * 4))) return rc;
-        if ((rc = ensure(c, c->d_pairs[i], (size_t)std::max<long long>(total_pairs, 1) * 8))) return rc;
     }
     if ((rc = ensure(c, c->d_recs, (size_t)capS * 48))) return rc;
+    if ((rc = ensure(c, c->d_rects, (size_t)capS * 8))) return rc;
+    if ((rc = ensure(c, c->d_lists, (size_t)std::max<long long>(total_pairs, 1) * 4))) return rc;
+    if ((rc = ensure(c, c->d_cnt, (size_t)std::max<long long>(total_cnt, 1) * 4))) return rc;
     const int dpasses = (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS;
-    const int hpasses = std::max(dpasses, ppasses);
-    if ((rc = ensure(c, c->d_hist, (size_t)std::max(nv, 1) * hpasses * RADIX * 4))) return rc;
-    if ((rc = ensure(c, c->d_ranges, (size_t)std::max(c->range_off[nv], 1) * sizeof(int2)))) return rc;
-    const size_t lb_need = (size_t)std::max({(long long)dtiles * RADIX, (long long)ptiles * RADIX,
-                                             (long long)etiles, 1ll}) * sizeof(uint32_t);
-    if ((rc = ensure(c, c->d_lb, lb_need))) return rc;
+    if ((rc = ensure(c, c->d_hist, (size_t)std::max(nv, 1) * dpasses * RADIX * 4))) return rc;
+    if ((rc = ensure(c, c->d_ranges, (size_t)std::max(total_bins, 1) * sizeof(int2)))) return rc;
+    if ((rc = ensure(c, c->d_lb, (size_t)std::max(dtiles, 1) * RADIX * sizeof(uint32_t)))) return rc;
 
     // ================= K5a: depth sort: 8-bit LSD passes over (depth << gbits | index),
     // values = compacted slot j; gives the unique (depth, index) order (R11)
@@ -486,56 +474,14 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     }
     CU(cudaGetLastError());
 
-    // ================= K3/K4: permute to depth order, scan tile counts, emit pairs
+    // ================= K3/K4: depth-ordered permute + supertile counting sort
     {
         StageEvent e;
-        ev_begin(c, S3R_STAGE_EMIT, st, e);
-        if (etiles) CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)etiles * 4, st));
-        EmitArgs a{};
-        a.views = P<DevView>(c->d_views);
-        a.segs = P<Seg>(c->d_dsegs);
-        a.nsegs = nv;
-        a.seg_tile0 = P<int>(c->d_etile0);
-        a.total_tiles = etiles;
-        a.order = P<uint32_t>(c->d_sortv[c->final_order]);
-        a.rec = P<float4>(c->d_rec);
-        a.rec_sorted = P<float4>(c->d_recs);
-        a.pairs = P<unsigned long long>(c->d_pairs[0]);
-        a.lookback = P<uint32_t>(c->d_lb);
-        a.ticket = next_ticket(c);
-        launch_emit(a, st);
-        ev_end(c, st, e);
-    }
-    CU(cudaGetLastError());
-
-    // ================= K5b: stable tile sort of the pair words
-    {
-        StageEvent e;
-        ev_begin(c, S3R_STAGE_PAIR_SORT, st, e);
-        CU(cudaMemsetAsync(c->d_hist.p, 0, (size_t)std::max(nv, 1) * ppasses * RADIX * 4, st));
-        launch_hist64(P<unsigned long long>(c->d_pairs[0]), P<Seg>(c->d_psegs), nv,
-                      P<int>(c->d_ptile0), ptiles, 32, ppasses, P<uint32_t>(c->d_hist), st);
-        launch_hist_scan(P<uint32_t>(c->d_hist), nv, ppasses, st);
-        for (int pass = 0; pass < ppasses; ++pass) {
-            if (ptiles) CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)ptiles * RADIX * 4, st));
-            launch_onesweep64(P<unsigned long long>(c->d_pairs[pass & 1]),
-                              P<unsigned long long>(c->d_pairs[(pass + 1) & 1]), P<Seg>(c->d_psegs),
-                              nv, P<int>(c->d_ptile0), ptiles, P<uint32_t>(c->d_hist), pass,
-                              ppasses, P<uint32_t>(c->d_lb), next_ticket(c), 32 + 8 * pass, st);
-        }
-        c->final_pairs = ppasses & 1;
-        ev_end(c, st, e);
-    }
-    CU(cudaGetLastError());
-
-    // ================= K6: tile ranges
-    {
-        StageEvent e;
-        ev_begin(c, S3R_STAGE_RANGES, st, e);
-        CU(cudaMemsetAsync(c->d_ranges.p, 0, (size_t)std::max(c->range_off[nv], 1) * sizeof(int2), st));
-        launch_ranges(P<unsigned long long>(c->d_pairs[c->final_pairs]), total_pairs,
-                      P<DevView>(c->d_views), nv, P<long long>(c->d_vpo), P<int>(c->d_range_off),
-                      P<int2>(c->d_ranges), st);
+        ev_begin(c, S3R_STAGE_BIN, st, e);
+        launch_permute(P<DevView>(c->d_views), nv, max_r, P<uint32_t>(c->d_sortv[c->final_order]),
+                       P<float4>(c->d_rec), P<float4>(c->d_recs), P<uint2>(c->d_rects), st);
+        launch_bin(P<DevView>(c->d_views), nv, max_chunks, max_bins, P<uint2>(c->d_rects),
+                   P<uint32_t>(c->d_cnt), P<int2>(c->d_ranges), P<uint32_t>(c->d_lists), st);
         ev_end(c, st, e);
     }
     CU(cudaGetLastError());
@@ -549,8 +495,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.n_views = nv;
         a.max_tiles = max_tiles;
         a.ranges = P<int2>(c->d_ranges);
-        a.range_off = P<int>(c->d_range_off);
-        a.pairs = P<unsigned long long>(c->d_pairs[c->final_pairs]);
+        a.lists = P<uint32_t>(c->d_lists);
+        a.rect_sorted = P<uint2>(c->d_rects);
         a.rec_sorted = P<float4>(c->d_recs);
         a.evals = nullptr;
         if (c->counters && nv) {
@@ -613,11 +559,10 @@ void s3r_destroy(s3r_ctx* c)
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     Buf* bufs[] = {&c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
-                   &c->d_tile0, &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0],
-                   &c->d_sortk[1], &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_pairs[0],
-                   &c->d_pairs[1], &c->d_hist, &c->d_dsegs, &c->d_dtile0, &c->d_etile0,
-                   &c->d_psegs, &c->d_ptile0, &c->d_ranges, &c->d_range_off, &c->d_vpo, &c->d_err,
-                   &c->d_dbg_keys, &c->d_dbg_flags, &c->d_dbg_rect, &c->d_evals};
+                   &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
+                   &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_rects, &c->d_lists,
+                   &c->d_cnt, &c->d_hist, &c->d_dsegs, &c->d_dtile0, &c->d_ranges, &c->d_err,
+                   &c->d_dbg_keys, &c->d_dbg_flags, &c->d_dbg_rect, &c->d_dbg_tcnt, &c->d_evals};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& b : c->m_scene)
@@ -840,13 +785,35 @@ int s3r_dump_intermediates(s3r_ctx* c, int32_t vi, const s3r_debug* dbg, void* s
     const uint32_t* order = P<uint32_t>(c->d_sortv[c->final_order]);
     if (dbg->depth_order)
         launch_dump_order(order, P<int32_t>(c->d_gidx), d.cap_off, d.n_rendered, dbg->depth_order, st);
-    if (dbg->pair_tile || dbg->pair_gauss)
-        launch_dump_pairs(P<unsigned long long>(c->d_pairs[c->final_pairs]) + d.pair_off, d.n_pairs,
-                          order, c->last_debug ? P<int32_t>(c->d_gidx) : nullptr, d.cap_off,
-                          dbg->pair_tile, dbg->pair_gauss, st);
-    if (dbg->ranges)
-        CU(cudaMemcpyAsync(dbg->ranges, P<int2>(c->d_ranges) + c->range_off[vi],
-                           (size_t)d.ntiles * sizeof(int2), cudaMemcpyDeviceToDevice, st));
+    if (dbg->pair_tile || dbg->pair_gauss || dbg->ranges) {
+        // expand the view's supertile lists into its per-tile lists (reading R11/R12):
+        // count per tile, exclusive scan (host; debug path), write in list order
+        int rc;
+        const int nt = d.ntiles;
+        if ((rc = ensure(c, c->d_dbg_tcnt, (size_t)(2 * nt + 1) * 4))) return rc;
+        uint32_t* tcnt = P<uint32_t>(c->d_dbg_tcnt);
+        uint32_t* toff = tcnt + nt;
+        launch_dbg_tile_lists(P<DevView>(c->d_views), vi, nt, P<uint2>(c->d_rects),
+                              P<uint32_t>(c->d_lists), P<int2>(c->d_ranges), tcnt, nullptr, order,
+                              nullptr, nullptr, nullptr, nullptr, true, st);
+        std::vector<uint32_t> h(nt);
+        CU(cudaMemcpyAsync(h.data(), tcnt, (size_t)nt * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        uint32_t run = 0;
+        for (int t = 0; t < nt; ++t) {
+            const uint32_t x = h[t];
+            h[t] = run;
+            run += x;
+        }
+        if ((long long)run != d.n_pairs)
+            return fail(c, S3R_ECUDA, "dump: tile lists hold %u pairs, expected %lld", run, d.n_pairs);
+        CU(cudaMemcpyAsync(toff, h.data(), (size_t)nt * 4, cudaMemcpyHostToDevice, st));
+        launch_dbg_tile_lists(P<DevView>(c->d_views), vi, nt, P<uint2>(c->d_rects),
+                              P<uint32_t>(c->d_lists), P<int2>(c->d_ranges), nullptr, toff, order,
+                              c->last_debug ? P<int32_t>(c->d_gidx) : nullptr, dbg->pair_tile,
+                              dbg->pair_gauss, dbg->ranges, false, st);
+        CU(cudaStreamSynchronize(st));
+    }
     CU(cudaGetLastError());
     return S3R_OK;
 }

@@ -84,15 +84,19 @@ struct DevView {
     // filled per phase by the host
     long long cap_off;       // offset of the view's segment in per-rendered arrays
     long long n_temporal;
-    long long pair_off;      // offset of the view's pairs
+    long long pair_off;      // offset of the view's supertile lists
     long long n_rendered;
-    long long n_pairs;
+    long long n_pairs;       // (tile, splat) pairs P (K2 count); capacity of the lists
     long long dbg_off;       // offset in the debug arrays (keys/flags/rect)
+    // supertile binning (k_bin.cu): S = 2^sshift tiles per supertile edge
+    int sshift, STX, STY, nbins, nchunks;
+    int range_off;           // offset of the view's supertile ranges
+    long long cnt_off;       // offset of the view's (bin, chunk) counts
 };
 
 // Per-view counters written by K2 (device, zeroed per batch)
 struct ViewCounters {
-    unsigned long long n_visible, n_small, n_dropped, n_rendered, n_pairs, n_bad;
+    unsigned long long n_visible, n_small, n_dropped, n_rendered, n_pairs, n_bad, n_spairs;
 };
 
 // Segment of a segmented onesweep sort / scan (one per view)
@@ -171,37 +175,32 @@ int onesweep32_tile();
 int onesweep64_tile();
 int hist_tile();
 
-// K3/K4: depth-ordered permute + tile-count scan + key emission.
-struct EmitArgs {
-    const DevView* views;
-    const Seg* segs;             // per view: rendered segment (base = cap_off)
-    int nsegs;
-    const int* seg_tile0;
-    int total_tiles;
-    const uint32_t* order;       // [cap] depth-sorted local index j
-    const float4* rec;           // [cap][3] unsorted records
-    float4* rec_sorted;          // [cap][3]
-    unsigned long long* pairs;   // [total pairs] (tile << 32) | rank
-    uint32_t* lookback;
-    int* ticket;
-};
-void launch_emit(const EmitArgs& a, cudaStream_t st);
-int emit_tile();
-
-// K6: tile ranges from sorted pair words.
-void launch_ranges(const unsigned long long* pairs, long long total_pairs,
-                   const DevView* views, int n_views, const long long* view_pair_off,
-                   const int* range_off, int2* ranges, cudaStream_t st);
+// K3: depth-ordered permute of the records (+ compact rectangles by rank).
+void launch_permute(const DevView* views, int n_views, long long max_rendered,
+                    const uint32_t* order, const float4* rec, float4* rec_sorted,
+                    uint2* rect_sorted, cudaStream_t st);
+// K4: stable counting sort of (supertile, rank) pairs: count, scan, scatter.
+int bin_chunk();
+constexpr int MAX_BINS = 1024;   // supertiles per view (S grows for huge images)
+void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
+                const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
+                cudaStream_t st);
+// Debug: expand supertile lists into the per-tile lists of view vi.
+void launch_dbg_tile_lists(const DevView* views, int vi, int ntiles, const uint2* rect_sorted,
+                           const uint32_t* lists, const int2* ranges, uint32_t* tcount,
+                           const uint32_t* toff, const uint32_t* order, const int32_t* gidx,
+                           int32_t* tile_out, int32_t* gauss_out, int32_t* tranges, bool count,
+                           cudaStream_t st);
 
 // K7: rasterizer.
 struct RasterArgs {
     const DevView* views;
     int n_views;
     int max_tiles;
-    const int2* ranges;          // per view at range_off[v]
-    const int* range_off;
-    const unsigned long long* pairs;
-    const float4* rec_sorted;
+    const int2* ranges;          // supertile ranges, per view at V.range_off
+    const uint32_t* lists;       // supertile lists of depth ranks, per view at V.pair_off
+    const uint2* rect_sorted;    // tile rectangles by rank, per view at V.cap_off
+    const float4* rec_sorted;    // splat records by rank, per view at V.cap_off
     unsigned long long* evals;   // [n_views][2] (E_alg, E_exec) or NULL
     float exp2_c0;               // 1.535336188319500e-4f (set by launch_raster)
 };
@@ -215,8 +214,5 @@ void launch_life_flip(float2* life, long long n, cudaStream_t st);
 // Debug helpers.
 void launch_dump_order(const uint32_t* order, const int32_t* gidx, long long base,
                        long long count, int32_t* out, cudaStream_t st);
-void launch_dump_pairs(const unsigned long long* pairs, long long count, const uint32_t* order,
-                       const int32_t* gidx, long long base, int32_t* tile_out,
-                       int32_t* gauss_out, cudaStream_t st);
 
 }  // namespace s3r

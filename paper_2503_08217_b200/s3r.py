@@ -23,7 +23,7 @@ _lock = threading.Lock()
 _lib = None
 
 S3R_OK, S3R_EINVAL, S3R_EINSTANCE, S3R_ENOMEM, S3R_ECUDA, S3R_ESTATE = 0, -1, -2, -3, -4, -5
-STAGES = ["filter", "project", "depth_sort", "emit", "pair_sort", "ranges", "raster"]
+STAGES = ["filter", "project", "depth_sort", "bin", "raster"]
 TILE = 16
 # every symbol include/s3r.h declares
 EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_set_debug",
@@ -62,7 +62,7 @@ class Outputs_(C.Structure):
 class Stats_(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("n_scene", "n_temporal", "n_visible", "n_lod_small",
                                          "n_lod_dropped", "n_rendered", "n_pairs",
-                                         "n_bad_instance", "n_blend_evals",
+                                         "n_bad_instance", "n_bin_pairs", "n_blend_evals",
                                          "n_blend_exec")]
 
 
