@@ -131,6 +131,7 @@ def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
     Nv = sum(s["n_visible"] for s in stats)
     Nr = sum(s["n_rendered"] for s in stats)
     Ps = sum(s["n_bin_pairs"] for s in stats)
+    P = sum(s["n_pairs"] for s in stats)
     px = sum(v.width * v.height for v in views)
     tiles = sum(((v.width + 15) // 16) * ((v.height + 15) // 16) for v in views)
     # K1 writes each distinct time's list once
@@ -139,10 +140,11 @@ def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
         "filter": 8 * n_scene * math.ceil(max(n_distinct_t, 1) / 64) + 4 * nt_distinct,
         "project": 56 * Nt + 8 * Nv + (16 + 48 + 8) * Nr,
         "depth_sort": 8 * Nr + depth_passes * 24 * Nr,
-        # permute (order + record in/out + rectangle) + count + scatter (rect + 4 B/pair)
-        "bin": (4 + 48 + 48 + 8) * Nr + 8 * Nr + 8 * Nr + 4 * Ps,
-        # one read of the supertile lists (rank + rectangle), unique records, images
-        "raster": 12 * Ps + 48 * Nr + 20 * px,
+        # permute (order + record in/out + rectangle) + count + scatter (rect + 4 B per
+        # supertile pair) + expand (supertile list + rectangle in, 4 B per tile pair out)
+        "bin": (4 + 48 + 48 + 8) * Nr + 8 * Nr + 8 * Nr + 4 * Ps + 12 * Ps + 4 * P,
+        # tile lists (4 B per pair), unique records, images
+        "raster": 4 * P + 48 * Nr + 20 * px,
     }
 
 

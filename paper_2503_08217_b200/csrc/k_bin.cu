@@ -125,9 +125,82 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
     const uint32_t total = s_carry;
     int2* R = ranges + V.range_off;
     for (int b = tid; b < V.nbins; b += 1024) {
+        if (V.nchunks == 0) {           // nothing rendered in this view
+            R[b] = make_int2(0, 0);
+            continue;
+        }
         const uint32_t s = a[(long long)b * V.nchunks];
         const uint32_t e = (b + 1 < V.nbins) ? a[(long long)(b + 1) * V.nchunks] : total;
         R[b] = make_int2((int)s, (int)e);
+    }
+}
+
+// ------------------------------------------------------------------ K4 expand
+// One CTA per (supertile, view): the supertile's list is staged in shared
+// memory 512 entries at a time; warp w keeps, for each of its tiles, the
+// entries whose rectangle contains the tile (ballot + popc: list order is
+// kept), and appends them to the tile's list.  Tile t (local index in the
+// supertile, S*S of them) owns [S*S*start + t*len, +len) of the view's tile-list
+// area, len = supertile list length, so no count pass is needed.
+constexpr int XT = 512;
+__global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ views,
+                                                   const uint2* __restrict__ rect_sorted,
+                                                   const uint32_t* __restrict__ lists,
+                                                   const int2* __restrict__ ranges,
+                                                   uint32_t* __restrict__ tlists,
+                                                   int2* __restrict__ tranges)
+{
+    __shared__ uint32_t s_r[XT];
+    __shared__ uint2 s_rect[XT];
+    const DevView& V = views[blockIdx.y];
+    const int b = blockIdx.x;
+    if (b >= V.nbins) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int S = 1 << V.sshift, SS = S * S;
+    const int bx = b % V.STX, by = b / V.STX;
+    const int2 rg = ranges[V.range_off + b];
+    const int len = rg.y - rg.x;
+    const uint32_t* lst = lists + V.pair_off;
+    const uint2* rects = rect_sorted + V.cap_off;
+    uint32_t* out = tlists + V.tlist_off + (long long)SS * rg.x;
+    // running count of each tile's list (tile t is owned by warp t % 16)
+    __shared__ int s_tcnt[MAX_BINS];              // S*S <= MAX_BINS tiles per supertile
+    for (int t = tid; t < SS; t += XT) s_tcnt[t] = 0;
+    __syncthreads();
+    for (int base = rg.x; base < rg.y; base += XT) {
+        const int n = min(XT, rg.y - base);
+        if (tid < n) {
+            const uint32_t r = lst[base + tid];
+            s_r[tid] = r;
+            s_rect[tid] = rects[r];
+        }
+        __syncthreads();
+        for (int t = warp; t < SS; t += XT / 32) {
+            const int tx = bx * S + (t % S), ty = by * S + (t / S);
+            if (tx >= V.TX || ty >= V.TY) continue;
+            int c = s_tcnt[t];
+            for (int k = 0; k < n; k += 32) {
+                const int e = k + lane;
+                bool pass = false;
+                if (e < n) {
+                    const uint2 rr = s_rect[e];
+                    pass = tx >= (int)(rr.x & 0xffff) && tx <= (int)(rr.x >> 16) &&
+                           ty >= (int)(rr.y & 0xffff) && ty <= (int)(rr.y >> 16);
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, pass);
+                if (pass) out[(long long)t * len + c + __popc(bal & ((1u << lane) - 1u))] = s_r[e];
+                c += __popc(bal);
+            }
+            __syncwarp();
+            if (lane == 0) s_tcnt[t] = c;
+        }
+        __syncthreads();
+    }
+    for (int t = tid; t < SS; t += XT) {
+        const int tx = bx * S + (t % S), ty = by * S + (t / S);
+        if (tx >= V.TX || ty >= V.TY) continue;
+        const long long s0 = (long long)SS * rg.x + (long long)t * len;
+        tranges[V.trange_off + ty * V.TX + tx] = make_int2((int)s0, (int)(s0 + s_tcnt[t]));
     }
 }
 
@@ -197,54 +270,31 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
 }
 
 // ------------------------------------------------------------------ debug
-// Per-tile list of view V: entries of the tile's supertile list whose tile
-// rectangle contains the tile, in list order (== (tile, depth, index) order).
-__global__ void k_dbg_tile_count(const DevView* __restrict__ views, int vi,
-                                 const uint2* __restrict__ rect_sorted,
-                                 const uint32_t* __restrict__ lists, const int2* __restrict__ ranges,
-                                 uint32_t* __restrict__ tcount)
+// The per-tile lists of view vi packed in tile order as (tile, Gaussian) pairs
+// ((tile, depth, index) order) with [start, end) ranges; toff = exclusive scan
+// of the tile list lengths.
+__global__ void k_dbg_tile_pairs(const DevView* __restrict__ views, int vi,
+                                 const uint32_t* __restrict__ tlists,
+                                 const int2* __restrict__ tranges, const uint32_t* __restrict__ toff,
+                                 const uint32_t* __restrict__ order, const int32_t* __restrict__ gidx,
+                                 int32_t* __restrict__ tile_out, int32_t* __restrict__ gauss_out,
+                                 int32_t* __restrict__ ranges_out)
 {
     const DevView& V = views[vi];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= V.ntiles) return;
-    const int tx = t % V.TX, ty = t / V.TX;
-    const int b = (ty >> V.sshift) * V.STX + (tx >> V.sshift);
-    const int2 rg = ranges[V.range_off + b];
-    uint32_t n = 0;
+    const int2 rg = tranges[V.trange_off + t];
+    const uint32_t o0 = toff[t];
     for (int i = rg.x; i < rg.y; ++i) {
-        int tx0, tx1, ty0, ty1;
-        rect_of(rect_sorted[V.cap_off + lists[V.pair_off + i]], tx0, tx1, ty0, ty1);
-        n += (tx >= tx0 && tx <= tx1 && ty >= ty0 && ty <= ty1) ? 1u : 0u;
+        const uint32_t r = tlists[V.tlist_off + i];
+        const uint32_t o = o0 + (uint32_t)(i - rg.x);
+        if (tile_out) tile_out[o] = t;
+        if (gauss_out) gauss_out[o] = gidx[V.cap_off + order[V.cap_off + r]];
     }
-    tcount[t] = n;
-}
-
-__global__ void k_dbg_tile_write(const DevView* __restrict__ views, int vi,
-                                 const uint2* __restrict__ rect_sorted,
-                                 const uint32_t* __restrict__ lists, const int2* __restrict__ ranges,
-                                 const uint32_t* __restrict__ toff, const uint32_t* __restrict__ order,
-                                 const int32_t* __restrict__ gidx, int32_t* __restrict__ tile_out,
-                                 int32_t* __restrict__ gauss_out, int32_t* __restrict__ tranges)
-{
-    const DevView& V = views[vi];
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= V.ntiles) return;
-    const int tx = t % V.TX, ty = t / V.TX;
-    const int b = (ty >> V.sshift) * V.STX + (tx >> V.sshift);
-    const int2 rg = ranges[V.range_off + b];
-    uint32_t o = toff[t];
-    if (tranges) tranges[2 * t] = (int32_t)o;
-    for (int i = rg.x; i < rg.y; ++i) {
-        const uint32_t r = lists[V.pair_off + i];
-        int tx0, tx1, ty0, ty1;
-        rect_of(rect_sorted[V.cap_off + r], tx0, tx1, ty0, ty1);
-        if (tx >= tx0 && tx <= tx1 && ty >= ty0 && ty <= ty1) {
-            if (tile_out) tile_out[o] = t;
-            if (gauss_out) gauss_out[o] = gidx[V.cap_off + order[V.cap_off + r]];
-            ++o;
-        }
+    if (ranges_out) {
+        ranges_out[2 * t] = (int32_t)o0;
+        ranges_out[2 * t + 1] = (int32_t)(o0 + (uint32_t)(rg.y - rg.x));
     }
-    if (tranges) tranges[2 * t + 1] = (int32_t)o;
 }
 
 }  // namespace
@@ -262,31 +312,31 @@ void launch_permute(const DevView* views, int n_views, long long max_rendered,
 
 void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
                 const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
-                cudaStream_t st)
+                uint32_t* tlists, int2* tranges, cudaStream_t st)
 {
-    if (n_views == 0 || max_chunks == 0) return;
+    if (n_views == 0) return;
     dim3 grid(max_chunks, n_views);
-    k_bin_count<<<grid, KT, (size_t)max_bins * 4, st>>>(views, rect_sorted, cnt);
+    if (max_chunks) k_bin_count<<<grid, KT, (size_t)max_bins * 4, st>>>(views, rect_sorted, cnt);
     k_bin_scan<<<n_views, 1024, 0, st>>>(views, cnt, ranges);
-    const size_t smem = (size_t)max_bins * 4 * (1 + KWARPS);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bin_scatter<<<grid, KT, smem, st>>>(views, rect_sorted, cnt, lists);
+    if (max_chunks) {
+        const size_t smem = (size_t)max_bins * 4 * (1 + KWARPS);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        k_bin_scatter<<<grid, KT, smem, st>>>(views, rect_sorted, cnt, lists);
+    }
+    k_bin_expand<<<dim3(max_bins, n_views), XT, 0, st>>>(views, rect_sorted, lists, ranges, tlists,
+                                                       tranges);
 }
 
-void launch_dbg_tile_lists(const DevView* views, int vi, int ntiles, const uint2* rect_sorted,
-                           const uint32_t* lists, const int2* ranges, uint32_t* tcount,
-                           const uint32_t* toff, const uint32_t* order, const int32_t* gidx,
-                           int32_t* tile_out, int32_t* gauss_out, int32_t* tranges, bool count,
-                           cudaStream_t st)
+void launch_dbg_tile_pairs(const DevView* views, int vi, int ntiles, const uint32_t* tlists,
+                           const int2* tranges, const uint32_t* toff, const uint32_t* order,
+                           const int32_t* gidx, int32_t* tile_out, int32_t* gauss_out,
+                           int32_t* ranges_out, cudaStream_t st)
 {
     if (ntiles == 0) return;
-    const unsigned g = (unsigned)((ntiles + 127) / 128);
-    if (count)
-        k_dbg_tile_count<<<g, 128, 0, st>>>(views, vi, rect_sorted, lists, ranges, tcount);
-    else
-        k_dbg_tile_write<<<g, 128, 0, st>>>(views, vi, rect_sorted, lists, ranges, toff, order,
-                                            gidx, tile_out, gauss_out, tranges);
+    k_dbg_tile_pairs<<<(unsigned)((ntiles + 127) / 128), 128, 0, st>>>(
+        views, vi, tlists, tranges, toff, order, gidx, tile_out, gauss_out, ranges_out);
 }
 
 }  // namespace s3r

@@ -13,11 +13,10 @@
 // Layout: one 64-thread CTA per (view, tile); each thread owns 4 pixels of one
 // column (rows ly, ly+4, ly+8, ly+12), so the per-splat dx terms and the
 // shared-memory record loads are amortised over 4 pixel evaluations.  The CTA
-// walks its SUPERTILE's depth-ordered list (k_bin.cu) 64 entries at a time,
-// keeps the entries whose rectangle contains its tile (ballot + popc, order
-// preserved) and stages up to 256 of their 48-byte records in shared memory;
-// every pixel then blends the batch.  A pixel stops at its termination; the
-// CTA stops when all its pixels have (__syncthreads_count).
+// walks its tile's depth-ordered list of ranks (k_bin.cu) and stages 256 of
+// the 48-byte records at a time in shared memory; every pixel then blends the
+// batch.  A pixel stops at its termination; the CTA stops when all its pixels
+// have (__syncthreads_count).
 #include "s3r_internal.cuh"
 
 namespace s3r {
@@ -45,7 +44,6 @@ __device__ __forceinline__ float s3r_exp2(float x, float c0)
 }
 
 constexpr int RT = 64;      // threads per tile CTA: 16 columns x 4 row groups
-constexpr int RW = RT / 32;
 constexpr int RPIX = 4;     // pixels per thread: rows ly, ly+4, ly+8, ly+12 of one column
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
@@ -53,12 +51,11 @@ template <bool COUNT>
 __global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
-    __shared__ int s_wsum[RW];
     const int v = blockIdx.y;
     const DevView& V = a.views[v];
     const int tile = blockIdx.x;
     if (tile >= V.ntiles) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % V.TX, ty = tile / V.TX;
     const int px = tx * TILE + (tid & 15);
     const int py0 = ty * TILE + (tid >> 4);
@@ -79,10 +76,8 @@ __global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
         inside |= (in ? 1u : 0u) << k;
         nlive += in ? 1 : 0;
     }
-    const int bin = (ty >> V.sshift) * V.STX + (tx >> V.sshift);
-    const int2 rg = a.ranges[V.range_off + bin];
-    const uint32_t* lst = a.lists + V.pair_off;
-    const uint2* rects = a.rect_sorted + V.cap_off;
+    const int2 rg = a.tranges[V.trange_off + tile];
+    const uint32_t* lst = a.tlists + V.tlist_off;
     const float4* recs = a.rec_sorted + 3 * V.cap_off;
     // first Horner coefficient of s3r_exp2 (1.535336188319500e-4f), a kernel
     // argument so it stays in a register (an immediate is re-materialised per use)
@@ -93,39 +88,16 @@ __global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
     uint32_t n_exec = 0;
     while (cur < rg.y) {
         if (__syncthreads_count(nlive) == 0) break;
-        // ---- fill: keep the supertile-list entries whose rectangle holds this tile
-        int nb = 0;
-        while (cur < rg.y && nb <= RB - RT) {
-            const int i = cur + tid;
-            bool pass = false;
-            uint32_t r = 0;
-            if (i < rg.y) {
-                r = lst[i];
-                const uint2 rr = rects[r];
-                pass = tx >= (int)(rr.x & 0xffff) && tx <= (int)(rr.x >> 16) &&
-                       ty >= (int)(rr.y & 0xffff) && ty <= (int)(rr.y >> 16);
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, pass);
-            if (lane == 0) s_wsum[warp] = __popc(bal);
-            __syncthreads();
-            int before = 0, tot = 0;
-#pragma unroll
-            for (int w = 0; w < RW; ++w) {
-                const int c = s_wsum[w];
-                before += (w < warp) ? c : 0;
-                tot += c;
-            }
-            if (pass) {
-                const int slot = nb + before + __popc(bal & ((1u << lane) - 1u));
-                const float4* src = recs + 3ll * r;
-                s_rec[3 * slot + 0] = src[0];
-                s_rec[3 * slot + 1] = src[1];
-                s_rec[3 * slot + 2] = src[2];
-            }
-            nb += tot;
-            cur += RT;
-            __syncthreads();
+        // ---- stage the next RB records of the tile's list (16-byte loads)
+        const int nb = min(RB, rg.y - cur);
+        for (int i = tid; i < nb; i += RT) {
+            const float4* src = recs + 3ll * lst[cur + i];
+            s_rec[3 * i + 0] = src[0];
+            s_rec[3 * i + 1] = src[1];
+            s_rec[3 * i + 2] = src[2];
         }
+        __syncthreads();
+        cur += nb;
         n_exec += nb;
         if (nlive) {
             for (int j = 0; j < nb; ++j) {

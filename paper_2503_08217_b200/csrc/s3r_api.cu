@@ -52,7 +52,8 @@ struct s3r_ctx {
     cudaStream_t last_stream = nullptr;
     // device scratch
     Buf d_views, d_times, d_tidx, d_counts, d_lb, d_ticket, d_ctr, d_rec, d_dkey, d_gidx,
-        d_sortk[2], d_sortv[2], d_recs, d_rects, d_lists, d_cnt, d_hist, d_dsegs, d_dtile0,
+        d_sortk[2], d_sortv[2], d_recs, d_rects, d_lists, d_tlists, d_tranges, d_cnt, d_hist,
+        d_dsegs, d_dtile0,
         d_ranges, d_err, d_dbg_keys, d_dbg_flags, d_dbg_rect, d_dbg_tcnt;
     int ticket_slot = 0;
     int gbits = 1;
@@ -380,7 +381,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->stats.assign(nv, s3r_stats{});
     std::vector<int> dt0(nv + 1, 0);
     long long total_pairs = 0, total_cnt = 0, max_r = 0;
-    int total_bins = 0, max_chunks = 0, max_bins = 0;
+    int total_bins = 0, max_chunks = 0, max_bins = 0, total_tiles = 0;
+    long long total_tlist = 0;
     int max_tiles = 0;
     bool bad = false;
     const int stile = onesweep64_tile();
@@ -395,6 +397,13 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         d.range_off = total_bins;
         d.cnt_off = total_cnt;
         d.pair_off = total_pairs;
+        d.tlist_off = total_tlist;
+        d.trange_off = total_tiles;
+        const long long SS = 1ll << (2 * d.sshift);
+        if (SS * (long long)k.n_spairs >= (1ll << 31))
+            return fail(c, S3R_EINVAL, "view %d: tile-list area exceeds 2^31 entries", v);
+        total_tlist += SS * (long long)k.n_spairs;
+        total_tiles += d.ntiles;
         total_bins += d.nbins;
         total_cnt += (long long)d.nbins * d.nchunks;
         total_pairs += (long long)k.n_spairs;
@@ -442,6 +451,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if ((rc = ensure(c, c->d_recs, (size_t)capS * 48))) return rc;
     if ((rc = ensure(c, c->d_rects, (size_t)capS * 8))) return rc;
     if ((rc = ensure(c, c->d_lists, (size_t)std::max<long long>(total_pairs, 1) * 4))) return rc;
+    if ((rc = ensure(c, c->d_tlists, (size_t)std::max<long long>(total_tlist, 1) * 4))) return rc;
+    if ((rc = ensure(c, c->d_tranges, (size_t)std::max(total_tiles, 1) * sizeof(int2)))) return rc;
     if ((rc = ensure(c, c->d_cnt, (size_t)std::max<long long>(total_cnt, 1) * 4))) return rc;
     const int dpasses = (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS;
     if ((rc = ensure(c, c->d_hist, (size_t)std::max(nv, 1) * dpasses * RADIX * 4))) return rc;
@@ -481,7 +492,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         launch_permute(P<DevView>(c->d_views), nv, max_r, P<uint32_t>(c->d_sortv[c->final_order]),
                        P<float4>(c->d_rec), P<float4>(c->d_recs), P<uint2>(c->d_rects), st);
         launch_bin(P<DevView>(c->d_views), nv, max_chunks, max_bins, P<uint2>(c->d_rects),
-                   P<uint32_t>(c->d_cnt), P<int2>(c->d_ranges), P<uint32_t>(c->d_lists), st);
+                   P<uint32_t>(c->d_cnt), P<int2>(c->d_ranges), P<uint32_t>(c->d_lists),
+                   P<uint32_t>(c->d_tlists), P<int2>(c->d_tranges), st);
         ev_end(c, st, e);
     }
     CU(cudaGetLastError());
@@ -494,9 +506,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.views = P<DevView>(c->d_views);
         a.n_views = nv;
         a.max_tiles = max_tiles;
-        a.ranges = P<int2>(c->d_ranges);
-        a.lists = P<uint32_t>(c->d_lists);
-        a.rect_sorted = P<uint2>(c->d_rects);
+        a.tranges = P<int2>(c->d_tranges);
+        a.tlists = P<uint32_t>(c->d_tlists);
         a.rec_sorted = P<float4>(c->d_recs);
         a.evals = nullptr;
         if (c->counters && nv) {
@@ -561,6 +572,7 @@ void s3r_destroy(s3r_ctx* c)
     Buf* bufs[] = {&c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
                    &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
                    &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_rects, &c->d_lists,
+                   &c->d_tlists, &c->d_tranges,
                    &c->d_cnt, &c->d_hist, &c->d_dsegs, &c->d_dtile0, &c->d_ranges, &c->d_err,
                    &c->d_dbg_keys, &c->d_dbg_flags, &c->d_dbg_rect, &c->d_dbg_tcnt, &c->d_evals};
     for (Buf* b : bufs)
@@ -786,32 +798,29 @@ int s3r_dump_intermediates(s3r_ctx* c, int32_t vi, const s3r_debug* dbg, void* s
     if (dbg->depth_order)
         launch_dump_order(order, P<int32_t>(c->d_gidx), d.cap_off, d.n_rendered, dbg->depth_order, st);
     if (dbg->pair_tile || dbg->pair_gauss || dbg->ranges) {
-        // expand the view's supertile lists into its per-tile lists (reading R11/R12):
-        // count per tile, exclusive scan (host; debug path), write in list order
+        // pack the view's per-tile lists in tile order (exclusive scan of their
+        // lengths on the host; debug path) as (tile, Gaussian) pairs + ranges
         int rc;
         const int nt = d.ntiles;
-        if ((rc = ensure(c, c->d_dbg_tcnt, (size_t)(2 * nt + 1) * 4))) return rc;
-        uint32_t* tcnt = P<uint32_t>(c->d_dbg_tcnt);
-        uint32_t* toff = tcnt + nt;
-        launch_dbg_tile_lists(P<DevView>(c->d_views), vi, nt, P<uint2>(c->d_rects),
-                              P<uint32_t>(c->d_lists), P<int2>(c->d_ranges), tcnt, nullptr, order,
-                              nullptr, nullptr, nullptr, nullptr, true, st);
-        std::vector<uint32_t> h(nt);
-        CU(cudaMemcpyAsync(h.data(), tcnt, (size_t)nt * 4, cudaMemcpyDeviceToHost, st));
+        if ((rc = ensure(c, c->d_dbg_tcnt, (size_t)(nt + 1) * 4))) return rc;
+        uint32_t* toff = P<uint32_t>(c->d_dbg_tcnt);
+        std::vector<int2> tr(nt);
+        CU(cudaMemcpyAsync(tr.data(), P<int2>(c->d_tranges) + d.trange_off, (size_t)nt * sizeof(int2),
+                           cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
+        std::vector<uint32_t> h(nt);
         uint32_t run = 0;
         for (int t = 0; t < nt; ++t) {
-            const uint32_t x = h[t];
             h[t] = run;
-            run += x;
+            run += (uint32_t)(tr[t].y - tr[t].x);
         }
         if ((long long)run != d.n_pairs)
             return fail(c, S3R_ECUDA, "dump: tile lists hold %u pairs, expected %lld", run, d.n_pairs);
         CU(cudaMemcpyAsync(toff, h.data(), (size_t)nt * 4, cudaMemcpyHostToDevice, st));
-        launch_dbg_tile_lists(P<DevView>(c->d_views), vi, nt, P<uint2>(c->d_rects),
-                              P<uint32_t>(c->d_lists), P<int2>(c->d_ranges), nullptr, toff, order,
+        launch_dbg_tile_pairs(P<DevView>(c->d_views), vi, nt, P<uint32_t>(c->d_tlists),
+                              P<int2>(c->d_tranges), toff, order,
                               c->last_debug ? P<int32_t>(c->d_gidx) : nullptr, dbg->pair_tile,
-                              dbg->pair_gauss, dbg->ranges, false, st);
+                              dbg->pair_gauss, dbg->ranges, st);
         CU(cudaStreamSynchronize(st));
     }
     CU(cudaGetLastError());

@@ -92,6 +92,8 @@ struct DevView {
     int sshift, STX, STY, nbins, nchunks;
     int range_off;           // offset of the view's supertile ranges
     long long cnt_off;       // offset of the view's (bin, chunk) counts
+    long long tlist_off;     // offset of the view's tile-list area (S*S * supertile pairs)
+    int trange_off;          // offset of the view's tile ranges (ntiles entries)
 };
 
 // Per-view counters written by K2 (device, zeroed per batch)
@@ -182,24 +184,23 @@ void launch_permute(const DevView* views, int n_views, long long max_rendered,
 // K4: stable counting sort of (supertile, rank) pairs: count, scan, scatter.
 int bin_chunk();
 constexpr int MAX_BINS = 1024;   // supertiles per view (S grows for huge images)
+// ... then K4 expand: per-tile lists (ranks) + tile ranges from the supertile lists.
 void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
                 const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
-                cudaStream_t st);
-// Debug: expand supertile lists into the per-tile lists of view vi.
-void launch_dbg_tile_lists(const DevView* views, int vi, int ntiles, const uint2* rect_sorted,
-                           const uint32_t* lists, const int2* ranges, uint32_t* tcount,
-                           const uint32_t* toff, const uint32_t* order, const int32_t* gidx,
-                           int32_t* tile_out, int32_t* gauss_out, int32_t* tranges, bool count,
-                           cudaStream_t st);
+                uint32_t* tlists, int2* tranges, cudaStream_t st);
+// Debug: the per-tile lists of view vi as (tile, Gaussian) pairs + [start,end) ranges.
+void launch_dbg_tile_pairs(const DevView* views, int vi, int ntiles, const uint32_t* tlists,
+                           const int2* tranges, const uint32_t* toff, const uint32_t* order,
+                           const int32_t* gidx, int32_t* tile_out, int32_t* gauss_out,
+                           int32_t* ranges_out, cudaStream_t st);
 
 // K7: rasterizer.
 struct RasterArgs {
     const DevView* views;
     int n_views;
     int max_tiles;
-    const int2* ranges;          // supertile ranges, per view at V.range_off
-    const uint32_t* lists;       // supertile lists of depth ranks, per view at V.pair_off
-    const uint2* rect_sorted;    // tile rectangles by rank, per view at V.cap_off
+    const int2* tranges;         // tile ranges, per view at V.trange_off
+    const uint32_t* tlists;      // tile lists of depth ranks, per view at V.tlist_off
     const float4* rec_sorted;    // splat records by rank, per view at V.cap_off
     unsigned long long* evals;   // [n_views][2] (E_alg, E_exec) or NULL
     float exp2_c0;               // 1.535336188319500e-4f (set by launch_raster)
