@@ -48,7 +48,7 @@ constexpr int RPIX = 4;     // pixels per thread: rows ly, ly+4, ly+8, ly+12 of 
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
 template <bool COUNT>
-__global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
+__global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
     const int v = blockIdx.y;
@@ -116,19 +116,24 @@ __global__ void __launch_bounds__(RT) k_raster(RasterArgs a)
                     const float dy = q0.y - fpy[k];
                     const float c1 = __fmaf_rn(q1.z, dy, b1);
                     const float e2 = fminf(0.0f, __fmaf_rn(dy, c1, a2));
-                    // live pixel (T >= 1e-4) and a non-zero exp2 (s3r_exp2 flushes
-                    // below -44: alpha = 0 would leave C, D and T bit-identical)
-                    if (e2 >= -44.0f && T[k] >= 1e-4f) {
-                        const float alpha = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
-                        const float w = alpha * T[k];
-                        cr[k] = __fmaf_rn(q2.x, w, cr[k]);
-                        cg[k] = __fmaf_rn(q2.y, w, cg[k]);
-                        cb[k] = __fmaf_rn(q2.z, w, cb[k]);
-                        dp[k] = __fmaf_rn(q0.z, w, dp[k]);
-                        T[k] = T[k] - w;
-                        // include-then-stop (R14): the pixel is dead once T < 1e-4
-                        if (COUNT && T[k] < 1e-4f) stop[k] = tpos + j + 1;
-                    }
+                    // Branch-free: a dead pixel (T < 1e-4) or a flushed exp2 (e2 < -44,
+                    // s3r_exp2 = 0) gets alpha = 0, which leaves C, D and T
+                    // bit-identical (fma(c, 0, C) == C, T - 0 == T); s3r_exp2's value
+                    // for e2 < -44 is discarded by the select.
+                    const bool on = (e2 >= -44.0f) && (T[k] >= 1e-4f);
+                    const float a_on = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
+                    float alpha;   // selp keeps the exp2 unconditional (no branch)
+                    asm("{ .reg .pred p; setp.ne.u32 p, %3, 0; selp.f32 %0, %1, %2, p; }"
+                        : "=f"(alpha)
+                        : "f"(a_on), "f"(0.0f), "r"((unsigned)on));
+                    const float w = alpha * T[k];
+                    cr[k] = __fmaf_rn(q2.x, w, cr[k]);
+                    cg[k] = __fmaf_rn(q2.y, w, cg[k]);
+                    cb[k] = __fmaf_rn(q2.z, w, cb[k]);
+                    dp[k] = __fmaf_rn(q0.z, w, dp[k]);
+                    // include-then-stop (R14): the pixel is dead once T < 1e-4
+                    if (COUNT && on && T[k] - w < 1e-4f) stop[k] = tpos + j + 1;
+                    T[k] = T[k] - w;
                 }
                 const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
                 if (tmax < 1e-4f) {
