@@ -57,8 +57,11 @@ __global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
     if (tile >= V.ntiles) return;
     const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % V.TX, ty = tile / V.TX;
-    const int px = tx * TILE + (tid & 15);
-    const int py0 = ty * TILE + (tid >> 4);
+    // warp w owns columns 8w..8w+7; for pixel k a warp covers a compact 8x4 block
+    // (rows 4k..4k+3), so a small splat leaves most (warp, k) blocks untouched and
+    // they are skipped warp-uniformly
+    const int px = tx * TILE + ((tid >> 5) << 3) + (lane & 7);
+    const int py0 = ty * TILE + (lane >> 3);
     const float fpx = (float)px;
     float fpy[RPIX], T[RPIX], cr[RPIX], cg[RPIX], cb[RPIX], dp[RPIX];
     int stop[RPIX];
@@ -121,19 +124,22 @@ __global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
                     // bit-identical (fma(c, 0, C) == C, T - 0 == T); s3r_exp2's value
                     // for e2 < -44 is discarded by the select.
                     const bool on = (e2 >= -44.0f) && (T[k] >= 1e-4f);
-                    const float a_on = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
-                    float alpha;   // selp keeps the exp2 unconditional (no branch)
-                    asm("{ .reg .pred p; setp.ne.u32 p, %3, 0; selp.f32 %0, %1, %2, p; }"
-                        : "=f"(alpha)
-                        : "f"(a_on), "f"(0.0f), "r"((unsigned)on));
-                    const float w = alpha * T[k];
-                    cr[k] = __fmaf_rn(q2.x, w, cr[k]);
-                    cg[k] = __fmaf_rn(q2.y, w, cg[k]);
-                    cb[k] = __fmaf_rn(q2.z, w, cb[k]);
-                    dp[k] = __fmaf_rn(q0.z, w, dp[k]);
-                    // include-then-stop (R14): the pixel is dead once T < 1e-4
-                    if (COUNT && on && T[k] - w < 1e-4f) stop[k] = tpos + j + 1;
-                    T[k] = T[k] - w;
+                    // warp-uniform skip when no lane of the warp needs this pixel
+                    if (__any_sync(0xffffffffu, on)) {
+                        const float a_on = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
+                        float alpha;   // selp: lanes that are off get alpha = 0
+                        asm("{ .reg .pred p; setp.ne.u32 p, %3, 0; selp.f32 %0, %1, %2, p; }"
+                            : "=f"(alpha)
+                            : "f"(a_on), "f"(0.0f), "r"((unsigned)on));
+                        const float w = alpha * T[k];
+                        cr[k] = __fmaf_rn(q2.x, w, cr[k]);
+                        cg[k] = __fmaf_rn(q2.y, w, cg[k]);
+                        cb[k] = __fmaf_rn(q2.z, w, cb[k]);
+                        dp[k] = __fmaf_rn(q0.z, w, dp[k]);
+                        // include-then-stop (R14): the pixel is dead once T < 1e-4
+                        if (COUNT && on && T[k] - w < 1e-4f) stop[k] = tpos + j + 1;
+                        T[k] = T[k] - w;
+                    }
                 }
                 const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
                 if (tmax < 1e-4f) {
