@@ -102,7 +102,9 @@ __global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
         __syncthreads();
         cur += nb;
         n_exec += nb;
-        if (nlive) {
+        // the blend loop is warp-uniform (every lane runs it while any lane of
+        // its warp is live) so that the votes below see the full warp
+        if (__any_sync(0xffffffffu, nlive != 0)) {
             for (int j = 0; j < nb; ++j) {
                 const float4* sr = s_rec + 3 * j;
                 const float4 q0 = sr[0];   // mx, my, z, o
@@ -142,10 +144,8 @@ __global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
                     }
                 }
                 const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
-                if (tmax < 1e-4f) {
-                    nlive = 0;
-                    break;
-                }
+                nlive = tmax >= 1e-4f ? 1 : 0;
+                if (!__any_sync(0xffffffffu, nlive != 0)) break;   // whole warp done
             }
         }
         tpos += nb;
