@@ -13,15 +13,17 @@
 /* ------------------------------------------------------------------------
  * s3r_exp2 (DESIGN.md R-ARITH, exp2 form of Eq.2's exponential): 2^x for
  * x <= 0, written so that any IEEE-754 machine evaluates it bit-identically.
- *   x < -44             -> 0        (2^-44 = 5.7e-14; the result is flushed)
+ *   x < -24             -> 0        (flush: a contribution alpha T < 2^-24,
+ *                                    below fp32 resolution of the pixel, is
+ *                                    dropped; reading R14)
  *   t = x + 1.5*2^23;  n = t - 1.5*2^23   (exact rint, ties to even)
  *   r = x - n           (exact, |r| <= 1/2)
  *   y = 1 + r P(r)      Cephes exp2f minimax P (degree 5), Horner with fma
- *   return y * 2^n      (exact: 2^-44 is normal)
+ *   return y * 2^n      (exact: 2^-24 is normal)
  * ---------------------------------------------------------------------- */
 float so_exp2_f32(float x)
 {
-    if (!(x >= -44.0f)) return 0.0f;
+    if (!(x >= -24.0f)) return 0.0f;
     float t = x + 12582912.0f;
     float n = t - 12582912.0f;
     float r = x - n;

@@ -4,6 +4,10 @@ Flags that are part of the numerical contract (DESIGN.md R-ARITH):
   -fmad=false            no multiply-add contraction; FMAs are explicit
   (no --use_fast_math)   IEEE division and square root (-prec-div/-prec-sqrt)
   -ffp-contract=off      for the host compiler as well
+
+``build_variant(name, defines)`` builds an experimental copy
+(``libs3r_<name>.so``, objects under build/<name>/) with extra -D flags; the
+binding loads it when the environment variable S3R_LIB points at it.
 """
 from __future__ import annotations
 
@@ -33,16 +37,17 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def _build(out: str, bdir: str, defines=(), force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(bdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [__file__]
+    dflags = [f"-D{d}" for d in defines]
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            jobs.append([NVCC, *FLAGS, "-c", s, "-o", o])
+            jobs.append([NVCC, *FLAGS, *dflags, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -53,9 +58,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(OUT, objs):
-        run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT, *objs])
-    return OUT
+    if force or jobs or _stale(out, objs):
+        run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out, *objs])
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    return _build(OUT, BUILD, (), force, verbose)
+
+
+def build_variant(name: str, defines, force: bool = False) -> str:
+    return _build(os.path.join(HERE, f"libs3r_{name}.so"), os.path.join(BUILD, name), defines,
+                  force)
 
 
 if __name__ == "__main__":

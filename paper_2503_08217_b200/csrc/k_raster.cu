@@ -23,7 +23,7 @@ namespace s3r {
 
 namespace {
 
-// R-ARITH s3r_exp2 for -44 <= x <= 0 (the caller handles x < -44 -> 0):
+// R-ARITH s3r_exp2 for -24 <= x <= 0 (the caller handles the flush x < -24 -> 0):
 // n = rint(x) by the 1.5*2^23 shifter (all full-rate FADDs, no F2I/FRND),
 // r = x - n exact, 2^r by the Cephes exp2f polynomial, times 2^n built from
 // the shifter's bits: bits(t) = 0x4B400000 + n, so (bits(t) << 23) +
@@ -47,8 +47,30 @@ constexpr int RT = 64;      // threads per tile CTA: 16 columns x 4 row groups
 constexpr int RPIX = 4;     // pixels per thread: rows ly, ly+4, ly+8, ly+12 of one column
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
+// Build-time variants (for A/B measurement; the defaults are the product):
+//   S3R_RASTER_LAYOUT 0: a warp's pixel k is a 16x2 strip; 1: a compact 8x4 block
+//   S3R_RASTER_MODE   0: per-lane branch; 1: warp vote + select; 2: select only
+//   S3R_RASTER_MINB   minimum resident CTAs per SM for __launch_bounds__ (0: none)
+#ifndef S3R_RASTER_LAYOUT
+#define S3R_RASTER_LAYOUT 1
+#endif
+#ifndef S3R_RASTER_MODE
+#define S3R_RASTER_MODE 0
+#endif
+#ifndef S3R_RASTER_MINB
+#define S3R_RASTER_MINB 0
+#endif
+#ifndef S3R_FLUSH_E2
+#define S3R_FLUSH_E2 -24.0f   // s3r_exp2(x) = 0 for x < -24 (R-ARITH flush, reading R14)
+#endif
+#if S3R_RASTER_MINB > 0
+#define S3R_RASTER_BOUNDS __launch_bounds__(RT, S3R_RASTER_MINB)
+#else
+#define S3R_RASTER_BOUNDS __launch_bounds__(RT)
+#endif
+
 template <bool COUNT>
-__global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
+__global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
     const int v = blockIdx.y;
@@ -60,8 +82,13 @@ __global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
     // warp w owns columns 8w..8w+7; for pixel k a warp covers a compact 8x4 block
     // (rows 4k..4k+3), so a small splat leaves most (warp, k) blocks untouched and
     // they are skipped warp-uniformly
+#if S3R_RASTER_LAYOUT == 1
     const int px = tx * TILE + ((tid >> 5) << 3) + (lane & 7);
     const int py0 = ty * TILE + (lane >> 3);
+#else
+    const int px = tx * TILE + (tid & 15);
+    const int py0 = ty * TILE + (tid >> 4);
+#endif
     const float fpx = (float)px;
     float fpy[RPIX], T[RPIX], cr[RPIX], cg[RPIX], cb[RPIX], dp[RPIX];
     int stop[RPIX];
@@ -121,18 +148,26 @@ __global__ void __launch_bounds__(RT, 12) k_raster(RasterArgs a)
                     const float dy = q0.y - fpy[k];
                     const float c1 = __fmaf_rn(q1.z, dy, b1);
                     const float e2 = fminf(0.0f, __fmaf_rn(dy, c1, a2));
-                    // Branch-free: a dead pixel (T < 1e-4) or a flushed exp2 (e2 < -44,
-                    // s3r_exp2 = 0) gets alpha = 0, which leaves C, D and T
-                    // bit-identical (fma(c, 0, C) == C, T - 0 == T); s3r_exp2's value
-                    // for e2 < -44 is discarded by the select.
-                    const bool on = (e2 >= -44.0f) && (T[k] >= 1e-4f);
+                    // A dead pixel (T < 1e-4) or a flushed exp2 (e2 < -24, s3r_exp2 = 0)
+                    // has alpha = 0, which leaves C, D and T bit-identical
+                    // (fma(c, 0, C) == C, T - 0 == T): such evaluations are skipped.
+                    const bool on = (e2 >= S3R_FLUSH_E2) && (T[k] >= 1e-4f);
+#if S3R_RASTER_MODE == 0
+                    if (on) {
+                        const float alpha = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
+#else
+#if S3R_RASTER_MODE == 1
                     // warp-uniform skip when no lane of the warp needs this pixel
                     if (__any_sync(0xffffffffu, on)) {
+#else
+                    {
+#endif
                         const float a_on = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
                         float alpha;   // selp: lanes that are off get alpha = 0
                         asm("{ .reg .pred p; setp.ne.u32 p, %3, 0; selp.f32 %0, %1, %2, p; }"
                             : "=f"(alpha)
                             : "f"(a_on), "f"(0.0f), "r"((unsigned)on));
+#endif
                         const float w = alpha * T[k];
                         cr[k] = __fmaf_rn(q2.x, w, cr[k]);
                         cg[k] = __fmaf_rn(q2.y, w, cg[k]);

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libs3r.so")
+_SO = os.environ.get("S3R_LIB") or os.path.join(_HERE, "libs3r.so")   # S3R_LIB: A/B builds
 _lock = threading.Lock()
 _lib = None
 

@@ -626,8 +626,8 @@ def test_f32_contract_tracks_f64_shadow():
 
 
 def test_exp2_contract():
-    """s3r_exp2 vs the exact 2^x: < 2 ulp on [-44, 0]; 2^0 = 1 and 2^-n exact; flush below -44."""
-    xs = np.float32(-np.linspace(0, 44, 44001))
+    """s3r_exp2 vs the exact 2^x: < 2 ulp on [-24, 0]; 2^0 = 1 and 2^-n exact; flush below -24."""
+    xs = np.float32(-np.linspace(0, 24, 24001))
     worst = 0.0
     for x in xs[::7]:
         got = np.float32(oracle.exp2_32(float(x)))
@@ -635,6 +635,6 @@ def test_exp2_contract():
         ulp = float(np.spacing(np.float32(want)))
         worst = max(worst, abs(float(got) - want) / ulp)
     assert worst < WORK["exp"]["max_ulp"]
-    for k in range(45):
+    for k in range(25):
         assert oracle.exp2_32(-float(k)) == 2.0 ** -k
-    assert oracle.exp2_32(-44.01) == 0.0 and oracle.exp2_32(-1e30) == 0.0
+    assert oracle.exp2_32(-24.01) == 0.0 and oracle.exp2_32(-1e30) == 0.0
