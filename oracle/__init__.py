@@ -19,7 +19,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["s3r_oracle_f32.c", "s3r_oracle_f64.c", "s3r_oracle_impl.inc", "s3r_oracle.h", "Makefile"]
+_SRCS = ["s3r_oracle_f32.c", "s3r_oracle_f64.c", "s3r_oracle_bwd.c", "s3r_oracle_impl.inc",
+         "s3r_oracle.h", "Makefile"]
 _lock = threading.Lock()
 _lib = None
 
@@ -89,6 +90,7 @@ def lib():
                 "so_render_view_f64": (C.c_int, [P, P, P]),
                 "so_blend_bruteforce_f32": (C.c_int, [P, P, P, P, P, P, P, P]),
                 "so_blend_bruteforce_f64": (C.c_int, [P, P, P, P, P, P, P, P]),
+                "so_backward_f64": (C.c_int, [P, P, P, P, P, P]),
                 "so_update_life_f32": (None, [P, P, C.c_float]),
                 "so_commit_visibility": (None, [P, C.c_float]),
                 "so_reset_visibility": (None, [P]),
@@ -197,6 +199,20 @@ def blend_bruteforce(scene, view, flags, keys, rect, precision="f32", table=None
     fn(C.byref(sr.s), C.byref(vr.v), _ptr(flags), _ptr(keys), _ptr(rect), _ptr(rgb),
        _ptr(depth), _ptr(T))
     return rgb, depth, T
+
+
+def backward(scene, view, g_rgb, g_depth=None, g_T=None, table=None, grads=None) -> np.ndarray:
+    """fp64 adjoint: dL/d(raw params) (n, 16) for one view given dL/d(rgb, depth, T)
+    (accumulated into `grads` if given)."""
+    L = lib()
+    sr, vr = _SceneRef(scene, life=False), _ViewRef(view, table)
+    g = np.zeros((scene.n, 16), np.float64) if grads is None else grads
+    f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)
+    a_rgb, a_d, a_t = f(g_rgb), f(g_depth), f(g_T)
+    rc = L.so_backward_f64(C.byref(sr.s), C.byref(vr.v), _ptr(a_rgb), _ptr(a_d), _ptr(a_t),
+                           _ptr(g))
+    assert rc == 0
+    return g
 
 
 def temporal_filter(scene, t, precision="f32") -> np.ndarray:

@@ -110,6 +110,13 @@ void     so_update_life_f32(so_scene* s, const uint8_t* visible, float t);
 void     so_commit_visibility(so_scene* s, float margin);
 void     so_reset_visibility(so_scene* s);
 
+/* ---- f64 adjoint (config 5; s3r_oracle_bwd.c) ------------------------ */
+/* grads += dL/d(raw params) of view v, double[n][16] in scene-row layout
+ * {mu xyz, opacity, sigma xyz, 0, q wxyz, rgb, 0}; g_rgb [H][W][3] required,
+ * g_depth [H][W] and g_T [H][W] optional (NULL = 0). */
+int      so_backward_f64(const so_scene* s, const so_view* v, const double* g_rgb,
+                         const double* g_depth, const double* g_T, double* grads);
+
 /* ---- f64 shadow ------------------------------------------------------ */
 double   so_exp_f64(double x);
 int64_t  so_temporal_filter_f64(const so_scene* s, double t, int32_t* idx);

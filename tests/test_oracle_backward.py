@@ -1,0 +1,110 @@
+"""Pins for the oracle's fp64 adjoint (config 5): central finite differences of
+the fp64 forward, on tiny scenes built so that no piecewise boundary is crossed
+by the perturbation (every Gaussian's 3-sigma box stays inside one 16x16 tile,
+opacities <= 0.6 so neither the 0.99 clamp nor termination is reached).
+Gate (north_star): per attribute, max|g_adjoint - g_fd| <= 1e-3 max|g_fd|."""
+import numpy as np
+import pytest
+from scipy.spatial.transform import Rotation
+
+import oracle
+from helpers import make_scene, make_view
+
+ATTR = {"mean": [0, 1, 2], "opacity": [3], "scale": [4, 5, 6], "rot": [8, 9, 10, 11],
+        "color": [12, 13, 14]}
+
+
+def _scene(seed, n_static=8, n_dyn=4):
+    """Gaussians centred on tile centres of a 64x48 image (f = 80, z in [3, 6])."""
+    rng = np.random.default_rng(seed)
+    centres = [(8 + 16 * i, 8 + 16 * j) for i in range(4) for j in range(3)]
+    pick = rng.permutation(len(centres))
+    n = n_static + n_dyn
+    f, cx, cy = 80.0, 32.0, 24.0
+    pts, ids = [], []
+    Rk = Rotation.from_euler("z", 0.4).as_matrix()
+    tk = np.array([0.1, -0.05, 0.3])
+    for k in range(n):
+        px, py = centres[pick[k % len(centres)]]
+        px += rng.uniform(-1.5, 1.5)
+        py += rng.uniform(-1.5, 1.5)
+        z = rng.uniform(3.0, 6.0)
+        pw = np.array([(px - cx) * z / f, (py - cy) * z / f, z])
+        if k >= n_static:           # dynamic: store in the object's local frame
+            ids.append(1)
+            pts.append(Rk.T @ (pw - tk))
+        else:
+            ids.append(0)
+            pts.append(pw)
+    sig = np.exp(rng.uniform(np.log(0.01), np.log(0.03), (n, 3)))
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    s = make_scene(np.array(pts), sig, quats=q, opacity=rng.uniform(0.2, 0.6, n),
+                   rgb=rng.random((n, 3)), ids=np.array(ids, np.int32), num_instances=2)
+    i2g = np.concatenate([Rk, tk[:, None]], 1)[None]
+    v = make_view(f, cx, 64, 48, cy=cy, i2g=i2g)
+    return s, v, rng
+
+
+def _loss(scene, view, wr, wd, wt):
+    o = oracle.render_view(scene, view, "f64", pairs=False)
+    return float((o["rgb"] * wr).sum() + (o["depth"] * wd).sum() + (o["final_T"] * wt).sum())
+
+
+def _field(scene, col):
+    arr = [scene.means_opacity, scene.scales, scene.rotations, scene.colors][col // 4]
+    return arr, col % 4
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_adjoint_matches_central_differences(seed):
+    s, v, rng = _scene(seed)
+    H, W = v.height, v.width
+    wr = rng.standard_normal((H, W, 3))
+    wd = rng.standard_normal((H, W)) * 0.1
+    wt = rng.standard_normal((H, W))
+    o = oracle.render_view(s, v, "f64", pairs=False)
+    assert o["stats"]["n_rendered"] == s.n and o["final_T"].min() > 1e-3   # no termination
+    g = oracle.backward(s, v, wr, wd, wt)
+    fd = np.zeros_like(g)
+    for gi in range(s.n):
+        for cols in ATTR.values():
+            for col in cols:
+                arr, c = _field(s, col)
+                x0 = arr[gi, c]
+                h = np.float32(max(abs(float(x0)) * 2e-4, 2e-5))
+                arr[gi, c] = x0 + h
+                xp = float(arr[gi, c])
+                lp = _loss(s, v, wr, wd, wt)
+                arr[gi, c] = x0 - h
+                xm = float(arr[gi, c])
+                lm = _loss(s, v, wr, wd, wt)
+                arr[gi, c] = x0
+                fd[gi, col] = (lp - lm) / (xp - xm)
+    for name, cols in ATTR.items():
+        d = np.abs(g[:, cols] - fd[:, cols]).max()
+        ref = np.abs(fd[:, cols]).max()
+        assert ref > 0
+        assert d <= 1e-3 * ref, (name, d, ref)
+
+
+def test_adjoint_is_linear_and_zero_for_zero_cotangent():
+    s, v, rng = _scene(3)
+    H, W = v.height, v.width
+    z = np.zeros((H, W, 3))
+    assert np.all(oracle.backward(s, v, z) == 0)
+    a, b = rng.standard_normal((H, W, 3)), rng.standard_normal((H, W, 3))
+    ga, gb = oracle.backward(s, v, a), oracle.backward(s, v, b)
+    gab = oracle.backward(s, v, 2.0 * a - b)
+    assert np.allclose(gab, 2.0 * ga - gb, rtol=1e-9, atol=1e-12)
+
+
+def test_color_gradient_is_blend_weight_sum():
+    """dL/dc_i for L = sum(rgb) is sum over pixels of w_i (closed form)."""
+    s, v, _ = _scene(4)
+    H, W = v.height, v.width
+    g = oracle.backward(s, v, np.ones((H, W, 3)))
+    # with all colours set to 1, rgb = sum_i w_i per pixel, so sum of dL/dc_r = sum rgb
+    s.colors[:, :3] = 1.0
+    o = oracle.render_view(s, v, "f64", pairs=False)
+    assert abs(g[:, 12].sum() - o["rgb"][..., 0].sum()) < 1e-9 * o["rgb"][..., 0].sum()
