@@ -226,6 +226,49 @@ int s3r_commit_visibility(s3r_ctx* ctx, const s3r_scene* scene, float margin, vo
 /* Periodic reset: v = (-1, 1) for every Gaussian.                   */
 int s3r_reset_visibility(s3r_ctx* ctx, const s3r_scene* scene, void* stream);
 
+/* ---------------------------------------------------------------- training
+ * Backward pass (config 5): the adjoint of the alpha blend (Eq.2) and of the
+ * instance-specific projection (Eq.1) for the views of the LAST
+ * s3r_render_batch, which must have run with s3r_set_training(ctx, 1) (the
+ * forward then keeps, per pixel, the final transmittance and the number of
+ * list entries it blended).  Piecewise decisions (LOD drops, the 0.99 and
+ * power clamps, the 2^-24 flush, termination, tile membership, the tangent
+ * clamp) are held fixed.  The per-Gaussian gradients of all views are
+ * ACCUMULATED (+=) with atomics into `grads` (order of the float additions is
+ * not fixed, so results agree to rounding, not bit for bit).              */
+int s3r_set_training(s3r_ctx* ctx, int enable);
+
+/* Cotangents of one view: DEVICE pointers, dL/d(output) in the output layout;
+ * rgb required, depth / final_T may be NULL (= 0).                         */
+typedef struct {
+    const float* rgb;            /* float[height][width][3]                     */
+    const float* depth;          /* float[height][width] or NULL                */
+    const float* final_T;        /* float[height][width] or NULL                */
+} s3r_cotangents;
+
+/* Gradient accumulators, DEVICE float4[n] each, scene-row layout:
+ * means_opacity = dL/d(mu_x, mu_y, mu_z, opacity); scales = dL/d(sigma), .w
+ * untouched; rotations = dL/dq (w,x,y,z) of the unnormalised quaternion;
+ * colors = dL/d(r,g,b), .w untouched.                                      */
+typedef struct {
+    float* means_opacity;
+    float* scales;
+    float* rotations;
+    float* colors;
+} s3r_grads;
+
+/* scene and views must be the ones of the last render; cots: HOST array of
+ * n_views structs (device pointers inside).                                */
+int s3r_render_backward(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* views,
+                        int32_t n_views, const s3r_cotangents* cots, const s3r_grads* grads,
+                        void* stream);
+
+/* Mean-squared-error helper for a training step: over n floats,
+ * grad[i] = 2 scale (x[i] - y[i]) and *loss += scale sum (x - y)^2 (loss is a
+ * DEVICE float, accumulated with atomics).  x, y, grad: DEVICE float[n].    */
+int s3r_mse(s3r_ctx* ctx, const float* x, const float* y, int64_t n, float scale, float* grad,
+            float* loss, void* stream);
+
 /* Multi-GPU point-life merge helper (Eq.5 is a min/max, so replicas merge
  * exactly): negates l_s of every Gaussian in place (an involution).  Between
  * two calls an all-reduce MAX over the float[2n] life array (NCCL) yields

@@ -1,0 +1,352 @@
+// k_backward.cu — config 5: adjoint of the alpha blend (Eq.2) and
+// of the instance-specific projection (Eq.1 P:107-112 through W_{t,i} of
+// P:158-159), for the views of the last forward batch; plus the MSE helper.
+//
+// K7b k_raster_bwd: same CTA layout as K7 (64 threads, 4 pixels per thread).
+// Every pixel knows from the forward its final transmittance and how many list
+// entries it blended; the CTA walks its tile list BACK TO FRONT in batches of
+// 256 staged records, recomputes alpha with the forward's R-ARITH ops (so the
+// flush / clamps / skips are the forward's), recovers T before each splat as
+// T / (1 - alpha), and forms
+//     dL/dc = w gC,  dL/dz = w gD,
+//     dL/dalpha = T (c.gC + z gD) - (R + gT T_final) / (1 - alpha),
+//     R += (c.gC + z gD) w,
+// then dL/do = dL/dalpha exp(power) (unless alpha hit 0.99) and dL/dpower =
+// dL/dalpha alpha (unless power was clamped at 0), and the conic / mean
+// gradients of power = -1/2 (A dx^2 + C dy^2) - B dx dy.  The 10 per-splat
+// sums are reduced over the warp with shuffles and added with one atomic per
+// value per warp into the splat's accumulator (by depth rank).
+//
+// K2b k_project_bwd: per (view, rank): the chain rule from (mx, my, z, A, B,
+// C, o, rgb) to the Gaussian's raw parameters (mean in its instance frame,
+// linear scales, unnormalised quaternion, opacity, colour), atomically added
+// into the caller's gradient arrays.
+#include <algorithm>
+
+#include "s3r_internal.cuh"
+
+namespace s3r {
+
+namespace {
+
+constexpr int RT = 64;
+constexpr int RPIX = 4;
+constexpr int RB = 256;
+
+__device__ __forceinline__ float s3r_exp2_b(float x)
+{
+    const float t = x + 12582912.0f;
+    const float n = t - 12582912.0f;
+    const float r = x - n;
+    float p = 1.535336188319500e-4f;
+    p = __fmaf_rn(p, r, 1.339887440266574e-3f);
+    p = __fmaf_rn(p, r, 9.618437357674640e-3f);
+    p = __fmaf_rn(p, r, 5.550332471162809e-2f);
+    p = __fmaf_rn(p, r, 2.402264791363012e-1f);
+    p = __fmaf_rn(p, r, 6.931472028550421e-1f);
+    const float y = __fmaf_rn(p, r, 1.0f);
+    return y * __uint_as_float((__float_as_uint(t) << 23) + 0x3F800000u);
+}
+
+__device__ __forceinline__ float warp_sum(float x)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+__global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
+{
+    __shared__ float4 s_rec[3 * RB];
+    __shared__ int s_max;
+    const int v = blockIdx.y;
+    const DevView& V = a.views[v];
+    const int tile = blockIdx.x;
+    if (tile >= V.ntiles) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int tx = tile % V.TX, ty = tile / V.TX;
+    const int px = tx * TILE + ((tid >> 5) << 3) + (lane & 7);   // layout of K7
+    const int py0 = ty * TILE + (lane >> 3);
+    const float fpx = (float)px;
+    const s3r_cot C = a.cots[v];
+    float fpy[RPIX], Tc[RPIX], Tf[RPIX], Rr[RPIX], gr[RPIX], gg[RPIX], gb[RPIX], gd[RPIX], gt[RPIX];
+    int last[RPIX];
+    int mymax = 0;
+#pragma unroll
+    for (int k = 0; k < RPIX; ++k) {
+        const int py = py0 + 4 * k;
+        fpy[k] = (float)py;
+        last[k] = 0;
+        Tc[k] = Tf[k] = 1.0f;
+        Rr[k] = gr[k] = gg[k] = gb[k] = gd[k] = gt[k] = 0.0f;
+        if (px < V.W && py < V.H) {
+            const long long pix = (long long)py * V.W + px;
+            last[k] = a.train_n[V.pix_off + pix];
+            Tc[k] = Tf[k] = a.train_T[V.pix_off + pix];
+            gr[k] = C.rgb[3 * pix];
+            gg[k] = C.rgb[3 * pix + 1];
+            gb[k] = C.rgb[3 * pix + 2];
+            if (C.depth) gd[k] = C.depth[pix];
+            if (C.final_T) gt[k] = C.final_T[pix];
+            mymax = max(mymax, last[k]);
+        }
+    }
+    if (tid == 0) s_max = 0;
+    __syncthreads();
+    atomicMax(&s_max, mymax);
+    __syncthreads();
+    const int2 rg = a.tranges[V.trange_off + tile];
+    const uint32_t* lst = a.tlists + V.tlist_off;
+    const float4* recs = a.rec_sorted + 3 * V.cap_off;
+    float* acc = a.splat_grads + 10 * V.cap_off;
+    // -2 ln 2: conic A = qa * (-2 ln2) etc. (qa = A * (-log2(e) / 2))
+    const float k2 = -1.3862943611198906f;
+    for (int hi = s_max; hi > 0;) {
+        const int lo = max(0, hi - RB);
+        const int nb = hi - lo;
+        __syncthreads();
+        for (int i = tid; i < nb; i += RT) {
+            const float4* src = recs + 3ll * lst[rg.x + lo + i];
+            s_rec[3 * i + 0] = src[0];
+            s_rec[3 * i + 1] = src[1];
+            s_rec[3 * i + 2] = src[2];
+        }
+        __syncthreads();
+        for (int jj = nb - 1; jj >= 0; --jj) {
+            const int j = lo + jj;
+            const float4 q0 = s_rec[3 * jj], q1 = s_rec[3 * jj + 1], q2 = s_rec[3 * jj + 2];
+            const float dx = q0.x - fpx;
+            const float a1 = q1.x * dx;
+            const float a2 = a1 * dx;
+            const float b1 = q1.y * dx;
+            const float A = q1.x * k2, B = q1.y * k2, Cc = q1.z * k2;
+            float s_mx = 0.f, s_my = 0.f, s_z = 0.f, s_A = 0.f, s_B = 0.f, s_C = 0.f, s_o = 0.f,
+                  s_r = 0.f, s_g = 0.f, s_b = 0.f;
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < RPIX; ++k) {
+                if (j >= last[k]) continue;
+                const float dy = q0.y - fpy[k];
+                const float c1 = __fmaf_rn(q1.z, dy, b1);
+                const float e2raw = __fmaf_rn(dy, c1, a2);
+                const float e2 = fminf(0.0f, e2raw);
+                if (!(e2 >= -24.0f)) continue;             // flushed in the forward: alpha = 0
+                const float G = s3r_exp2_b(e2);
+                const float og = q0.w * G;
+                const float alpha = fminf(0.99f, og);
+                const float Tb = Tc[k] / (1.0f - alpha);    // T before this splat
+                const float w = alpha * Tb;
+                const float cdot = q2.x * gr[k] + q2.y * gg[k] + q2.z * gb[k] + q0.z * gd[k];
+                const float galpha = Tb * cdot - (Rr[k] + gt[k] * Tf[k]) / (1.0f - alpha);
+                Rr[k] += cdot * w;
+                Tc[k] = Tb;
+                any = true;
+                s_r += w * gr[k];
+                s_g += w * gg[k];
+                s_b += w * gb[k];
+                s_z += w * gd[k];
+                if (og < 0.99f) {
+                    s_o += galpha * G;
+                    if (e2raw <= 0.0f) {
+                        const float gP = galpha * alpha;
+                        const float dyy = dy;
+                        s_A += -0.5f * dx * dx * gP;
+                        s_C += -0.5f * dyy * dyy * gP;
+                        s_B += -dx * dyy * gP;
+                        s_mx += -(A * dx + B * dyy) * gP;
+                        s_my += -(B * dx + Cc * dyy) * gP;
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, any)) {
+                s_mx = warp_sum(s_mx); s_my = warp_sum(s_my); s_z = warp_sum(s_z);
+                s_A = warp_sum(s_A); s_B = warp_sum(s_B); s_C = warp_sum(s_C);
+                s_o = warp_sum(s_o); s_r = warp_sum(s_r); s_g = warp_sum(s_g);
+                s_b = warp_sum(s_b);
+                if (lane == 0) {
+                    float* d = acc + 10ll * lst[rg.x + j];
+                    atomicAdd(d + 0, s_mx); atomicAdd(d + 1, s_my); atomicAdd(d + 2, s_z);
+                    atomicAdd(d + 3, s_A); atomicAdd(d + 4, s_B); atomicAdd(d + 5, s_C);
+                    atomicAdd(d + 6, s_o); atomicAdd(d + 7, s_r); atomicAdd(d + 8, s_g);
+                    atomicAdd(d + 9, s_b);
+                }
+            }
+        }
+        hi = lo;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_project_bwd(BackwardArgs a)
+{
+    const DevView& V = a.views[blockIdx.y];
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= V.n_rendered) return;
+    const float* acc = a.splat_grads + 10 * (V.cap_off + r);
+    const float gmx = acc[0], gmy = acc[1], gz = acc[2], gA = acc[3], gB = acc[4], gC = acc[5],
+                go = acc[6], gcr = acc[7], gcg = acc[8], gcb = acc[9];
+    if (gmx == 0.f && gmy == 0.f && gz == 0.f && gA == 0.f && gB == 0.f && gC == 0.f &&
+        go == 0.f && gcr == 0.f && gcg == 0.f && gcb == 0.f)
+        return;
+    const long long g = (long long)(a.dkey_sorted[V.cap_off + r] & a.gmask);
+    const int id = a.ids[g];
+    const float* M = V.table + 12 * id;
+    const float4 mo = a.means_opacity[g], sc = a.scales[g], qq = a.rotations[g];
+    float p[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) p[i] = M[4 * i] * mo.x + M[4 * i + 1] * mo.y + M[4 * i + 2] * mo.z + M[4 * i + 3];
+    const float qn = sqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
+    const float w = qq.x / qn, x = qq.y / qn, y = qq.z / qn, zq = qq.w / qn;
+    float Rq[9];
+    Rq[0] = 1.f - 2.f * (y * y + zq * zq); Rq[1] = 2.f * (x * y - w * zq); Rq[2] = 2.f * (x * zq + w * y);
+    Rq[3] = 2.f * (x * y + w * zq); Rq[4] = 1.f - 2.f * (x * x + zq * zq); Rq[5] = 2.f * (y * zq - w * x);
+    Rq[6] = 2.f * (x * zq - w * y); Rq[7] = 2.f * (y * zq + w * x); Rq[8] = 1.f - 2.f * (x * x + y * y);
+    const float sg[3] = {sc.x, sc.y, sc.z};
+    float WR[9], T[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            WR[3 * i + c] = M[4 * i] * Rq[c] + M[4 * i + 1] * Rq[3 + c] + M[4 * i + 2] * Rq[6 + c];
+            T[3 * i + c] = WR[3 * i + c] * sg[c];
+        }
+    const float fx = V.fx, fy = V.fy;
+    const float Wf = (float)V.W, Hf = (float)V.H;
+    const float lox = (-(0.15f * Wf) - V.cx) / fx, hix = ((1.15f * Wf) - V.cx) / fx;
+    const float loy = (-(0.15f * Hf) - V.cy) / fy, hiy = ((1.15f * Hf) - V.cy) / fy;
+    const float pz = p[2];
+    const float u = p[0] / pz, vv = p[1] / pz;
+    const bool uclamp = (u < lox || u > hix), vclamp = (vv < loy || vv > hiy);
+    const float uc = fminf(fmaxf(u, lox), hix), vc = fminf(fmaxf(vv, loy), hiy);
+    const float J[6] = {fx / pz, 0.f, -fx * uc / pz, 0.f, fy / pz, -fy * vc / pz};
+    float U[6];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) U[3 * i + c] = J[3 * i] * T[c] + J[3 * i + 1] * T[3 + c] + J[3 * i + 2] * T[6 + c];
+    const float ka = U[0] * U[0] + U[1] * U[1] + U[2] * U[2];
+    const float kb = U[0] * U[3] + U[1] * U[4] + U[2] * U[5];
+    const float kc = U[3] * U[3] + U[4] * U[4] + U[5] * U[5];
+    const float ad = ka + 0.3f, cd = kc + 0.3f, det = ad * cd - kb * kb;
+    const float Q[4] = {cd / det, -kb / det, -kb / det, ad / det};
+    // conic -> Sigma'_dil: G_S = -Q G_Q Q, G_Q = [[gA, gB/2], [gB/2, gC]]
+    const float GQ[4] = {gA, 0.5f * gB, 0.5f * gB, gC};
+    float QG[4], GS[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) QG[2 * i + j] = Q[2 * i] * GQ[j] + Q[2 * i + 1] * GQ[2 + j];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) GS[2 * i + j] = -(QG[2 * i] * Q[j] + QG[2 * i + 1] * Q[2 + j]);
+    float gU[6];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) gU[3 * i + k] = 2.f * (GS[2 * i] * U[k] + GS[2 * i + 1] * U[3 + k]);
+    float gJ[6], gT[9];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) gJ[3 * i + k] = gU[3 * i] * T[3 * k] + gU[3 * i + 1] * T[3 * k + 1] + gU[3 * i + 2] * T[3 * k + 2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gT[3 * k + c] = J[k] * gU[c] + J[3 + k] * gU[3 + c];
+    float gs[3] = {0.f, 0.f, 0.f}, gWR[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            gs[c] += gT[3 * i + c] * WR[3 * i + c];
+            gWR[3 * i + c] = gT[3 * i + c] * sg[c];
+        }
+    float gR[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gR[3 * i + c] = M[i] * gWR[c] + M[4 + i] * gWR[3 + c] + M[8 + i] * gWR[6 + c];
+    const float dRw[9] = {0.f, -2.f * zq, 2.f * y, 2.f * zq, 0.f, -2.f * x, -2.f * y, 2.f * x, 0.f};
+    const float dRx[9] = {0.f, 2.f * y, 2.f * zq, 2.f * y, -4.f * x, -2.f * w, 2.f * zq, 2.f * w, -4.f * x};
+    const float dRy[9] = {-4.f * y, 2.f * x, 2.f * w, 2.f * x, 0.f, 2.f * zq, -2.f * w, 2.f * zq, -4.f * y};
+    const float dRz[9] = {-4.f * zq, -2.f * w, 2.f * x, 2.f * w, -4.f * zq, 2.f * y, 2.f * x, 2.f * y, 0.f};
+    float gq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        gq[0] += gR[k] * dRw[k];
+        gq[1] += gR[k] * dRx[k];
+        gq[2] += gR[k] * dRy[k];
+        gq[3] += gR[k] * dRz[k];
+    }
+    const float qh[4] = {w, x, y, zq};
+    const float dotq = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
+    float gp0 = 0.f, gp1 = 0.f, gp2 = 0.f;
+    const float iz2 = 1.f / (pz * pz);
+    gp2 += gJ[0] * (-fx * iz2) + gJ[4] * (-fy * iz2);
+    if (uclamp) {
+        gp2 += gJ[2] * (fx * uc * iz2);
+    } else {
+        gp0 += gJ[2] * (-fx * iz2);
+        gp2 += gJ[2] * (2.f * fx * p[0] * iz2 / pz);
+    }
+    if (vclamp) {
+        gp2 += gJ[5] * (fy * vc * iz2);
+    } else {
+        gp1 += gJ[5] * (-fy * iz2);
+        gp2 += gJ[5] * (2.f * fy * p[1] * iz2 / pz);
+    }
+    gp0 += gmx * fx / pz;
+    gp2 += gmx * (-fx * p[0] * iz2);
+    gp1 += gmy * fy / pz;
+    gp2 += gmy * (-fy * p[1] * iz2);
+    gp2 += gz;
+    float* gm = a.g_means + 4 * g;
+    atomicAdd(gm + 0, M[0] * gp0 + M[4] * gp1 + M[8] * gp2);
+    atomicAdd(gm + 1, M[1] * gp0 + M[5] * gp1 + M[9] * gp2);
+    atomicAdd(gm + 2, M[2] * gp0 + M[6] * gp1 + M[10] * gp2);
+    atomicAdd(gm + 3, go);
+    float* gsc = a.g_scales + 4 * g;
+    atomicAdd(gsc + 0, gs[0]);
+    atomicAdd(gsc + 1, gs[1]);
+    atomicAdd(gsc + 2, gs[2]);
+    float* gro = a.g_rot + 4 * g;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) atomicAdd(gro + k, (gq[k] - qh[k] * dotq) / qn);
+    float* gco = a.g_colors + 4 * g;
+    atomicAdd(gco + 0, gcr);
+    atomicAdd(gco + 1, gcg);
+    atomicAdd(gco + 2, gcb);
+}
+
+__global__ void k_mse(const float* __restrict__ x, const float* __restrict__ y, long long n,
+                      float scale, float* __restrict__ grad, float* __restrict__ loss)
+{
+    float s = 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float d = x[i] - y[i];
+        grad[i] = 2.f * scale * d;
+        s += d * d;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0 && s != 0.f) atomicAdd(loss, scale * s);
+}
+}  // namespace
+
+void launch_backward(const BackwardArgs& a, int max_tiles, long long max_rendered, cudaStream_t st)
+{
+    if (a.n_views == 0) return;
+    if (max_tiles) k_raster_bwd<<<dim3(max_tiles, a.n_views), RT, 0, st>>>(a);
+    if (max_rendered)
+        k_project_bwd<<<dim3((unsigned)((max_rendered + 255) / 256), a.n_views), 256, 0, st>>>(a);
+}
+
+void launch_mse(const float* x, const float* y, long long n, float scale, float* grad,
+                float* loss, cudaStream_t st)
+{
+    if (n == 0) return;
+    const long long blocks = std::min<long long>((n + 255) / 256, 148ll * 16);
+    k_mse<<<(unsigned)blocks, 256, 0, st>>>(x, y, n, scale, grad, loss);
+}
+
+}  // namespace s3r

@@ -69,7 +69,7 @@ constexpr int RB = 256;     // splat records staged in shared memory per batch
 #define S3R_RASTER_BOUNDS __launch_bounds__(RT)
 #endif
 
-template <bool COUNT>
+template <bool COUNT, bool TRAIN>
 __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
@@ -174,7 +174,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                         cb[k] = __fmaf_rn(q2.z, w, cb[k]);
                         dp[k] = __fmaf_rn(q0.z, w, dp[k]);
                         // include-then-stop (R14): the pixel is dead once T < 1e-4
-                        if (COUNT && on && T[k] - w < 1e-4f) stop[k] = tpos + j + 1;
+                        if ((COUNT || TRAIN) && on && T[k] - w < 1e-4f) stop[k] = tpos + j + 1;
                         T[k] = T[k] - w;
                     }
                 }
@@ -207,6 +207,10 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
         o[2] = cb[k];
         if (V.depth) V.depth[pix] = dp[k];
         if (V.finalT) V.finalT[pix] = T[k];
+        if (TRAIN) {      // state the backward (k_raster_bwd) starts from
+            a.train_T[V.pix_off + pix] = T[k];
+            a.train_n[V.pix_off + pix] = stop[k] >= 0 ? stop[k] : tpos;
+        }
     }
 }
 
@@ -225,8 +229,13 @@ void launch_raster(const RasterArgs& args, cudaStream_t st)
     RasterArgs a = args;
     a.exp2_c0 = 1.535336188319500e-4f;
     dim3 grid(a.max_tiles, a.n_views);
-    if (a.evals) k_raster<true><<<grid, RT, 0, st>>>(a);
-    else k_raster<false><<<grid, RT, 0, st>>>(a);
+    if (a.evals) {
+        if (a.train_T) k_raster<true, true><<<grid, RT, 0, st>>>(a);
+        else k_raster<true, false><<<grid, RT, 0, st>>>(a);
+    } else {
+        if (a.train_T) k_raster<false, true><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, false><<<grid, RT, 0, st>>>(a);
+    }
 }
 
 void launch_dump_order(const uint32_t* order, const int32_t* gidx, long long base,

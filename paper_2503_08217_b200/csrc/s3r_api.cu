@@ -39,7 +39,11 @@ struct StageEvent {
 struct s3r_ctx {
     int device = 0;
     std::string err;
-    bool debug = false, timing = false, counters = false;
+    bool debug = false, timing = false, counters = false, training = false;
+    bool last_training = false;
+    int last_nviews = 0, last_max_tiles = 0;
+    long long last_max_r = 0, last_N = -1;
+    Buf d_train_T, d_train_n, d_sgrads, d_cots;
     bool last_counters = false, evals_fetched = false;
     Buf d_evals;
     bool last_debug = false;
@@ -248,6 +252,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     const int T = (int)tk.size();
 
     c->hv.assign(nv, DevView{});
+    long long total_px = 0;
     for (int v = 0; v < nv; ++v) {
         const s3r_view& V = views[v];
         DevView& d = c->hv[v];
@@ -271,6 +276,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         d.nbins = d.STX * d.STY;
         d.rgb = outs[v].rgb; d.depth = outs[v].depth; d.finalT = outs[v].final_T;
         d.visible = outs[v].visible;
+        d.pix_off = total_px;
+        total_px += (long long)d.W * d.H;
+    }
+    if (c->training) {
+        if ((rc = ensure(c, c->d_train_T, (size_t)std::max(total_px, 1ll) * 4))) return rc;
+        if ((rc = ensure(c, c->d_train_n, (size_t)std::max(total_px, 1ll) * 4))) return rc;
     }
 
     // staging layout for this batch
@@ -515,12 +526,19 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
             CU(cudaMemsetAsync(c->d_evals.p, 0, (size_t)nv * 16, st));
             a.evals = P<unsigned long long>(c->d_evals);
         }
+        a.train_T = c->training ? P<float>(c->d_train_T) : nullptr;
+        a.train_n = c->training ? P<int>(c->d_train_n) : nullptr;
         launch_raster(a, st);
         ev_end(c, st, e);
         c->last_counters = a.evals != nullptr;
         c->evals_fetched = false;
     }
     CU(cudaGetLastError());
+    c->last_training = c->training;
+    c->last_nviews = nv;
+    c->last_max_tiles = max_tiles;
+    c->last_max_r = max_r;
+    c->last_N = N;
     if (c->timing) c->timed_renders++;
     CU(cudaEventRecord(c->staging_free, st));
     c->staging_recorded = true;
@@ -572,7 +590,8 @@ void s3r_destroy(s3r_ctx* c)
     Buf* bufs[] = {&c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
                    &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
                    &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_rects, &c->d_lists,
-                   &c->d_tlists, &c->d_tranges,
+                   &c->d_tlists, &c->d_tranges, &c->d_train_T, &c->d_train_n, &c->d_sgrads,
+                   &c->d_cots,
                    &c->d_cnt, &c->d_hist, &c->d_dsegs, &c->d_dtile0, &c->d_ranges, &c->d_err,
                    &c->d_dbg_keys, &c->d_dbg_flags, &c->d_dbg_rect, &c->d_dbg_tcnt, &c->d_evals};
     for (Buf* b : bufs)
@@ -846,6 +865,82 @@ int s3r_reset_visibility(s3r_ctx* c, const s3r_scene* s, void* stream)
         return fail(c, S3R_EINVAL, "reset: bad arguments");
     CU(cudaSetDevice(c->device));
     launch_reset(reinterpret_cast<float2*>(s->visibility), s->n, (cudaStream_t)stream);
+    CU(cudaGetLastError());
+    return S3R_OK;
+}
+
+int s3r_set_training(s3r_ctx* c, int enable)
+{
+    if (!c) return S3R_EINVAL;
+    c->training = enable != 0;
+    return S3R_OK;
+}
+
+int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int32_t nv,
+                        const s3r_cotangents* cots, const s3r_grads* grads, void* stream)
+{
+    if (!c || !sc || !grads) return S3R_EINVAL;
+    if (!c->have_render || !c->last_training)
+        return fail(c, S3R_ESTATE, "backward: no training forward (s3r_set_training(1) + render)");
+    if (nv != c->last_nviews || sc->n != c->last_N)
+        return fail(c, S3R_ESTATE, "backward: scene/views differ from the last forward");
+    if (nv > 0 && (!views || !cots)) return fail(c, S3R_EINVAL, "backward: views/cots NULL");
+    if (sc->n > 0 && (!grads->means_opacity || !grads->scales || !grads->rotations ||
+                      !grads->colors))
+        return fail(c, S3R_EINVAL, "backward: gradient arrays required");
+    for (int v = 0; v < nv; ++v) {
+        if (!cots[v].rgb) return fail(c, S3R_EINVAL, "backward: cots[%d].rgb is NULL", v);
+        if (views[v].width != c->hv[v].W || views[v].height != c->hv[v].H)
+            return fail(c, S3R_ESTATE, "backward: view %d differs from the last forward", v);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(c->device));
+    int rc;
+    long long cap = 0;
+    for (int v = 0; v < nv; ++v) cap = std::max(cap, c->hv[v].cap_off + c->hv[v].n_temporal);
+    if ((rc = ensure(c, c->d_sgrads, (size_t)std::max(cap, 1ll) * 40))) return rc;
+    CU(cudaMemsetAsync(c->d_sgrads.p, 0, (size_t)std::max(cap, 1ll) * 40, st));
+    if ((rc = ensure(c, c->d_cots, (size_t)std::max(nv, 1) * sizeof(s3r_cot)))) return rc;
+    if ((rc = stage_reserve(c, (size_t)std::max(nv, 1) * sizeof(s3r_cot) + 512))) return rc;
+    if (c->staging_recorded) CU(cudaEventSynchronize(c->staging_free));
+    c->h_stage_top = 0;
+    s3r_cot* h = (s3r_cot*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(s3r_cot));
+    for (int v = 0; v < nv; ++v) h[v] = s3r_cot{cots[v].rgb, cots[v].depth, cots[v].final_T};
+    if (nv) CU(cudaMemcpyAsync(c->d_cots.p, h, nv * sizeof(s3r_cot), cudaMemcpyHostToDevice, st));
+    BackwardArgs a{};
+    a.views = P<DevView>(c->d_views);
+    a.n_views = nv;
+    a.cots = P<s3r_cot>(c->d_cots);
+    a.tranges = P<int2>(c->d_tranges);
+    a.tlists = P<uint32_t>(c->d_tlists);
+    a.rec_sorted = P<float4>(c->d_recs);
+    a.train_T = P<float>(c->d_train_T);
+    a.train_n = P<int>(c->d_train_n);
+    a.splat_grads = P<float>(c->d_sgrads);
+    a.dkey_sorted = P<unsigned long long>(c->d_sortk[c->final_order]);
+    a.gmask = (1ull << c->gbits) - 1ull;
+    a.ids = sc->instance_ids;
+    a.means_opacity = reinterpret_cast<const float4*>(sc->means_opacity);
+    a.scales = reinterpret_cast<const float4*>(sc->scales);
+    a.rotations = reinterpret_cast<const float4*>(sc->rotations);
+    a.g_means = grads->means_opacity;
+    a.g_scales = grads->scales;
+    a.g_rot = grads->rotations;
+    a.g_colors = grads->colors;
+    launch_backward(a, c->last_max_tiles, c->last_max_r, st);
+    CU(cudaEventRecord(c->staging_free, st));
+    CU(cudaGetLastError());
+    return S3R_OK;
+}
+
+int s3r_mse(s3r_ctx* c, const float* x, const float* y, int64_t n, float scale, float* grad,
+            float* loss, void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    if (n < 0 || (n > 0 && (!x || !y || !grad || !loss)))
+        return fail(c, S3R_EINVAL, "mse: bad arguments");
+    CU(cudaSetDevice(c->device));
+    launch_mse(x, y, n, scale, grad, loss, (cudaStream_t)stream);
     CU(cudaGetLastError());
     return S3R_OK;
 }

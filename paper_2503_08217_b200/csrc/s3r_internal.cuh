@@ -94,6 +94,7 @@ struct DevView {
     long long cnt_off;       // offset of the view's (bin, chunk) counts
     long long tlist_off;     // offset of the view's tile-list area (S*S * supertile pairs)
     int trange_off;          // offset of the view's tile ranges (ntiles entries)
+    long long pix_off;       // offset of the view's pixels in the training buffers
 };
 
 // Per-view counters written by K2 (device, zeroed per batch)
@@ -203,9 +204,42 @@ struct RasterArgs {
     const uint32_t* tlists;      // tile lists of depth ranks, per view at V.tlist_off
     const float4* rec_sorted;    // splat records by rank, per view at V.cap_off
     unsigned long long* evals;   // [n_views][2] (E_alg, E_exec) or NULL
+    float* train_T;              // per pixel final T (training) or NULL, at V.pix_off
+    int* train_n;                // per pixel blended list entries (training), at V.pix_off
     float exp2_c0;               // 1.535336188319500e-4f (set by launch_raster)
 };
 void launch_raster(const RasterArgs& a, cudaStream_t st);
+
+// Config 5: backward of K7 and K2.
+struct s3r_cot {
+    const float* rgb;
+    const float* depth;
+    const float* final_T;
+};
+struct BackwardArgs {
+    const DevView* views;
+    int n_views;
+    const s3r_cot* cots;                 // [n_views]
+    const int2* tranges;
+    const uint32_t* tlists;
+    const float4* rec_sorted;
+    const float* train_T;
+    const int* train_n;
+    float* splat_grads;                  // [cap][10] per depth rank
+    const unsigned long long* dkey_sorted;
+    unsigned long long gmask;            // (1 << gbits) - 1
+    const int32_t* ids;
+    const float4* means_opacity;
+    const float4* scales;
+    const float4* rotations;
+    float* g_means;
+    float* g_scales;
+    float* g_rot;
+    float* g_colors;
+};
+void launch_backward(const BackwardArgs& a, int max_tiles, long long max_rendered, cudaStream_t st);
+void launch_mse(const float* x, const float* y, long long n, float scale, float* grad,
+                float* loss, cudaStream_t st);
 
 // K9: commit / reset.
 void launch_commit(float2* vis, float2* life, long long n, float margin, cudaStream_t st);

@@ -30,7 +30,8 @@ EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_se
            "s3r_set_counters", "s3r_set_timing", "s3r_get_stage_times", "s3r_compose_instance_cameras", "s3r_render",
            "s3r_render_batch", "s3r_render_batch_host", "s3r_get_stats",
            "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
-           "s3r_life_flip", "s3r_check"]
+           "s3r_life_flip", "s3r_check", "s3r_set_training", "s3r_render_backward",
+           "s3r_mse"]
 
 
 class S3RError(RuntimeError):
@@ -64,6 +65,15 @@ class Stats_(C.Structure):
                                          "n_lod_dropped", "n_rendered", "n_pairs",
                                          "n_bad_instance", "n_bin_pairs", "n_blend_evals",
                                          "n_blend_exec")]
+
+
+class Cot_(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("final_T", C.c_void_p)]
+
+
+class Grads_(C.Structure):
+    _fields_ = [("means_opacity", C.c_void_p), ("scales", C.c_void_p),
+                ("rotations", C.c_void_p), ("colors", C.c_void_p)]
 
 
 class Debug_(C.Structure):
@@ -104,6 +114,9 @@ def lib():
                 "s3r_commit_visibility": (I, [P, P, C.c_float, P]),
                 "s3r_reset_visibility": (I, [P, P, P]),
                 "s3r_life_flip": (I, [P, P, I64, P]),
+                "s3r_set_training": (I, [P, I]),
+                "s3r_render_backward": (I, [P, P, P, C.c_int32, P, P, P]),
+                "s3r_mse": (I, [P, P, P, I64, C.c_float, P, P, P]),
                 "s3r_check": (I, [P, P]),
             }
             for name, (res, args) in sig.items():
@@ -290,6 +303,31 @@ class Context:
     def reset_visibility(self, scene: DeviceScene, stream=None):
         sc = scene.struct()
         self._check(self.L.s3r_reset_visibility(self.h, C.byref(sc), _stream(stream)))
+
+    # -- training (config 5)
+    def set_training(self, on: bool):
+        self._check(self.L.s3r_set_training(self.h, int(on)))
+
+    def render_backward(self, scene: DeviceScene, views: Sequence, tables: Sequence[torch.Tensor],
+                        cots: Sequence[Dict[str, torch.Tensor]], grads: Dict[str, torch.Tensor],
+                        stream=None):
+        """Accumulate dL/d(scene params) of the last (training) forward into grads
+        (keys means_opacity, scales, rotations, colors: (N,4) float32 tensors)."""
+        n = len(views)
+        vs = (View_ * max(n, 1))(*[view_struct(v, t) for v, t in zip(views, tables)])
+        cs = (Cot_ * max(n, 1))(*[Cot_(_ptr(c["rgb"]), _ptr(c.get("depth")),
+                                       _ptr(c.get("final_T"))) for c in cots])
+        g = Grads_(_ptr(grads["means_opacity"]), _ptr(grads["scales"]),
+                   _ptr(grads["rotations"]), _ptr(grads["colors"]))
+        sc = scene.struct()
+        self._check(self.L.s3r_render_backward(self.h, C.byref(sc), vs, n, cs, C.byref(g),
+                                               _stream(stream)))
+
+    def mse(self, x: torch.Tensor, y: torch.Tensor, scale: float, grad: torch.Tensor,
+            loss: torch.Tensor, stream=None):
+        """grad = 2 scale (x - y); loss += scale sum (x - y)^2 (device scalar)."""
+        self._check(self.L.s3r_mse(self.h, _ptr(x), _ptr(y), int(x.numel()), float(scale),
+                                   _ptr(grad), _ptr(loss), _stream(stream)))
 
     def life_flip(self, life: torch.Tensor, stream=None):
         """Negate l_s in place (see s3r_life_flip): brackets an all-reduce MAX."""

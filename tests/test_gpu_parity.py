@@ -256,3 +256,96 @@ def test_full_size_av2_sampled(ctx):
     rng = np.random.default_rng(0)
     for vi in sorted(rng.choice(len(views), 2, replace=False)):
         check_view(ctx, scene, views[vi], tabs[vi], outs[vi], int(vi))
+
+
+# --------------------------------------------------------------------------
+# config 5: backward (adjoint of the blend and the projection) vs the fp64 oracle
+# --------------------------------------------------------------------------
+
+def _grads_like(ds):
+    return {k: torch.zeros_like(getattr(ds, k)) for k in
+            ("means_opacity", "scales", "rotations", "colors")}
+
+
+def _gpu_backward(ctx, scene, views, cot_np):
+    ds = s3r.DeviceScene.from_numpy(scene)
+    tabs = s3r.view_tables(ctx, views)
+    outs = s3r.alloc_outputs(views)
+    ctx.set_training(True)
+    try:
+        ctx.render_batch(ds, views, list(tabs), outs)
+        cots = [{k: torch.from_numpy(np.ascontiguousarray(c[k], np.float32)).cuda()
+                 for k in c} for c in cot_np]
+        grads = _grads_like(ds)
+        ctx.render_backward(ds, views, list(tabs), cots, grads)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_training(False)
+    g = np.concatenate([grads[k].cpu().numpy() for k in
+                        ("means_opacity", "scales", "rotations", "colors")], 1)
+    return g, tabs
+
+
+GRAD_ATTR = {"mean": [0, 1, 2], "opacity": [3], "scale": [4, 5, 6], "rot": [8, 9, 10, 11],
+             "color": [12, 13, 14]}
+
+
+def _check_grads(g_gpu, g_ref, tol=1e-3):
+    for name, cols in GRAD_ATTR.items():
+        ref = np.abs(g_ref[:, cols]).max()
+        d = np.abs(g_gpu[:, cols] - g_ref[:, cols]).max()
+        assert ref > 0, name
+        assert d <= tol * ref, (name, d, ref)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_backward_matches_oracle(ctx, seed):
+    """north_star gate: per attribute max|g_gpu - g_oracle| <= 1e-3 max|g_oracle|."""
+    scene, views = sg.make_random_dynamic(seed, 1500, 3, 150, 131, 97, 3, lod=(2.0, 0.5, 12.0))
+    rng = np.random.default_rng(seed)
+    cot = [{"rgb": rng.standard_normal((v.height, v.width, 3)),
+            "depth": 0.05 * rng.standard_normal((v.height, v.width)),
+            "final_T": rng.standard_normal((v.height, v.width))} for v in views]
+    g_gpu, tabs = _gpu_backward(ctx, scene, views, cot)
+    g_ref = np.zeros((scene.n, 16))
+    for v, t, c in zip(views, tabs, cot):
+        oracle.backward(scene, v, c["rgb"], c["depth"], c["final_T"], table=t.cpu().numpy(),
+                        grads=g_ref)
+    _check_grads(g_gpu, g_ref)
+
+
+def test_training_step_mse_street(ctx):
+    """MSE loss against noisy targets (the bench's config-5 step) on C2 geometry:
+    s3r_mse gradient + backward vs the oracle adjoint of the same cotangent."""
+    scene, views = sg.make_config("street", scale=0.05, n_views=2, width=320, height=224)
+    ds = s3r.DeviceScene.from_numpy(scene)
+    tabs = s3r.view_tables(ctx, views)
+    outs = s3r.alloc_outputs(views)
+    ctx.render_batch(ds, views, list(tabs), outs)
+    rng = np.random.default_rng(0)
+    targets = [torch.clamp(o["rgb"] + 0.05 * torch.from_numpy(
+        rng.standard_normal(o["rgb"].shape).astype(np.float32)).cuda(), 0, 1) for o in outs]
+    ctx.set_training(True)
+    try:
+        ctx.render_batch(ds, views, list(tabs), outs)
+        loss = torch.zeros(1, device="cuda")
+        npix = sum(v.width * v.height * 3 for v in views)
+        cots = []
+        for o, tg in zip(outs, targets):
+            gr = torch.empty_like(o["rgb"])
+            ctx.mse(o["rgb"], tg, 1.0 / npix, gr, loss)
+            cots.append({"rgb": gr})
+        grads = _grads_like(ds)
+        ctx.render_backward(ds, views, list(tabs), cots, grads)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_training(False)
+    want_loss = sum(float(((o["rgb"] - tg) ** 2).sum()) for o, tg in zip(outs, targets)) / npix
+    assert abs(float(loss) - want_loss) <= 1e-4 * want_loss
+    g_gpu = np.concatenate([grads[k].cpu().numpy() for k in
+                            ("means_opacity", "scales", "rotations", "colors")], 1)
+    g_ref = np.zeros((scene.n, 16))
+    for v, t, c in zip(views, tabs, cots):
+        oracle.backward(scene, v, c["rgb"].cpu().numpy().astype(np.float64), table=t.cpu().numpy(),
+                        grads=g_ref)
+    _check_grads(g_gpu, g_ref)
