@@ -99,8 +99,9 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
     const uint32_t* lst = a.tlists + V.tlist_off;
     const float4* recs = a.rec_sorted + 3 * V.cap_off;
     float* acc = a.splat_grads + 10 * V.cap_off;
-    // -2 ln 2: conic A = qa * (-2 ln2) etc. (qa = A * (-log2(e) / 2))
-    const float k2 = -1.3862943611198906f;
+    // conic from the exp2-form coefficients: qa = A (-log2e/2), qb = B (-log2e),
+    // qc = C (-log2e/2)  =>  A = qa (-2 ln2), B = qb (-ln2), C = qc (-2 ln2)
+    const float k2 = -1.3862943611198906f, k1 = -0.6931471805599453f;
     for (int hi = s_max; hi > 0;) {
         const int lo = max(0, hi - RB);
         const int nb = hi - lo;
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
             const float a1 = q1.x * dx;
             const float a2 = a1 * dx;
             const float b1 = q1.y * dx;
-            const float A = q1.x * k2, B = q1.y * k2, Cc = q1.z * k2;
+            const float A = q1.x * k2, B = q1.y * k1, Cc = q1.z * k2;
             float s_mx = 0.f, s_my = 0.f, s_z = 0.f, s_A = 0.f, s_B = 0.f, s_C = 0.f, s_o = 0.f,
                   s_r = 0.f, s_g = 0.f, s_b = 0.f;
             bool any = false;
