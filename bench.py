@@ -177,6 +177,71 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
+    """Config 5: one step = training forward of the batch, MSE against noisy
+    targets (s3r_mse), backward of blend + projection (s3r_render_backward)
+    and, for N > 1, an NCCL all-reduce (SUM) of the per-Gaussian gradients."""
+    import torch
+    import torch.distributed as dist
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5)
+    ctx.render_batch(ds, views, tables, outs)
+    targets = [torch.clamp(o["rgb"] + 0.05 * torch.randn(o["rgb"].shape, generator=gen,
+                                                          device=dev), 0, 1) for o in outs]
+    gimg = [torch.empty_like(o["rgb"]) for o in outs]
+    grads = {k: torch.zeros_like(getattr(ds, k)) for k in
+             ("means_opacity", "scales", "rotations", "colors")}
+    loss = torch.zeros(1, device=dev)
+    npix = sum(v.width * v.height * 3 for v in views)
+    cots = [{"rgb": g} for g in gimg]
+    ctx.set_training(True)
+    e_fwd = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def step():
+        for g in grads.values():
+            g.zero_()
+        loss.zero_()
+        e_fwd[0].record(stream)
+        ctx.render_batch(ds, views, tables, outs)
+        e_fwd[1].record(stream)
+        for o, t, g in zip(outs, targets, gimg):
+            ctx.mse(o["rgb"], t, 1.0 / npix, g, loss)
+        e_fwd[2].record(stream)
+        ctx.render_backward(ds, views, tables, cots, grads)
+        e_fwd[3].record(stream)
+        if world > 1:
+            for g in grads.values():
+                dist.all_reduce(g, op=dist.ReduceOp.SUM)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms, fwd_ms, bwd_ms = 0.0, 0.0, 0.0
+    for _ in range(args.train_steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+        fwd_ms += e_fwd[0].elapsed_time(e_fwd[1])
+        bwd_ms += e_fwd[2].elapsed_time(e_fwd[3])
+    ctx.set_training(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    k = args.train_steps
+    return {"metric": "training views/s (forward + MSE + backward"
+                      + (" + NCCL grad all-reduce" if world > 1 else "") + ")",
+            "value": len(views) * world * k / (ms / 1e3), "unit": "views/s",
+            "ms_per_step": ms / k, "forward_ms": fwd_ms / k, "backward_ms": bwd_ms / k,
+            "loss": float(loss.item()), "views_per_gpu_per_step": len(views), "steps": k,
+            "grads": "mean, opacity, scales, quaternion, colour (14 fp32 per Gaussian)"}
+
+
 def cpu_baseline(cfg_name, budget_s=12.0):
     import oracle
     scene, views = sg.make_config(cfg_name, n_views=8)
@@ -204,6 +269,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool", type=int, default=4, help="distinct view batches cycled per step")
+    ap.add_argument("--no-train", action="store_true", help="skip the config-5 training step")
+    ap.add_argument("--train-steps", type=int, default=5)
     args = ap.parse_args()
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     args.warmup = max(args.warmup, 3)
@@ -320,6 +387,11 @@ def main():
                 "frac": ach / hbm_peak, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
                 "alg_bytes_per_launch": bytes_[dom], "traffic": None}
 
+    # ---------------- config 5: training step (forward + MSE + backward [+ grad all-reduce])
+    train = None
+    if not args.no_train and args.config != "toy":
+        train = run_train(args, ctx, ds, pools[0], tables[0], outs, world, dev, stream)
+
     # ---------------- e2e through the host-buffer C-ABI entry point
     e2e = None
     if not args.no_e2e:
@@ -388,6 +460,7 @@ def main():
                                    "n_blend_exec")},
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "train": train,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
