@@ -24,6 +24,10 @@ BUILD = os.path.join(HERE, "build")
 SOURCES = ["k_filter.cu", "k_project.cu", "k_sort.cu", "k_bin.cu", "k_raster.cu",
            "k_backward.cu", "s3r_api.cu"]
 HEADERS = ["s3r_internal.cuh", os.path.join("..", "..", "include", "s3r.h")]
+# The backward (config 5) is compared with the oracle at 1e-3, not bit for bit:
+# it may contract multiply-adds (its forward recomputation uses explicit
+# __fmaf_rn / separate ops where it must match the forward's decisions).
+CONTRACTED = {"k_backward.cu"}
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -48,7 +52,10 @@ def _build(out: str, bdir: str, defines=(), force: bool = False, verbose: bool =
         o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            jobs.append([NVCC, *FLAGS, *dflags, "-c", s, "-o", o])
+            flags = list(FLAGS)
+            if src in CONTRACTED:      # not part of the bit-exact forward contract
+                flags[flags.index("-fmad=false")] = "-fmad=true"
+            jobs.append([NVCC, *flags, *dflags, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

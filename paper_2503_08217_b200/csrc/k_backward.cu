@@ -135,10 +135,11 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
                 const float G = s3r_exp2_b(e2);
                 const float og = q0.w * G;
                 const float alpha = fminf(0.99f, og);
-                const float Tb = Tc[k] / (1.0f - alpha);    // T before this splat
+                const float inv = __frcp_rn(1.0f - alpha);
+                const float Tb = Tc[k] * inv;               // T before this splat
                 const float w = alpha * Tb;
                 const float cdot = q2.x * gr[k] + q2.y * gg[k] + q2.z * gb[k] + q0.z * gd[k];
-                const float galpha = Tb * cdot - (Rr[k] + gt[k] * Tf[k]) / (1.0f - alpha);
+                const float galpha = Tb * cdot - (Rr[k] + gt[k] * Tf[k]) * inv;
                 Rr[k] += cdot * w;
                 Tc[k] = Tb;
                 any = true;
@@ -160,16 +161,37 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
                 }
             }
             if (__any_sync(0xffffffffu, any)) {
-                s_mx = warp_sum(s_mx); s_my = warp_sum(s_my); s_z = warp_sum(s_z);
-                s_A = warp_sum(s_A); s_B = warp_sum(s_B); s_C = warp_sum(s_C);
-                s_o = warp_sum(s_o); s_r = warp_sum(s_r); s_g = warp_sum(s_g);
-                s_b = warp_sum(s_b);
-                if (lane == 0) {
+                // 10-value warp reduction by halving exchanges (12 padded values:
+                // 6 + 3 shuffles split them over 4 lane groups, 3 x 3 finish the
+                // sums), then 4 lanes add 3 values each to the splat's accumulator
+                float v12[12] = {s_mx, s_my, s_z, s_A, s_B, s_C, s_o, s_r, s_g, s_b, 0.f, 0.f};
+                const bool up16 = (lane & 16) != 0;
+                float v6[6];
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const float send = up16 ? v12[i] : v12[6 + i];
+                    const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+                    v6[i] = (up16 ? v12[6 + i] : v12[i]) + recv;
+                }
+                const bool up8 = (lane & 8) != 0;
+                float v3[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const float send = up8 ? v6[i] : v6[3 + i];
+                    const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
+                    v3[i] = (up8 ? v6[3 + i] : v6[i]) + recv;
+                }
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) v3[i] += __shfl_xor_sync(0xffffffffu, v3[i], o);
+                if ((lane & 7) == 0) {
+                    // lane group (up16, up8) holds values 6*up16 + 3*up8 + {0,1,2}
+                    const int base = (up16 ? 6 : 0) + (up8 ? 3 : 0);
                     float* d = acc + 10ll * lst[rg.x + j];
-                    atomicAdd(d + 0, s_mx); atomicAdd(d + 1, s_my); atomicAdd(d + 2, s_z);
-                    atomicAdd(d + 3, s_A); atomicAdd(d + 4, s_B); atomicAdd(d + 5, s_C);
-                    atomicAdd(d + 6, s_o); atomicAdd(d + 7, s_r); atomicAdd(d + 8, s_g);
-                    atomicAdd(d + 9, s_b);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        if (base + i < 10) atomicAdd(d + base + i, v3[i]);
                 }
             }
         }
