@@ -48,6 +48,13 @@ __device__ __forceinline__ float s3r_exp2_b(float x)
     return y * __uint_as_float((__float_as_uint(t) << 23) + 0x3F800000u);
 }
 
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float warp_sum(float x)
 {
 #pragma unroll
@@ -69,7 +76,7 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
     const int py0 = ty * TILE + (lane >> 3);
     const float fpx = (float)px;
     const s3r_cot C = a.cots[v];
-    float fpy[RPIX], Tc[RPIX], Tf[RPIX], Rr[RPIX], gr[RPIX], gg[RPIX], gb[RPIX], gd[RPIX], gt[RPIX];
+    float fpy[RPIX], Tc[RPIX], gtTf[RPIX], Rr[RPIX], gr[RPIX], gg[RPIX], gb[RPIX], gd[RPIX];
     int last[RPIX];
     int mymax = 0;
 #pragma unroll
@@ -77,17 +84,17 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
         const int py = py0 + 4 * k;
         fpy[k] = (float)py;
         last[k] = 0;
-        Tc[k] = Tf[k] = 1.0f;
-        Rr[k] = gr[k] = gg[k] = gb[k] = gd[k] = gt[k] = 0.0f;
+        Tc[k] = 1.0f;
+        Rr[k] = gr[k] = gg[k] = gb[k] = gd[k] = gtTf[k] = 0.0f;
         if (px < V.W && py < V.H) {
             const long long pix = (long long)py * V.W + px;
             last[k] = a.train_n[V.pix_off + pix];
-            Tc[k] = Tf[k] = a.train_T[V.pix_off + pix];
+            Tc[k] = a.train_T[V.pix_off + pix];
             gr[k] = C.rgb[3 * pix];
             gg[k] = C.rgb[3 * pix + 1];
             gb[k] = C.rgb[3 * pix + 2];
             if (C.depth) gd[k] = C.depth[pix];
-            if (C.final_T) gt[k] = C.final_T[pix];
+            if (C.final_T) gtTf[k] = C.final_T[pix] * Tc[k];
             mymax = max(mymax, last[k]);
         }
     }
@@ -121,8 +128,11 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
             const float a2 = a1 * dx;
             const float b1 = q1.y * dx;
             const float A = q1.x * k2, B = q1.y * k1, Cc = q1.z * k2;
-            float s_mx = 0.f, s_my = 0.f, s_z = 0.f, s_A = 0.f, s_B = 0.f, s_C = 0.f, s_o = 0.f,
-                  s_r = 0.f, s_g = 0.f, s_b = 0.f;
+            // per-thread partial sums; the conic / mean terms factor through the
+            // thread's shared column offset dx: with gP the power gradient,
+            //   sum gP dx^2 = dx^2 S0, sum gP dx dy = dx S1, sum gP dy^2 = S2
+            float S0 = 0.f, S1 = 0.f, S2 = 0.f, s_z = 0.f, s_o = 0.f, s_r = 0.f, s_g = 0.f,
+                  s_b = 0.f;
             bool any = false;
 #pragma unroll
             for (int k = 0; k < RPIX; ++k) {
@@ -135,11 +145,11 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
                 const float G = s3r_exp2_b(e2);
                 const float og = q0.w * G;
                 const float alpha = fminf(0.99f, og);
-                const float inv = __frcp_rn(1.0f - alpha);
+                const float inv = rcp_approx(1.0f - alpha);
                 const float Tb = Tc[k] * inv;               // T before this splat
                 const float w = alpha * Tb;
                 const float cdot = q2.x * gr[k] + q2.y * gg[k] + q2.z * gb[k] + q0.z * gd[k];
-                const float galpha = Tb * cdot - (Rr[k] + gt[k] * Tf[k]) * inv;
+                const float galpha = Tb * cdot - (Rr[k] + gtTf[k]) * inv;
                 Rr[k] += cdot * w;
                 Tc[k] = Tb;
                 any = true;
@@ -147,23 +157,23 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
                 s_g += w * gg[k];
                 s_b += w * gb[k];
                 s_z += w * gd[k];
-                if (og < 0.99f) {
-                    s_o += galpha * G;
-                    if (e2raw <= 0.0f) {
-                        const float gP = galpha * alpha;
-                        const float dyy = dy;
-                        s_A += -0.5f * dx * dx * gP;
-                        s_C += -0.5f * dyy * dyy * gP;
-                        s_B += -dx * dyy * gP;
-                        s_mx += -(A * dx + B * dyy) * gP;
-                        s_my += -(B * dx + Cc * dyy) * gP;
-                    }
-                }
+                // alpha clamped at 0.99: no gradient to o or the power;
+                // power clamped at 0 (e2raw > 0): no gradient to the power
+                const float go = og < 0.99f ? galpha : 0.0f;
+                s_o += go * G;
+                const float gP = e2raw <= 0.0f ? go * alpha : 0.0f;
+                const float t = gP * dy;
+                S0 += gP;
+                S1 += t;
+                S2 += t * dy;
             }
             if (__any_sync(0xffffffffu, any)) {
                 // 10-value warp reduction by halving exchanges (12 padded values:
                 // 6 + 3 shuffles split them over 4 lane groups, 3 x 3 finish the
                 // sums), then 4 lanes add 3 values each to the splat's accumulator
+                const float dS0 = dx * S0;
+                const float s_mx = -(A * dS0 + B * S1), s_my = -(B * dS0 + Cc * S1);
+                const float s_A = -0.5f * dx * dS0, s_B = -dx * S1, s_C = -0.5f * S2;
                 float v12[12] = {s_mx, s_my, s_z, s_A, s_B, s_C, s_o, s_r, s_g, s_b, 0.f, 0.f};
                 const bool up16 = (lane & 16) != 0;
                 float v6[6];
