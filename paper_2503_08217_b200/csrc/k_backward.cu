@@ -29,8 +29,17 @@ namespace s3r {
 
 namespace {
 
-constexpr int RT = 64;
-constexpr int RPIX = 4;
+#ifndef S3R_BWD_RPIX
+#define S3R_BWD_RPIX 4
+#endif
+#ifndef S3R_BWD_EX2
+#define S3R_BWD_EX2 1
+#endif
+// pixels per thread; a tile is 256 pixels, so RT = 256 / RPIX threads, each
+// warp covering BW columns of the tile and 32 / BW rows per k step
+constexpr int RPIX = S3R_BWD_RPIX;
+constexpr int RT = TILE * TILE / RPIX;
+constexpr int BW = TILE / (RT / 32);
 constexpr int RB = 256;
 
 __device__ __forceinline__ float s3r_exp2_b(float x)
@@ -55,6 +64,13 @@ __device__ __forceinline__ float rcp_approx(float x)
     return y;
 }
 
+__device__ __forceinline__ float ex2_approx(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float warp_sum(float x)
 {
 #pragma unroll
@@ -72,8 +88,8 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
     if (tile >= V.ntiles) return;
     const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % V.TX, ty = tile / V.TX;
-    const int px = tx * TILE + ((tid >> 5) << 3) + (lane & 7);   // layout of K7
-    const int py0 = ty * TILE + (lane >> 3);
+    const int px = tx * TILE + (tid >> 5) * BW + (lane % BW);
+    const int py0 = ty * TILE + (lane / BW);
     const float fpx = (float)px;
     const s3r_cot C = a.cots[v];
     float fpy[RPIX], Tc[RPIX], gtTf[RPIX], Rr[RPIX], gr[RPIX], gg[RPIX], gb[RPIX], gd[RPIX];
@@ -81,7 +97,7 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
     int mymax = 0;
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
-        const int py = py0 + 4 * k;
+        const int py = py0 + (32 / BW) * k;
         fpy[k] = (float)py;
         last[k] = 0;
         Tc[k] = 1.0f;
@@ -114,9 +130,12 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
         const int nb = hi - lo;
         __syncthreads();
         for (int i = tid; i < nb; i += RT) {
-            const float4* src = recs + 3ll * lst[rg.x + lo + i];
+            const uint32_t e = lst[rg.x + lo + i];
+            const float4* src = recs + 3ll * e;
             s_rec[3 * i + 0] = src[0];
-            s_rec[3 * i + 1] = src[1];
+            float4 r1 = src[1];
+            r1.w = __uint_as_float(e);            // rect x unused here
+            s_rec[3 * i + 1] = r1;
             s_rec[3 * i + 2] = src[2];
         }
         __syncthreads();
@@ -142,8 +161,20 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
                 const float e2raw = __fmaf_rn(dy, c1, a2);
                 const float e2 = fminf(0.0f, e2raw);
                 if (!(e2 >= -24.0f)) continue;             // flushed in the forward: alpha = 0
+#if S3R_BWD_EX2
+                // hardware exp2 (rel. error ~2^-22); the forward's clamp decision
+                // (o G < 0.99) is re-taken with the exact R-ARITH exp2 whenever
+                // the approximate product lies within 1e-5 of the threshold
+                float G = ex2_approx(e2);
+                float og = q0.w * G;
+                if (fabsf(og - 0.99f) < 1e-5f) {
+                    G = s3r_exp2_b(e2);
+                    og = q0.w * G;
+                }
+#else
                 const float G = s3r_exp2_b(e2);
                 const float og = q0.w * G;
+#endif
                 const float alpha = fminf(0.99f, og);
                 const float inv = rcp_approx(1.0f - alpha);
                 const float Tb = Tc[k] * inv;               // T before this splat
@@ -168,40 +199,38 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
                 S2 += t * dy;
             }
             if (__any_sync(0xffffffffu, any)) {
-                // 10-value warp reduction by halving exchanges (12 padded values:
-                // 6 + 3 shuffles split them over 4 lane groups, 3 x 3 finish the
-                // sums), then 4 lanes add 3 values each to the splat's accumulator
+                // 10-value warp reduction by halving exchanges: at xor-distance
+                // 16 / 8 / 4 / 2 each lane keeps the lower or upper half of its
+                // (zero-padded) values and adds its partner's copy of that half:
+                // 10 -> 5 -> 3 -> 2 -> 1, then one xor-1 step; 12 shuffles. The
+                // lane pair (u16, u8, u4, u2) ends with value 5 u16 + 3 u8 + 2 u4 + u2
+                // (valid when 2 u4 + u2 <= 2 and 3 u8 + 2 u4 + u2 <= 4).
                 const float dS0 = dx * S0;
-                const float s_mx = -(A * dS0 + B * S1), s_my = -(B * dS0 + Cc * S1);
-                const float s_A = -0.5f * dx * dS0, s_B = -dx * S1, s_C = -0.5f * S2;
-                float v12[12] = {s_mx, s_my, s_z, s_A, s_B, s_C, s_o, s_r, s_g, s_b, 0.f, 0.f};
-                const bool up16 = (lane & 16) != 0;
-                float v6[6];
+                const float v10[10] = {-(A * dS0 + B * S1), -(B * dS0 + Cc * S1), s_z,
+                                       -0.5f * dx * dS0, -dx * S1, -0.5f * S2,
+                                       s_o, s_r, s_g, s_b};
+                const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
+                float v5[5], v3[3], v2[2];
 #pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    const float send = up16 ? v12[i] : v12[6 + i];
-                    const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-                    v6[i] = (up16 ? v12[6 + i] : v12[i]) + recv;
-                }
-                const bool up8 = (lane & 8) != 0;
-                float v3[3];
+                for (int i = 0; i < 5; ++i)
+                    v5[i] = (u16 ? v10[5 + i] : v10[i]) +
+                            __shfl_xor_sync(0xffffffffu, u16 ? v10[i] : v10[5 + i], 16);
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    const float send = up8 ? v6[i] : v6[3 + i];
-                    const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
-                    v3[i] = (up8 ? v6[3 + i] : v6[i]) + recv;
+                    const float hiv = i < 2 ? v5[3 + i] : 0.0f;
+                    v3[i] = (u8 ? hiv : v5[i]) + __shfl_xor_sync(0xffffffffu, u8 ? v5[i] : hiv, 8);
                 }
 #pragma unroll
-                for (int o = 4; o > 0; o >>= 1)
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) v3[i] += __shfl_xor_sync(0xffffffffu, v3[i], o);
-                if ((lane & 7) == 0) {
-                    // lane group (up16, up8) holds values 6*up16 + 3*up8 + {0,1,2}
-                    const int base = (up16 ? 6 : 0) + (up8 ? 3 : 0);
-                    float* d = acc + 10ll * lst[rg.x + j];
-#pragma unroll
-                    for (int i = 0; i < 3; ++i)
-                        if (base + i < 10) atomicAdd(d + base + i, v3[i]);
+                for (int i = 0; i < 2; ++i) {
+                    const float hiv = i < 1 ? v3[2 + i] : 0.0f;
+                    v2[i] = (u4 ? hiv : v3[i]) + __shfl_xor_sync(0xffffffffu, u4 ? v3[i] : hiv, 4);
+                }
+                float v1 = (u2 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, u2 ? v2[0] : v2[1], 2);
+                v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+                const int inner = 3 * u8 + 2 * u4 + u2;
+                if (!(lane & 1) && 2 * u4 + u2 <= 2 && inner <= 4) {
+                    const uint32_t g = __float_as_uint(q1.w);    // list entry staged in .w
+                    atomicAdd(acc + 10ll * g + 5 * u16 + inner, v1);
                 }
             }
         }
@@ -351,14 +380,30 @@ __global__ void __launch_bounds__(256) k_project_bwd(BackwardArgs a)
     atomicAdd(gco + 2, gcb);
 }
 
-__global__ void k_mse(const float* __restrict__ x, const float* __restrict__ y, long long n,
-                      float scale, float* __restrict__ grad, float* __restrict__ loss)
+__global__ void __launch_bounds__(256) k_mse(const float* __restrict__ x,
+                                             const float* __restrict__ y, long long n,
+                                             float scale, float* __restrict__ grad,
+                                             float* __restrict__ loss)
 {
+    // float4 body over the 16-byte-aligned prefix (all three pointers share the
+    // alignment when n4 > 0), scalar tail
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                       reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    const long long n4 = vec ? n / 4 : 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const float s2 = 2.f * scale;
     float s = 0.f;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
+    for (long long i = t0; i < n4; i += stride) {
+        const float4 a = reinterpret_cast<const float4*>(x)[i];
+        const float4 b = reinterpret_cast<const float4*>(y)[i];
+        const float4 d = make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+        reinterpret_cast<float4*>(grad)[i] = make_float4(s2 * d.x, s2 * d.y, s2 * d.z, s2 * d.w);
+        s += d.x * d.x + d.y * d.y + d.z * d.z + d.w * d.w;
+    }
+    for (long long i = 4 * n4 + t0; i < n; i += stride) {
         const float d = x[i] - y[i];
-        grad[i] = 2.f * scale * d;
+        grad[i] = s2 * d;
         s += d * d;
     }
     s = warp_sum(s);
@@ -378,7 +423,7 @@ void launch_mse(const float* x, const float* y, long long n, float scale, float*
                 float* loss, cudaStream_t st)
 {
     if (n == 0) return;
-    const long long blocks = std::min<long long>((n + 255) / 256, 148ll * 16);
+    const long long blocks = std::min<long long>((n / 4 + 255) / 256 + 1, 148ll * 8);
     k_mse<<<(unsigned)blocks, 256, 0, st>>>(x, y, n, scale, grad, loss);
 }
 

@@ -314,6 +314,24 @@ def test_backward_matches_oracle(ctx, seed):
     _check_grads(g_gpu, g_ref)
 
 
+@pytest.mark.parametrize("n,off", [(1, 0), (7, 1), (4099, 0), (4099, 3), (1 << 20, 1)])
+def test_mse_ragged(ctx, n, off):
+    """s3r_mse on sizes with a scalar tail and on views that are not 16-byte
+    aligned: grad = 2 s (x - y) elementwise, loss += s sum (x - y)^2."""
+    g = torch.Generator().manual_seed(n + off)
+    x = torch.rand(n + off, generator=g).cuda()[off:]
+    y = torch.rand(n + off, generator=g).cuda()[off:]
+    grad = torch.full((n + off,), 7.0, device="cuda")[off:]
+    loss = torch.full((1,), 0.5, device="cuda")
+    s = 1.0 / n
+    ctx.mse(x, y, s, grad, loss)
+    torch.cuda.synchronize()
+    xd, yd = x.cpu().double(), y.cpu().double()
+    assert torch.equal(grad.cpu(), (2 * s * (x - y)).cpu())
+    want = 0.5 + s * float(((xd - yd) ** 2).sum())
+    assert abs(float(loss) - want) <= 1e-5 * want
+
+
 def test_training_step_mse_street(ctx):
     """MSE loss against noisy targets (the bench's config-5 step) on C2 geometry:
     s3r_mse gradient + backward vs the oracle adjoint of the same cotangent."""

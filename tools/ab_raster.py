@@ -1,5 +1,6 @@
-"""Build raster variants (tools/ab_raster.py build) and time them on a GPU
-(tools/ab_raster.py run): one bench.py run per variant, stage times printed."""
+"""Build kernel variants (tools/ab_raster.py build SET) and time them on a GPU
+(tools/ab_raster.py run SET): one bench.py run per variant, stage times and the
+config-5 training step printed.  SET names one of the dicts in VARIANT_SETS."""
 import json
 import os
 import subprocess
@@ -7,28 +8,40 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VARIANTS = {
-    "base": [],
-    "flush32": ["S3R_FLUSH_E2=-32.0f"],
-    "flush24": ["S3R_FLUSH_E2=-24.0f"],
-    "flush20": ["S3R_FLUSH_E2=-20.0f"],
+VARIANT_SETS = {
+    "flush": {
+        "base": [],
+        "flush32": ["S3R_FLUSH_E2=-32.0f"],
+        "flush20": ["S3R_FLUSH_E2=-20.0f"],
+    },
+    "bwd": {
+        "base": [],
+        "noex2": ["S3R_BWD_EX2=0"],
+        "rp8": ["S3R_BWD_RPIX=8"],
+        "rp2": ["S3R_BWD_RPIX=2"],
+    },
 }
 
 if __name__ == "__main__":
-    if sys.argv[1] == "build":
+    cmd, vset = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "flush"
+    variants = VARIANT_SETS[vset]
+    if cmd == "build":
         from paper_2503_08217_b200 import build as B
-        for name, d in VARIANTS.items():
+        for name, d in variants.items():
             print(B.build_variant(name, d))
     else:
-        for name in VARIANTS:
+        for name in variants:
             env = dict(os.environ, S3R_LIB=os.path.join(ROOT, "paper_2503_08217_b200",
                                                         f"libs3r_{name}.so"))
             r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3",
-                                "--no-e2e", "--no-cpu-baseline"], cwd=ROOT, env=env,
-                               capture_output=True, text=True, timeout=400)
+                                "--no-e2e", "--no-cpu-baseline", "--pool", "1"], cwd=ROOT,
+                               env=env, capture_output=True, text=True, timeout=400)
             try:
                 d = json.loads(r.stdout.strip().splitlines()[-1])
-                print(name, round(d["value"], 1), {k: round(v["ms"], 3) for k, v in d["stages"].items()},
-                      flush=True)
+                t = d.get("train") or {}
+                print(name, round(d["value"], 1),
+                      {k: round(v["ms"], 3) for k, v in d["stages"].items()},
+                      "train", round(t.get("value", 0), 1), "fwd", round(t.get("forward_ms", 0), 2),
+                      "bwd", round(t.get("backward_ms", 0), 2), flush=True)
             except Exception:
-                print(name, "FAILED", r.stderr[-500:], flush=True)
+                print(name, "FAILED", r.stderr[-800:], flush=True)
