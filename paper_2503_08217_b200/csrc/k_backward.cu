@@ -81,6 +81,7 @@ __device__ __forceinline__ float warp_sum(float x)
 __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
 {
     __shared__ float4 s_rec[3 * RB];
+    __shared__ float s_hx[RB];
     __shared__ int s_max;
     const int v = blockIdx.y;
     const DevView& V = a.views[v];
@@ -91,6 +92,10 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
     const int px = tx * TILE + (tid >> 5) * BW + (lane % BW);
     const int py0 = ty * TILE + (lane / BW);
     const float fpx = (float)px;
+    // centre and half size of the warp's BW x TILE pixel block (flush-ellipse culling)
+    const float hbx = 0.5f * (BW - 1), hby = 0.5f * (TILE - 1);
+    const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + hbx;
+    const float bcy = (float)(ty * TILE) + hby;
     const s3r_cot C = a.cots[v];
     float fpy[RPIX], Tc[RPIX], gtTf[RPIX], Rr[RPIX], gr[RPIX], gg[RPIX], gb[RPIX], gd[RPIX];
     int last[RPIX];
@@ -133,15 +138,20 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
             const uint32_t e = lst[rg.x + lo + i];
             const float4* src = recs + 3ll * e;
             s_rec[3 * i + 0] = src[0];
-            float4 r1 = src[1];
-            r1.w = __uint_as_float(e);            // rect x unused here
+            float4 r1 = src[1], r2 = src[2];
+            s_hx[i] = r1.w;                       // flush half extent x
+            r1.w = __uint_as_float(e);            // list entry, for the atomics
             s_rec[3 * i + 1] = r1;
-            s_rec[3 * i + 2] = src[2];
+            s_rec[3 * i + 2] = r2;
         }
         __syncthreads();
         for (int jj = nb - 1; jj >= 0; --jj) {
             const int j = lo + jj;
             const float4 q0 = s_rec[3 * jj], q1 = s_rec[3 * jj + 1], q2 = s_rec[3 * jj + 2];
+            // no evaluation of the warp's block passes the forward's flush test
+            // (s3r_internal.cuh flush_extent): nothing to differentiate
+            if (S3R_CULL && (fabsf(q0.x - bcx) > s_hx[jj] + hbx || fabsf(q0.y - bcy) > q2.w + hby))
+                continue;
             const float dx = q0.x - fpx;
             const float a1 = q1.x * dx;
             const float a2 = a1 * dx;

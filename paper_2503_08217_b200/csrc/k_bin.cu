@@ -44,12 +44,15 @@ __global__ void __launch_bounds__(256) k_permute(const DevView* __restrict__ vie
     const long long base = V.cap_off;
     const uint32_t j = order[base + r];
     const float4* src = rec + 3 * (base + j);
-    const float4 q0 = src[0], q1 = src[1], q2 = src[2];
+    const float4 q0 = src[0];
+    float4 q1 = src[1], q2 = src[2];
+    rect_sorted[base + r] = make_uint2(__float_as_uint(q1.w), __float_as_uint(q2.w));
+    // the rasterizers read the flush-ellipse half extents where the rectangle was
+    flush_extent(q1.x, q1.y, q1.z, q1.w, q2.w);
     float4* dst = rec_sorted + 3 * (base + r);
     dst[0] = q0;
     dst[1] = q1;
     dst[2] = q2;
-    rect_sorted[base + r] = make_uint2(__float_as_uint(q1.w), __float_as_uint(q2.w));
 }
 
 // ------------------------------------------------------------------ K4 count

@@ -48,12 +48,9 @@ constexpr int RPIX = 4;     // pixels per thread: rows ly, ly+4, ly+8, ly+12 of 
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
 // Build-time variants (for A/B measurement; the defaults are the product):
-//   S3R_RASTER_LAYOUT 0: a warp's pixel k is a 16x2 strip; 1: a compact 8x4 block
+//   S3R_CULL          1: skip records whose flush ellipse misses the warp's block
 //   S3R_RASTER_MODE   0: per-lane branch; 1: warp vote + select; 2: select only
 //   S3R_RASTER_MINB   minimum resident CTAs per SM for __launch_bounds__ (0: none)
-#ifndef S3R_RASTER_LAYOUT
-#define S3R_RASTER_LAYOUT 1
-#endif
 #ifndef S3R_RASTER_MODE
 #define S3R_RASTER_MODE 0
 #endif
@@ -61,7 +58,7 @@ constexpr int RB = 256;     // splat records staged in shared memory per batch
 #define S3R_RASTER_MINB 0
 #endif
 #ifndef S3R_FLUSH_E2
-#define S3R_FLUSH_E2 -24.0f   // s3r_exp2(x) = 0 for x < -24 (R-ARITH flush, reading R14)
+#define S3R_FLUSH_E2 FLUSH_E2
 #endif
 #if S3R_RASTER_MINB > 0
 #define S3R_RASTER_BOUNDS __launch_bounds__(RT, S3R_RASTER_MINB)
@@ -82,14 +79,12 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     // warp w owns columns 8w..8w+7; for pixel k a warp covers a compact 8x4 block
     // (rows 4k..4k+3), so a small splat leaves most (warp, k) blocks untouched and
     // they are skipped warp-uniformly
-#if S3R_RASTER_LAYOUT == 1
     const int px = tx * TILE + ((tid >> 5) << 3) + (lane & 7);
     const int py0 = ty * TILE + (lane >> 3);
-#else
-    const int px = tx * TILE + (tid & 15);
-    const int py0 = ty * TILE + (tid >> 4);
-#endif
     const float fpx = (float)px;
+    // centre of the warp's 8 x 16 pixel block (flush-ellipse culling)
+    const float bcx = (float)(tx * TILE + ((tid >> 5) << 3)) + 3.5f;
+    const float bcy = (float)(ty * TILE) + 7.5f;
     float fpy[RPIX], T[RPIX], cr[RPIX], cg[RPIX], cb[RPIX], dp[RPIX];
     int stop[RPIX];
     int nlive = 0;                     // pixels of this thread still blending
@@ -135,8 +130,14 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
             for (int j = 0; j < nb; ++j) {
                 const float4* sr = s_rec + 3 * j;
                 const float4 q0 = sr[0];   // mx, my, z, o
-                const float4 q1 = sr[1];   // qa, qb, qc, rect
-                const float4 q2 = sr[2];   // r, g, b, rect
+                const float4 q1 = sr[1];   // qa, qb, qc, flush half extent x
+                const float4 q2 = sr[2];   // r, g, b, flush half extent y
+#if S3R_CULL
+                // every evaluation of the warp's block lies outside the splat's
+                // flush ellipse (alpha = 0 for all of them): skip the record,
+                // warp-uniformly (s3r_internal.cuh flush_extent)
+                if (fabsf(q0.x - bcx) > q1.w + 3.5f || fabsf(q0.y - bcy) > q2.w + 7.5f) continue;
+#endif
                 // e2 = log2(e) * power = qa dx^2 + qb dx dy + qc dy^2 (R-ARITH exp2
                 // form); the dx terms are shared by the thread's 4 pixels
                 const float dx = q0.x - fpx;

@@ -14,6 +14,37 @@
 namespace s3r {
 
 constexpr int TILE = 16;                 // tile edge (reading R12)
+constexpr float FLUSH_E2 = -24.0f;       // s3r_exp2(x) = 0 for x < -24 (R-ARITH flush, R14)
+
+// Flush-ellipse culling (exact).  For a splat with exp2-form
+// coefficients (qa, qb, qc), every pixel offset d = (dx, dy) with
+// -(qa dx^2 + qb dx dy + qc dy^2) > CULL_TAU evaluates, in R-ARITH fp32, to
+// e2 < FLUSH_E2, i.e. alpha = 0: the relative rounding error of that evaluation
+// is below 6 * 2^-24 * kappa, kappa = (|qa| + |qb| + |qc|) / lambda_min, and the
+// extent is only used (finite) when kappa <= CULL_KAPPA, where that error is
+// <= 3.6e-3 << CULL_TAU / 24 - 1 = 5 %.  The half extents of the CULL_TAU
+// ellipse (inflated by 0.1 % + 0.01 px for their own rounding) are stored in
+// the sorted splat record's two .w slots; +inf disables culling for the splat.
+#ifndef S3R_CULL
+#define S3R_CULL 1       // build-time switch (A/B measurement); 1 is the product
+#endif
+constexpr float CULL_TAU = 25.2f;
+constexpr float CULL_KAPPA = 1.0e4f;
+
+__device__ __forceinline__ void flush_extent(float qa, float qb, float qc, float& hx, float& hy)
+{
+    const float a = -qa, b = -qb, c = -qc;
+    const float det4 = a * c - 0.25f * b * b;
+    const float h = 0.5f * (a + c);
+    const float g = sqrtf(0.25f * (a - c) * (a - c) + 0.25f * b * b);
+    const float lmin = det4 / (h + g);
+    hx = hy = __int_as_float(0x7f800000);
+    if (a > 0.0f && c > 0.0f && det4 > 0.0f && lmin > 0.0f &&
+        a + fabsf(b) + c <= CULL_KAPPA * lmin) {
+        hx = sqrtf(CULL_TAU * c / det4) * 1.001f + 0.01f;
+        hy = sqrtf(CULL_TAU * a / det4) * 1.001f + 0.01f;
+    }
+}
 constexpr int MAX_TSLOTS = 64;           // distinct times per K1 launch
 constexpr int RADIX_BITS = 8;
 constexpr int RADIX = 1 << RADIX_BITS;   // 256 bins per onesweep pass

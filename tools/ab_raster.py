@@ -14,6 +14,10 @@ VARIANT_SETS = {
         "flush32": ["S3R_FLUSH_E2=-32.0f"],
         "flush20": ["S3R_FLUSH_E2=-20.0f"],
     },
+    "cull": {
+        "base": [],
+        "nocull": ["S3R_CULL=0"],
+    },
     "bwd": {
         "base": [],
         "noex2": ["S3R_BWD_EX2=0"],
