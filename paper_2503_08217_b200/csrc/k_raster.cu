@@ -23,25 +23,12 @@ namespace s3r {
 
 namespace {
 
-// R-ARITH s3r_exp2 for -24 <= x <= 0 (the caller handles the flush x < -24 -> 0):
-// n = rint(x) by the 1.5*2^23 shifter (all full-rate FADDs, no F2I/FRND),
-// r = x - n exact, 2^r by the Cephes exp2f polynomial, times 2^n built from
-// the shifter's bits: bits(t) = 0x4B400000 + n, so (bits(t) << 23) +
-// 0x3F800000 = bits(2^n).
+// R-ARITH s3r_exp2 for -24 <= x <= 0 (the caller handles the flush x < -24 -> 0),
+// evaluated on pixel pairs by s3r_exp2_x2 below: n = rint(x) by the 1.5*2^23
+// shifter (full-rate FADDs, no F2I/FRND), r = x - n exact, 2^r by the Cephes
+// exp2f polynomial, times 2^n built from the shifter's bits: bits(t) =
+// 0x4B400000 + n, so (bits(t) << 23) + 0x3F800000 = bits(2^n).
 // c0 = 1.535336188319500e-4f is passed in a register (see k_raster).
-__device__ __forceinline__ float s3r_exp2(float x, float c0)
-{
-    const float t = x + 12582912.0f;
-    const float n = t - 12582912.0f;
-    const float r = x - n;
-    float p = __fmaf_rn(c0, r, 1.339887440266574e-3f);
-    p = __fmaf_rn(p, r, 9.618437357674640e-3f);
-    p = __fmaf_rn(p, r, 5.550332471162809e-2f);
-    p = __fmaf_rn(p, r, 2.402264791363012e-1f);
-    p = __fmaf_rn(p, r, 6.931472028550421e-1f);
-    const float y = __fmaf_rn(p, r, 1.0f);
-    return y * __uint_as_float((__float_as_uint(t) << 23) + 0x3F800000u);
-}
 
 constexpr int RT = 64;      // threads per tile CTA: 16 columns x 4 row groups
 constexpr int RPIX = 4;     // pixels per thread: rows ly, ly+4, ly+8, ly+12 of one column
@@ -49,11 +36,7 @@ constexpr int RB = 256;     // splat records staged in shared memory per batch
 
 // Build-time variants (for A/B measurement; the defaults are the product):
 //   S3R_CULL          1: skip records whose flush ellipse misses the warp's block
-//   S3R_RASTER_MODE   0: per-lane branch; 1: warp vote + select; 2: select only
 //   S3R_RASTER_MINB   minimum resident CTAs per SM for __launch_bounds__ (0: none)
-#ifndef S3R_RASTER_MODE
-#define S3R_RASTER_MODE 0
-#endif
 #ifndef S3R_RASTER_MINB
 #define S3R_RASTER_MINB 0
 #endif
@@ -66,6 +49,32 @@ constexpr int RB = 256;     // splat records staged in shared memory per batch
 #define S3R_RASTER_BOUNDS __launch_bounds__(RT)
 #endif
 
+// Packed pairs: sm_100a executes two fp32 operations per instruction
+// (FADD2 / FMUL2 / FFMA2, __fadd2_rn / __fmul2_rn / __ffma2_rn), each component
+// rounded exactly like the scalar __fadd_rn / __fmul_rn / __fmaf_rn.  A thread's
+// 4 pixels are blended as 2 pairs (rows k, k+4 | k+8, k+12), which halves the
+// issue slots of the FP32 work while the result stays bit-identical to the
+// scalar R-ARITH sequence.
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 neg2(float2 x) { return make_float2(-x.x, -x.y); }
+
+// s3r_exp2 on a pair (same operations as s3r_exp2, component-wise)
+__device__ __forceinline__ float2 s3r_exp2_x2(float2 x, float c0)
+{
+    const float2 t = __fadd2_rn(x, f2(12582912.0f));
+    const float2 n = __fadd2_rn(t, f2(-12582912.0f));
+    const float2 r = __fadd2_rn(x, neg2(n));
+    float2 p = __ffma2_rn(f2(c0), r, f2(1.339887440266574e-3f));
+    p = __ffma2_rn(p, r, f2(9.618437357674640e-3f));
+    p = __ffma2_rn(p, r, f2(5.550332471162809e-2f));
+    p = __ffma2_rn(p, r, f2(2.402264791363012e-1f));
+    p = __ffma2_rn(p, r, f2(6.931472028550421e-1f));
+    const float2 y = __ffma2_rn(p, r, f2(1.0f));
+    const float2 sc = make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + 0x3F800000u),
+                                  __uint_as_float((__float_as_uint(t.y) << 23) + 0x3F800000u));
+    return __fmul2_rn(y, sc);
+}
+
 template <bool COUNT, bool TRAIN>
 __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 {
@@ -77,29 +86,33 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % V.TX, ty = tile / V.TX;
     // warp w owns columns 8w..8w+7; for pixel k a warp covers a compact 8x4 block
-    // (rows 4k..4k+3), so a small splat leaves most (warp, k) blocks untouched and
-    // they are skipped warp-uniformly
+    // (rows 4k..4k+3)
     const int px = tx * TILE + ((tid >> 5) << 3) + (lane & 7);
     const int py0 = ty * TILE + (lane >> 3);
     const float fpx = (float)px;
     // centre of the warp's 8 x 16 pixel block (flush-ellipse culling)
     const float bcx = (float)(tx * TILE + ((tid >> 5) << 3)) + 3.5f;
     const float bcy = (float)(ty * TILE) + 7.5f;
-    float fpy[RPIX], T[RPIX], cr[RPIX], cg[RPIX], cb[RPIX], dp[RPIX];
+    // pair P holds pixels k = 2P (.x) and 2P + 1 (.y)
+    float2 nfpy[2], T[2], cr[2], cg[2], cb[2], dp[2];
     int stop[RPIX];
     int nlive = 0;                     // pixels of this thread still blending
     unsigned inside = 0;
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
         const int py = py0 + 4 * k;
-        fpy[k] = (float)py;
-        cr[k] = cg[k] = cb[k] = dp[k] = 0.0f;
         stop[k] = -1;
         const bool in = px < V.W && py < V.H;
-        // a pixel outside the image starts "terminated" (T = 0 is never written)
-        T[k] = in ? 1.0f : 0.0f;
         inside |= (in ? 1u : 0u) << k;
         nlive += in ? 1 : 0;
+    }
+#pragma unroll
+    for (int P = 0; P < 2; ++P) {
+        nfpy[P] = make_float2(-(float)(py0 + 8 * P), -(float)(py0 + 8 * P + 4));
+        // a pixel outside the image starts "terminated" (T = 0 is never written)
+        T[P] = make_float2((inside >> (2 * P)) & 1 ? 1.0f : 0.0f,
+                           (inside >> (2 * P + 1)) & 1 ? 1.0f : 0.0f);
+        cr[P] = cg[P] = cb[P] = dp[P] = f2(0.0f);
     }
     const int2 rg = a.tranges[V.trange_off + tile];
     const uint32_t* lst = a.tlists + V.tlist_off;
@@ -145,41 +158,36 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                 const float a2 = a1 * dx;
                 const float b1 = q1.y * dx;
 #pragma unroll
-                for (int k = 0; k < RPIX; ++k) {
-                    const float dy = q0.y - fpy[k];
-                    const float c1 = __fmaf_rn(q1.z, dy, b1);
-                    const float e2 = fminf(0.0f, __fmaf_rn(dy, c1, a2));
+                for (int P = 0; P < 2; ++P) {
+                    const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
+                    const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
+                    const float2 e2r = __ffma2_rn(dy, c1, f2(a2));
+                    const float2 e2 = make_float2(fminf(0.0f, e2r.x), fminf(0.0f, e2r.y));
                     // A dead pixel (T < 1e-4) or a flushed exp2 (e2 < -24, s3r_exp2 = 0)
                     // has alpha = 0, which leaves C, D and T bit-identical
-                    // (fma(c, 0, C) == C, T - 0 == T): such evaluations are skipped.
-                    const bool on = (e2 >= S3R_FLUSH_E2) && (T[k] >= 1e-4f);
-#if S3R_RASTER_MODE == 0
-                    if (on) {
-                        const float alpha = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
-#else
-#if S3R_RASTER_MODE == 1
-                    // warp-uniform skip when no lane of the warp needs this pixel
-                    if (__any_sync(0xffffffffu, on)) {
-#else
-                    {
-#endif
-                        const float a_on = fminf(0.99f, q0.w * s3r_exp2(e2, c0));
-                        float alpha;   // selp: lanes that are off get alpha = 0
-                        asm("{ .reg .pred p; setp.ne.u32 p, %3, 0; selp.f32 %0, %1, %2, p; }"
-                            : "=f"(alpha)
-                            : "f"(a_on), "f"(0.0f), "r"((unsigned)on));
-#endif
-                        const float w = alpha * T[k];
-                        cr[k] = __fmaf_rn(q2.x, w, cr[k]);
-                        cg[k] = __fmaf_rn(q2.y, w, cg[k]);
-                        cb[k] = __fmaf_rn(q2.z, w, cb[k]);
-                        dp[k] = __fmaf_rn(q0.z, w, dp[k]);
+                    // (fma(c, 0, C) == C, T - 0 == T): such evaluations are skipped
+                    // (both of the pair) or get alpha = 0 (one of the pair).
+                    const bool onx = (e2.x >= S3R_FLUSH_E2) && (T[P].x >= 1e-4f);
+                    const bool ony = (e2.y >= S3R_FLUSH_E2) && (T[P].y >= 1e-4f);
+                    if (onx || ony) {
+                        const float2 og = __fmul2_rn(f2(q0.w), s3r_exp2_x2(e2, c0));
+                        const float2 alpha = make_float2(onx ? fminf(0.99f, og.x) : 0.0f,
+                                                         ony ? fminf(0.99f, og.y) : 0.0f);
+                        const float2 w = __fmul2_rn(alpha, T[P]);
+                        cr[P] = __ffma2_rn(f2(q2.x), w, cr[P]);
+                        cg[P] = __ffma2_rn(f2(q2.y), w, cg[P]);
+                        cb[P] = __ffma2_rn(f2(q2.z), w, cb[P]);
+                        dp[P] = __ffma2_rn(f2(q0.z), w, dp[P]);
+                        const float2 Tn = __fadd2_rn(T[P], neg2(w));
                         // include-then-stop (R14): the pixel is dead once T < 1e-4
-                        if ((COUNT || TRAIN) && on && T[k] - w < 1e-4f) stop[k] = tpos + j + 1;
-                        T[k] = T[k] - w;
+                        if (COUNT || TRAIN) {
+                            if (onx && Tn.x < 1e-4f) stop[2 * P] = tpos + j + 1;
+                            if (ony && Tn.y < 1e-4f) stop[2 * P + 1] = tpos + j + 1;
+                        }
+                        T[P] = Tn;
                     }
                 }
-                const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
+                const float tmax = fmaxf(fmaxf(T[0].x, T[0].y), fmaxf(T[1].x, T[1].y));
                 nlive = tmax >= 1e-4f ? 1 : 0;
                 if (!__any_sync(0xffffffffu, nlive != 0)) break;   // whole warp done
             }
@@ -201,15 +209,18 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
         if (!(inside & (1u << k))) continue;
+        const int P = k >> 1;
+        const bool hi = k & 1;
         const long long pix = (long long)(py0 + 4 * k) * V.W + px;
         float* o = V.rgb + 3 * pix;
-        o[0] = cr[k];
-        o[1] = cg[k];
-        o[2] = cb[k];
-        if (V.depth) V.depth[pix] = dp[k];
-        if (V.finalT) V.finalT[pix] = T[k];
+        o[0] = hi ? cr[P].y : cr[P].x;
+        o[1] = hi ? cg[P].y : cg[P].x;
+        o[2] = hi ? cb[P].y : cb[P].x;
+        const float Tk = hi ? T[P].y : T[P].x;
+        if (V.depth) V.depth[pix] = hi ? dp[P].y : dp[P].x;
+        if (V.finalT) V.finalT[pix] = Tk;
         if (TRAIN) {      // state the backward (k_raster_bwd) starts from
-            a.train_T[V.pix_off + pix] = T[k];
+            a.train_T[V.pix_off + pix] = Tk;
             a.train_n[V.pix_off + pix] = stop[k] >= 0 ? stop[k] : tpos;
         }
     }
