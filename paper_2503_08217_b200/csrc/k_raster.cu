@@ -38,7 +38,7 @@ constexpr int RB = 256;     // splat records staged in shared memory per batch
 //   S3R_CULL          1: skip records whose flush ellipse misses the warp's block
 //   S3R_RASTER_MINB   minimum resident CTAs per SM for __launch_bounds__ (0: none)
 #ifndef S3R_RASTER_MINB
-#define S3R_RASTER_MINB 0
+#define S3R_RASTER_MINB 16    // 64 registers, 32 resident warps per SM (A/B: 16.6 vs 17.2 ms)
 #endif
 #ifndef S3R_FLUSH_E2
 #define S3R_FLUSH_E2 FLUSH_E2

@@ -14,6 +14,24 @@ VARIANT_SETS = {
         "flush32": ["S3R_FLUSH_E2=-32.0f"],
         "flush20": ["S3R_FLUSH_E2=-20.0f"],
     },
+    "minb": {
+        "base": [],
+        "minb12": ["S3R_RASTER_MINB=12"],
+        "minb14": ["S3R_RASTER_MINB=14"],
+        "minb16": ["S3R_RASTER_MINB=16"],
+    },
+    "mb": {
+        "base": [],
+        "minb16": ["S3R_RASTER_MINB=16"],
+        "minb14": ["S3R_RASTER_MINB=14"],
+    },
+    "live": {
+        "base": [],
+        "live1": ["S3R_LIVE_EVERY=1"],
+        "live8": ["S3R_LIVE_EVERY=8"],
+        "live0": ["S3R_LIVE_EVERY=0"],
+        "live0_mb0": ["S3R_LIVE_EVERY=0", "S3R_RASTER_MINB=0"],
+    },
     "cull": {
         "base": [],
         "nocull": ["S3R_CULL=0"],
