@@ -32,6 +32,9 @@ namespace {
 #ifndef S3R_BWD_RPIX
 #define S3R_BWD_RPIX 4
 #endif
+#ifndef S3R_BWD_MINB
+#define S3R_BWD_MINB 12     // 80 registers (A/B: 41.9 ms vs 46.1 at 128 registers)
+#endif
 #ifndef S3R_BWD_EX2
 #define S3R_BWD_EX2 1
 #endif
@@ -78,7 +81,10 @@ __device__ __forceinline__ float warp_sum(float x)
     return x;
 }
 
-__global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 neg2(float2 x) { return make_float2(-x.x, -x.y); }
+
+__global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
 {
     __shared__ float4 s_rec[3 * RB];
     __shared__ float s_hx[RB];
@@ -97,27 +103,41 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
     const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + hbx;
     const float bcy = (float)(ty * TILE) + hby;
     const s3r_cot C = a.cots[v];
-    float fpy[RPIX], Tc[RPIX], gtTf[RPIX], Rr[RPIX], gr[RPIX], gg[RPIX], gb[RPIX], gd[RPIX];
+    // the thread's 4 pixels (rows py0 + 4k) as 2 packed pairs: pair P holds
+    // k = 2P (.x) and 2P + 1 (.y); sm_100a FADD2/FMUL2/FFMA2 work on both
+    float Tk[RPIX], gtTk[RPIX], grk[RPIX], ggk[RPIX], gbk[RPIX], gdk[RPIX], nfk[RPIX];
     int last[RPIX];
     int mymax = 0;
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
         const int py = py0 + (32 / BW) * k;
-        fpy[k] = (float)py;
+        nfk[k] = -(float)py;
         last[k] = 0;
-        Tc[k] = 1.0f;
-        Rr[k] = gr[k] = gg[k] = gb[k] = gd[k] = gtTf[k] = 0.0f;
+        Tk[k] = 1.0f;
+        grk[k] = ggk[k] = gbk[k] = gdk[k] = gtTk[k] = 0.0f;
         if (px < V.W && py < V.H) {
             const long long pix = (long long)py * V.W + px;
             last[k] = a.train_n[V.pix_off + pix];
-            Tc[k] = a.train_T[V.pix_off + pix];
-            gr[k] = C.rgb[3 * pix];
-            gg[k] = C.rgb[3 * pix + 1];
-            gb[k] = C.rgb[3 * pix + 2];
-            if (C.depth) gd[k] = C.depth[pix];
-            if (C.final_T) gtTf[k] = C.final_T[pix] * Tc[k];
+            Tk[k] = a.train_T[V.pix_off + pix];
+            grk[k] = C.rgb[3 * pix];
+            ggk[k] = C.rgb[3 * pix + 1];
+            gbk[k] = C.rgb[3 * pix + 2];
+            if (C.depth) gdk[k] = C.depth[pix];
+            if (C.final_T) gtTk[k] = C.final_T[pix] * Tk[k];
             mymax = max(mymax, last[k]);
         }
+    }
+    float2 Tc[2], gtTf[2], Rr[2], gr[2], gg[2], gb[2], gd[2], nfpy[2];
+#pragma unroll
+    for (int P = 0; P < 2; ++P) {
+        Tc[P] = make_float2(Tk[2 * P], Tk[2 * P + 1]);
+        gtTf[P] = make_float2(gtTk[2 * P], gtTk[2 * P + 1]);
+        gr[P] = make_float2(grk[2 * P], grk[2 * P + 1]);
+        gg[P] = make_float2(ggk[2 * P], ggk[2 * P + 1]);
+        gb[P] = make_float2(gbk[2 * P], gbk[2 * P + 1]);
+        gd[P] = make_float2(gdk[2 * P], gdk[2 * P + 1]);
+        nfpy[P] = make_float2(nfk[2 * P], nfk[2 * P + 1]);
+        Rr[P] = f2(0.0f);
     }
     if (tid == 0) s_max = 0;
     __syncthreads();
@@ -157,56 +177,76 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
             const float a2 = a1 * dx;
             const float b1 = q1.y * dx;
             const float A = q1.x * k2, B = q1.y * k1, Cc = q1.z * k2;
-            // per-thread partial sums; the conic / mean terms factor through the
-            // thread's shared column offset dx: with gP the power gradient,
+            // per-thread partial sums (pairs, summed before the warp reduction);
+            // the conic / mean terms factor through the thread's shared column
+            // offset dx: with gP the power gradient,
             //   sum gP dx^2 = dx^2 S0, sum gP dx dy = dx S1, sum gP dy^2 = S2
-            float S0 = 0.f, S1 = 0.f, S2 = 0.f, s_z = 0.f, s_o = 0.f, s_r = 0.f, s_g = 0.f,
-                  s_b = 0.f;
+            float2 S0 = f2(0.f), S1 = f2(0.f), S2 = f2(0.f), s_z = f2(0.f), s_o = f2(0.f),
+                   s_r = f2(0.f), s_g = f2(0.f), s_b = f2(0.f);
             bool any = false;
 #pragma unroll
-            for (int k = 0; k < RPIX; ++k) {
-                if (j >= last[k]) continue;
-                const float dy = q0.y - fpy[k];
-                const float c1 = __fmaf_rn(q1.z, dy, b1);
-                const float e2raw = __fmaf_rn(dy, c1, a2);
-                const float e2 = fminf(0.0f, e2raw);
-                if (!(e2 >= -24.0f)) continue;             // flushed in the forward: alpha = 0
+            for (int P = 0; P < 2; ++P) {
+                const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
+                const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
+                const float2 e2raw = __ffma2_rn(dy, c1, f2(a2));
+                const float2 e2 = make_float2(fminf(0.0f, e2raw.x), fminf(0.0f, e2raw.y));
+                // entries after the pixel's termination, or flushed in the forward
+                // (alpha = 0): nothing to differentiate
+                const bool okx = j < last[2 * P] && e2.x >= -24.0f;
+                const bool oky = j < last[2 * P + 1] && e2.y >= -24.0f;
+                if (!(okx || oky)) continue;
 #if S3R_BWD_EX2
                 // hardware exp2 (rel. error ~2^-22); the forward's clamp decision
                 // (o G < 0.99) is re-taken with the exact R-ARITH exp2 whenever
                 // the approximate product lies within 1e-5 of the threshold
-                float G = ex2_approx(e2);
-                float og = q0.w * G;
-                if (fabsf(og - 0.99f) < 1e-5f) {
-                    G = s3r_exp2_b(e2);
-                    og = q0.w * G;
+                float2 G = make_float2(ex2_approx(e2.x), ex2_approx(e2.y));
+                float2 og = __fmul2_rn(f2(q0.w), G);
+                if (fabsf(og.x - 0.99f) < 1e-5f) {
+                    G.x = s3r_exp2_b(e2.x);
+                    og.x = q0.w * G.x;
+                }
+                if (fabsf(og.y - 0.99f) < 1e-5f) {
+                    G.y = s3r_exp2_b(e2.y);
+                    og.y = q0.w * G.y;
                 }
 #else
-                const float G = s3r_exp2_b(e2);
-                const float og = q0.w * G;
+                const float2 G = make_float2(s3r_exp2_b(e2.x), s3r_exp2_b(e2.y));
+                const float2 og = __fmul2_rn(f2(q0.w), G);
 #endif
-                const float alpha = fminf(0.99f, og);
-                const float inv = rcp_approx(1.0f - alpha);
-                const float Tb = Tc[k] * inv;               // T before this splat
-                const float w = alpha * Tb;
-                const float cdot = q2.x * gr[k] + q2.y * gg[k] + q2.z * gb[k] + q0.z * gd[k];
-                const float galpha = Tb * cdot - (Rr[k] + gtTf[k]) * inv;
-                Rr[k] += cdot * w;
-                Tc[k] = Tb;
+                // a pixel of the pair that is not ok gets alpha = 0: T, R and the
+                // sums are then unchanged, and its o / power gradients are masked
+                const float2 alpha = make_float2(okx ? fminf(0.99f, og.x) : 0.0f,
+                                                 oky ? fminf(0.99f, og.y) : 0.0f);
+                const float2 om = __fadd2_rn(f2(1.0f), neg2(alpha));
+                const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+                const float2 Tb = __fmul2_rn(Tc[P], inv);        // T before this splat
+                const float2 w = __fmul2_rn(alpha, Tb);
+                float2 cdot = __fmul2_rn(f2(q2.x), gr[P]);
+                cdot = __ffma2_rn(f2(q2.y), gg[P], cdot);
+                cdot = __ffma2_rn(f2(q2.z), gb[P], cdot);
+                cdot = __ffma2_rn(f2(q0.z), gd[P], cdot);
+                // dL/dalpha = T (c.gC + z gD) - (R + gT T_final) / (1 - alpha)
+                const float2 rest = __fmul2_rn(__fadd2_rn(Rr[P], gtTf[P]), inv);
+                const float2 galpha = __ffma2_rn(Tb, cdot, neg2(rest));
+                Rr[P] = __ffma2_rn(cdot, w, Rr[P]);
+                Tc[P] = Tb;
                 any = true;
-                s_r += w * gr[k];
-                s_g += w * gg[k];
-                s_b += w * gb[k];
-                s_z += w * gd[k];
+                s_r = __ffma2_rn(w, gr[P], s_r);
+                s_g = __ffma2_rn(w, gg[P], s_g);
+                s_b = __ffma2_rn(w, gb[P], s_b);
+                s_z = __ffma2_rn(w, gd[P], s_z);
                 // alpha clamped at 0.99: no gradient to o or the power;
                 // power clamped at 0 (e2raw > 0): no gradient to the power
-                const float go = og < 0.99f ? galpha : 0.0f;
-                s_o += go * G;
-                const float gP = e2raw <= 0.0f ? go * alpha : 0.0f;
-                const float t = gP * dy;
-                S0 += gP;
-                S1 += t;
-                S2 += t * dy;
+                const float2 go = make_float2(okx && og.x < 0.99f ? galpha.x : 0.0f,
+                                              oky && og.y < 0.99f ? galpha.y : 0.0f);
+                s_o = __ffma2_rn(go, G, s_o);
+                float2 gP = __fmul2_rn(go, alpha);
+                gP.x = e2raw.x <= 0.0f ? gP.x : 0.0f;
+                gP.y = e2raw.y <= 0.0f ? gP.y : 0.0f;
+                const float2 t = __fmul2_rn(gP, dy);
+                S0 = __fadd2_rn(S0, gP);
+                S1 = __fadd2_rn(S1, t);
+                S2 = __ffma2_rn(t, dy, S2);
             }
             if (__any_sync(0xffffffffu, any)) {
                 // 10-value warp reduction by halving exchanges: at xor-distance
@@ -215,10 +255,11 @@ __global__ void __launch_bounds__(RT) k_raster_bwd(BackwardArgs a)
                 // 10 -> 5 -> 3 -> 2 -> 1, then one xor-1 step; 12 shuffles. The
                 // lane pair (u16, u8, u4, u2) ends with value 5 u16 + 3 u8 + 2 u4 + u2
                 // (valid when 2 u4 + u2 <= 2 and 3 u8 + 2 u4 + u2 <= 4).
-                const float dS0 = dx * S0;
-                const float v10[10] = {-(A * dS0 + B * S1), -(B * dS0 + Cc * S1), s_z,
-                                       -0.5f * dx * dS0, -dx * S1, -0.5f * S2,
-                                       s_o, s_r, s_g, s_b};
+                const float S0s = S0.x + S0.y, S1s = S1.x + S1.y, S2s = S2.x + S2.y;
+                const float dS0 = dx * S0s;
+                const float v10[10] = {-(A * dS0 + B * S1s), -(B * dS0 + Cc * S1s), s_z.x + s_z.y,
+                                       -0.5f * dx * dS0, -dx * S1s, -0.5f * S2s,
+                                       s_o.x + s_o.y, s_r.x + s_r.y, s_g.x + s_g.y, s_b.x + s_b.y};
                 const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
                 float v5[5], v3[3], v2[2];
 #pragma unroll

@@ -38,9 +38,10 @@ VARIANT_SETS = {
     },
     "bwd": {
         "base": [],
-        "noex2": ["S3R_BWD_EX2=0"],
-        "rp8": ["S3R_BWD_RPIX=8"],
-        "rp2": ["S3R_BWD_RPIX=2"],
+        "bmb13": ["S3R_BWD_MINB=13"],
+        "bmb14": ["S3R_BWD_MINB=14"],
+        "bmb12": ["S3R_BWD_MINB=12"],
+        "bmb11": ["S3R_BWD_MINB=11"],
     },
 }
 
