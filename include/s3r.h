@@ -207,7 +207,12 @@ int s3r_render_batch(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* views
 /* Same as s3r_render_batch, but every pointer of scene, views (including
  * instance_w2c) and outs is a HOST pointer (page-locked memory recommended).
  * The library copies the inputs to device scratch, renders, copies the
- * outputs (and the updated life) back and synchronises the stream.         */
+ * outputs (and the updated life) back and synchronises the stream.  Batches of
+ * more than 8 views are rendered 8 views at a time while finished views are
+ * copied back on an internal second stream (results identical to one batch);
+ * s3r_get_stats then covers every view, s3r_dump_intermediates returns
+ * S3R_ESTATE.  With debug, counters, timing or training enabled the batch is
+ * rendered in one piece.                                                    */
 int s3r_render_batch_host(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* views,
                           int32_t n_views, const s3r_outputs* outs, void* stream);
 

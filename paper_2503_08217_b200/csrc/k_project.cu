@@ -395,7 +395,22 @@ __global__ void k_life_flip(float2* __restrict__ life, long long n)
     const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (g < n) life[g].x = -life[g].x;
 }
+
+// small device -> host readback by stores into mapped page-locked memory: it
+// does not queue on the copy engines, so it never waits behind bulk copies
+// that other streams have in flight
+__global__ void k_readback(const uint32_t* __restrict__ src, volatile uint32_t* dst, int words)
+{
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
 }  // namespace
+
+void launch_readback(void* host_mapped, const void* dev, size_t bytes, cudaStream_t st)
+{
+    if (bytes == 0) return;
+    k_readback<<<1, 256, 0, st>>>(static_cast<const uint32_t*>(dev),
+                                  static_cast<uint32_t*>(host_mapped), (int)(bytes / 4));
+}
 
 void launch_project(const ProjectArgs& a, cudaStream_t st)
 {

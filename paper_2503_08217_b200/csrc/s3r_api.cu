@@ -49,6 +49,7 @@ struct s3r_ctx {
     bool last_debug = false;
     // pinned staging
     char* h_stage = nullptr;
+    char* h_stage_dev = nullptr;             // its device address (mapped)
     size_t h_stage_cap = 0;
     size_t h_stage_top = 0;
     cudaEvent_t staging_free = nullptr;
@@ -63,6 +64,9 @@ struct s3r_ctx {
     int gbits = 1;
     // mirrors for s3r_render_batch_host
     Buf m_scene[7];
+    cudaStream_t copy_stream = nullptr;      // D2H of finished chunks (host path)
+    std::vector<cudaEvent_t> chunk_done;
+    bool host_chunked = false;               // last render was a chunked host batch
     std::vector<Buf> m_tab, m_rgb, m_depth, m_T, m_vis;
     // last batch
     std::vector<DevView> hv;
@@ -134,15 +138,20 @@ int stage_reserve(s3r_ctx* c, size_t bytes)
         c->h_stage = nullptr;
     }
     size_t want = std::max<size_t>(bytes * 2, 1 << 16);
-    if (cudaHostAlloc((void**)&c->h_stage, want, cudaHostAllocDefault) != cudaSuccess) {
+    if (cudaHostAlloc((void**)&c->h_stage, want, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&c->h_stage_dev, c->h_stage, 0) != cudaSuccess) {
         cudaGetLastError();
+        if (c->h_stage) cudaFreeHost(c->h_stage);
         c->h_stage = nullptr;
         c->h_stage_cap = 0;
-        return fail(c, S3R_ENOMEM, "cudaHostAlloc of %zu bytes failed", want);
+        return fail(c, S3R_ENOMEM, "cudaHostAlloc (mapped) of %zu bytes failed", want);
     }
     c->h_stage_cap = want;
     return S3R_OK;
 }
+
+// device address of a pointer into the (mapped) staging buffer
+void* mapped(s3r_ctx* c, void* host) { return c->h_stage_dev + ((char*)host - c->h_stage); }
 
 void* stage_alloc(s3r_ctx* c, size_t bytes)
 {
@@ -231,6 +240,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     CU(cudaSetDevice(c->device));
     c->last_stream = st;
     c->have_render = false;
+    c->host_chunked = false;
     if (c->staging_recorded) CU(cudaEventSynchronize(c->staging_free));
     const long long N = sc->n;
     c->N_last = N;
@@ -320,8 +330,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     CU(cudaGetLastError());
     unsigned long long* h_counts =
         (unsigned long long*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(unsigned long long));
-    if (T) CU(cudaMemcpyAsync(h_counts, c->d_counts.p, T * sizeof(unsigned long long),
-                              cudaMemcpyDeviceToHost, st));
+    if (T) launch_readback(mapped(c, h_counts), c->d_counts.p, T * sizeof(unsigned long long), st);
     CU(cudaStreamSynchronize(st));
 
     // ================= K2: projection + LOD + life + compaction
@@ -385,7 +394,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     }
     CU(cudaGetLastError());
     ViewCounters* h_ctr = (ViewCounters*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(ViewCounters));
-    if (nv) CU(cudaMemcpyAsync(h_ctr, c->d_ctr.p, nv * sizeof(ViewCounters), cudaMemcpyDeviceToHost, st));
+    if (nv) launch_readback(mapped(c, h_ctr), c->d_ctr.p, nv * sizeof(ViewCounters), st);
     CU(cudaStreamSynchronize(st));
 
     // ================= sizes of the sort / emit / raster phase
@@ -607,6 +616,8 @@ void s3r_destroy(s3r_ctx* c)
     }
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->staging_free) cudaEventDestroy(c->staging_free);
+    for (cudaEvent_t e : c->chunk_done) cudaEventDestroy(e);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
 }
 
@@ -748,17 +759,57 @@ int s3r_render_batch_host(s3r_ctx* c, const s3r_scene* hs, const s3r_view* hview
             dout[v].visible = P<uint8_t>(c->m_vis[v]);
         }
     }
-    rc = render_impl(c, &ds, dv.data(), nv, dout.data(), st);
-    if (rc != S3R_OK && rc != S3R_EINSTANCE) return rc;
-    for (int v = 0; v < nv; ++v) {
+    auto d2h = [&](int v, cudaStream_t cs) -> int {
         const size_t px = (size_t)hviews[v].width * hviews[v].height;
-        CU(cudaMemcpyAsync(houts[v].rgb, dout[v].rgb, px * 12, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(houts[v].rgb, dout[v].rgb, px * 12, cudaMemcpyDeviceToHost, cs));
         if (houts[v].depth)
-            CU(cudaMemcpyAsync(houts[v].depth, dout[v].depth, px * 4, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(houts[v].depth, dout[v].depth, px * 4, cudaMemcpyDeviceToHost, cs));
         if (houts[v].final_T)
-            CU(cudaMemcpyAsync(houts[v].final_T, dout[v].final_T, px * 4, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(houts[v].final_T, dout[v].final_T, px * 4, cudaMemcpyDeviceToHost, cs));
         if (houts[v].visible && N > 0)
-            CU(cudaMemcpyAsync(houts[v].visible, dout[v].visible, (size_t)N, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(houts[v].visible, dout[v].visible, (size_t)N, cudaMemcpyDeviceToHost, cs));
+        return S3R_OK;
+    };
+    // Chunked pipeline: the views are rendered HOST_CHUNK at a time on `st`
+    // while the finished chunks' outputs stream back to the host on a second
+    // stream, so the device->host copies (the bound of this entry point) overlap
+    // the rendering.  Debug / counters / timing / training keep the one-batch
+    // semantics of s3r_render_batch (their state describes one whole batch).
+    constexpr int HOST_CHUNK = 8;
+    const bool chunked = nv > HOST_CHUNK && !(c->debug || c->counters || c->timing || c->training);
+    if (!chunked) {
+        rc = render_impl(c, &ds, dv.data(), nv, dout.data(), st);
+        if (rc != S3R_OK && rc != S3R_EINSTANCE) return rc;
+        for (int v = 0; v < nv; ++v)
+            if (int r2 = d2h(v, st)) return r2;
+    } else {
+        if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        const int nchunks = (nv + HOST_CHUNK - 1) / HOST_CHUNK;
+        while ((int)c->chunk_done.size() < nchunks) {
+            cudaEvent_t e;
+            CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->chunk_done.push_back(e);
+        }
+        std::vector<s3r_stats> all(nv);
+        int worst = S3R_OK;
+        for (int k = 0; k < nchunks; ++k) {
+            const int v0 = k * HOST_CHUNK, n = std::min(HOST_CHUNK, nv - v0);
+            rc = render_impl(c, &ds, dv.data() + v0, n, dout.data() + v0, st);
+            if (rc != S3R_OK && rc != S3R_EINSTANCE) {
+                cudaStreamSynchronize(c->copy_stream);
+                return rc;
+            }
+            if (rc) worst = rc;
+            std::copy(c->stats.begin(), c->stats.begin() + n, all.begin() + v0);
+            CU(cudaEventRecord(c->chunk_done[k], st));
+            CU(cudaStreamWaitEvent(c->copy_stream, c->chunk_done[k], 0));
+            for (int v = v0; v < v0 + n; ++v)
+                if (int r2 = d2h(v, c->copy_stream)) return r2;
+        }
+        rc = worst;
+        c->stats = all;
+        c->host_chunked = true;
+        CU(cudaStreamSynchronize(c->copy_stream));
     }
     if (hs->life && N > 0)
         CU(cudaMemcpyAsync(hs->life, ds.life, (size_t)N * 8, cudaMemcpyDeviceToHost, st));
@@ -794,6 +845,9 @@ int s3r_dump_intermediates(s3r_ctx* c, int32_t vi, const s3r_debug* dbg, void* s
     if (!c || !dbg) return S3R_EINVAL;
     if (!c->have_render || vi < 0 || vi >= (int)c->hv.size())
         return fail(c, S3R_ESTATE, "dump: no render or view index out of range");
+    if (c->host_chunked)
+        return fail(c, S3R_ESTATE, "dump: the last render was a chunked s3r_render_batch_host "
+                                   "batch (enable debug mode to dump it)");
     cudaStream_t st = (cudaStream_t)stream;
     CU(cudaSetDevice(c->device));
     const DevView& d = c->hv[vi];

@@ -274,6 +274,10 @@ void launch_mse(const float* x, const float* y, long long n, float scale, float*
 
 // K9: commit / reset.
 void launch_commit(float2* vis, float2* life, long long n, float margin, cudaStream_t st);
+
+// bytes (a multiple of 4) from device memory into mapped page-locked host
+// memory (cudaHostAlloc under unified addressing), by a kernel
+void launch_readback(void* host_mapped, const void* dev, size_t bytes, cudaStream_t st);
 void launch_reset(float2* vis, long long n, cudaStream_t st);
 void launch_life_flip(float2* life, long long n, cudaStream_t st);
 

@@ -198,6 +198,35 @@ def test_host_entry_point_matches_device(ctx):
     assert np.array_equal(host_scene.life, ds.life.cpu().numpy())
 
 
+def test_host_entry_point_chunked(ctx):
+    """More than 8 views through s3r_render_batch_host: rendered 8 at a time with
+    the copies back overlapped; outputs, life and per-view stats must equal one
+    device-side batch; dumps are refused after a chunked host batch."""
+    scene, views = sg.make_random_dynamic(17, 1500, 3, 80, 70, 41, 19)
+    ds, tabs, outs, _ = gpu_render(ctx, scene, views, visible=True)
+    want = [ctx.stats(i) for i in range(len(views))]
+    host_scene = scene.copy()
+    htabs = [t.cpu().numpy() for t in tabs]
+    houts = [{"rgb": np.zeros((v.height, v.width, 3), np.float32),
+              "final_T": np.zeros((v.height, v.width), np.float32),
+              "visible": np.zeros(scene.n, np.uint8)} for v in views]
+    ctx.set_debug(False)
+    try:
+        ctx.render_batch_host(host_scene, views, htabs, houts)
+        got = [ctx.stats(i) for i in range(len(views))]
+        with pytest.raises(RuntimeError):
+            ctx.dump(0, views[0].width, views[0].height)
+    finally:
+        ctx.set_debug(True)
+    for o, h in zip(outs, houts):
+        for k in ("rgb", "final_T", "visible"):
+            assert np.array_equal(o[k].cpu().numpy(), h[k])
+    assert np.array_equal(host_scene.life, ds.life.cpu().numpy())
+    for g, w in zip(got, want):
+        for k in ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped", "n_rendered", "n_pairs"):
+            assert g[k] == w[k], k
+
+
 def test_edge_cases(ctx):
     # empty scene
     s0 = make_scene(np.zeros((0, 3)), 0.1)
