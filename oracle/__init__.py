@@ -10,6 +10,7 @@ directory are the oracle; this file only marshals numpy arrays to them.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import os
 import subprocess
 import threading
@@ -92,6 +93,12 @@ def lib():
                 "so_blend_bruteforce_f64": (C.c_int, [P, P, P, P, P, P, P, P]),
                 "so_backward_f64": (C.c_int, [P, P, P, P, P, P]),
                 "so_update_life_f32": (None, [P, P, C.c_float]),
+                "so_quat_from_rot_f32": (None, [P, P]),
+                "so_quat_from_rot_f64": (None, [P, P]),
+                "so_quat_mul_f32": (None, [P, P, P]),
+                "so_quat_mul_f64": (None, [P, P, P]),
+                "so_world_transform_f32": (C.c_int64, [P, P, P, P]),
+                "so_world_transform_f64": (C.c_int64, [P, P, P, P]),
                 "so_commit_visibility": (None, [P, C.c_float]),
                 "so_reset_visibility": (None, [P]),
             }
@@ -213,6 +220,55 @@ def backward(scene, view, g_rgb, g_depth=None, g_T=None, table=None, grads=None)
                            _ptr(g))
     assert rc == 0
     return g
+
+
+def quat_from_rot(R, precision="f32") -> np.ndarray:
+    """C0 quat(R) (Shepperd), (w, x, y, z)."""
+    real = np.float32 if precision == "f32" else np.float64
+    R = np.ascontiguousarray(R, real).reshape(9)
+    q = np.zeros(4, real)
+    getattr(lib(), "so_quat_from_rot_" + precision)(_ptr(R), _ptr(q))
+    return q
+
+
+def quat_mul(a, b, precision="f32") -> np.ndarray:
+    real = np.float32 if precision == "f32" else np.float64
+    a, b = np.ascontiguousarray(a, real), np.ascontiguousarray(b, real)
+    o = np.zeros(4, real)
+    getattr(lib(), "so_quat_mul_" + precision)(_ptr(a), _ptr(b), _ptr(o))
+    return o
+
+
+def world_scene(scene, i2g, precision="f32"):
+    """C0 of the conventional pipeline: the scene moved to the world frame for
+    one frame's poses i2g (K, 3, 4) — every Gaussian static (id 0, K = 0),
+    visibility fresh (-1, 1) so that no temporal filter applies."""
+    K1 = scene.num_instances
+    tab = np.zeros((max(K1, 1), 12), np.float32)
+    if K1 > 1:
+        tab[1:] = np.asarray(i2g, np.float32).reshape(-1, 12)[: K1 - 1]
+    sr = _SceneRef(scene, life=False)
+    mo = np.zeros((scene.n, 4), np.float32)
+    rot = np.zeros((scene.n, 4), np.float32)
+    getattr(lib(), "so_world_transform_" + precision)(C.byref(sr.s), _ptr(tab), _ptr(mo),
+                                                       _ptr(rot))
+    w = scene.copy()
+    w.means_opacity, w.rotations = mo, rot
+    bad = (scene.instance_ids < 0) | (scene.instance_ids >= K1)
+    w.instance_ids = np.where(bad, scene.instance_ids, 0).astype(np.int32)
+    w.num_instances = 1
+    w.visibility = np.tile(np.array([-1.0, 1.0], np.float32), (scene.n, 1))
+    return w
+
+
+def render_view_conventional(scene, view, precision="f32", **kw) -> Dict[str, np.ndarray]:
+    """The conventional pipeline (NEXT-2) for one view: C0 world transform with
+    the view's i2g poses, then O2-O6 for ALL Gaussians through W_t, no LOD."""
+    w = world_scene(scene, view.i2g, precision)
+    v = dataclasses.replace(view, i2g=np.zeros((0, 3, 4), np.float32), lod_r=0.0)
+    o = render_view(w, v, precision, **kw)
+    o["world_scene"] = w
+    return o
 
 
 def temporal_filter(scene, t, precision="f32") -> np.ndarray:

@@ -107,6 +107,11 @@ int      so_blend_bruteforce_f32(const so_scene* s, const so_view* v, const uint
                                  const float* keys, const int16_t* rect,
                                  float* rgb, float* depth, float* final_T);
 void     so_update_life_f32(so_scene* s, const uint8_t* visible, float t);
+/* conventional pipeline C0 (NEXT-2): local -> world copy of the scene */
+void     so_quat_from_rot_f32(const float R[9], float q[4]);
+void     so_quat_mul_f32(const float a[4], const float b[4], float o[4]);
+int64_t  so_world_transform_f32(const so_scene* s, const float* i2g, float* mo_out,
+                                float* rot_out);
 void     so_commit_visibility(so_scene* s, float margin);
 void     so_reset_visibility(so_scene* s);
 
@@ -123,6 +128,10 @@ int64_t  so_temporal_filter_f64(const so_scene* s, double t, int32_t* idx);
 int      so_project_f64(const so_scene* s, const so_view* v, int64_t g, double keys[6]);
 double   so_drop_probability_f64(double d, double pmax, double D);
 int      so_render_view_f64(const so_scene* s, const so_view* v, so_out_f64* o);
+void     so_quat_from_rot_f64(const double R[9], double q[4]);
+void     so_quat_mul_f64(const double a[4], const double b[4], double o[4]);
+int64_t  so_world_transform_f64(const so_scene* s, const float* i2g, float* mo_out,
+                                float* rot_out);
 int      so_blend_bruteforce_f64(const so_scene* s, const so_view* v, const uint8_t* flags,
                                  const double* keys, const int16_t* rect,
                                  double* rgb, double* depth, double* final_T);
