@@ -243,6 +243,22 @@ int s3r_reset_visibility(s3r_ctx* ctx, const s3r_scene* scene, void* stream);
  * not fixed, so results agree to rounding, not bit for bit).              */
 int s3r_set_training(s3r_ctx* ctx, int enable);
 
+/* Pipeline of the following renders (NEXT-2 of SURVEY.md §8(f)):
+ *   S3R_PIPELINE_STREAMLINED (default) — the paper's streamlined stage
+ *     (P:148-199): temporal filter, instance-specific cameras, adaptive LOD.
+ *   S3R_PIPELINE_CONVENTIONAL — the baseline it replaces (Fig.1a; P:20,
+ *     P:45): per view, every dynamic Gaussian is moved to the world
+ *     frame (mu_w = R mu + t, q_w = quat(R) (x) q, R-ARITH op order of
+ *     DESIGN.md §4), then ALL Gaussians are projected through
+ *     W_t; no temporal filter, no LOD.  In this mode views[v].instance_w2c
+ *     slot 0 is W_t (world->camera) and slot i >= 1 the instance's
+ *     local->WORLD pose W_{t,i2g} (not the composed local->camera table).
+ *     Scratch: 32 B per Gaussian per view of the batch.  The backward
+ *     (s3r_render_backward) supports the streamlined pipeline only.
+ * Returns S3R_EINVAL for an unknown value.                                  */
+enum { S3R_PIPELINE_STREAMLINED = 0, S3R_PIPELINE_CONVENTIONAL = 1 };
+int s3r_set_pipeline(s3r_ctx* ctx, int pipeline);
+
 /* Cotangents of one view: DEVICE pointers, dL/d(output) in the output layout;
  * rgb required, depth / final_T may be NULL (= 0).                         */
 typedef struct {

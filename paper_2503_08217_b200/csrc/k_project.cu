@@ -22,6 +22,8 @@
 // 64-bit depth key (depth bits << gbits | Gaussian index).  The record order
 // is therefore not deterministic; the depth sort (K5a) on those keys restores
 // the unique (depth, index) order, so everything downstream is deterministic.
+#include <algorithm>
+
 #include "s3r_internal.cuh"
 
 namespace s3r {
@@ -235,10 +237,19 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
                 for (int j = 0; j < 6; ++j) sp.k[j] = __int_as_float(0x7fc00000);
                 c_bad++;
             } else {
-                const float4 mo = __ldg(a.means_opacity + g);
                 const float4 sc = __ldg(a.scales + g);
-                const float4 q = __ldg(a.rotations + g);
-                project_one(s_tab + 12 * id, mo, sc, q, V, lox, hix, loy, hiy, g, sp);
+                float4 mo, q;
+                int slot = id;
+                if (a.world_mo) {      // conventional: the view's world copy, camera W_t
+                    const long long wg = (long long)vi * a.n + g;
+                    mo = __ldg(a.world_mo + wg);
+                    q = __ldg(a.world_rot + wg);
+                    slot = 0;
+                } else {
+                    mo = __ldg(a.means_opacity + g);
+                    q = __ldg(a.rotations + g);
+                }
+                project_one(s_tab + 12 * slot, mo, sc, q, V, lox, hix, loy, hiy, g, sp);
                 if (sp.flags & F_VISIBLE) {
                     c_vis++;
                     if (vis_out) vis_out[g] = 1;
@@ -396,6 +407,105 @@ __global__ void k_life_flip(float2* __restrict__ life, long long n)
     if (g < n) life[g].x = -life[g].x;
 }
 
+// ---- conventional pipeline C0 (NEXT-2; Fig.1a): the
+// local-to-global transformation of every dynamic Gaussian, per view, that the
+// streamlined stage removes.  mu_w = R mu + t, q_w = quat(R) (x) q, in the
+// R-ARITH op order written out in DESIGN.md §4 (conventional pipeline C0).
+__device__ void quat_from_rot(const float* M, float* q)   // M: 3x4 row-major pose
+{
+    const float r00 = M[0], r01 = M[1], r02 = M[2];
+    const float r10 = M[4], r11 = M[5], r12 = M[6];
+    const float r20 = M[8], r21 = M[9], r22 = M[10];
+    const float tr = (r00 + r11) + r22;
+    if (tr > 0.0f) {
+        const float s = sqrtf(tr + 1.0f) * 2.0f;
+        q[0] = 0.25f * s;
+        q[1] = (r21 - r12) / s;
+        q[2] = (r02 - r20) / s;
+        q[3] = (r10 - r01) / s;
+    } else if (r00 > r11 && r00 > r22) {
+        const float s = sqrtf(((1.0f + r00) - r11) - r22) * 2.0f;
+        q[0] = (r21 - r12) / s;
+        q[1] = 0.25f * s;
+        q[2] = (r01 + r10) / s;
+        q[3] = (r02 + r20) / s;
+    } else if (r11 > r22) {
+        const float s = sqrtf(((1.0f + r11) - r00) - r22) * 2.0f;
+        q[0] = (r02 - r20) / s;
+        q[1] = (r01 + r10) / s;
+        q[2] = 0.25f * s;
+        q[3] = (r12 + r21) / s;
+    } else {
+        const float s = sqrtf(((1.0f + r22) - r00) - r11) * 2.0f;
+        q[0] = (r10 - r01) / s;
+        q[1] = (r02 + r20) / s;
+        q[2] = (r12 + r21) / s;
+        q[3] = 0.25f * s;
+    }
+}
+
+constexpr int WT = 256;
+
+__global__ void __launch_bounds__(WT) k_to_world(const float4* __restrict__ mo,
+                                                 const float4* __restrict__ rot,
+                                                 const int32_t* __restrict__ ids, int K1,
+                                                 long long n, const DevView* __restrict__ views,
+                                                 float4* __restrict__ wmo, float4* __restrict__ wrot)
+{
+    extern __shared__ float s_w[];          // [K1][12] poses, then [K1][4] quat(R)
+    const int vi = blockIdx.y;
+    const DevView& V = views[vi];
+    float* s_q = s_w + 12 * K1;
+    for (int i = threadIdx.x; i < 12 * K1; i += WT) s_w[i] = V.table[i];
+    __syncthreads();
+    for (int i = 1 + threadIdx.x; i < K1; i += WT) quat_from_rot(s_w + 12 * i, s_q + 4 * i);
+    __syncthreads();
+    const long long stride = (long long)gridDim.x * WT;
+    for (long long g = blockIdx.x * (long long)WT + threadIdx.x; g < n; g += stride) {
+        const int id = __ldg(ids + g);
+        float4 m = __ldg(mo + g), q = __ldg(rot + g);
+        if (id > 0 && id < K1) {
+            const float* M = s_w + 12 * id;
+            float p[3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                float acc = __fmaf_rn(M[4 * r + 0], m.x, M[4 * r + 3]);
+                acc = __fmaf_rn(M[4 * r + 1], m.y, acc);
+                acc = __fmaf_rn(M[4 * r + 2], m.z, acc);
+                p[r] = acc;
+            }
+            m = make_float4(p[0], p[1], p[2], m.w);
+            const float* a = s_q + 4 * id;
+            float w = a[0] * q.x;
+            w = __fmaf_rn(-a[1], q.y, w);
+            w = __fmaf_rn(-a[2], q.z, w);
+            w = __fmaf_rn(-a[3], q.w, w);
+            float x = a[0] * q.y;
+            x = __fmaf_rn(a[1], q.x, x);
+            x = __fmaf_rn(a[2], q.w, x);
+            x = __fmaf_rn(-a[3], q.z, x);
+            float y = a[0] * q.z;
+            y = __fmaf_rn(-a[1], q.w, y);
+            y = __fmaf_rn(a[2], q.x, y);
+            y = __fmaf_rn(a[3], q.y, y);
+            float z = a[0] * q.w;
+            z = __fmaf_rn(a[1], q.z, z);
+            z = __fmaf_rn(-a[2], q.y, z);
+            z = __fmaf_rn(a[3], q.x, z);
+            q = make_float4(w, x, y, z);
+        }
+        const long long o = (long long)vi * n + g;
+        wmo[o] = m;
+        wrot[o] = q;
+    }
+}
+
+__global__ void k_iota(int32_t* __restrict__ idx, long long n)
+{
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) idx[i] = (int32_t)i;
+}
+
 // small device -> host readback by stores into mapped page-locked memory: it
 // does not queue on the copy engines, so it never waits behind bulk copies
 // that other streams have in flight
@@ -404,6 +514,25 @@ __global__ void k_readback(const uint32_t* __restrict__ src, volatile uint32_t* 
     for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
 }
 }  // namespace
+
+void launch_world(const float4* mo, const float4* rot, const int32_t* ids, int num_instances,
+                  long long n, const DevView* views, int n_views, float4* wmo, float4* wrot,
+                  cudaStream_t st)
+{
+    if (n == 0 || n_views == 0) return;
+    const size_t smem = (size_t)num_instances * 16 * sizeof(float);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_to_world, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const long long blocks = std::min<long long>((n + WT - 1) / WT, 148ll * 8);
+    k_to_world<<<dim3((unsigned)blocks, n_views), WT, smem, st>>>(mo, rot, ids, num_instances, n,
+                                                                   views, wmo, wrot);
+}
+
+void launch_iota(int32_t* idx, long long n, cudaStream_t st)
+{
+    if (n == 0) return;
+    k_iota<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(idx, n);
+}
 
 void launch_readback(void* host_mapped, const void* dev, size_t bytes, cudaStream_t st)
 {

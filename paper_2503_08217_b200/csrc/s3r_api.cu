@@ -40,6 +40,8 @@ struct s3r_ctx {
     int device = 0;
     std::string err;
     bool debug = false, timing = false, counters = false, training = false;
+    int pipeline = S3R_PIPELINE_STREAMLINED, last_pipeline = S3R_PIPELINE_STREAMLINED;
+    Buf d_wmo, d_wrot;                       // conventional pipeline: world copies
     bool last_training = false;
     int last_nviews = 0, last_max_tiles = 0;
     long long last_max_r = 0, last_N = -1;
@@ -247,12 +249,15 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->ticket_slot = 0;
     c->last_debug = c->debug;
     c->gbits = bits_for(std::max<long long>(N, 2));   // Gaussian-index bits of the depth key
+    const bool conv = c->pipeline == S3R_PIPELINE_CONVENTIONAL;
+    c->last_pipeline = c->pipeline;
 
-    // ---- distinct times (views sharing t share K1's compaction)
+    // ---- distinct times (views sharing t share K1's compaction); the
+    // conventional pipeline has no temporal filter: one identity list
     std::vector<float> tk;
     std::vector<int> slot(nv);
     for (int v = 0; v < nv; ++v) {
-        const float t = views[v].t + 0.0f;
+        const float t = conv ? 0.0f : views[v].t + 0.0f;
         int s = -1;
         for (size_t i = 0; i < tk.size(); ++i)
             if (tk[i] == t) { s = (int)i; break; }
@@ -270,7 +275,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         d.W = V.width; d.H = V.height;
         d.fx = V.fx; d.fy = V.fy; d.cx = V.cx; d.cy = V.cy; d.near_plane = V.near_plane;
         d.table = V.instance_w2c;
-        d.lod_r = V.lod_r; d.lod_pmax = V.lod_pmax; d.lod_D = V.lod_D;
+        d.lod_r = conv ? 0.0f : V.lod_r;          // no LOD in the conventional pipeline
+        d.lod_pmax = V.lod_pmax; d.lod_D = V.lod_D;
         d.seed = (unsigned long long)V.lod_seed;
         d.tslot = slot[v];
         d.TX = (V.width + TILE - 1) / TILE;
@@ -312,7 +318,16 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     float* h_times = (float*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(float));
     for (int i = 0; i < T; ++i) h_times[i] = tk[i];
     if (T) CU(cudaMemcpyAsync(c->d_times.p, h_times, T * sizeof(float), cudaMemcpyHostToDevice, st));
-    {
+    unsigned long long* h_counts =
+        (unsigned long long*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(unsigned long long));
+    if (conv) {
+        // no temporal filter: every Gaussian is projected (identity list)
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_FILTER, st, e);
+        launch_iota(P<int32_t>(c->d_tidx), N, st);
+        ev_end(c, st, e);
+        h_counts[0] = (unsigned long long)N;
+    } else {
         StageEvent e;
         ev_begin(c, S3R_STAGE_FILTER, st, e);
         const long long ntf = (N + filter_tile() - 1) / filter_tile();
@@ -326,12 +341,10 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
                           next_ticket(c), st);
         }
         ev_end(c, st, e);
+        CU(cudaGetLastError());
+        if (T) launch_readback(mapped(c, h_counts), c->d_counts.p, T * sizeof(unsigned long long), st);
+        CU(cudaStreamSynchronize(st));
     }
-    CU(cudaGetLastError());
-    unsigned long long* h_counts =
-        (unsigned long long*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(unsigned long long));
-    if (T) launch_readback(mapped(c, h_counts), c->d_counts.p, T * sizeof(unsigned long long), st);
-    CU(cudaStreamSynchronize(st));
 
     // ================= K2: projection + LOD + life + compaction
     long long cap = 0;
@@ -363,8 +376,22 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     }
     for (int v = 0; v < nv; ++v)
         if (outs[v].visible && N > 0) CU(cudaMemsetAsync(outs[v].visible, 0, (size_t)N, st));
+    if (conv && N > 0 && nv > 0) {
+        // ---- C0: local-to-world transformation of every view's Gaussians
+        if ((rc = ensure(c, c->d_wmo, (size_t)nv * N * 16))) return rc;
+        if ((rc = ensure(c, c->d_wrot, (size_t)nv * N * 16))) return rc;
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_PROJECT, st, e);
+        launch_world(reinterpret_cast<const float4*>(sc->means_opacity),
+                     reinterpret_cast<const float4*>(sc->rotations), sc->instance_ids,
+                     sc->num_instances, N, P<DevView>(c->d_views), nv, P<float4>(c->d_wmo),
+                     P<float4>(c->d_wrot), st);
+        ev_end(c, st, e);
+    }
     {
         ProjectArgs a{};
+        a.world_mo = conv ? P<float4>(c->d_wmo) : nullptr;
+        a.world_rot = conv ? P<float4>(c->d_wrot) : nullptr;
         a.means_opacity = reinterpret_cast<const float4*>(sc->means_opacity);
         a.scales = reinterpret_cast<const float4*>(sc->scales);
         a.rotations = reinterpret_cast<const float4*>(sc->rotations);
@@ -596,7 +623,7 @@ void s3r_destroy(s3r_ctx* c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    Buf* bufs[] = {&c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
+    Buf* bufs[] = {&c->d_wmo, &c->d_wrot, &c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
                    &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
                    &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_rects, &c->d_lists,
                    &c->d_tlists, &c->d_tranges, &c->d_train_T, &c->d_train_n, &c->d_sgrads,
@@ -930,12 +957,23 @@ int s3r_set_training(s3r_ctx* c, int enable)
     return S3R_OK;
 }
 
+int s3r_set_pipeline(s3r_ctx* c, int pipeline)
+{
+    if (!c) return S3R_EINVAL;
+    if (pipeline != S3R_PIPELINE_STREAMLINED && pipeline != S3R_PIPELINE_CONVENTIONAL)
+        return fail(c, S3R_EINVAL, "set_pipeline: unknown pipeline %d", pipeline);
+    c->pipeline = pipeline;
+    return S3R_OK;
+}
+
 int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int32_t nv,
                         const s3r_cotangents* cots, const s3r_grads* grads, void* stream)
 {
     if (!c || !sc || !grads) return S3R_EINVAL;
     if (!c->have_render || !c->last_training)
         return fail(c, S3R_ESTATE, "backward: no training forward (s3r_set_training(1) + render)");
+    if (c->last_pipeline != S3R_PIPELINE_STREAMLINED)
+        return fail(c, S3R_ESTATE, "backward: the last render used the conventional pipeline");
     if (nv != c->last_nviews || sc->n != c->last_N)
         return fail(c, S3R_ESTATE, "backward: scene/views differ from the last forward");
     if (nv > 0 && (!views || !cots)) return fail(c, S3R_EINVAL, "backward: views/cots NULL");

@@ -168,6 +168,10 @@ struct ProjectArgs {
     const int32_t* tidx;         // [T][idx_stride]
     long long idx_stride;
     int max_tiles;               // grid.x: max over views of ceil(n_temporal / project_tile)
+    // conventional pipeline: world-frame means / rotations per view (NULL:
+    // streamlined, instance-specific cameras); every valid id uses slot 0
+    const float4* world_mo;
+    const float4* world_rot;
     // outputs
     float4* rec;                 // [cap][3] splat records (compacted, unordered)
     unsigned long long* dkey;    // [cap] (depth bits << gbits) | Gaussian index
@@ -182,6 +186,15 @@ struct ProjectArgs {
 };
 void launch_project(const ProjectArgs& a, cudaStream_t st);
 int project_tile();
+
+// Conventional pipeline (NEXT-2): K0 moves every Gaussian to the world frame
+// of each view's time (views[v].table slot i >= 1 = local->world pose of
+// instance i), writing wmo / wrot [n_views][n]; K1 is replaced by the identity
+// index list (no temporal filter).
+void launch_world(const float4* mo, const float4* rot, const int32_t* ids, int num_instances,
+                  long long n, const DevView* views, int n_views, float4* wmo, float4* wrot,
+                  cudaStream_t st);
+void launch_iota(int32_t* idx, long long n, cudaStream_t st);
 
 // Segmented LSD radix sort helpers (onesweep with decoupled look-back).
 // keys: u32 (depth) or u64 (pair words).  digit = (key >> shift) & 255.

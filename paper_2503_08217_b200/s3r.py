@@ -31,7 +31,8 @@ EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_se
            "s3r_render_batch", "s3r_render_batch_host", "s3r_get_stats",
            "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
            "s3r_life_flip", "s3r_check", "s3r_set_training", "s3r_render_backward",
-           "s3r_mse"]
+           "s3r_mse", "s3r_set_pipeline"]
+S3R_PIPELINE_STREAMLINED, S3R_PIPELINE_CONVENTIONAL = 0, 1
 
 
 class S3RError(RuntimeError):
@@ -115,6 +116,7 @@ def lib():
                 "s3r_reset_visibility": (I, [P, P, P]),
                 "s3r_life_flip": (I, [P, P, I64, P]),
                 "s3r_set_training": (I, [P, I]),
+                "s3r_set_pipeline": (I, [P, I]),
                 "s3r_render_backward": (I, [P, P, P, C.c_int32, P, P, P]),
                 "s3r_mse": (I, [P, P, P, I64, C.c_float, P, P, P]),
                 "s3r_check": (I, [P, P]),
@@ -304,6 +306,14 @@ class Context:
         sc = scene.struct()
         self._check(self.L.s3r_reset_visibility(self.h, C.byref(sc), _stream(stream)))
 
+    def set_pipeline(self, conventional: bool):
+        """NEXT-2: the conventional pipeline (world transform of every dynamic
+        Gaussian, all Gaussians projected, no temporal filter, no LOD) for the
+        following renders; tables then carry [W_t, W_{t,i2g}...] (see
+        conventional_tables)."""
+        self._check(self.L.s3r_set_pipeline(
+            self.h, S3R_PIPELINE_CONVENTIONAL if conventional else S3R_PIPELINE_STREAMLINED))
+
     # -- training (config 5)
     def set_training(self, on: bool):
         self._check(self.L.s3r_set_training(self.h, int(on)))
@@ -352,6 +362,18 @@ def alloc_outputs(views: Sequence, device="cuda", depth=True, final_T=True, n_vi
             o["visible"] = torch.empty(n_visible, dtype=torch.uint8, device=device)
         outs.append(o)
     return outs
+
+
+def conventional_tables(views: Sequence, device="cuda") -> torch.Tensor:
+    """Per-view tables of the conventional pipeline: slot 0 = W_t (world ->
+    camera), slot i = W_{t,i2g} (instance i local -> world), float[V][K+1][12]."""
+    K = views[0].i2g.shape[0] if len(views) else 0
+    t = np.zeros((len(views), K + 1, 12), np.float32)
+    for j, v in enumerate(views):
+        t[j, 0] = np.asarray(v.w2c, np.float32).reshape(12)
+        if K:
+            t[j, 1:] = np.asarray(v.i2g, np.float32).reshape(K, 12)
+    return torch.from_numpy(t).to(device)
 
 
 def view_tables(ctx: Context, views: Sequence, device="cuda", stream=None) -> torch.Tensor:

@@ -41,9 +41,10 @@ def gpu_render(ctx, scene, views, life=True, visible=True):
     return ds, tabs, outs, rc
 
 
-def check_view(ctx, scene, view, table, out, vi, exact=True):
+def check_view(ctx, scene, view, table, out, vi, exact=True, o=None):
     """Compare view `vi` of the last GPU render with the oracle (f32 contract)."""
-    o = oracle.render_view(scene, view, "f32", table=table.cpu().numpy())
+    if o is None:
+        o = oracle.render_view(scene, view, "f32", table=table.cpu().numpy())
     st = ctx.stats(vi)
     d = {k: v.cpu().numpy() for k, v in ctx.dump(vi, view.width, view.height).items()}
     # counts
@@ -196,6 +197,29 @@ def test_host_entry_point_matches_device(ctx):
         for k in ("rgb", "depth", "final_T", "visible"):
             assert np.array_equal(o[k].cpu().numpy(), h[k])
     assert np.array_equal(host_scene.life, ds.life.cpu().numpy())
+
+
+@pytest.mark.parametrize("seed", [51, 52])
+def test_conventional_pipeline(ctx, seed):
+    """NEXT-2: the conventional pipeline (C0 world transform of every dynamic
+    Gaussian, all Gaussians projected through W_t, no temporal filter, no LOD)
+    vs the oracle's conventional path, bit for bit: keys, decisions, order,
+    ranges, images.  Random intervals and LOD on (both must be ignored)."""
+    scene, views = sg.make_random_dynamic(seed, 2500, 4, 250, 181, 133, 4, lod=(3.0, 0.6, 12.0))
+    ds = s3r.DeviceScene.from_numpy(scene)
+    tabs = s3r.conventional_tables(views)
+    outs = s3r.alloc_outputs(views, n_visible=scene.n)
+    ctx.set_pipeline(True)
+    try:
+        rc = ctx.render_batch(ds, views, list(tabs), outs)
+        torch.cuda.synchronize()
+        for i, v in enumerate(views):
+            o = oracle.render_view_conventional(scene, v, "f32")
+            o = check_view(ctx, o["world_scene"], v, None, outs[i], i, o=o)
+            assert o["stats"]["n_temporal"] == scene.n and o["stats"]["n_lod_small"] == 0
+    finally:
+        ctx.set_pipeline(False)
+    assert rc == 0
 
 
 def test_host_entry_point_chunked(ctx):
