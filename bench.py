@@ -177,6 +177,68 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_conventional(args, ctx, ds, views, outs, world, dev, stream, streamlined_value):
+    """NEXT-2: the same views through the conventional pipeline (per-view world
+    transform of every dynamic Gaussian, all Gaussians projected, no temporal
+    filter, no LOD) — the paper's baseline (Fig.1a); `speedup` is the
+    streamlined views/s over this one (the paper's central claim, Fig.4)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_08217_b200 import s3r
+    tabs = list(s3r.conventional_tables(views, device=dev))
+    ctx.set_pipeline(True)
+    try:
+        for _ in range(2):
+            ctx.render_batch(ds, views, tabs, outs)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        k = max(2, min(args.steps, 5))
+        ctx.set_timing(True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(k)]
+        for a, b in evs:
+            a.record(stream)
+            ctx.render_batch(ds, views, tabs, outs)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        st = ctx.stage_times()
+        ctx.set_timing(False)
+        ctx.set_counters(True)
+        ctx.render_batch(ds, views, tabs, outs)
+        torch.cuda.synchronize()
+        stats = [ctx.stats(i) for i in range(len(views))]
+        ctx.set_counters(False)
+    finally:
+        ctx.set_pipeline(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = len(views) * world * k / (ms / 1e3)
+    renders = max(st["renders"], 1)
+    return {"metric": "conventional-pipeline views/s (world transform + project all, no "
+                      "temporal filter, no LOD)", "value": value, "unit": UNIT,
+            "ms_per_step": ms / k, "steps": k, "speedup": streamlined_value / value,
+            "stages_ms": {s_: st[s_] / renders for s_ in s3r.STAGES},
+            "workload_per_view": {q: sum(s[q] for s in stats) / len(views) for q in
+                                  ("n_temporal", "n_visible", "n_rendered", "n_pairs",
+                                   "n_blend_evals")}}
+
+
+def load_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of this
+    bench command (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)[kernel]
+        return d["dram_bytes_per_launch"], d["source"]
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
     """Config 5: one step = training forward of the batch, MSE against noisy
     targets (s3r_mse), backward of blend + projection (s3r_render_backward)
@@ -270,6 +332,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool", type=int, default=4, help="distinct view batches cycled per step")
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training step")
+    ap.add_argument("--no-conventional", action="store_true",
+                    help="skip the conventional-pipeline comparison (NEXT-2)")
     ap.add_argument("--train-steps", type=int, default=5)
     args = ap.parse_args()
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
@@ -381,6 +445,11 @@ def main():
                 "unit": "TFLOP/s", "frac": ach / alu_peak,
                 "peak_source": f"148 SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (B200_PROFILING.md unit counts)",
                 "alg_flops_per_launch": FLOPS_PER_EVAL * E_alg, "traffic": None}
+        tr, tr_src = load_traffic("k_raster<0,0>")
+        if tr is not None:
+            roof["traffic"] = tr
+            roof["traffic_source"] = f"{tr_src} (ncu --set full, one launch of this command)"
+            roof["alg_bytes_per_launch"] = bytes_["raster"]
     else:
         ach = stages[dom]["GBps"]
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
@@ -391,6 +460,11 @@ def main():
     train = None
     if not args.no_train and args.config != "toy":
         train = run_train(args, ctx, ds, pools[0], tables[0], outs, world, dev, stream)
+
+    # ---------------- NEXT-2: the conventional pipeline on the same views
+    conventional = None
+    if not args.no_conventional and args.config != "toy":
+        conventional = run_conventional(args, ctx, ds, pools[0], outs, world, dev, stream, value)
 
     # ---------------- e2e through the host-buffer C-ABI entry point
     e2e = None
@@ -434,7 +508,9 @@ def main():
         n_scene = scene.n
         # K1 chunks + K2 + (hist, scan, depth passes) + (permute, count, scan, scatter) + raster
         depth_passes = math.ceil((32 + max(1, (max(n_scene, 2) - 1).bit_length())) / 8)
-        launches_per_step = math.ceil(max(n_t, 1) / 64) + 1 + 2 + depth_passes + 4 + 1
+        # K1 chunks + K2 + (hist, scan) + depth passes + (permute, count, scan,
+        # scatter, expand) + raster + 2 counter readbacks (after K1 and K2)
+        launches_per_step = math.ceil(max(n_t, 1) / 64) + 1 + 2 + depth_passes + 5 + 1 + 2
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -461,6 +537,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "train": train,
+            "conventional": conventional,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
