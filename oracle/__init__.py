@@ -25,7 +25,7 @@ _SRCS = ["s3r_oracle_f32.c", "s3r_oracle_f64.c", "s3r_oracle_bwd.c", "s3r_oracle
 _lock = threading.Lock()
 _lib = None
 
-F_TEMPORAL, F_VISIBLE, F_SMALL, F_DROPPED, F_RENDERED, F_BADID = 1, 2, 4, 8, 16, 32
+F_TEMPORAL, F_VISIBLE, F_SMALL, F_DROPPED, F_RENDERED, F_BADID, F_JITTERED = 1, 2, 4, 8, 16, 32, 64
 TILE = 16
 
 
@@ -50,7 +50,7 @@ class View(C.Structure):
                 ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
                 ("near_plane", C.c_float), ("instance_w2c", C.c_void_p),
                 ("lod_r", C.c_float), ("lod_pmax", C.c_float), ("lod_D", C.c_float),
-                ("lod_seed", C.c_uint64)]
+                ("lod_seed", C.c_uint64), ("lod_jitter", C.c_float * 3)]
 
 
 class Stats(C.Structure):
@@ -93,6 +93,10 @@ def lib():
                 "so_blend_bruteforce_f64": (C.c_int, [P, P, P, P, P, P, P, P]),
                 "so_backward_f64": (C.c_int, [P, P, P, P, P, P]),
                 "so_update_life_f32": (None, [P, P, C.c_float]),
+                "so_lod_normal3": (None, [C.c_uint64, C.c_int64, P]),
+                "so_lod_uniform_k": (C.c_float, [C.c_uint64, C.c_int64, C.c_int]),
+                "so_log2_f32": (C.c_float, [C.c_float]),
+                "so_sincos_turn_f32": (None, [C.c_float, P, P]),
                 "so_quat_from_rot_f32": (None, [P, P]),
                 "so_quat_from_rot_f64": (None, [P, P]),
                 "so_quat_mul_f32": (None, [P, P, P]),
@@ -145,9 +149,10 @@ def compose(view) -> np.ndarray:
 class _ViewRef:
     def __init__(self, view, table: Optional[np.ndarray] = None):
         self.table = np.ascontiguousarray(compose(view) if table is None else table, np.float32)
+        jit = tuple(float(x) for x in getattr(view, "lod_jitter", (0.0, 0.0, 0.0)))
         self.v = View(view.t, view.width, view.height, view.fx, view.fy, view.cx, view.cy,
                       view.near, _ptr(self.table), view.lod_r, view.lod_pmax, view.lod_D,
-                      view.lod_seed & ((1 << 64) - 1))
+                      view.lod_seed & ((1 << 64) - 1), (C.c_float * 3)(*jit))
 
 
 def render_view(scene, view, precision: str = "f32", table: Optional[np.ndarray] = None,
@@ -269,6 +274,27 @@ def render_view_conventional(scene, view, precision="f32", **kw) -> Dict[str, np
     o = render_view(w, v, precision, **kw)
     o["world_scene"] = w
     return o
+
+
+def lod_normal3(seed: int, g: int) -> np.ndarray:
+    """NEXT-3 noise: the three standard normals of Gaussian g (R-ARITH Box-Muller)."""
+    o = np.zeros(3, np.float32)
+    lib().so_lod_normal3(seed & ((1 << 64) - 1), g, _ptr(o))
+    return o
+
+
+def log2_32(x: float) -> float:
+    return lib().so_log2_f32(x)
+
+
+def sincos_turn(u: float):
+    s, c = C.c_float(), C.c_float()
+    lib().so_sincos_turn_f32(u, C.byref(s), C.byref(c))
+    return s.value, c.value
+
+
+def lod_uniform_k(seed: int, g: int, k: int) -> float:
+    return lib().so_lod_uniform_k(seed & ((1 << 64) - 1), g, k)
 
 
 def temporal_filter(scene, t, precision="f32") -> np.ndarray:

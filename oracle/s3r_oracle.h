@@ -54,6 +54,7 @@ typedef struct {
     const float* instance_w2c;    /* [num_instances][12] row-major 3x4          */
     float lod_r, lod_pmax, lod_D; /* Eq.7 r, p_max, D                           */
     uint64_t lod_seed;
+    float lod_jitter[3];          /* Eq.7 row 4 [dx, dy, dz]; 0 = no offset     */
 } so_view;
 
 /* Per-view statistics. */
@@ -69,6 +70,7 @@ typedef struct {
 #define SO_F_DROPPED  8u   /* culled by the Bernoulli draw (Eq.7 row 2)     */
 #define SO_F_RENDERED 16u  /* blended (visible and not dropped)             */
 #define SO_F_BADID    32u  /* instance id outside [0, K]                    */
+#define SO_F_JITTERED 64u  /* small, kept, mean moved by the LOD noisy offset */
 
 #define SO_TILE 16
 
@@ -97,6 +99,12 @@ double   so_normalize_time(int64_t frame, int64_t frame_count);
 float    so_exp2_f32(float x);
 uint64_t so_splitmix64(uint64_t x);
 float    so_lod_uniform(uint64_t seed, int64_t g);
+/* NEXT-3 noise: three standard normals for Gaussian g of a view (R-ARITH
+ * Box-Muller, so_log2_f32 / so_sincos_turn_f32), and its building blocks */
+void     so_lod_normal3(uint64_t seed, int64_t g, float out[3]);
+float    so_lod_uniform_k(uint64_t seed, int64_t g, int k);
+float    so_log2_f32(float x);
+void     so_sincos_turn_f32(float u, float* s, float* c);
 void     so_compose_instance_cameras(const float* w2c, const float* i2g,
                                      int32_t K, float* out);
 int64_t  so_temporal_filter_f32(const so_scene* s, float t, int32_t* idx);

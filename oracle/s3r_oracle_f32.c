@@ -56,6 +56,92 @@ float so_lod_uniform(uint64_t seed, int64_t g)
     return (float)(uint32_t)(h >> 40) * 5.9604644775390625e-8f;
 }
 
+/* ------------------------------------------------------------------------
+ * NEXT-3 noise for the LOD noisy offset (Eq.7 row 4, "N(0,1)"): three
+ * standard normals per (view seed, Gaussian), by Box-Muller on counter-based
+ * uniforms, every step an R-ARITH fp32 operation so that any IEEE-754 machine
+ * draws the same numbers.
+ *   u_k = top 24 bits of splitmix64((seed ^ splitmix64(g)) + (k+1) C) * 2^-24,
+ *         C = 0xD1B54A32D192ED03, k = 0..3 (streams distinct from the
+ *         Bernoulli draw of so_lod_uniform)
+ *   (n0, n1) = sqrt(-2 ln(1 - u_0)) (cos, sin)(2 pi u_1),
+ *   (n2, -)  = sqrt(-2 ln(1 - u_2)) (cos, sin)(2 pi u_3).
+ * ---------------------------------------------------------------------- */
+float so_lod_uniform_k(uint64_t seed, int64_t g, int k)
+{
+    uint64_t base = seed ^ so_splitmix64((uint64_t)g);
+    uint64_t h = so_splitmix64(base + (uint64_t)(k + 1) * 0xD1B54A32D192ED03ull);
+    return (float)(uint32_t)(h >> 40) * 5.9604644775390625e-8f;
+}
+
+/* log2(x), x > 0 normal: x = m 2^e with m in [sqrt(2)/2, sqrt(2)) (exact bit
+ * split), s = (m - 1) / (m + 1), log2(m) = s (c1 + s^2 (c3 + s^2 (c5 + s^2 (c7
+ * + s^2 c9)))), c_k = 2 / (k ln 2) (the atanh series; |s| <= 0.1716, so the
+ * first omitted term is < 1e-9). */
+float so_log2_f32(float x)
+{
+    union { float f; uint32_t u; } b = {x};
+    int e = (int)((b.u >> 23) & 0xffu) - 127;
+    b.u = (b.u & 0x007fffffu) | 0x3f800000u;          /* m in [1, 2) */
+    float m = b.f;
+    if (m > 1.41421356f) {
+        m = m * 0.5f;
+        e = e + 1;
+    }
+    float s = (m - 1.0f) / (m + 1.0f);
+    float s2 = s * s;
+    float p = 0.320598898f;                        /* 2 / (9 ln 2) */
+    p = fmaf(p, s2, 0.412198583f);                 /* 2 / (7 ln 2) */
+    p = fmaf(p, s2, 0.577078016f);                 /* 2 / (5 ln 2) */
+    p = fmaf(p, s2, 0.961796694f);                 /* 2 / (3 ln 2) */
+    p = fmaf(p, s2, 2.885390082f);                 /* 2 / ln 2     */
+    return fmaf(s, p, (float)e);
+}
+
+/* (sin, cos)(2 pi u) for u in [0, 1) a multiple of 2^-24: quadrant q =
+ * floor(4u), f = 4u - q (both exact), phi = f pi/2, Taylor polynomials of sin
+ * (to phi^11) and cos (to phi^12) on [0, pi/2) in Horner form in phi^2, then
+ * the quadrant rotation. */
+void so_sincos_turn_f32(float u, float* sn, float* cs)
+{
+    float x4 = u * 4.0f;
+    float q = floorf(x4);
+    float f = x4 - q;
+    float ph = f * 1.57079637f;
+    float p2 = ph * ph;
+    float sp = -2.50521084e-8f;                    /* -1/11! */
+    sp = fmaf(sp, p2, 2.75573192e-6f);             /*  1/9!  */
+    sp = fmaf(sp, p2, -1.98412698e-4f);            /* -1/7!  */
+    sp = fmaf(sp, p2, 8.33333333e-3f);             /*  1/5!  */
+    sp = fmaf(sp, p2, -1.66666667e-1f);            /* -1/3!  */
+    sp = fmaf(sp, p2, 1.0f);
+    float s = ph * sp;
+    float cp = 2.08767570e-9f;                     /*  1/12! */
+    cp = fmaf(cp, p2, -2.75573192e-7f);            /* -1/10! */
+    cp = fmaf(cp, p2, 2.48015873e-5f);             /*  1/8!  */
+    cp = fmaf(cp, p2, -1.38888889e-3f);            /* -1/6!  */
+    cp = fmaf(cp, p2, 4.16666667e-2f);             /*  1/4!  */
+    cp = fmaf(cp, p2, -0.5f);                      /* -1/2!  */
+    float c = fmaf(cp, p2, 1.0f);
+    int qi = (int)q;
+    if (qi == 0) { *sn = s; *cs = c; }
+    else if (qi == 1) { *sn = c; *cs = -s; }
+    else if (qi == 2) { *sn = -s; *cs = -c; }
+    else { *sn = -c; *cs = s; }
+}
+
+void so_lod_normal3(uint64_t seed, int64_t g, float out[3])
+{
+    float sn, cs;
+    float r0 = sqrtf(so_log2_f32(1.0f - so_lod_uniform_k(seed, g, 0)) * -1.38629436f);
+    so_sincos_turn_f32(so_lod_uniform_k(seed, g, 1), &sn, &cs);
+    out[0] = r0 * cs;
+    out[1] = r0 * sn;
+    float r1 = sqrtf(so_log2_f32(1.0f - so_lod_uniform_k(seed, g, 2)) * -1.38629436f);
+    so_sincos_turn_f32(so_lod_uniform_k(seed, g, 3), &sn, &cs);
+    out[2] = r1 * cs;
+}
+
 /* Time normalisation ("we first normalize the rendering time of the
  * whole scene to [-1,1]"): frame i of F -> -1 + 2 i / (F - 1); F = 1 -> 0. */
 double so_normalize_time(int64_t frame, int64_t frame_count)

@@ -66,6 +66,7 @@ class View:
     lod_D: float = 50.0
     lod_seed: int = 0
     near: float = 0.01
+    lod_jitter: Tuple[float, float, float] = (0.0, 0.0, 0.0)   # Eq.7 row 4 [dx, dy, dz]
     frame: int = 0
     cam: int = 0
 
