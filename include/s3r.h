@@ -259,6 +259,20 @@ int s3r_set_training(s3r_ctx* ctx, int enable);
 enum { S3R_PIPELINE_STREAMLINED = 0, S3R_PIPELINE_CONVENTIONAL = 1 };
 int s3r_set_pipeline(s3r_ctx* ctx, int pipeline);
 
+/* Adaptive-LOD noisy offset (Eq.7 row 4; NEXT-3) for the following
+ * streamlined renders: every small Gaussian that survives the Bernoulli cull
+ * has its mean moved, in the frame of its instance, by
+ *   mu_a <- fma(d_a * min(1, z / D), n_a, mu_a),   a = x, y, z
+ * (reading R10: normalize(d) = min(1, d / D) with z the projected depth and D
+ * the view's lod_D), n = three standard normals drawn per (view lod_seed,
+ * Gaussian) by the R-ARITH Box-Muller sampler of DESIGN.md §4, and is
+ * projected again: its splat, depth key and tile rectangle come from the moved
+ * mean (it is not rendered if that leaves the frustum); M_t, the small set and
+ * the drop set come from the original one.  (0, 0, 0) = off (the default).
+ * Ignored by the conventional pipeline (no LOD); s3r_render_backward refuses
+ * (S3R_ESTATE) a render made with it.  S3R_EINVAL if non-finite.            */
+int s3r_set_lod_jitter(s3r_ctx* ctx, float dx, float dy, float dz);
+
 /* Cotangents of one view: DEVICE pointers, dL/d(output) in the output layout;
  * rgb required, depth / final_T may be NULL (= 0).                         */
 typedef struct {

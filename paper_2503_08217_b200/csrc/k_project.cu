@@ -55,20 +55,20 @@ __device__ __forceinline__ void atomic_max_f(float* addr, float v)
 }
 
 struct Splat {
-    float k[6];          // mx, my, z, a, b, c
+    float k[6];          // mx, my, z, a, b, c of the projection (dump keys)
+    float rm[3];         // mx, my, z of the splat (the jittered mean's, if moved)
     float A, B, C;
     int tx0, tx1, ty0, ty1;
     uint8_t flags;
 };
 
-// O2 + O3 + O4 of DESIGN.md for Gaussian g in view V; M = the 12 floats of
-// its instance camera.  Sets s.flags.
-__device__ __forceinline__ void project_one(const float* __restrict__ M, float4 mo, float4 sc,
-                                            float4 q, const DevView& V, float lox, float hix,
-                                            float loy, float hiy, long long g, Splat& s)
+// O2: keys of a Gaussian with mean (x, y, z) in the frame of camera M (the 12
+// floats of its instance camera).  Returns false behind the near plane.
+__device__ __forceinline__ bool project_keys(const float* __restrict__ M, float x, float y,
+                                             float z, float4 sc, float4 q, const DevView& V,
+                                             float lox, float hix, float loy, float hiy,
+                                             float* k)
 {
-    s.flags = F_TEMPORAL;
-    const float x = mo.x, y = mo.y, z = mo.z;
     float p[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
@@ -78,11 +78,7 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
         p[r] = acc;
     }
     const float pz = p[2];
-    if (!(pz > V.near_plane)) {
-#pragma unroll
-        for (int j = 0; j < 6; ++j) s.k[j] = __int_as_float(0x7fc00000);
-        return;
-    }
+    if (!(pz > V.near_plane)) return false;
     float n2 = q.x * q.x;
     n2 = __fmaf_rn(q.y, q.y, n2);
     n2 = __fmaf_rn(q.z, q.z, n2);
@@ -137,41 +133,169 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
     float kc = U1[0] * U1[0];
     kc = __fmaf_rn(U1[1], U1[1], kc);
     kc = __fmaf_rn(U1[2], U1[2], kc);
-    const float mx = __fmaf_rn(V.fx, u, V.cx);
-    const float my = __fmaf_rn(V.fy, vv, V.cy);
-    s.k[0] = mx; s.k[1] = my; s.k[2] = pz; s.k[3] = ka; s.k[4] = kb; s.k[5] = kc;
+    k[0] = __fmaf_rn(V.fx, u, V.cx);
+    k[1] = __fmaf_rn(V.fy, vv, V.cy);
+    k[2] = pz;
+    k[3] = ka;
+    k[4] = kb;
+    k[5] = kc;
+    return true;
+}
 
-    // ---- O3 decisions ----
+struct Dec {
+    float A, B, C, disc;
+    int tx0, tx1, ty0, ty1;
+};
+
+// O3: dilation, conic, radius, pixel box, frustum membership, tile rectangle.
+__device__ __forceinline__ bool decide(const float* k, const DevView& V, Dec& d)
+{
+    const float mx = k[0], my = k[1], pz = k[2], ka = k[3], kb = k[4], kc = k[5];
     if (!(isfinite(mx) && isfinite(my) && isfinite(pz) && isfinite(ka) && isfinite(kb) &&
           isfinite(kc)))
-        return;
+        return false;
     const float ad = ka + 0.3f;
     const float cd = kc + 0.3f;
     const float d1 = ad * cd;
     const float d2 = kb * kb;
     const float det = d1 - d2;
-    if (!(det > 0.0f)) return;
-    s.A = cd / det;
-    s.B = (-kb) / det;
-    s.C = ad / det;
+    if (!(det > 0.0f)) return false;
+    d.A = cd / det;
+    d.B = (-kb) / det;
+    d.C = ad / det;
     const float h = 0.5f * (ka - kc);
     const float e1 = h * h;
     const float e2 = kb * kb;
-    const float disc = sqrtf(e1 + e2);
-    const float lamd = (0.5f * (ad + cd)) + disc;
+    d.disc = sqrtf(e1 + e2);
+    const float lamd = (0.5f * (ad + cd)) + d.disc;
     const float rf = ceilf(3.0f * sqrtf(lamd));
-    if (!isfinite(rf)) return;
+    if (!isfinite(rf)) return false;
     const float xlo = ceilf(mx - rf), xhi = floorf(mx + rf);
     const float ylo = ceilf(my - rf), yhi = floorf(my + rf);
     const float Wm1 = (float)(V.W - 1), Hm1 = (float)(V.H - 1);
-    if (!(xlo <= Wm1 && xhi >= 0.0f && ylo <= Hm1 && yhi >= 0.0f)) return;
+    if (!(xlo <= Wm1 && xhi >= 0.0f && ylo <= Hm1 && yhi >= 0.0f)) return false;
     const int x0 = (int)fmaxf(xlo, 0.0f), x1 = (int)fminf(xhi, Wm1);
     const int y0 = (int)fmaxf(ylo, 0.0f), y1 = (int)fminf(yhi, Hm1);
-    s.tx0 = x0 >> 4; s.tx1 = x1 >> 4; s.ty0 = y0 >> 4; s.ty1 = y1 >> 4;
+    d.tx0 = x0 >> 4; d.tx1 = x1 >> 4; d.ty0 = y0 >> 4; d.ty1 = y1 >> 4;
+    return true;
+}
+
+// ---- NEXT-3 noise (Eq.7 row 4, "N(0,1)"; reading R10): three standard
+// normals per (view seed, Gaussian) by Box-Muller on counter-based uniforms,
+// each step an R-ARITH fp32 operation (DESIGN.md §4 "LOD noisy offset").
+__device__ __forceinline__ float lod_uniform_k(unsigned long long base, int k)
+{
+    const unsigned long long h = splitmix64(base + (unsigned long long)(k + 1) * 0xD1B54A32D192ED03ull);
+    return (float)(uint32_t)(h >> 40) * 5.9604644775390625e-8f;
+}
+
+__device__ __forceinline__ float log2_rarith(float x)
+{
+    uint32_t u = __float_as_uint(x);
+    int e = (int)((u >> 23) & 0xffu) - 127;
+    float m = __uint_as_float((u & 0x007fffffu) | 0x3f800000u);
+    if (m > 1.41421356f) {
+        m = m * 0.5f;
+        e = e + 1;
+    }
+    const float s = (m - 1.0f) / (m + 1.0f);
+    const float s2 = s * s;
+    float p = 0.320598898f;
+    p = __fmaf_rn(p, s2, 0.412198583f);
+    p = __fmaf_rn(p, s2, 0.577078016f);
+    p = __fmaf_rn(p, s2, 0.961796694f);
+    p = __fmaf_rn(p, s2, 2.885390082f);
+    return __fmaf_rn(s, p, (float)e);
+}
+
+__device__ __forceinline__ void sincos_turn(float u, float& sn, float& cs)
+{
+    const float x4 = u * 4.0f;
+    const float q = floorf(x4);
+    const float f = x4 - q;
+    const float ph = f * 1.57079637f;
+    const float p2 = ph * ph;
+    float sp = -2.50521084e-8f;
+    sp = __fmaf_rn(sp, p2, 2.75573192e-6f);
+    sp = __fmaf_rn(sp, p2, -1.98412698e-4f);
+    sp = __fmaf_rn(sp, p2, 8.33333333e-3f);
+    sp = __fmaf_rn(sp, p2, -1.66666667e-1f);
+    sp = __fmaf_rn(sp, p2, 1.0f);
+    const float s = ph * sp;
+    float cp = 2.08767570e-9f;
+    cp = __fmaf_rn(cp, p2, -2.75573192e-7f);
+    cp = __fmaf_rn(cp, p2, 2.48015873e-5f);
+    cp = __fmaf_rn(cp, p2, -1.38888889e-3f);
+    cp = __fmaf_rn(cp, p2, 4.16666667e-2f);
+    cp = __fmaf_rn(cp, p2, -0.5f);
+    const float c = __fmaf_rn(cp, p2, 1.0f);
+    const int qi = (int)q;
+    if (qi == 0) { sn = s; cs = c; }
+    else if (qi == 1) { sn = c; cs = -s; }
+    else if (qi == 2) { sn = -s; cs = -c; }
+    else { sn = -c; cs = s; }
+}
+
+__device__ __noinline__ void lod_normal3(unsigned long long seed, long long g, float* out)
+{
+    const unsigned long long base = seed ^ splitmix64((unsigned long long)g);
+    float sn, cs;
+    const float r0 = sqrtf(log2_rarith(1.0f - lod_uniform_k(base, 0)) * -1.38629436f);
+    sincos_turn(lod_uniform_k(base, 1), sn, cs);
+    out[0] = r0 * cs;
+    out[1] = r0 * sn;
+    const float r1 = sqrtf(log2_rarith(1.0f - lod_uniform_k(base, 2)) * -1.38629436f);
+    sincos_turn(lod_uniform_k(base, 3), sn, cs);
+    out[2] = r1 * cs;
+}
+
+// NEXT-3 (rare path, kept out of line): move the mean of a kept small Gaussian
+// by the noisy offset, project it again, and take the splat, depth and tile
+// rectangle from the moved mean.  False if the moved mean is not visible.
+__device__ __noinline__ bool jitter_reproject(const float* __restrict__ M, float4 mo, float4 sc,
+                                              float4 q, const DevView& V, float lox, float hix,
+                                              float loy, float hiy, long long g, float pz,
+                                              Splat& s)
+{
+    float nz[3];
+    lod_normal3(V.seed, g, nz);
+    const float nd = fminf(1.0f, pz / V.lod_D);
+    const float mu[3] = {mo.x, mo.y, mo.z};
+    float mj[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) mj[ax] = __fmaf_rn(V.jit[ax] * nd, nz[ax], mu[ax]);
+    float kj[6];
+    if (!project_keys(M, mj[0], mj[1], mj[2], sc, q, V, lox, hix, loy, hiy, kj)) return false;
+    Dec dj;
+    if (!decide(kj, V, dj)) return false;
+    s.A = dj.A; s.B = dj.B; s.C = dj.C;
+    s.tx0 = dj.tx0; s.tx1 = dj.tx1; s.ty0 = dj.ty0; s.ty1 = dj.ty1;
+    s.rm[0] = kj[0]; s.rm[1] = kj[1]; s.rm[2] = kj[2];
+    return true;
+}
+
+// O2 + O3 + O4 (+ the NEXT-3 noisy offset) of DESIGN.md for Gaussian g in
+// view V; M = the 12 floats of its instance camera.  Sets s.flags.
+__device__ __forceinline__ void project_one(const float* __restrict__ M, float4 mo, float4 sc,
+                                            float4 q, const DevView& V, float lox, float hix,
+                                            float loy, float hiy, long long g, Splat& s)
+{
+    s.flags = F_TEMPORAL;
+    if (!project_keys(M, mo.x, mo.y, mo.z, sc, q, V, lox, hix, loy, hiy, s.k)) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) s.k[j] = __int_as_float(0x7fc00000);
+        return;
+    }
+    Dec d;
+    if (!decide(s.k, V, d)) return;
+    s.A = d.A; s.B = d.B; s.C = d.C;
+    s.tx0 = d.tx0; s.tx1 = d.tx1; s.ty0 = d.ty0; s.ty1 = d.ty1;
+    s.rm[0] = s.k[0]; s.rm[1] = s.k[1]; s.rm[2] = s.k[2];
     s.flags |= F_VISIBLE;
 
     // ---- O4 adaptive LOD ----
-    const float lam = (0.5f * (ka + kc)) + disc;
+    const float ka = s.k[3], kc = s.k[5], pz = s.k[2];
+    const float lam = (0.5f * (ka + kc)) + d.disc;
     const float sc2 = 3.0f * sqrtf(fmaxf(lam, 0.0f));
     if (V.lod_r > 0.0f && sc2 <= V.lod_r) {
         s.flags |= F_SMALL;
@@ -183,6 +307,12 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
         if (uu < pd) {
             s.flags |= F_DROPPED;
             return;
+        }
+        // ---- NEXT-3 noisy offset (Eq.7 row 4): mu += jit normalize(d) N(0,1),
+        // normalize(d) = min(1, d / D) (reading R10), then project again
+        if (V.jit[0] != 0.0f || V.jit[1] != 0.0f || V.jit[2] != 0.0f) {
+            s.flags |= F_JITTERED;
+            if (!jitter_reproject(M, mo, sc, q, V, lox, hix, loy, hiy, g, pz, s)) return;
         }
     }
     s.flags |= F_RENDERED;
@@ -308,7 +438,7 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
             const uint32_t rx = (uint32_t)sp.tx0 | ((uint32_t)sp.tx1 << 16);
             const uint32_t ry = (uint32_t)sp.ty0 | ((uint32_t)sp.ty1 << 16);
             float4* r = a.rec + 3 * o;
-            r[0] = make_float4(sp.k[0], sp.k[1], sp.k[2], col.w);
+            r[0] = make_float4(sp.rm[0], sp.rm[1], sp.rm[2], col.w);
             // exp2-form blend coefficients (R-ARITH): qa = A (-log2e/2), qb = B (-log2e),
             // qc = C (-log2e/2)
             r[1] = make_float4(sp.A * -0x1.715476p-1f, sp.B * -0x1.715476p+0f,
@@ -316,7 +446,7 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
             r[2] = make_float4(col.x, col.y, col.z, __uint_as_float(ry));
             // depth-sort key (reading R11): depth bits above the Gaussian index,
             // so the order is (depth, index) whatever the compaction order was
-            a.dkey[o] = ((unsigned long long)__float_as_uint(sp.k[2]) << a.gbits) |
+            a.dkey[o] = ((unsigned long long)__float_as_uint(sp.rm[2]) << a.gbits) |
                         (unsigned long long)g;
             if (a.gidx) a.gidx[o] = (int32_t)g;
         }

@@ -41,6 +41,8 @@ struct s3r_ctx {
     std::string err;
     bool debug = false, timing = false, counters = false, training = false;
     int pipeline = S3R_PIPELINE_STREAMLINED, last_pipeline = S3R_PIPELINE_STREAMLINED;
+    float lod_jitter[3] = {0.0f, 0.0f, 0.0f};   // NEXT-3 noisy offset scale
+    bool last_jitter = false;
     Buf d_wmo, d_wrot;                       // conventional pipeline: world copies
     bool last_training = false;
     int last_nviews = 0, last_max_tiles = 0;
@@ -251,6 +253,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->gbits = bits_for(std::max<long long>(N, 2));   // Gaussian-index bits of the depth key
     const bool conv = c->pipeline == S3R_PIPELINE_CONVENTIONAL;
     c->last_pipeline = c->pipeline;
+    c->last_jitter = !conv && (c->lod_jitter[0] != 0.0f || c->lod_jitter[1] != 0.0f ||
+                               c->lod_jitter[2] != 0.0f);
 
     // ---- distinct times (views sharing t share K1's compaction); the
     // conventional pipeline has no temporal filter: one identity list
@@ -277,6 +281,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         d.table = V.instance_w2c;
         d.lod_r = conv ? 0.0f : V.lod_r;          // no LOD in the conventional pipeline
         d.lod_pmax = V.lod_pmax; d.lod_D = V.lod_D;
+        for (int a = 0; a < 3; ++a) d.jit[a] = conv ? 0.0f : c->lod_jitter[a];
         d.seed = (unsigned long long)V.lod_seed;
         d.tslot = slot[v];
         d.TX = (V.width + TILE - 1) / TILE;
@@ -957,6 +962,17 @@ int s3r_set_training(s3r_ctx* c, int enable)
     return S3R_OK;
 }
 
+int s3r_set_lod_jitter(s3r_ctx* c, float dx, float dy, float dz)
+{
+    if (!c) return S3R_EINVAL;
+    if (!(std::isfinite(dx) && std::isfinite(dy) && std::isfinite(dz)))
+        return fail(c, S3R_EINVAL, "set_lod_jitter: non-finite offset scale");
+    c->lod_jitter[0] = dx;
+    c->lod_jitter[1] = dy;
+    c->lod_jitter[2] = dz;
+    return S3R_OK;
+}
+
 int s3r_set_pipeline(s3r_ctx* c, int pipeline)
 {
     if (!c) return S3R_EINVAL;
@@ -974,6 +990,8 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
         return fail(c, S3R_ESTATE, "backward: no training forward (s3r_set_training(1) + render)");
     if (c->last_pipeline != S3R_PIPELINE_STREAMLINED)
         return fail(c, S3R_ESTATE, "backward: the last render used the conventional pipeline");
+    if (c->last_jitter)
+        return fail(c, S3R_ESTATE, "backward: the last render used the LOD noisy offset");
     if (nv != c->last_nviews || sc->n != c->last_N)
         return fail(c, S3R_ESTATE, "backward: scene/views differ from the last forward");
     if (nv > 0 && (!views || !cots)) return fail(c, S3R_EINVAL, "backward: views/cots NULL");

@@ -93,7 +93,7 @@ __device__ __forceinline__ uint32_t warp_lookback(const uint32_t* lb, long long 
 
 // Per-Gaussian flag bits (debug dump; same meaning as the header)
 constexpr uint8_t F_TEMPORAL = 1, F_VISIBLE = 2, F_SMALL = 4, F_DROPPED = 8,
-                  F_RENDERED = 16, F_BADID = 32;
+                  F_RENDERED = 16, F_BADID = 32, F_JITTERED = 64;
 
 // Device error bits
 constexpr uint32_t ERR_BADID = 1;
@@ -106,6 +106,7 @@ struct DevView {
     const float* table;      // [K1][12]
     float lod_r, lod_pmax, lod_D;
     unsigned long long seed;
+    float jit[3];            // NEXT-3 LOD noisy offset scale [dx, dy, dz] (0: off)
     int tslot;               // index of the view's distinct time
     int TX, TY, ntiles;
     float* rgb;

@@ -64,7 +64,7 @@ def check_view(ctx, scene, view, table, out, vi, exact=True, o=None):
         assert np.array_equal(out["visible"].cpu().numpy(), o["visible"])
     # depth order of rendered Gaussians: (z, index)
     rend = np.nonzero(o["flags"] & oracle.F_RENDERED)[0]
-    want_order = rend[np.lexsort((rend, o["keys"][rend, 2]))]
+    want_order = rend[np.lexsort((rend, o["splat_mz"][rend, 2]))]
     assert np.array_equal(d["depth_order"], want_order)
     # K3-K6: pair list and ranges
     assert np.array_equal(d["pair_tile"], o["pair_tile"])
@@ -220,6 +220,28 @@ def test_conventional_pipeline(ctx, seed):
     finally:
         ctx.set_pipeline(False)
     assert rc == 0
+
+
+@pytest.mark.parametrize("seed", [61, 62])
+def test_lod_noisy_offset(ctx, seed):
+    """NEXT-3: kept small Gaussians re-projected from the jittered mean (Eq.7
+    row 4) — keys, decisions (incl. the JITTERED flag), order, ranges and
+    images bit-exact vs the oracle; M_t unchanged by the offset."""
+    import dataclasses
+    jit = (0.3, 0.2, 0.6)
+    scene, views = sg.make_random_dynamic(seed, 4000, 3, 300, 197, 149, 4, lod=(6.0, 0.4, 8.0))
+    ctx.set_lod_jitter(*jit)
+    try:
+        _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    finally:
+        ctx.set_lod_jitter(0.0, 0.0, 0.0)
+    n_jit = 0
+    for vi, v in enumerate(views):
+        vj = dataclasses.replace(v, lod_jitter=jit)
+        o = oracle.render_view(scene, vj, "f32", table=tabs[vi].cpu().numpy())
+        check_view(ctx, scene, vj, tabs[vi], outs[vi], vi, o=o)
+        n_jit += int(np.count_nonzero(o["flags"] & oracle.F_JITTERED))
+    assert n_jit > 100
 
 
 def test_host_entry_point_chunked(ctx):
