@@ -145,6 +145,8 @@ def stage_bytes(stats, views, n_scene, n_distinct_t, pair_passes):
         "bin": (4 + 48 + 48 + 8) * Nr + 8 * Nr + 8 * Nr + 4 * Ps + 12 * Ps + 4 * P,
         # tile lists (4 B per pair), unique records, images
         "raster": 4 * P + 48 * Nr + 20 * px,
+        # NeurF query (when on): own-frame mean + id in, colour float4 out
+        "color": 32 * Nr,
     }
 
 

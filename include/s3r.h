@@ -142,12 +142,15 @@ typedef struct {
     int32_t* temporal_idx;       /* [n_temporal] ascending Gaussian indices     */
     float* keys;                 /* [n_temporal][6] mx,my,z,a,b,c (fp32 keys)   */
     uint8_t* flags;              /* [n_temporal] bit 1 visible, 2 small,
-                                    3 dropped, 4 rendered, 5 bad id (bit 0 set)  */
+                                    3 dropped, 4 rendered, 5 bad id, 6 mean moved
+                                    by the LOD noisy offset (bit 0 set)          */
     int16_t* rect;               /* [n_temporal][4] tile rect tx0,tx1,ty0,ty1   */
     int32_t* depth_order;        /* [n_rendered] Gaussian indices by (z, index) */
     int32_t* pair_tile;          /* [n_pairs] sorted pairs: tile id (row-major) */
     int32_t* pair_gauss;         /* [n_pairs] sorted pairs: Gaussian index      */
     int32_t* ranges;             /* [tiles][2] [start,end) per tile             */
+    float* splat_rgb;            /* [n_rendered][3] splat colour by depth rank
+                                    (the NeurF query's output when enabled)     */
 } s3r_debug;
 
 /* Stage timers (milliseconds, summed over renders since the last reset).    */
@@ -159,6 +162,7 @@ enum {
                                     counting sort (count, scan, scatter) with
                                     supertile ranges                            */
     S3R_STAGE_RASTER,            /* K7 tile filter + alpha-blend rasterizer     */
+    S3R_STAGE_COLOR,             /* K6 NeurF colour query (0 unless enabled)    */
     S3R_NUM_STAGES
 };
 
@@ -272,6 +276,41 @@ int s3r_set_pipeline(s3r_ctx* ctx, int pipeline);
  * Ignored by the conventional pipeline (no LOD); s3r_render_backward refuses
  * (S3R_ESTATE) a render made with it.  S3R_EINVAL if non-finite.            */
 int s3r_set_lod_jitter(s3r_ctx* ctx, float dx, float dy, float dz);
+
+/* NeurF colour query (Eq.7 rows 5-6; NEXT-4): with it enabled the
+ * colour of every rendered Gaussian is c = NeurF_sta(mu, d, dir, emb(t)) for
+ * static and NeurF_dyn(mu, d, dir, emb(t), class) for dynamic ones instead of
+ * scene->colors, computed on the tensor cores (tcgen05, bf16 operands, fp32
+ * accumulation) between projection and depth sort.  Architecture (DESIGN.md
+ * reading R22): 64 features in the Gaussian's own frame — mu / S, sin / cos of
+ * 2^l pi mu / S for l = 0..3 (index 3 + 6 l + 2 axis + {0 sin, 1 cos}),
+ * min(1, d / lod_D), the viewing direction R^T p / |p| (p = W_{t,i} mu),
+ * emb(t) (8, linear interpolation of time_emb on t_j = -1 + 2 j / (n_time-1)),
+ * the class embedding (4; 0 for static), zero padding — then per network
+ * h1 = relu(W1 f + b1), h2 = relu(W2 h1 + b2), c = sigmoid(W3 h2 + b3).
+ * All pointers DEVICE fp32, copied (weights converted to bf16) by this call:
+ *   w1 [2][64][64], b1 [2][64], w2 [2][64][64], b2 [2][64], w3 [2][3][64],
+ *   b3 [2][3]  (index 0 = NeurF_sta, 1 = NeurF_dyn; weight rows = outputs);
+ *   time_emb [n_time][8] (n_time >= 1); class_emb [num_instances][4] (row 0
+ *   unused).  pos_scale = S > 0.
+ * Applies to streamlined renders whose scene has num_instances <=
+ * num_instances given here (S3R_EINVAL otherwise); the conventional pipeline
+ * keeps scene->colors.  params = NULL disables it.  s3r_render_backward
+ * refuses (S3R_ESTATE) a render made with it.                               */
+typedef struct {
+    const float* w1;
+    const float* b1;
+    const float* w2;
+    const float* b2;
+    const float* w3;
+    const float* b3;
+    const float* time_emb;
+    int32_t n_time;
+    const float* class_emb;
+    int32_t num_instances;
+    float pos_scale;
+} s3r_neurf;
+int s3r_set_neural_colors(s3r_ctx* ctx, const s3r_neurf* params, void* stream);
 
 /* Cotangents of one view: DEVICE pointers, dL/d(output) in the output layout;
  * rgb required, depth / final_T may be NULL (= 0).                         */

@@ -22,12 +22,13 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libs3r.so")
 BUILD = os.path.join(HERE, "build")
 SOURCES = ["k_filter.cu", "k_project.cu", "k_sort.cu", "k_bin.cu", "k_raster.cu",
-           "k_backward.cu", "s3r_api.cu"]
+           "k_backward.cu", "k_neurf.cu", "s3r_api.cu"]
 HEADERS = ["s3r_internal.cuh", os.path.join("..", "..", "include", "s3r.h")]
 # The backward (config 5) is compared with the oracle at 1e-3, not bit for bit:
 # it may contract multiply-adds (its forward recomputation uses explicit
 # __fmaf_rn / separate ops where it must match the forward's decisions).
-CONTRACTED = {"k_backward.cu"}
+# The NeurF query (bf16 tensor-core contract, R22) likewise.
+CONTRACTED = {"k_backward.cu", "k_neurf.cu"}
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -57,6 +57,7 @@ __device__ __forceinline__ void atomic_max_f(float* addr, float v)
 struct Splat {
     float k[6];          // mx, my, z, a, b, c of the projection (dump keys)
     float rm[3];         // mx, my, z of the splat (the jittered mean's, if moved)
+    float mu[3];         // own-frame mean of the splat (moved by the noisy offset)
     float A, B, C;
     int tx0, tx1, ty0, ty1;
     uint8_t flags;
@@ -271,6 +272,7 @@ __device__ __noinline__ bool jitter_reproject(const float* __restrict__ M, float
     s.A = dj.A; s.B = dj.B; s.C = dj.C;
     s.tx0 = dj.tx0; s.tx1 = dj.tx1; s.ty0 = dj.ty0; s.ty1 = dj.ty1;
     s.rm[0] = kj[0]; s.rm[1] = kj[1]; s.rm[2] = kj[2];
+    s.mu[0] = mj[0]; s.mu[1] = mj[1]; s.mu[2] = mj[2];
     return true;
 }
 
@@ -291,6 +293,7 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
     s.A = d.A; s.B = d.B; s.C = d.C;
     s.tx0 = d.tx0; s.tx1 = d.tx1; s.ty0 = d.ty0; s.ty1 = d.ty1;
     s.rm[0] = s.k[0]; s.rm[1] = s.k[1]; s.rm[2] = s.k[2];
+    s.mu[0] = mo.x; s.mu[1] = mo.y; s.mu[2] = mo.z;
     s.flags |= F_VISIBLE;
 
     // ---- O4 adaptive LOD ----
@@ -357,10 +360,12 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
         Splat sp;
         sp.flags = 0;
         long long g = -1;
+        int gid_id = 0;
         float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < n_t) {
             g = tl[i];
             const int id = __ldg(a.ids + g);
+            gid_id = id;
             if (id < 0 || id >= K1) {
                 sp.flags = F_TEMPORAL | F_BADID;
 #pragma unroll
@@ -449,6 +454,7 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
             a.dkey[o] = ((unsigned long long)__float_as_uint(sp.rm[2]) << a.gbits) |
                         (unsigned long long)g;
             if (a.gidx) a.gidx[o] = (int32_t)g;
+            if (a.rec_mu) a.rec_mu[o] = make_float4(sp.mu[0], sp.mu[1], sp.mu[2], __int_as_float(gid_id));
         }
     }
     // ---- per-view counters: one set of atomics per CTA ----

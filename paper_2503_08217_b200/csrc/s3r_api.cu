@@ -43,6 +43,11 @@ struct s3r_ctx {
     int pipeline = S3R_PIPELINE_STREAMLINED, last_pipeline = S3R_PIPELINE_STREAMLINED;
     float lod_jitter[3] = {0.0f, 0.0f, 0.0f};   // NEXT-3 noisy offset scale
     bool last_jitter = false;
+    // NEXT-4 NeurF colour query
+    bool neurf = false, last_neurf = false;
+    Buf d_nw, d_nb, d_temb, d_cemb, d_recmu, d_toff;
+    int neurf_ntime = 0, neurf_ninst = 0;
+    float neurf_scale = 1.0f;
     Buf d_wmo, d_wrot;                       // conventional pipeline: world copies
     bool last_training = false;
     int last_nviews = 0, last_max_tiles = 0;
@@ -255,6 +260,11 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->last_pipeline = c->pipeline;
     c->last_jitter = !conv && (c->lod_jitter[0] != 0.0f || c->lod_jitter[1] != 0.0f ||
                                c->lod_jitter[2] != 0.0f);
+    const bool neurf = c->neurf && !conv;
+    c->last_neurf = neurf;
+    if (neurf && sc->num_instances > c->neurf_ninst)
+        return fail(c, S3R_EINVAL, "NeurF: class table has %d rows, scene has %d instances",
+                    c->neurf_ninst, sc->num_instances);
 
     // ---- distinct times (views sharing t share K1's compaction); the
     // conventional pipeline has no temporal filter: one identity list
@@ -366,6 +376,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if ((rc = ensure(c, c->d_rec, (size_t)capS * 48))) return rc;
     if ((rc = ensure(c, c->d_dkey, (size_t)capS * 8))) return rc;
     if (c->debug && (rc = ensure(c, c->d_gidx, (size_t)capS * 4))) return rc;
+    if (neurf && (rc = ensure(c, c->d_recmu, (size_t)capS * 16))) return rc;
     if (c->debug) {
         if ((rc = ensure(c, c->d_dbg_keys, (size_t)capS * 24))) return rc;
         if ((rc = ensure(c, c->d_dbg_flags, (size_t)capS))) return rc;
@@ -397,6 +408,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         ProjectArgs a{};
         a.world_mo = conv ? P<float4>(c->d_wmo) : nullptr;
         a.world_rot = conv ? P<float4>(c->d_wrot) : nullptr;
+        a.rec_mu = neurf ? P<float4>(c->d_recmu) : nullptr;
         a.means_opacity = reinterpret_cast<const float4*>(sc->means_opacity);
         a.scales = reinterpret_cast<const float4*>(sc->scales);
         a.rotations = reinterpret_cast<const float4*>(sc->rotations);
@@ -510,6 +522,37 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if ((rc = ensure(c, c->d_hist, (size_t)std::max(nv, 1) * dpasses * RADIX * 4))) return rc;
     if ((rc = ensure(c, c->d_ranges, (size_t)std::max(total_bins, 1) * sizeof(int2)))) return rc;
     if ((rc = ensure(c, c->d_lb, (size_t)std::max(dtiles, 1) * RADIX * sizeof(uint32_t)))) return rc;
+
+    // ================= K6: NeurF colour query (NEXT-4) into the compacted records
+    if (neurf && nv) {
+        int* h_toff = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
+        int tt = 0;
+        for (int v = 0; v < nv; ++v) {
+            h_toff[v] = tt;
+            tt += (int)((c->hv[v].n_rendered + 127) / 128);
+        }
+        h_toff[nv] = tt;
+        if ((rc = ensure(c, c->d_toff, (size_t)(nv + 1) * sizeof(int)))) return rc;
+        CU(cudaMemcpyAsync(c->d_toff.p, h_toff, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_COLOR, st, e);
+        NeurfArgs na{};
+        na.views = P<DevView>(c->d_views);
+        na.n_views = nv;
+        na.tile_off = P<int>(c->d_toff);
+        na.total_tiles = tt;
+        na.rec_mu = P<float4>(c->d_recmu);
+        na.rec = P<float4>(c->d_rec);
+        na.wpack = c->d_nw.p;
+        na.bias = P<float>(c->d_nb);
+        na.time_emb = P<float>(c->d_temb);
+        na.n_time = c->neurf_ntime;
+        na.class_emb = P<float>(c->d_cemb);
+        na.pos_scale = c->neurf_scale;
+        launch_neurf(na, st);
+        ev_end(c, st, e);
+        CU(cudaGetLastError());
+    }
 
     // ================= K5a: depth sort: 8-bit LSD passes over (depth << gbits | index),
     // values = compacted slot j; gives the unique (depth, index) order (R11)
@@ -628,7 +671,8 @@ void s3r_destroy(s3r_ctx* c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    Buf* bufs[] = {&c->d_wmo, &c->d_wrot, &c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
+    Buf* bufs[] = {&c->d_nw, &c->d_nb, &c->d_temb, &c->d_cemb, &c->d_recmu, &c->d_toff,
+                   &c->d_wmo, &c->d_wrot, &c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
                    &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
                    &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_rects, &c->d_lists,
                    &c->d_tlists, &c->d_tranges, &c->d_train_T, &c->d_train_n, &c->d_sgrads,
@@ -899,6 +943,9 @@ int s3r_dump_intermediates(s3r_ctx* c, int32_t vi, const s3r_debug* dbg, void* s
     if (dbg->rect && d.n_temporal)
         CU(cudaMemcpyAsync(dbg->rect, P<int16_t>(c->d_dbg_rect) + 4 * d.dbg_off, d.n_temporal * 8,
                            cudaMemcpyDeviceToDevice, st));
+    if (dbg->splat_rgb && d.n_rendered)   // .xyz of the third float4 of each sorted record
+        CU(cudaMemcpy2DAsync(dbg->splat_rgb, 12, P<char>(c->d_recs) + 48 * d.cap_off + 32, 48, 12,
+                             (size_t)d.n_rendered, cudaMemcpyDeviceToDevice, st));
     const uint32_t* order = P<uint32_t>(c->d_sortv[c->final_order]);
     if (dbg->depth_order)
         launch_dump_order(order, P<int32_t>(c->d_gidx), d.cap_off, d.n_rendered, dbg->depth_order, st);
@@ -973,6 +1020,36 @@ int s3r_set_lod_jitter(s3r_ctx* c, float dx, float dy, float dz)
     return S3R_OK;
 }
 
+int s3r_set_neural_colors(s3r_ctx* c, const s3r_neurf* p, void* stream)
+{
+    if (!c) return S3R_EINVAL;
+    if (!p) {
+        c->neurf = false;
+        return S3R_OK;
+    }
+    if (!p->w1 || !p->b1 || !p->w2 || !p->b2 || !p->w3 || !p->b3 || !p->time_emb ||
+        !p->class_emb || p->n_time < 1 || p->num_instances < 1 || !(p->pos_scale > 0.0f) ||
+        !std::isfinite(p->pos_scale))
+        return fail(c, S3R_EINVAL, "set_neural_colors: bad parameters");
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = ensure(c, c->d_nw, neurf_pack_bytes()))) return rc;
+    if ((rc = ensure(c, c->d_nb, (size_t)neurf_bias_count() * 4))) return rc;
+    if ((rc = ensure(c, c->d_temb, (size_t)p->n_time * 8 * 4))) return rc;
+    if ((rc = ensure(c, c->d_cemb, (size_t)p->num_instances * 4 * 4))) return rc;
+    launch_neurf_pack(p->w1, p->b1, p->w2, p->b2, p->w3, p->b3, c->d_nw.p, P<float>(c->d_nb), st);
+    CU(cudaMemcpyAsync(c->d_temb.p, p->time_emb, (size_t)p->n_time * 32, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(c->d_cemb.p, p->class_emb, (size_t)p->num_instances * 16,
+                       cudaMemcpyDeviceToDevice, st));
+    CU(cudaGetLastError());
+    c->neurf = true;
+    c->neurf_ntime = p->n_time;
+    c->neurf_ninst = p->num_instances;
+    c->neurf_scale = p->pos_scale;
+    return S3R_OK;
+}
+
 int s3r_set_pipeline(s3r_ctx* c, int pipeline)
 {
     if (!c) return S3R_EINVAL;
@@ -992,6 +1069,8 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
         return fail(c, S3R_ESTATE, "backward: the last render used the conventional pipeline");
     if (c->last_jitter)
         return fail(c, S3R_ESTATE, "backward: the last render used the LOD noisy offset");
+    if (c->last_neurf)
+        return fail(c, S3R_ESTATE, "backward: the last render used NeurF colours");
     if (nv != c->last_nviews || sc->n != c->last_N)
         return fail(c, S3R_ESTATE, "backward: scene/views differ from the last forward");
     if (nv > 0 && (!views || !cots)) return fail(c, S3R_EINVAL, "backward: views/cots NULL");

@@ -173,6 +173,9 @@ struct ProjectArgs {
     // streamlined, instance-specific cameras); every valid id uses slot 0
     const float4* world_mo;
     const float4* world_rot;
+    // NeurF colour query on: per record the own-frame mean of the splat (the
+    // moved one under the LOD noisy offset) and the instance id bits (NULL: off)
+    float4* rec_mu;
     // outputs
     float4* rec;                 // [cap][3] splat records (compacted, unordered)
     unsigned long long* dkey;    // [cap] (depth bits << gbits) | Gaussian index
@@ -196,6 +199,29 @@ void launch_world(const float4* mo, const float4* rot, const int32_t* ids, int n
                   long long n, const DevView* views, int n_views, float4* wmo, float4* wrot,
                   cudaStream_t st);
 void launch_iota(int32_t* idx, long long n, cudaStream_t st);
+
+// K6 NeurF colour query on the tensor cores (NEXT-4, k_neurf.cu): colours of
+// the compacted records of every view, written into rec[3 o + 2].xyz.
+struct NeurfArgs {
+    const DevView* views;
+    int n_views;
+    const int* tile_off;         // [n_views] first 128-record tile of each view
+    int total_tiles;
+    const float4* rec_mu;        // [cap] own-frame mean + instance id bits
+    float4* rec;                 // [cap][3] splat records
+    const void* wpack;           // bf16 core-matrix weight tiles (neurf_pack_bytes)
+    const float* bias;           // [neurf_bias_count] fp32
+    const float* time_emb;       // [n_time][8]
+    int n_time;
+    const float* class_emb;      // [num_instances][4]
+    float pos_scale;
+};
+size_t neurf_pack_bytes();
+int neurf_bias_count();
+void launch_neurf_pack(const float* w1, const float* b1, const float* w2, const float* b2,
+                       const float* w3, const float* b3, void* wpack, float* bias,
+                       cudaStream_t st);
+void launch_neurf(const NeurfArgs& a, cudaStream_t st);
 
 // Segmented LSD radix sort helpers (onesweep with decoupled look-back).
 // keys: u32 (depth) or u64 (pair words).  digit = (key >> shift) & 255.

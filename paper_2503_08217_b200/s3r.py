@@ -23,7 +23,7 @@ _lock = threading.Lock()
 _lib = None
 
 S3R_OK, S3R_EINVAL, S3R_EINSTANCE, S3R_ENOMEM, S3R_ECUDA, S3R_ESTATE = 0, -1, -2, -3, -4, -5
-STAGES = ["filter", "project", "depth_sort", "bin", "raster"]
+STAGES = ["filter", "project", "depth_sort", "bin", "raster", "color"]
 TILE = 16
 # every symbol include/s3r.h declares
 EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_set_debug",
@@ -31,7 +31,7 @@ EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_se
            "s3r_render_batch", "s3r_render_batch_host", "s3r_get_stats",
            "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
            "s3r_life_flip", "s3r_check", "s3r_set_training", "s3r_render_backward",
-           "s3r_mse", "s3r_set_pipeline", "s3r_set_lod_jitter"]
+           "s3r_mse", "s3r_set_pipeline", "s3r_set_lod_jitter", "s3r_set_neural_colors"]
 S3R_PIPELINE_STREAMLINED, S3R_PIPELINE_CONVENTIONAL = 0, 1
 
 
@@ -80,7 +80,14 @@ class Grads_(C.Structure):
 class Debug_(C.Structure):
     _fields_ = [("temporal_idx", C.c_void_p), ("keys", C.c_void_p), ("flags", C.c_void_p),
                 ("rect", C.c_void_p), ("depth_order", C.c_void_p), ("pair_tile", C.c_void_p),
-                ("pair_gauss", C.c_void_p), ("ranges", C.c_void_p)]
+                ("pair_gauss", C.c_void_p), ("ranges", C.c_void_p), ("splat_rgb", C.c_void_p)]
+
+
+class Neurf_(C.Structure):
+    _fields_ = [("w1", C.c_void_p), ("b1", C.c_void_p), ("w2", C.c_void_p), ("b2", C.c_void_p),
+                ("w3", C.c_void_p), ("b3", C.c_void_p), ("time_emb", C.c_void_p),
+                ("n_time", C.c_int32), ("class_emb", C.c_void_p), ("num_instances", C.c_int32),
+                ("pos_scale", C.c_float)]
 
 
 def lib_path() -> str:
@@ -118,6 +125,7 @@ def lib():
                 "s3r_set_training": (I, [P, I]),
                 "s3r_set_pipeline": (I, [P, I]),
                 "s3r_set_lod_jitter": (I, [P, C.c_float, C.c_float, C.c_float]),
+                "s3r_set_neural_colors": (I, [P, P, P]),
                 "s3r_render_backward": (I, [P, P, P, C.c_int32, P, P, P]),
                 "s3r_mse": (I, [P, P, P, I64, C.c_float, P, P, P]),
                 "s3r_check": (I, [P, P]),
@@ -286,7 +294,8 @@ class Context:
         ntiles = ((width + TILE - 1) // TILE) * ((height + TILE - 1) // TILE)
         d = {"temporal_idx": torch.empty(nt, dtype=torch.int32, device=dev),
              "pair_tile": torch.empty(npairs, dtype=torch.int32, device=dev),
-             "ranges": torch.empty((ntiles, 2), dtype=torch.int32, device=dev)}
+             "ranges": torch.empty((ntiles, 2), dtype=torch.int32, device=dev),
+             "splat_rgb": torch.empty((nr, 3), dtype=torch.float32, device=dev)}
         if keys:
             d.update(keys=torch.empty((nt, 6), dtype=torch.float32, device=dev),
                      flags=torch.empty(nt, dtype=torch.uint8, device=dev),
@@ -318,6 +327,25 @@ class Context:
     def set_lod_jitter(self, dx: float, dy: float, dz: float):
         """NEXT-3: LOD noisy offset scale [dx, dy, dz] (Eq.7 row 4); 0 = off."""
         self._check(self.L.s3r_set_lod_jitter(self.h, float(dx), float(dy), float(dz)))
+
+    def set_neural_colors(self, params: Optional[Dict[str, torch.Tensor]], stream=None):
+        """NEXT-4: NeurF colour query (R22) with these weights (device
+        fp32 tensors w1 [2,64,64], b1 [2,64], w2, b2, w3 [2,3,64], b3 [2,3],
+        time_emb [n_time,8], class_emb [K+1,4], and the float pos_scale), or
+        None to switch it off."""
+        if params is None:
+            self._check(self.L.s3r_set_neural_colors(self.h, None, _stream(stream)))
+            return
+        t = {k: v.contiguous() for k, v in params.items() if torch.is_tensor(v)}
+        for v in t.values():
+            assert v.is_cuda and v.dtype == torch.float32
+        self._neurf_keep = t
+        p = Neurf_(_ptr(t["w1"]), _ptr(t["b1"]), _ptr(t["w2"]), _ptr(t["b2"]), _ptr(t["w3"]),
+                   _ptr(t["b3"]), _ptr(t["time_emb"]), int(t["time_emb"].shape[0]),
+                   _ptr(t["class_emb"]), int(t["class_emb"].shape[0]),
+                   float(params["pos_scale"]))
+        self._check(self.L.s3r_set_neural_colors(self.h, C.byref(p), _stream(stream)))
+        torch.cuda.synchronize(self.device)
 
     # -- training (config 5)
     def set_training(self, on: bool):
