@@ -229,6 +229,74 @@ def run_conventional(args, ctx, ds, views, outs, world, dev, stream, streamlined
                                    "n_blend_evals")}}
 
 
+def random_neurf_params(num_instances, dev, seed=11):
+    """Random weights of the R22 NeurF shapes (no trained weights here), made
+    on the device; He-style scales keep activations O(1)."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    r = lambda *sh, s=1.0: torch.randn(*sh, generator=g, device=dev) * s
+    p = {"w1": r(2, 64, 64, s=(2 / 44) ** 0.5), "b1": r(2, 64, s=0.1),
+         "w2": r(2, 64, 64, s=(2 / 64) ** 0.5), "b2": r(2, 64, s=0.1),
+         "w3": r(2, 3, 64, s=(2 / 64) ** 0.5), "b3": r(2, 3, s=0.1),
+         "time_emb": r(16, 8), "class_emb": r(num_instances, 4)}
+    p["w1"][:, :, 43:] = 0
+    p["pos_scale"] = 100.0
+    return p
+
+
+def run_neurf(args, ctx, ds, scene, views, tables, outs, world, dev, stream, peaks):
+    """NEXT-4: the streamlined render with the NeurF colour query (k_neurf on
+    the tcgen05 tensor cores, random weights of the R22 architecture)."""
+    import torch
+    import torch.distributed as dist
+    prm = random_neurf_params(scene.num_instances, dev)
+    ctx.set_neural_colors(prm)
+    try:
+        for _ in range(2):
+            ctx.render_batch(ds, views, tables, outs)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        k = max(2, min(args.steps, 5))
+        ctx.set_timing(True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(k)]
+        for a, b in evs:
+            a.record(stream)
+            ctx.render_batch(ds, views, tables, outs)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        st = ctx.stage_times()
+        ctx.set_timing(False)
+        stats = [ctx.stats(i) for i in range(len(views))]
+    finally:
+        ctx.set_neural_colors(None)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    renders = max(st["renders"], 1)
+    color_ms = st["color"] / renders
+    rows = sum(s["n_rendered"] for s in stats)
+    tiles = sum((s["n_rendered"] + 127) // 128 for s in stats)
+    # executed: both networks on every 128-row tile (N = 128, 128, 32; K = 64)
+    exec_flops = tiles * 128 * 2 * 64 * (128 + 128 + 32)
+    alg_flops = rows * 2 * (64 * 64 + 64 * 64 + 64 * 3)      # one network per Gaussian
+    peak = float(peaks.get("bf16_tflops", 1695.8))
+    return {"metric": "views/s with the NeurF colour query (tcgen05 bf16 MLP, NEXT-4)",
+            "value": len(views) * world * k / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / k,
+            "color_stage_ms": color_ms, "rows_per_step": rows,
+            "roofline": {"kernel": "k_neurf", "bound": "tensor",
+                         "achieved": exec_flops / (color_ms / 1e3) / 1e12 if color_ms else None,
+                         "peak": peak, "unit": "TFLOP/s",
+                         "frac": exec_flops / (color_ms / 1e3) / 1e12 / peak if color_ms else None,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 burst)",
+                         "exec_flops_per_launch": exec_flops, "alg_flops_per_launch": alg_flops,
+                         "alg_bytes_per_launch": 32 * rows}}
+
+
 def load_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture of this
     bench command (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
@@ -334,6 +402,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool", type=int, default=4, help="distinct view batches cycled per step")
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training step")
+    ap.add_argument("--no-neurf", action="store_true",
+                    help="skip the NeurF colour-query measurement (NEXT-4)")
     ap.add_argument("--no-conventional", action="store_true",
                     help="skip the conventional-pipeline comparison (NEXT-2)")
     ap.add_argument("--train-steps", type=int, default=5)
@@ -468,6 +538,12 @@ def main():
     if not args.no_conventional and args.config != "toy":
         conventional = run_conventional(args, ctx, ds, pools[0], outs, world, dev, stream, value)
 
+    # ---------------- NEXT-4: NeurF colour query on the tensor cores
+    neurf_line = None
+    if not args.no_neurf and args.config != "toy":
+        neurf_line = run_neurf(args, ctx, ds, scene, pools[0], tables[0], outs, world, dev, stream,
+                               peaks)
+
     # ---------------- e2e through the host-buffer C-ABI entry point
     e2e = None
     if not args.no_e2e:
@@ -540,6 +616,7 @@ def main():
             "cpu_baseline": cpu,
             "train": train,
             "conventional": conventional,
+            "neurf": neurf_line,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
