@@ -8,7 +8,7 @@ $CMD > gpurun_out/plain_$TAG.json 2> gpurun_out/plain_$TAG.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
-for K in k_raster k_project k_bin_expand k_bin_scatter k_permute k_filter k_raster_bwd k_project_bwd; do
+for K in k_raster k_project k_bin_expand k_bin_scatter k_permute k_filter k_raster_bwd k_project_bwd k_neurf k_to_world; do
   ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 \
       -o gpurun_out/prof_${TAG}_$K $CMD > gpurun_out/ncu_${TAG}_$K.log 2>&1
   echo "$K rc=$?"
