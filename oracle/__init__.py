@@ -91,7 +91,7 @@ def lib():
                 "so_render_view_f64": (C.c_int, [P, P, P]),
                 "so_blend_bruteforce_f32": (C.c_int, [P, P, P, P, P, P, P, P]),
                 "so_blend_bruteforce_f64": (C.c_int, [P, P, P, P, P, P, P, P]),
-                "so_backward_f64": (C.c_int, [P, P, P, P, P, P]),
+                "so_backward_f64": (C.c_int, [P, P, P, P, P, P, P]),
                 "so_update_life_f32": (None, [P, P, C.c_float]),
                 "so_lod_normal3": (None, [C.c_uint64, C.c_int64, P]),
                 "so_lod_uniform_k": (C.c_float, [C.c_uint64, C.c_int64, C.c_int]),
@@ -214,16 +214,20 @@ def blend_bruteforce(scene, view, flags, keys, rect, precision="f32", table=None
     return rgb, depth, T
 
 
-def backward(scene, view, g_rgb, g_depth=None, g_T=None, table=None, grads=None) -> np.ndarray:
+def backward(scene, view, g_rgb, g_depth=None, g_T=None, table=None, grads=None,
+             g_table=None) -> np.ndarray:
     """fp64 adjoint: dL/d(raw params) (n, 16) for one view given dL/d(rgb, depth, T)
-    (accumulated into `grads` if given)."""
+    (accumulated into `grads` if given); g_table (num_instances, 12) float64, if
+    given, accumulates dL/d(instance camera table) (the NEXT-1 pose gradient)."""
     L = lib()
     sr, vr = _SceneRef(scene, life=False), _ViewRef(view, table)
     g = np.zeros((scene.n, 16), np.float64) if grads is None else grads
     f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)
     a_rgb, a_d, a_t = f(g_rgb), f(g_depth), f(g_T)
+    if g_table is not None:
+        assert g_table.dtype == np.float64 and g_table.flags.c_contiguous
     rc = L.so_backward_f64(C.byref(sr.s), C.byref(vr.v), _ptr(a_rgb), _ptr(a_d), _ptr(a_t),
-                           _ptr(g))
+                           _ptr(g), _ptr(g_table))
     assert rc == 0
     return g
 

@@ -127,9 +127,12 @@ void     so_reset_visibility(so_scene* s);
 /* ---- f64 adjoint (config 5; s3r_oracle_bwd.c) ------------------------ */
 /* grads += dL/d(raw params) of view v, double[n][16] in scene-row layout
  * {mu xyz, opacity, sigma xyz, 0, q wxyz, rgb, 0}; g_rgb [H][W][3] required,
- * g_depth [H][W] and g_T [H][W] optional (NULL = 0). */
+ * g_depth [H][W] and g_T [H][W] optional (NULL = 0); g_table (optional)
+ * += dL/d(instance camera table) double[num_instances][12] (NEXT-1 pose
+ * gradient, row-major 3x4 [R | t] per slot). */
 int      so_backward_f64(const so_scene* s, const so_view* v, const double* g_rgb,
-                         const double* g_depth, const double* g_T, double* grads);
+                         const double* g_depth, const double* g_T, double* grads,
+                         double* g_table);
 
 /* ---- f64 shadow ------------------------------------------------------ */
 double   so_exp_f64(double x);

@@ -61,7 +61,7 @@ static void rotmat(double w, double x, double y, double z, double R[9])
 /* Projection adjoint of Gaussian g in view v: from the splat's accumulated
  * (gmx, gmy, gz, gA, gB, gC) to mean, scales and quaternion. */
 static void project_adjoint(const so_scene* s, const so_view* v, int64_t g, const bw_splat* sp,
-                            double* out)
+                            double* out, double* gtab)
 {
     const int32_t id = s->instance_ids[g];
     const float* Mf = v->instance_w2c + 12 * (int64_t)id;
@@ -168,6 +168,17 @@ static void project_adjoint(const so_scene* s, const so_view* v, int64_t g, cons
     gp[2] += sp->gmy * (-fy * p[1] / (pz * pz));
     gp[2] += sp->gz;
     for (int k = 0; k < 3; ++k) out[k] += Wr[k] * gp[0] + Wr[3 + k] * gp[1] + Wr[6 + k] * gp[2];
+    /* the instance camera M = [Wr | t] (NEXT-1 pose gradient): p = Wr mu + t and
+     * WR = Wr R_q give dL/dWr = gp mu^T + gWR R_q^T, dL/dt = gp */
+    if (gtab) {
+        double* G = gtab + 12 * (int64_t)id;
+        for (int r = 0; r < 3; ++r) {
+            for (int k = 0; k < 3; ++k)
+                G[4 * r + k] += gp[r] * mu[k] + gWR[3 * r] * Rq[3 * k] + gWR[3 * r + 1] * Rq[3 * k + 1] +
+                                gWR[3 * r + 2] * Rq[3 * k + 2];
+            G[4 * r + 3] += gp[r];
+        }
+    }
     out[3] += sp->go;
     out[12] += sp->gr;
     out[13] += sp->gg;
@@ -175,7 +186,7 @@ static void project_adjoint(const so_scene* s, const so_view* v, int64_t g, cons
 }
 
 int so_backward_f64(const so_scene* s, const so_view* v, const double* g_rgb,
-                    const double* g_depth, const double* g_T, double* grads)
+                    const double* g_depth, const double* g_T, double* grads, double* g_table)
 {
     if (!s || !v || !g_rgb || !grads) return -1;
     const int32_t W = v->width, H = v->height;
@@ -273,7 +284,7 @@ int so_backward_f64(const so_scene* s, const so_view* v, const double* g_rgb,
         }
     }
     for (int64_t g = 0; g < n; ++g)
-        if (flags[g] & SO_F_RENDERED) project_adjoint(s, v, g, &sp[g], grads + 16 * g);
+        if (flags[g] & SO_F_RENDERED) project_adjoint(s, v, g, &sp[g], grads + 16 * g, g_table);
 
     free(pw); free(Tk); free(al); free(start); free(pairs); free(sp);
     free(rect); free(flags); free(keys);

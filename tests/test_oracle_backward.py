@@ -108,3 +108,38 @@ def test_color_gradient_is_blend_weight_sum():
     s.colors[:, :3] = 1.0
     o = oracle.render_view(s, v, "f64", pairs=False)
     assert abs(g[:, 12].sum() - o["rgb"][..., 0].sum()) < 1e-9 * o["rgb"][..., 0].sum()
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_pose_gradient_matches_central_differences(seed):
+    """NEXT-1 pose gradient: dL/d(instance camera table) [K+1][12] (slot 0 =
+    W_t, slot 1 = the dynamic object's W_t W_{t,i2g}) vs central differences
+    of the fp64 forward with the perturbed table; gate 1e-3 of the largest."""
+    s, v, rng = _scene(seed)
+    H, W = v.height, v.width
+    wr = rng.standard_normal((H, W, 3))
+    wd = rng.standard_normal((H, W)) * 0.1
+    wt = rng.standard_normal((H, W))
+    tab = oracle.compose(v).copy()
+    gt = np.zeros((s.num_instances, 12))
+    oracle.backward(s, v, wr, wd, wt, table=tab, g_table=gt)
+
+    def loss(t):
+        o = oracle.render_view(s, v, "f64", table=t, pairs=False)
+        return float((o["rgb"] * wr).sum() + (o["depth"] * wd).sum() + (o["final_T"] * wt).sum())
+
+    fd = np.zeros_like(gt)
+    for i in range(s.num_instances):
+        for k in range(12):
+            x0 = tab[i, k]
+            h = np.float32(max(abs(float(x0)) * 1e-3, 1e-4))
+            tab[i, k] = x0 + h
+            xp, lp = float(tab[i, k]), loss(tab)
+            tab[i, k] = x0 - h
+            xm, lm = float(tab[i, k]), loss(tab)
+            tab[i, k] = x0
+            fd[i, k] = (lp - lm) / (xp - xm)
+    for i in range(s.num_instances):
+        ref = np.abs(fd[i]).max()
+        assert ref > 0
+        assert np.abs(gt[i] - fd[i]).max() <= 1e-3 * ref, (i, gt[i], fd[i])
