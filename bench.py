@@ -309,6 +309,10 @@ def load_traffic(kernel):
         return None, None
 
 
+def scene_instances(ds):
+    return int(ds.num_instances)
+
+
 def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
     """Config 5: one step = training forward of the batch, MSE against noisy
     targets (s3r_mse), backward of blend + projection (s3r_render_backward)
@@ -323,6 +327,8 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
     gimg = [torch.empty_like(o["rgb"]) for o in outs]
     grads = {k: torch.zeros_like(getattr(ds, k)) for k in
              ("means_opacity", "scales", "rotations", "colors")}
+    # NEXT-1 pose gradient: dL/d(instance camera table) per view and instance
+    grads["table"] = torch.zeros((len(views), scene_instances(ds), 12), device=dev)
     loss = torch.zeros(1, device=dev)
     npix = sum(v.width * v.height * 3 for v in views)
     cots = [{"rgb": g} for g in gimg]
@@ -342,8 +348,11 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
         ctx.render_backward(ds, views, tables, cots, grads)
         e_fwd[3].record(stream)
         if world > 1:
-            for g in grads.values():
-                dist.all_reduce(g, op=dist.ReduceOp.SUM)
+            # per-Gaussian gradients are summed over ranks; the pose gradient is
+            # per view (each rank owns its views' poses) and stays local
+            for k_, g in grads.items():
+                if k_ != "table":
+                    dist.all_reduce(g, op=dist.ReduceOp.SUM)
 
     for _ in range(2):
         step()
@@ -371,7 +380,8 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
             "value": len(views) * world * k / (ms / 1e3), "unit": "views/s",
             "ms_per_step": ms / k, "forward_ms": fwd_ms / k, "backward_ms": bwd_ms / k,
             "loss": float(loss.item()), "views_per_gpu_per_step": len(views), "steps": k,
-            "grads": "mean, opacity, scales, quaternion, colour (14 fp32 per Gaussian)"}
+            "grads": "mean, opacity, scales, quaternion, colour (14 fp32 per Gaussian) + "
+                     "instance-camera pose (12 fp32 per instance per view)"}
 
 
 def cpu_baseline(cfg_name, budget_s=12.0):

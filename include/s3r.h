@@ -323,12 +323,17 @@ typedef struct {
 /* Gradient accumulators, DEVICE float4[n] each, scene-row layout:
  * means_opacity = dL/d(mu_x, mu_y, mu_z, opacity); scales = dL/d(sigma), .w
  * untouched; rotations = dL/dq (w,x,y,z) of the unnormalised quaternion;
- * colors = dL/d(r,g,b), .w untouched.                                      */
+ * colors = dL/d(r,g,b), .w untouched.  table (optional, NULL = not wanted):
+ * DEVICE float[n_views][num_instances][12] += dL/d(instance camera table)
+ * (NEXT-1 pose gradient: slot 0 = dL/dW_t, slot i = dL/dW_{t,i}, row-major
+ * 3x4 [R | t]; the caller chains it through W_{t,i} = W_t W_{t,i2g} to the
+ * object poses, e.g. dL/dR_i2g = R_t^T dL/dR_{t,i}, dL/dt_i2g = R_t^T dL/dt_{t,i}). */
 typedef struct {
     float* means_opacity;
     float* scales;
     float* rotations;
     float* colors;
+    float* table;
 } s3r_grads;
 
 /* scene and views must be the ones of the last render; cots: HOST array of

@@ -289,17 +289,18 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     }
 }
 
-__global__ void __launch_bounds__(256) k_project_bwd(BackwardArgs a)
+// chain rule of one splat (view V, depth rank r): atomics into the caller's
+// per-Gaussian gradients; gm12 = its dL/d(instance camera) when requested.
+// Returns the instance id, or -1 when the splat has no gradient.
+__device__ __forceinline__ int project_bwd_one(const BackwardArgs& a, const DevView& V,
+                                               long long r, float* gm12)
 {
-    const DevView& V = a.views[blockIdx.y];
-    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= V.n_rendered) return;
     const float* acc = a.splat_grads + 10 * (V.cap_off + r);
     const float gmx = acc[0], gmy = acc[1], gz = acc[2], gA = acc[3], gB = acc[4], gC = acc[5],
                 go = acc[6], gcr = acc[7], gcg = acc[8], gcb = acc[9];
     if (gmx == 0.f && gmy == 0.f && gz == 0.f && gA == 0.f && gB == 0.f && gC == 0.f &&
         go == 0.f && gcr == 0.f && gcg == 0.f && gcb == 0.f)
-        return;
+        return -1;
     const long long g = (long long)(a.dkey_sorted[V.cap_off + r] & a.gmask);
     const int id = a.ids[g];
     const float* M = V.table + 12 * id;
@@ -413,6 +414,19 @@ __global__ void __launch_bounds__(256) k_project_bwd(BackwardArgs a)
     gp1 += gmy * fy / pz;
     gp2 += gmy * (-fy * p[1] * iz2);
     gp2 += gz;
+    if (a.g_table) {
+        // NEXT-1 pose gradient: M = [Wr | t], p = Wr mu + t, WR = Wr R_q:
+        // dL/dWr = gp mu^T + gWR R_q^T, dL/dt = gp
+        const float gpv[3] = {gp0, gp1, gp2}, muv[3] = {mo.x, mo.y, mo.z};
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                gm12[4 * i + k] = gpv[i] * muv[k] + gWR[3 * i] * Rq[3 * k] +
+                                  gWR[3 * i + 1] * Rq[3 * k + 1] + gWR[3 * i + 2] * Rq[3 * k + 2];
+            gm12[4 * i + 3] = gpv[i];
+        }
+    }
     float* gm = a.g_means + 4 * g;
     atomicAdd(gm + 0, M[0] * gp0 + M[4] * gp1 + M[8] * gp2);
     atomicAdd(gm + 1, M[1] * gp0 + M[5] * gp1 + M[9] * gp2);
@@ -429,6 +443,51 @@ __global__ void __launch_bounds__(256) k_project_bwd(BackwardArgs a)
     atomicAdd(gco + 0, gcr);
     atomicAdd(gco + 1, gcg);
     atomicAdd(gco + 2, gcb);
+    return id;
+}
+
+__global__ void __launch_bounds__(256) k_project_bwd(BackwardArgs a)
+{
+    extern __shared__ float s_gt[];          // [K1][12] pose-gradient partials (if requested)
+    const int vi = blockIdx.y;
+    const DevView& V = a.views[vi];
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool use_smem = a.g_table && a.smem_table;
+    if (use_smem)
+        for (int i = threadIdx.x; i < 12 * a.num_instances; i += blockDim.x) s_gt[i] = 0.0f;
+    if (use_smem) __syncthreads();
+    if ((long long)blockIdx.x * blockDim.x >= V.n_rendered) return;     // uniform for the CTA
+    float gm12[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) gm12[j] = 0.0f;
+    const int id = r < V.n_rendered ? project_bwd_one(a, V, r, gm12) : -1;
+    if (!a.g_table) return;
+    float* gt_view = a.g_table + (long long)vi * a.num_instances * 12;
+    // a warp whose active splats share one instance (the common case: static)
+    // reduces in registers first; otherwise per-splat shared atomics
+    const int lane = threadIdx.x & 31;
+    const bool act = id >= 0;
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    if (am) {
+        const int leader = __ffs(am) - 1;
+        const int idl = __shfl_sync(0xffffffffu, id, leader);
+        float* dst = use_smem ? s_gt : gt_view;
+        if (__all_sync(0xffffffffu, !act || id == idl)) {
+#pragma unroll
+            for (int j = 0; j < 12; ++j) {
+                const float v = warp_sum(gm12[j]);
+                if (lane == leader) atomicAdd(dst + 12 * idl + j, v);
+            }
+        } else if (act) {
+#pragma unroll
+            for (int j = 0; j < 12; ++j) atomicAdd(dst + 12 * id + j, gm12[j]);
+        }
+    }
+    if (use_smem) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 12 * a.num_instances; i += blockDim.x)
+            if (s_gt[i] != 0.0f) atomicAdd(gt_view + i, s_gt[i]);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_mse(const float* __restrict__ x,
@@ -466,8 +525,10 @@ void launch_backward(const BackwardArgs& a, int max_tiles, long long max_rendere
 {
     if (a.n_views == 0) return;
     if (max_tiles) k_raster_bwd<<<dim3(max_tiles, a.n_views), RT, 0, st>>>(a);
-    if (max_rendered)
-        k_project_bwd<<<dim3((unsigned)((max_rendered + 255) / 256), a.n_views), 256, 0, st>>>(a);
+    if (max_rendered) {
+        const size_t smem = a.g_table && a.smem_table ? (size_t)a.num_instances * 48 : 0;
+        k_project_bwd<<<dim3((unsigned)((max_rendered + 255) / 256), a.n_views), 256, smem, st>>>(a);
+    }
 }
 
 void launch_mse(const float* x, const float* y, long long n, float scale, float* grad,

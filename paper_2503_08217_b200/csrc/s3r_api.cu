@@ -1116,6 +1116,9 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
     a.g_scales = grads->scales;
     a.g_rot = grads->rotations;
     a.g_colors = grads->colors;
+    a.g_table = grads->table;
+    a.num_instances = sc->num_instances;
+    a.smem_table = sc->num_instances <= 1024;
     launch_backward(a, c->last_max_tiles, c->last_max_r, st);
     CU(cudaEventRecord(c->staging_free, st));
     CU(cudaGetLastError());

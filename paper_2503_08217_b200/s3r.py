@@ -74,7 +74,7 @@ class Cot_(C.Structure):
 
 class Grads_(C.Structure):
     _fields_ = [("means_opacity", C.c_void_p), ("scales", C.c_void_p),
-                ("rotations", C.c_void_p), ("colors", C.c_void_p)]
+                ("rotations", C.c_void_p), ("colors", C.c_void_p), ("table", C.c_void_p)]
 
 
 class Debug_(C.Structure):
@@ -361,7 +361,7 @@ class Context:
         cs = (Cot_ * max(n, 1))(*[Cot_(_ptr(c["rgb"]), _ptr(c.get("depth")),
                                        _ptr(c.get("final_T"))) for c in cots])
         g = Grads_(_ptr(grads["means_opacity"]), _ptr(grads["scales"]),
-                   _ptr(grads["rotations"]), _ptr(grads["colors"]))
+                   _ptr(grads["rotations"]), _ptr(grads["colors"]), _ptr(grads.get("table")))
         sc = scene.struct()
         self._check(self.L.s3r_render_backward(self.h, C.byref(sc), vs, n, cs, C.byref(g),
                                                _stream(stream)))

@@ -398,7 +398,7 @@ def _grads_like(ds):
             ("means_opacity", "scales", "rotations", "colors")}
 
 
-def _gpu_backward(ctx, scene, views, cot_np):
+def _gpu_backward(ctx, scene, views, cot_np, table_grads=None):
     ds = s3r.DeviceScene.from_numpy(scene)
     tabs = s3r.view_tables(ctx, views)
     outs = s3r.alloc_outputs(views)
@@ -408,6 +408,8 @@ def _gpu_backward(ctx, scene, views, cot_np):
         cots = [{k: torch.from_numpy(np.ascontiguousarray(c[k], np.float32)).cuda()
                  for k in c} for c in cot_np]
         grads = _grads_like(ds)
+        if table_grads is not None:
+            grads["table"] = table_grads
         ctx.render_backward(ds, views, list(tabs), cots, grads)
         torch.cuda.synchronize()
     finally:
@@ -437,11 +439,19 @@ def test_backward_matches_oracle(ctx, seed):
     cot = [{"rgb": rng.standard_normal((v.height, v.width, 3)),
             "depth": 0.05 * rng.standard_normal((v.height, v.width)),
             "final_T": rng.standard_normal((v.height, v.width))} for v in views]
-    g_gpu, tabs = _gpu_backward(ctx, scene, views, cot)
+    gt = torch.zeros((len(views), scene.num_instances, 12), device="cuda")
+    g_gpu, tabs = _gpu_backward(ctx, scene, views, cot, table_grads=gt)
     g_ref = np.zeros((scene.n, 16))
-    for v, t, c in zip(views, tabs, cot):
+    for vi, (v, t, c) in enumerate(zip(views, tabs, cot)):
+        gt_ref = np.zeros((scene.num_instances, 12))
         oracle.backward(scene, v, c["rgb"], c["depth"], c["final_T"], table=t.cpu().numpy(),
-                        grads=g_ref)
+                        grads=g_ref, g_table=gt_ref)
+        # NEXT-1 pose gradient per view and instance, same 1e-3 gate
+        got = gt[vi].cpu().numpy().astype(np.float64)
+        for i in range(scene.num_instances):
+            ref = np.abs(gt_ref[i]).max()
+            if ref > 0:
+                assert np.abs(got[i] - gt_ref[i]).max() <= 1e-3 * ref, (vi, i)
     _check_grads(g_gpu, g_ref)
 
 
