@@ -98,10 +98,11 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     const int px = tx * TILE + (tid >> 5) * BW + (lane % BW);
     const int py0 = ty * TILE + (lane / BW);
     const float fpx = (float)px;
-    // centre and half size of the warp's BW x TILE pixel block (flush-ellipse culling)
-    const float hbx = 0.5f * (BW - 1), hby = 0.5f * (TILE - 1);
-    const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + hbx;
-    const float bcy = (float)(ty * TILE) + hby;
+    // centre of the warp's BW x TILE pixel block (flush-ellipse culling; the
+    // stored extents include the block's half size, which needs BW = 8)
+    static_assert(BW == 8 && TILE == 16, "cull extents assume 8 x 16 warp blocks");
+    const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + CULL_HALF_BX;
+    const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
     const s3r_cot C = a.cots[v];
     // the thread's 4 pixels (rows py0 + 4k) as 2 packed pairs: pair P holds
     // k = 2P (.x) and 2P + 1 (.y); sm_100a FADD2/FMUL2/FFMA2 work on both
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
             const float4 q0 = s_rec[3 * jj], q1 = s_rec[3 * jj + 1], q2 = s_rec[3 * jj + 2];
             // no evaluation of the warp's block passes the forward's flush test
             // (s3r_internal.cuh flush_extent): nothing to differentiate
-            if (S3R_CULL && (fabsf(q0.x - bcx) > s_hx[jj] + hbx || fabsf(q0.y - bcy) > q2.w + hby))
+            if (S3R_CULL && (fabsf(q0.x - bcx) > s_hx[jj] || fabsf(q0.y - bcy) > q2.w))
                 continue;
             const float dx = q0.x - fpx;
             const float a1 = q1.x * dx;

@@ -91,8 +91,8 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     const int py0 = ty * TILE + (lane >> 3);
     const float fpx = (float)px;
     // centre of the warp's 8 x 16 pixel block (flush-ellipse culling)
-    const float bcx = (float)(tx * TILE + ((tid >> 5) << 3)) + 3.5f;
-    const float bcy = (float)(ty * TILE) + 7.5f;
+    const float bcx = (float)(tx * TILE + ((tid >> 5) << 3)) + CULL_HALF_BX;
+    const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
     // pair P holds pixels k = 2P (.x) and 2P + 1 (.y)
     float2 nfpy[2], T[2], cr[2], cg[2], cb[2], dp[2];
     int stop[RPIX];
@@ -149,7 +149,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                 // every evaluation of the warp's block lies outside the splat's
                 // flush ellipse (alpha = 0 for all of them): skip the record,
                 // warp-uniformly (s3r_internal.cuh flush_extent)
-                if (fabsf(q0.x - bcx) > q1.w + 3.5f || fabsf(q0.y - bcy) > q2.w + 7.5f) continue;
+                if (fabsf(q0.x - bcx) > q1.w || fabsf(q0.y - bcy) > q2.w) continue;
 #endif
                 // e2 = log2(e) * power = qa dx^2 + qb dx dy + qc dy^2 (R-ARITH exp2
                 // form); the dx terms are shared by the thread's 4 pixels

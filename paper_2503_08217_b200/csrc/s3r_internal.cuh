@@ -30,6 +30,10 @@ constexpr float FLUSH_E2 = -24.0f;       // s3r_exp2(x) = 0 for x < -24 (R-ARITH
 #endif
 constexpr float CULL_TAU = 25.2f;
 constexpr float CULL_KAPPA = 1.0e4f;
+// the rasterizers' warp pixel block is 8 columns x 16 rows (k_raster,
+// k_raster_bwd): the stored extents include its half size, so the per-record
+// test is |mean - block centre| > extent
+constexpr float CULL_HALF_BX = 3.5f, CULL_HALF_BY = 7.5f;
 
 __device__ __forceinline__ void flush_extent(float qa, float qb, float qc, float& hx, float& hy)
 {
@@ -41,8 +45,8 @@ __device__ __forceinline__ void flush_extent(float qa, float qb, float qc, float
     hx = hy = __int_as_float(0x7f800000);
     if (a > 0.0f && c > 0.0f && det4 > 0.0f && lmin > 0.0f &&
         a + fabsf(b) + c <= CULL_KAPPA * lmin) {
-        hx = sqrtf(CULL_TAU * c / det4) * 1.001f + 0.01f;
-        hy = sqrtf(CULL_TAU * a / det4) * 1.001f + 0.01f;
+        hx = sqrtf(CULL_TAU * c / det4) * 1.001f + (0.01f + CULL_HALF_BX);
+        hy = sqrtf(CULL_TAU * a / det4) * 1.001f + (0.01f + CULL_HALF_BY);
     }
 }
 constexpr int MAX_TSLOTS = 64;           // distinct times per K1 launch

@@ -22,8 +22,8 @@ VARIANT_SETS = {
     },
     "mb": {
         "base": [],
-        "minb16": ["S3R_RASTER_MINB=16"],
         "minb14": ["S3R_RASTER_MINB=14"],
+        "minb15": ["S3R_RASTER_MINB=15"],
     },
     "live": {
         "base": [],
