@@ -84,6 +84,9 @@ __device__ __forceinline__ float warp_sum(float x)
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 __device__ __forceinline__ float2 neg2(float2 x) { return make_float2(-x.x, -x.y); }
 
+// HAS_D / HAS_T: some view has a depth / final-T cotangent (otherwise those
+// terms are zero and compiled out)
+template <bool HAS_D, bool HAS_T>
 __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
 {
     __shared__ float4 s_rec[3 * RB];
@@ -123,8 +126,8 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
             grk[k] = C.rgb[3 * pix];
             ggk[k] = C.rgb[3 * pix + 1];
             gbk[k] = C.rgb[3 * pix + 2];
-            if (C.depth) gdk[k] = C.depth[pix];
-            if (C.final_T) gtTk[k] = C.final_T[pix] * Tk[k];
+            if (HAS_D && C.depth) gdk[k] = C.depth[pix];
+            if (HAS_T && C.final_T) gtTk[k] = C.final_T[pix] * Tk[k];
             mymax = max(mymax, last[k]);
         }
     }
@@ -225,9 +228,9 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 float2 cdot = __fmul2_rn(f2(q2.x), gr[P]);
                 cdot = __ffma2_rn(f2(q2.y), gg[P], cdot);
                 cdot = __ffma2_rn(f2(q2.z), gb[P], cdot);
-                cdot = __ffma2_rn(f2(q0.z), gd[P], cdot);
+                if (HAS_D) cdot = __ffma2_rn(f2(q0.z), gd[P], cdot);
                 // dL/dalpha = T (c.gC + z gD) - (R + gT T_final) / (1 - alpha)
-                const float2 rest = __fmul2_rn(__fadd2_rn(Rr[P], gtTf[P]), inv);
+                const float2 rest = __fmul2_rn(HAS_T ? __fadd2_rn(Rr[P], gtTf[P]) : Rr[P], inv);
                 const float2 galpha = __ffma2_rn(Tb, cdot, neg2(rest));
                 Rr[P] = __ffma2_rn(cdot, w, Rr[P]);
                 Tc[P] = Tb;
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 s_r = __ffma2_rn(w, gr[P], s_r);
                 s_g = __ffma2_rn(w, gg[P], s_g);
                 s_b = __ffma2_rn(w, gb[P], s_b);
-                s_z = __ffma2_rn(w, gd[P], s_z);
+                if (HAS_D) s_z = __ffma2_rn(w, gd[P], s_z);
                 // alpha clamped at 0.99: no gradient to o or the power;
                 // power clamped at 0 (e2raw > 0): no gradient to the power
                 const float2 go = make_float2(okx && og.x < 0.99f ? galpha.x : 0.0f,
@@ -525,7 +528,13 @@ __global__ void __launch_bounds__(256) k_mse(const float* __restrict__ x,
 void launch_backward(const BackwardArgs& a, int max_tiles, long long max_rendered, cudaStream_t st)
 {
     if (a.n_views == 0) return;
-    if (max_tiles) k_raster_bwd<<<dim3(max_tiles, a.n_views), RT, 0, st>>>(a);
+    if (max_tiles) {
+        const dim3 grid(max_tiles, a.n_views);
+        if (a.has_depth_cot && a.has_T_cot) k_raster_bwd<true, true><<<grid, RT, 0, st>>>(a);
+        else if (a.has_depth_cot) k_raster_bwd<true, false><<<grid, RT, 0, st>>>(a);
+        else if (a.has_T_cot) k_raster_bwd<false, true><<<grid, RT, 0, st>>>(a);
+        else k_raster_bwd<false, false><<<grid, RT, 0, st>>>(a);
+    }
     if (max_rendered) {
         const size_t smem = a.g_table && a.smem_table ? (size_t)a.num_instances * 48 : 0;
         k_project_bwd<<<dim3((unsigned)((max_rendered + 255) / 256), a.n_views), 256, smem, st>>>(a);

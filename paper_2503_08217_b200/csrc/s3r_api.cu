@@ -1119,6 +1119,10 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
     a.g_table = grads->table;
     a.num_instances = sc->num_instances;
     a.smem_table = sc->num_instances <= 1024;
+    for (int v = 0; v < nv; ++v) {
+        if (cots[v].depth) a.has_depth_cot = 1;
+        if (cots[v].final_T) a.has_T_cot = 1;
+    }
     launch_backward(a, c->last_max_tiles, c->last_max_r, st);
     CU(cudaEventRecord(c->staging_free, st));
     CU(cudaGetLastError());

@@ -314,6 +314,7 @@ struct BackwardArgs {
     float* g_table;                      // [n_views][num_instances][12] or NULL (pose gradient)
     int num_instances;
     int smem_table;                      // accumulate g_table per CTA in shared memory
+    int has_depth_cot, has_T_cot;        // some view has a depth / final_T cotangent
 };
 void launch_backward(const BackwardArgs& a, int max_tiles, long long max_rendered, cudaStream_t st);
 void launch_mse(const float* x, const float* y, long long n, float scale, float* grad,
