@@ -2,7 +2,10 @@
 // of the instance-specific projection (Eq.1 P:107-112 through W_{t,i} of
 // P:158-159), for the views of the last forward batch; plus the MSE helper.
 //
-// K7b k_raster_bwd: same CTA layout as K7 (64 threads, 4 pixels per thread).
+// K7b k_raster_bwd: one warp per (view, tile), 8 pixels per thread (one column,
+// every other row) as 4 packed fp32 pairs, so the per-splat warp reduction
+// below is shared by 256 pixels (A/B: 37.1 ms vs 40.7 ms with the forward's
+// 64-thread, 4-pixel layout).
 // Every pixel knows from the forward its final transmittance and how many list
 // entries it blended; the CTA walks its tile list BACK TO FRONT in batches of
 // 256 staged records, recomputes alpha with the forward's R-ARITH ops (so the
@@ -30,10 +33,10 @@ namespace s3r {
 namespace {
 
 #ifndef S3R_BWD_RPIX
-#define S3R_BWD_RPIX 4
+#define S3R_BWD_RPIX 8
 #endif
 #ifndef S3R_BWD_MINB
-#define S3R_BWD_MINB 12     // 80 registers (A/B: 41.9 ms vs 46.1 at 128 registers)
+#define S3R_BWD_MINB 20     // 96 registers at RPIX 8 (A/B: 37.1 ms; 16: 37.3, 24: 45.0)
 #endif
 #ifndef S3R_BWD_EX2
 #define S3R_BWD_EX2 1
@@ -102,9 +105,11 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     const int py0 = ty * TILE + (lane / BW);
     const float fpx = (float)px;
     // centre of the warp's BW x TILE pixel block (flush-ellipse culling; the
-    // stored extents include the block's half size, which needs BW = 8)
-    static_assert(BW == 8 && TILE == 16, "cull extents assume 8 x 16 warp blocks");
-    const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + CULL_HALF_BX;
+    // stored extents include the 8 x 16 block's half size, so a wider block
+    // adds the difference)
+    static_assert(TILE == 16 && BW >= 8, "cull extents assume >= 8 x 16 warp blocks");
+    constexpr float XPAD = 0.5f * (BW - 1) - CULL_HALF_BX;
+    const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + 0.5f * (BW - 1);
     const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
     const s3r_cot C = a.cots[v];
     // the thread's 4 pixels (rows py0 + 4k) as 2 packed pairs: pair P holds
@@ -131,9 +136,10 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
             mymax = max(mymax, last[k]);
         }
     }
-    float2 Tc[2], gtTf[2], Rr[2], gr[2], gg[2], gb[2], gd[2], nfpy[2];
+    constexpr int NP = RPIX / 2;
+    float2 Tc[NP], gtTf[NP], Rr[NP], gr[NP], gg[NP], gb[NP], gd[NP], nfpy[NP];
 #pragma unroll
-    for (int P = 0; P < 2; ++P) {
+    for (int P = 0; P < NP; ++P) {
         Tc[P] = make_float2(Tk[2 * P], Tk[2 * P + 1]);
         gtTf[P] = make_float2(gtTk[2 * P], gtTk[2 * P + 1]);
         gr[P] = make_float2(grk[2 * P], grk[2 * P + 1]);
@@ -174,7 +180,8 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
             const float4 q0 = s_rec[3 * jj], q1 = s_rec[3 * jj + 1], q2 = s_rec[3 * jj + 2];
             // no evaluation of the warp's block passes the forward's flush test
             // (s3r_internal.cuh flush_extent): nothing to differentiate
-            if (S3R_CULL && (fabsf(q0.x - bcx) > s_hx[jj] || fabsf(q0.y - bcy) > q2.w))
+            if (S3R_CULL && (fabsf(q0.x - bcx) > (XPAD != 0.0f ? s_hx[jj] + XPAD : s_hx[jj]) ||
+                             fabsf(q0.y - bcy) > q2.w))
                 continue;
             const float dx = q0.x - fpx;
             const float a1 = q1.x * dx;
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                    s_r = f2(0.f), s_g = f2(0.f), s_b = f2(0.f);
             bool any = false;
 #pragma unroll
-            for (int P = 0; P < 2; ++P) {
+            for (int P = 0; P < NP; ++P) {
                 const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
                 const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
                 const float2 e2raw = __ffma2_rn(dy, c1, f2(a2));

@@ -36,6 +36,12 @@ VARIANT_SETS = {
         "base": [],
         "nocull": ["S3R_CULL=0"],
     },
+    "bwd8": {
+        "base": [],
+        "rp8m16": ["S3R_BWD_RPIX=8", "S3R_BWD_MINB=16"],
+        "rp8m20": ["S3R_BWD_RPIX=8", "S3R_BWD_MINB=20"],
+        "rp8m24": ["S3R_BWD_RPIX=8", "S3R_BWD_MINB=24"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
