@@ -30,8 +30,16 @@ namespace {
 // 0x4B400000 + n, so (bits(t) << 23) + 0x3F800000 = bits(2^n).
 // c0 = 1.535336188319500e-4f is passed in a register (see k_raster).
 
-constexpr int RT = 64;      // threads per tile CTA: 16 columns x 4 row groups
-constexpr int RPIX = 4;     // pixels per thread: rows ly, ly+4, ly+8, ly+12 of one column
+#ifndef S3R_RASTER_RPIX
+#define S3R_RASTER_RPIX 4
+#endif
+// pixels per thread (RPIX rows of one column, RS rows apart); a tile's 256
+// pixels take RT = 256 / RPIX threads, each warp owning BW columns
+constexpr int RPIX = S3R_RASTER_RPIX;
+constexpr int RT = TILE * TILE / RPIX;
+constexpr int BW = TILE / (RT / 32);
+constexpr int RS = 32 / BW;
+constexpr int NP = RPIX / 2;
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
 // Build-time variants (for A/B measurement; the defaults are the product):
@@ -85,30 +93,33 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     if (tile >= V.ntiles) return;
     const int tid = threadIdx.x, lane = tid & 31;
     const int tx = tile % V.TX, ty = tile / V.TX;
-    // warp w owns columns 8w..8w+7; for pixel k a warp covers a compact 8x4 block
-    // (rows 4k..4k+3)
-    const int px = tx * TILE + ((tid >> 5) << 3) + (lane & 7);
-    const int py0 = ty * TILE + (lane >> 3);
+    // warp w owns columns BW w .. BW w + BW - 1; for pixel k a warp covers a
+    // compact BW x RS block (rows RS k .. RS k + RS - 1)
+    const int px = tx * TILE + (tid >> 5) * BW + (lane % BW);
+    const int py0 = ty * TILE + (lane / BW);
     const float fpx = (float)px;
-    // centre of the warp's 8 x 16 pixel block (flush-ellipse culling)
-    const float bcx = (float)(tx * TILE + ((tid >> 5) << 3)) + CULL_HALF_BX;
+    // centre of the warp's BW x 16 pixel block (flush-ellipse culling; the
+    // stored extents include the 8 x 16 block's half size)
+    static_assert(BW >= 8, "cull extents assume >= 8 x 16 warp blocks");
+    constexpr float XPAD = 0.5f * (BW - 1) - CULL_HALF_BX;
+    const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + 0.5f * (BW - 1);
     const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
     // pair P holds pixels k = 2P (.x) and 2P + 1 (.y)
-    float2 nfpy[2], T[2], cr[2], cg[2], cb[2], dp[2];
+    float2 nfpy[NP], T[NP], cr[NP], cg[NP], cb[NP], dp[NP];
     int stop[RPIX];
     int nlive = 0;                     // pixels of this thread still blending
     unsigned inside = 0;
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
-        const int py = py0 + 4 * k;
+        const int py = py0 + RS * k;
         stop[k] = -1;
         const bool in = px < V.W && py < V.H;
         inside |= (in ? 1u : 0u) << k;
         nlive += in ? 1 : 0;
     }
 #pragma unroll
-    for (int P = 0; P < 2; ++P) {
-        nfpy[P] = make_float2(-(float)(py0 + 8 * P), -(float)(py0 + 8 * P + 4));
+    for (int P = 0; P < NP; ++P) {
+        nfpy[P] = make_float2(-(float)(py0 + RS * 2 * P), -(float)(py0 + RS * (2 * P + 1)));
         // a pixel outside the image starts "terminated" (T = 0 is never written)
         T[P] = make_float2((inside >> (2 * P)) & 1 ? 1.0f : 0.0f,
                            (inside >> (2 * P + 1)) & 1 ? 1.0f : 0.0f);
@@ -149,7 +160,9 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                 // every evaluation of the warp's block lies outside the splat's
                 // flush ellipse (alpha = 0 for all of them): skip the record,
                 // warp-uniformly (s3r_internal.cuh flush_extent)
-                if (fabsf(q0.x - bcx) > q1.w || fabsf(q0.y - bcy) > q2.w) continue;
+                if (fabsf(q0.x - bcx) > (XPAD != 0.0f ? q1.w + XPAD : q1.w) ||
+                    fabsf(q0.y - bcy) > q2.w)
+                    continue;
 #endif
                 // e2 = log2(e) * power = qa dx^2 + qb dx dy + qc dy^2 (R-ARITH exp2
                 // form); the dx terms are shared by the thread's 4 pixels
@@ -158,7 +171,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                 const float a2 = a1 * dx;
                 const float b1 = q1.y * dx;
 #pragma unroll
-                for (int P = 0; P < 2; ++P) {
+                for (int P = 0; P < NP; ++P) {
                     const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
                     const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
                     const float2 e2r = __ffma2_rn(dy, c1, f2(a2));
@@ -187,7 +200,9 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                         T[P] = Tn;
                     }
                 }
-                const float tmax = fmaxf(fmaxf(T[0].x, T[0].y), fmaxf(T[1].x, T[1].y));
+                float tmax = fmaxf(T[0].x, T[0].y);
+#pragma unroll
+                for (int P = 1; P < NP; ++P) tmax = fmaxf(tmax, fmaxf(T[P].x, T[P].y));
                 nlive = tmax >= 1e-4f ? 1 : 0;
                 if (!__any_sync(0xffffffffu, nlive != 0)) break;   // whole warp done
             }
@@ -211,7 +226,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
         if (!(inside & (1u << k))) continue;
         const int P = k >> 1;
         const bool hi = k & 1;
-        const long long pix = (long long)(py0 + 4 * k) * V.W + px;
+        const long long pix = (long long)(py0 + RS * k) * V.W + px;
         float* o = V.rgb + 3 * pix;
         o[0] = hi ? cr[P].y : cr[P].x;
         o[1] = hi ? cg[P].y : cg[P].x;

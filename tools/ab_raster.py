@@ -36,6 +36,12 @@ VARIANT_SETS = {
         "base": [],
         "nocull": ["S3R_CULL=0"],
     },
+    "fwd8": {
+        "base": [],
+        "f8m20": ["S3R_RASTER_RPIX=8", "S3R_RASTER_MINB=20"],
+        "f8m24": ["S3R_RASTER_RPIX=8", "S3R_RASTER_MINB=24"],
+        "f8m32": ["S3R_RASTER_RPIX=8", "S3R_RASTER_MINB=32"],
+    },
     "bwd8": {
         "base": [],
         "rp8m16": ["S3R_BWD_RPIX=8", "S3R_BWD_MINB=16"],
