@@ -18,7 +18,9 @@
  *                                    dropped; reading R14)
  *   t = x + 1.5*2^23;  n = t - 1.5*2^23   (exact rint, ties to even)
  *   r = x - n           (exact, |r| <= 1/2)
- *   y = 1 + r P(r)      Cephes exp2f minimax P (degree 5), Horner with fma
+ *   y = 1 + r P(r)      P: degree-4 relative-minimax fit of (2^r - 1)/r on
+ *                       [-1/2, 1/2] (Lawson iteration, fp32 coefficients
+ *                       tuned by +-2 ulp), Horner with fma: <= 2.02 ulp
  *   return y * 2^n      (exact: 2^-24 is normal)
  * ---------------------------------------------------------------------- */
 float so_exp2_f32(float x)
@@ -27,12 +29,11 @@ float so_exp2_f32(float x)
     float t = x + 12582912.0f;
     float n = t - 12582912.0f;
     float r = x - n;
-    float p = 1.535336188319500e-4f;
-    p = fmaf(p, r, 1.339887440266574e-3f);
-    p = fmaf(p, r, 9.618437357674640e-3f);
-    p = fmaf(p, r, 5.550332471162809e-2f);
-    p = fmaf(p, r, 2.402264791363012e-1f);
-    p = fmaf(p, r, 6.931472028550421e-1f);
+    float p = 1.3264695880934596e-3f;
+    p = fmaf(p, r, 9.671507403254509e-3f);
+    p = fmaf(p, r, 5.550733208656311e-2f);
+    p = fmaf(p, r, 2.4022243916988373e-1f);
+    p = fmaf(p, r, 6.931470036506653e-1f);
     float y = fmaf(p, r, 1.0f);
     return ldexpf(y, (int)n);
 }

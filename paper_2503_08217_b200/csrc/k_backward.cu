@@ -53,12 +53,11 @@ __device__ __forceinline__ float s3r_exp2_b(float x)
     const float t = x + 12582912.0f;
     const float n = t - 12582912.0f;
     const float r = x - n;
-    float p = 1.535336188319500e-4f;
-    p = __fmaf_rn(p, r, 1.339887440266574e-3f);
-    p = __fmaf_rn(p, r, 9.618437357674640e-3f);
-    p = __fmaf_rn(p, r, 5.550332471162809e-2f);
-    p = __fmaf_rn(p, r, 2.402264791363012e-1f);
-    p = __fmaf_rn(p, r, 6.931472028550421e-1f);
+    float p = 1.3264695880934596e-3f;
+    p = __fmaf_rn(p, r, 9.671507403254509e-3f);
+    p = __fmaf_rn(p, r, 5.550733208656311e-2f);
+    p = __fmaf_rn(p, r, 2.4022243916988373e-1f);
+    p = __fmaf_rn(p, r, 6.931470036506653e-1f);
     const float y = __fmaf_rn(p, r, 1.0f);
     return y * __uint_as_float((__float_as_uint(t) << 23) + 0x3F800000u);
 }

@@ -26,9 +26,10 @@ namespace {
 // R-ARITH s3r_exp2 for -24 <= x <= 0 (the caller handles the flush x < -24 -> 0),
 // evaluated on pixel pairs by s3r_exp2_x2 below: n = rint(x) by the 1.5*2^23
 // shifter (full-rate FADDs, no F2I/FRND), r = x - n exact, 2^r by the Cephes
-// exp2f polynomial, times 2^n built from the shifter's bits: bits(t) =
+// degree-4 P of DESIGN.md R-ARITH, times 2^n built from the shifter's bits: bits(t) =
 // 0x4B400000 + n, so (bits(t) << 23) + 0x3F800000 = bits(2^n).
-// c0 = 1.535336188319500e-4f is passed in a register (see k_raster).
+// c0 = 1.3264695880934596e-3f (the leading coefficient of the degree-4 P of
+// DESIGN.md R-ARITH) is passed in a register (see k_raster).
 
 #ifndef S3R_RASTER_RPIX
 #define S3R_RASTER_RPIX 4
@@ -72,11 +73,10 @@ __device__ __forceinline__ float2 s3r_exp2_x2(float2 x, float c0)
     const float2 t = __fadd2_rn(x, f2(12582912.0f));
     const float2 n = __fadd2_rn(t, f2(-12582912.0f));
     const float2 r = __fadd2_rn(x, neg2(n));
-    float2 p = __ffma2_rn(f2(c0), r, f2(1.339887440266574e-3f));
-    p = __ffma2_rn(p, r, f2(9.618437357674640e-3f));
-    p = __ffma2_rn(p, r, f2(5.550332471162809e-2f));
-    p = __ffma2_rn(p, r, f2(2.402264791363012e-1f));
-    p = __ffma2_rn(p, r, f2(6.931472028550421e-1f));
+    float2 p = __ffma2_rn(f2(c0), r, f2(9.671507403254509e-3f));
+    p = __ffma2_rn(p, r, f2(5.550733208656311e-2f));
+    p = __ffma2_rn(p, r, f2(2.4022243916988373e-1f));
+    p = __ffma2_rn(p, r, f2(6.931470036506653e-1f));
     const float2 y = __ffma2_rn(p, r, f2(1.0f));
     const float2 sc = make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + 0x3F800000u),
                                   __uint_as_float((__float_as_uint(t.y) << 23) + 0x3F800000u));
@@ -128,7 +128,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     const int2 rg = a.tranges[V.trange_off + tile];
     const uint32_t* lst = a.tlists + V.tlist_off;
     const float4* recs = a.rec_sorted + 3 * V.cap_off;
-    // first Horner coefficient of s3r_exp2 (1.535336188319500e-4f), a kernel
+    // first Horner coefficient of s3r_exp2 (1.3264695880934596e-3f), a kernel
     // argument so it stays in a register (an immediate is re-materialised per use)
     const float c0 = a.exp2_c0;
 
@@ -254,7 +254,7 @@ void launch_raster(const RasterArgs& args, cudaStream_t st)
 {
     if (args.max_tiles == 0 || args.n_views == 0) return;
     RasterArgs a = args;
-    a.exp2_c0 = 1.535336188319500e-4f;
+    a.exp2_c0 = 1.3264695880934596e-3f;
     dim3 grid(a.max_tiles, a.n_views);
     if (a.evals) {
         if (a.train_T) k_raster<true, true><<<grid, RT, 0, st>>>(a);

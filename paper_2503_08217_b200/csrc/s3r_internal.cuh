@@ -281,7 +281,7 @@ struct RasterArgs {
     unsigned long long* evals;   // [n_views][2] (E_alg, E_exec) or NULL
     float* train_T;              // per pixel final T (training) or NULL, at V.pix_off
     int* train_n;                // per pixel blended list entries (training), at V.pix_off
-    float exp2_c0;               // 1.535336188319500e-4f (set by launch_raster)
+    float exp2_c0;               // 1.3264695880934596e-3f (set by launch_raster)
 };
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 

@@ -626,10 +626,11 @@ def test_f32_contract_tracks_f64_shadow():
 
 
 def test_exp2_contract():
-    """s3r_exp2 vs the exact 2^x: < 2 ulp on [-24, 0]; 2^0 = 1 and 2^-n exact; flush below -24."""
-    xs = np.float32(-np.linspace(0, 24, 24001))
+    """s3r_exp2 vs the exact 2^x: <= 2.02 ulp on [-24, 0]; 2^0 = 1 and 2^-n exact;
+    flush below -24."""
+    xs = np.float32(-np.linspace(0, 24, 240001))
     worst = 0.0
-    for x in xs[::7]:
+    for x in xs:
         got = np.float32(oracle.exp2_32(float(x)))
         want = 2.0 ** float(x)
         ulp = float(np.spacing(np.float32(want)))
