@@ -29,6 +29,9 @@
 namespace s3r {
 
 namespace {
+#ifndef S3R_K2_WARP_COMPACT
+#define S3R_K2_WARP_COMPACT 1
+#endif
 constexpr int PT = 256;
 constexpr int PR = 4;                 // rounds of PT entries per CTA
 constexpr int PTILE = PT * PR;
@@ -321,12 +324,17 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
     s.flags |= F_RENDERED;
 }
 
-__global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
+#ifndef S3R_K2_MINB
+#define S3R_K2_MINB 4     // 64 registers (A/B: K2 0.91 ms vs 1.03 at 3, 1.40 at 2)
+#endif
+__global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
 {
     extern __shared__ float s_tab[];          // [K1][12]
     __shared__ float s_bounds[4];
+#if !S3R_K2_WARP_COMPACT
     __shared__ uint32_t s_wcnt[PT / 32];
     __shared__ uint32_t s_base;
+#endif
     __shared__ unsigned long long s_red[6][PT / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -419,6 +427,17 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
                 a.dbg_rect[4 * di + 3] = (int16_t)(vis ? sp.ty1 : 0);
             }
         }
+#if S3R_K2_WARP_COMPACT
+        // ---- compaction: ballot/popc per warp, one atomic per warp-round (the
+        // record order is not needed: the depth sort restores (depth, index)) ----
+        const bool rend = (sp.flags & F_RENDERED) != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, rend);
+        unsigned long long wbase = 0;
+        if (bal) {
+            if (lane == 0) wbase = atomicAdd(&ctr->n_rendered, (unsigned long long)__popc(bal));
+            wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        }
+#else
         // ---- compaction: ballot/popc in the CTA, one atomic per CTA-round ----
         const bool rend = (sp.flags & F_RENDERED) != 0;
         const unsigned bal = __ballot_sync(0xffffffffu, rend);
@@ -438,8 +457,10 @@ __global__ void __launch_bounds__(PT, 3) k_project(ProjectArgs a)
                 s_base = tot ? (uint32_t)atomicAdd(&ctr->n_rendered, (unsigned long long)tot) : 0u;
         }
         __syncthreads();
+        const unsigned long long wbase = (unsigned long long)s_base + s_wcnt[warp];
+#endif
         if (rend) {
-            const long long o = cap_off + s_base + s_wcnt[warp] + __popc(bal & lt);
+            const long long o = cap_off + (long long)wbase + __popc(bal & lt);
             const uint32_t rx = (uint32_t)sp.tx0 | ((uint32_t)sp.tx1 << 16);
             const uint32_t ry = (uint32_t)sp.ty0 | ((uint32_t)sp.ty1 << 16);
             float4* r = a.rec + 3 * o;

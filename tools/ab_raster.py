@@ -36,6 +36,11 @@ VARIANT_SETS = {
         "base": [],
         "nocull": ["S3R_CULL=0"],
     },
+    "k2": {
+        "base": [],
+        "k2m5": ["S3R_K2_MINB=5"],
+        "k2m6": ["S3R_K2_MINB=6"],
+    },
     "fwd8": {
         "base": [],
         "f8m20": ["S3R_RASTER_RPIX=8", "S3R_RASTER_MINB=20"],
