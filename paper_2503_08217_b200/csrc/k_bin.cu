@@ -145,7 +145,10 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
 // kept), and appends them to the tile's list.  Tile t (local index in the
 // supertile, S*S of them) owns [S*S*start + t*len, +len) of the view's tile-list
 // area, len = supertile list length, so no count pass is needed.
-constexpr int XT = 512;
+#ifndef S3R_XT
+#define S3R_XT 256     // A/B: bin 1.21 ms vs 1.27 at 512, 1.40 at 128
+#endif
+constexpr int XT = S3R_XT;
 __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ views,
                                                    const uint2* __restrict__ rect_sorted,
                                                    const uint32_t* __restrict__ lists,

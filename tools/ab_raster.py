@@ -36,6 +36,11 @@ VARIANT_SETS = {
         "base": [],
         "nocull": ["S3R_CULL=0"],
     },
+    "xt": {
+        "base": [],
+        "xt256": ["S3R_XT=256"],
+        "xt128": ["S3R_XT=128"],
+    },
     "k2": {
         "base": [],
         "k2m5": ["S3R_K2_MINB=5"],
