@@ -39,7 +39,7 @@ namespace {
 #define S3R_BWD_MINB 20     // 96 registers at RPIX 8 (A/B: 37.1 ms; 16: 37.3, 24: 45.0)
 #endif
 #ifndef S3R_BWD_EX2
-#define S3R_BWD_EX2 1
+#define S3R_BWD_EX2 0   // 0: exact R-ARITH exp2 on pairs (A/B 35.9 ms); 1, 2: ex2.approx + re-decision (37.0, 36.6)
 #endif
 // pixels per thread; a tile is 256 pixels, so RT = 256 / RPIX threads, each
 // warp covering BW columns of the tile and 32 / BW rows per k step
@@ -85,6 +85,22 @@ __device__ __forceinline__ float warp_sum(float x)
 
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 __device__ __forceinline__ float2 neg2(float2 x) { return make_float2(-x.x, -x.y); }
+
+// s3r_exp2_b on a pair (component-wise the same operations; -24 <= x <= 0)
+__device__ __forceinline__ float2 s3r_exp2_pair(float2 x)
+{
+    const float2 t = __fadd2_rn(x, f2(12582912.0f));
+    const float2 n = __fadd2_rn(t, f2(-12582912.0f));
+    const float2 r = __fadd2_rn(x, neg2(n));
+    float2 p = __ffma2_rn(f2(1.3264695880934596e-3f), r, f2(9.671507403254509e-3f));
+    p = __ffma2_rn(p, r, f2(5.550733208656311e-2f));
+    p = __ffma2_rn(p, r, f2(2.4022243916988373e-1f));
+    p = __ffma2_rn(p, r, f2(6.931470036506653e-1f));
+    const float2 y = __ffma2_rn(p, r, f2(1.0f));
+    const float2 sc = make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + 0x3F800000u),
+                                  __uint_as_float((__float_as_uint(t.y) << 23) + 0x3F800000u));
+    return __fmul2_rn(y, sc);
+}
 
 // HAS_D / HAS_T: some view has a depth / final-T cotangent (otherwise those
 // terms are zero and compiled out)
@@ -205,7 +221,7 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 const bool okx = j < last[2 * P] && e2.x >= -24.0f;
                 const bool oky = j < last[2 * P + 1] && e2.y >= -24.0f;
                 if (!(okx || oky)) continue;
-#if S3R_BWD_EX2
+#if S3R_BWD_EX2 == 1
                 // hardware exp2 (rel. error ~2^-22); the forward's clamp decision
                 // (o G < 0.99) is re-taken with the exact R-ARITH exp2 whenever
                 // the approximate product lies within 1e-5 of the threshold
@@ -219,8 +235,18 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                     G.y = s3r_exp2_b(e2.y);
                     og.y = q0.w * G.y;
                 }
+#elif S3R_BWD_EX2 == 2
+                // as 1, one branch for the pair
+                float2 G = make_float2(ex2_approx(e2.x), ex2_approx(e2.y));
+                float2 og = __fmul2_rn(f2(q0.w), G);
+                const float2 dd = __fadd2_rn(og, f2(-0.99f));
+                if (fminf(fabsf(dd.x), fabsf(dd.y)) < 1e-5f) {
+                    G = s3r_exp2_pair(e2);
+                    og = __fmul2_rn(f2(q0.w), G);
+                }
 #else
-                const float2 G = make_float2(s3r_exp2_b(e2.x), s3r_exp2_b(e2.y));
+                // the exact R-ARITH exp2 on the pair (the forward's values)
+                const float2 G = s3r_exp2_pair(e2);
                 const float2 og = __fmul2_rn(f2(q0.w), G);
 #endif
                 // a pixel of the pair that is not ok gets alpha = 0: T, R and the

@@ -36,6 +36,11 @@ VARIANT_SETS = {
         "base": [],
         "nocull": ["S3R_CULL=0"],
     },
+    "bex": {
+        "base": [],
+        "ex2pair": ["S3R_BWD_EX2=2"],
+        "exact": ["S3R_BWD_EX2=0"],
+    },
     "xt": {
         "base": [],
         "xt256": ["S3R_XT=256"],
