@@ -373,6 +373,39 @@ def test_invalid_arguments(ctx):
     bad = sg.View(**{**views[0].__dict__, "width": 0})
     with pytest.raises(s3r.S3RError):
         ctx.render_batch(ds, [bad], [tabs[0]], outs)
+    # mode setters: unknown pipeline, non-finite offset, bad NeurF parameters
+    with pytest.raises(s3r.S3RError) as e:
+        ctx._check(ctx.L.s3r_set_pipeline(ctx.h, 7))
+    assert e.value.code == s3r.S3R_EINVAL
+    with pytest.raises(s3r.S3RError):
+        ctx.set_lod_jitter(float("nan"), 0.0, 0.0)
+    from oracle import neurf
+    prm = neurf.random_params(np.random.default_rng(0), scene.num_instances)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in prm.items()
+           if isinstance(v, np.ndarray)}
+    with pytest.raises(s3r.S3RError):
+        ctx.set_neural_colors(dict(dev, pos_scale=-1.0))
+    # a class table with fewer rows than the scene's instances is refused at render
+    if scene.num_instances > 1:
+        ctx.set_neural_colors(dict(dev, class_emb=dev["class_emb"][:1].contiguous(),
+                                   pos_scale=10.0))
+        try:
+            with pytest.raises(s3r.S3RError):
+                ctx.render_batch(ds, views, list(tabs), outs)
+        finally:
+            ctx.set_neural_colors(None)
+    # backward is refused after a render that used the noisy offset / NeurF
+    ctx.set_training(True)
+    try:
+        ctx.set_lod_jitter(0.1, 0.1, 0.1)
+        ctx.render_batch(ds, views, list(tabs), outs)
+        cots = [{"rgb": torch.zeros_like(outs[0]["rgb"])}]
+        with pytest.raises(s3r.S3RError) as e:
+            ctx.render_backward(ds, views, list(tabs), cots, _grads_like(ds))
+        assert e.value.code == s3r.S3R_ESTATE
+    finally:
+        ctx.set_lod_jitter(0.0, 0.0, 0.0)
+        ctx.set_training(False)
 
 
 @pytest.mark.slow
