@@ -297,13 +297,16 @@ def run_neurf(args, ctx, ds, scene, views, tables, outs, world, dev, stream, pea
                          "alg_bytes_per_launch": 32 * rows}}
 
 
-def load_traffic(kernel):
+def load_traffic(kernel, workload):
     """DRAM bytes per launch of `kernel` from the committed ncu capture of this
-    bench command (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    bench command (profiles/ncu_traffic.json, written by tools/ncu_traffic.py);
+    None unless the capture ran the same workload."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)[kernel]
+        if d.get("workload", "av2") != workload:
+            return None, None
         return d["dram_bytes_per_launch"], d["source"]
     except (OSError, KeyError, ValueError):
         return None, None
@@ -527,7 +530,7 @@ def main():
                 "unit": "TFLOP/s", "frac": ach / alu_peak,
                 "peak_source": f"148 SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (B200_PROFILING.md unit counts)",
                 "alg_flops_per_launch": FLOPS_PER_EVAL * E_alg, "traffic": None}
-        tr, tr_src = load_traffic("k_raster<0,0>")
+        tr, tr_src = load_traffic("k_raster<0,0>", args.config)
         if tr is not None:
             roof["traffic"] = tr
             roof["traffic_source"] = f"{tr_src} (ncu --set full, one launch of this command)"
