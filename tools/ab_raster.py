@@ -36,6 +36,10 @@ VARIANT_SETS = {
         "base": [],
         "nocull": ["S3R_CULL=0"],
     },
+    "clist": {
+        "base": [],
+        "noclist": ["S3R_RASTER_CLIST=0"],
+    },
     "bex": {
         "base": [],
         "ex2pair": ["S3R_BWD_EX2=2"],
