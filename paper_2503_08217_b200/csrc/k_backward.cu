@@ -47,7 +47,9 @@ constexpr int RPIX = S3R_BWD_RPIX;
 constexpr int RT = TILE * TILE / RPIX;
 constexpr int BW = TILE / (RT / 32);
 constexpr int RB = 256;
+constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 
+#if S3R_BWD_EX2
 __device__ __forceinline__ float s3r_exp2_b(float x)
 {
     const float t = x + 12582912.0f;
@@ -61,6 +63,7 @@ __device__ __forceinline__ float s3r_exp2_b(float x)
     const float y = __fmaf_rn(p, r, 1.0f);
     return y * __uint_as_float((__float_as_uint(t) << 23) + 0x3F800000u);
 }
+#endif
 
 __device__ __forceinline__ float rcp_approx(float x)
 {
@@ -69,12 +72,14 @@ __device__ __forceinline__ float rcp_approx(float x)
     return y;
 }
 
+#if S3R_BWD_EX2
 __device__ __forceinline__ float ex2_approx(float x)
 {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+#endif
 
 __device__ __forceinline__ float warp_sum(float x)
 {
@@ -108,13 +113,14 @@ template <bool HAS_D, bool HAS_T>
 __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
 {
     __shared__ float4 s_rec[3 * RB];
-    __shared__ float s_hx[RB];
+    __shared__ uint8_t s_cl[NW][RB];   // per warp block: staged records reaching it
+    __shared__ int s_wc[NW][NW];       // [staging warp][warp block] kept counts
     __shared__ int s_max;
     const int v = blockIdx.y;
     const DevView& V = a.views[v];
     const int tile = blockIdx.x;
     if (tile >= V.ntiles) return;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tx = tile % V.TX, ty = tile / V.TX;
     const int px = tx * TILE + (tid >> 5) * BW + (lane % BW);
     const int py0 = ty * TILE + (lane / BW);
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     // adds the difference)
     static_assert(TILE == 16 && BW >= 8, "cull extents assume >= 8 x 16 warp blocks");
     constexpr float XPAD = 0.5f * (BW - 1) - CULL_HALF_BX;
-    const float bcx = (float)(tx * TILE + (tid >> 5) * BW) + 0.5f * (BW - 1);
+    const float bcx0 = (float)(tx * TILE) + 0.5f * (BW - 1);     // warp block 0
     const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
     const s3r_cot C = a.cots[v];
     // the thread's 4 pixels (rows py0 + 4k) as 2 packed pairs: pair P holds
@@ -179,25 +185,58 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
         const int lo = max(0, hi - RB);
         const int nb = hi - lo;
         __syncthreads();
-        for (int i = tid; i < nb; i += RT) {
-            const uint32_t e = lst[rg.x + lo + i];
-            const float4* src = recs + 3ll * e;
-            s_rec[3 * i + 0] = src[0];
-            float4 r1 = src[1], r2 = src[2];
-            s_hx[i] = r1.w;                       // flush half extent x
-            r1.w = __uint_as_float(e);            // list entry, for the atomics
-            s_rec[3 * i + 1] = r1;
-            s_rec[3 * i + 2] = r2;
+        // stage the batch and, per warp block, the order-preserving list of the
+        // records whose flush ellipse reaches it (the others were flushed on
+        // every pixel of the block in the forward: nothing to differentiate)
+        int run[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) run[w] = 0;
+        for (int base = 0; base < nb; base += RT) {
+            const int i = base + tid;
+            bool keep[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) keep[w] = false;
+            if (i < nb) {
+                const uint32_t e = lst[rg.x + lo + i];
+                const float4* src = recs + 3ll * e;
+                const float4 r0 = src[0];
+                float4 r1 = src[1];
+                const float4 r2 = src[2];
+                const float hx = XPAD != 0.0f ? r1.w + XPAD : r1.w;
+                const bool yok = !S3R_CULL || !(fabsf(r0.y - bcy) > r2.w);
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    keep[w] = yok && (!S3R_CULL || !(fabsf(r0.x - (bcx0 + (float)(w * BW))) > hx));
+                r1.w = __uint_as_float(e);            // list entry, for the atomics
+                s_rec[3 * i + 0] = r0;
+                s_rec[3 * i + 1] = r1;
+                s_rec[3 * i + 2] = r2;
+            }
+            unsigned bal[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                bal[w] = __ballot_sync(0xffffffffu, keep[w]);
+                if (lane == 0) s_wc[warp][w] = __popc(bal[w]);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                int off = run[w], tot = 0;
+#pragma unroll
+                for (int sw = 0; sw < NW; ++sw) {
+                    const int c = s_wc[sw][w];
+                    if (sw < warp) off += c;
+                    tot += c;
+                }
+                if (keep[w]) s_cl[w][off + __popc(bal[w] & ((1u << lane) - 1u))] = (uint8_t)i;
+                run[w] += tot;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        for (int jj = nb - 1; jj >= 0; --jj) {
+        for (int kk = run[warp] - 1; kk >= 0; --kk) {
+            const int jj = s_cl[warp][kk];
             const int j = lo + jj;
             const float4 q0 = s_rec[3 * jj], q1 = s_rec[3 * jj + 1], q2 = s_rec[3 * jj + 2];
-            // no evaluation of the warp's block passes the forward's flush test
-            // (s3r_internal.cuh flush_extent): nothing to differentiate
-            if (S3R_CULL && (fabsf(q0.x - bcx) > (XPAD != 0.0f ? s_hx[jj] + XPAD : s_hx[jj]) ||
-                             fabsf(q0.y - bcy) > q2.w))
-                continue;
             const float dx = q0.x - fpx;
             const float a1 = q1.x * dx;
             const float a2 = a1 * dx;
