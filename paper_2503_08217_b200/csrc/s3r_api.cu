@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/s3r.h"
 #include "s3r_internal.cuh"
 
@@ -171,8 +173,13 @@ void* stage_alloc(s3r_ctx* c, size_t bytes)
 
 int* next_ticket(s3r_ctx* c) { return P<int>(c->d_ticket) + (c->ticket_slot++); }
 
+// NVTX range per stage (host-side enqueue span; free without a tool attached)
+const char* const kStageName[S3R_NUM_STAGES] = {"s3r.filter", "s3r.project", "s3r.depth_sort",
+                                                "s3r.bin", "s3r.raster", "s3r.color"};
+
 void ev_begin(s3r_ctx* c, int stage, cudaStream_t st, StageEvent& e)
 {
+    nvtxRangePushA(kStageName[stage]);
     e.stage = -1;
     if (!c->timing) return;
     if (c->ev.size() > 200000) return;
@@ -183,6 +190,7 @@ void ev_begin(s3r_ctx* c, int stage, cudaStream_t st, StageEvent& e)
 }
 void ev_end(s3r_ctx* c, cudaStream_t st, StageEvent& e)
 {
+    nvtxRangePop();
     if (e.stage < 0) return;
     cudaEventRecord(e.b, st);
     c->ev.push_back(e);

@@ -541,3 +541,57 @@ def test_training_step_mse_street(ctx):
         oracle.backward(scene, v, c["rgb"].cpu().numpy().astype(np.float64), table=t.cpu().numpy(),
                         grads=g_ref)
     _check_grads(g_gpu, g_ref)
+
+
+def test_run_to_run_determinism(ctx):
+    """the output does not depend on scheduling — two renders of the
+    same batch (atomic, unordered compaction inside) are bit-identical."""
+    scene, views = sg.make_random_dynamic(21, 6000, 3, 400, 190, 133, 6, lod=(3.0, 0.5, 12.0))
+    ds1, tabs, o1, _ = gpu_render(ctx, scene, views)
+    ds2, _, o2, _ = gpu_render(ctx, scene, views)
+    for a, b in zip(o1, o2):
+        for k in ("rgb", "depth", "final_T", "visible"):
+            assert torch.equal(a[k], b[k])
+    assert torch.equal(ds1.life, ds2.life)
+
+
+@pytest.mark.slow
+def test_scaling_acceptance():
+    """S:642 / S:682 acceptance 4 (the qualitative Fig.4 claim): with
+    the scene 8x longer (8x the Gaussians) the conventional pipeline's per-view
+    time grows >= 3x while the streamlined one's stays <= 1.5x.  C3 rig and
+    density at 960x640 images, 24 views per length."""
+    import dataclasses
+    c = s3r.Context(0)
+    try:
+        base = sg.CONFIGS["av2"]
+        res = {}
+        for f in (1, 8):
+            L = 100.0 * f
+            cfg = dataclasses.replace(base, n_static=int(base.n_static * L / base.length_m),
+                                      n_objects=max(1, int(round(base.n_objects * L / base.length_m))),
+                                      frames=max(8, int(base.frames * L / base.length_m)),
+                                      length_m=L, width=960, height=640, focal=1050.0, n_views=24)
+            scene, traj = sg.make_street_scene(cfg)
+            views = sg.make_views(cfg, traj, n_views=24, seed=3)
+            ds = s3r.DeviceScene.from_numpy(scene)
+            outs = s3r.alloc_outputs(views, depth=False, final_T=False)
+            for conv in (False, True):
+                tabs = list(s3r.conventional_tables(views) if conv else s3r.view_tables(c, views))
+                c.set_pipeline(conv)
+                c.render_batch(ds, views, tabs, outs)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(3):
+                    c.render_batch(ds, views, tabs, outs)
+                b.record()
+                torch.cuda.synchronize()
+                res[(f, conv)] = a.elapsed_time(b) / 3
+            c.set_pipeline(False)
+        s_ratio = res[(8, False)] / res[(1, False)]
+        c_ratio = res[(8, True)] / res[(1, True)]
+        print("streamlined x%.2f, conventional x%.2f" % (s_ratio, c_ratio))
+        assert s_ratio <= 1.5 and c_ratio >= 3.0, res
+    finally:
+        c.close()
