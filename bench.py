@@ -490,10 +490,15 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in evs)
     st_times = ctx.stage_times()
     ctx.set_timing(False)
+    rank_ms = {"max": ms / args.steps, "mean": ms / args.steps, "min": ms / args.steps}
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        # load balance over ranks (front vs side cameras, near vs far content):
+        # every rank's step time; `value` uses the max (the job's time)
+        allt = [torch.zeros(1, device=dev, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allt, torch.tensor([ms], device=dev, dtype=torch.float64))
+        per = [float(x.item()) / args.steps for x in allt]
+        rank_ms = {"max": max(per), "mean": sum(per) / world, "min": min(per)}
+        ms = max(per) * args.steps
         dist.barrier()
     views_per_step = len(pools[0])
     value = views_per_step * world * args.steps / (ms / 1e3)
@@ -618,6 +623,7 @@ def main():
             "gaussians_per_s": n_scene * value,
             "processed_gaussians_per_s": sum(s["n_temporal"] for s in stats) * world * value / views_per_step,
             "clocks": clocks,
+            "rank_ms_per_step": rank_ms,
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof,
             "stages": stages,
