@@ -45,6 +45,9 @@ constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 #ifndef S3R_RASTER_CLIST
 #define S3R_RASTER_CLIST 1
 #endif
+#ifndef S3R_RASTER_PMASK
+#define S3R_RASTER_PMASK 0   // per-pair-block skip (A/B: 15.59 vs 15.14 ms without)
+#endif
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
 // Build-time variants (for A/B measurement; the defaults are the product):
@@ -95,7 +98,8 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
 #if S3R_RASTER_CLIST
-    __shared__ uint8_t s_cl[NW][RB];   // per warp block: staged records reaching it
+    __shared__ uint16_t s_cl[NW][RB];  // per warp block: staged records reaching it
+                                       // (index | pair-block mask << 8)
     __shared__ int s_wc[NW][NW];       // [staging warp][warp block] kept counts
 #endif
     const int v = blockIdx.y;
@@ -164,6 +168,10 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
         for (int base = 0; base < nb; base += RT) {
             const int i = base + tid;
             bool keep[NW];
+            unsigned pmask = (1u << NP) - 1u;
+#if S3R_RASTER_PMASK
+            pmask = 0;
+#endif
 #pragma unroll
             for (int w = 0; w < NW; ++w) keep[w] = false;
             if (i < nb) {
@@ -177,6 +185,15 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
                     keep[w] = yok && !(fabsf(q0.x - (bcx0 + (float)(w * BW))) > hx);
+#if S3R_RASTER_PMASK
+                // pair P covers the tile rows 2 RS P .. 2 RS P + 2 RS - 1
+#pragma unroll
+                for (int P = 0; P < NP; ++P) {
+                    const float cy = (float)(ty * TILE + 2 * RS * P) + 0.5f * (2 * RS - 1);
+                    if (!(fabsf(q0.y - cy) > q2.w - (CULL_HALF_BY - 0.5f * (2 * RS - 1))))
+                        pmask |= 1u << P;
+                }
+#endif
             }
             unsigned bal[NW];
 #pragma unroll
@@ -194,7 +211,8 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                     if (sw < warp) off += c;
                     tot += c;
                 }
-                if (keep[w]) s_cl[w][off + __popc(bal[w] & ((1u << lane) - 1u))] = (uint8_t)i;
+                if (keep[w])
+                    s_cl[w][off + __popc(bal[w] & ((1u << lane) - 1u))] = (uint16_t)(i | (pmask << 8));
                 run[w] += tot;
             }
             __syncthreads();
@@ -216,7 +234,9 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
         if (__any_sync(0xffffffffu, nlive != 0)) {
 #if S3R_RASTER_CLIST
             for (int jj = 0; jj < nk; ++jj) {
-                const int j = s_cl[warp][jj];
+                const unsigned ent = s_cl[warp][jj];
+                const int j = ent & 0xff;
+                const unsigned pm = ent >> 8;
 #else
             for (int j = 0; j < nb; ++j) {
 #endif
@@ -240,6 +260,9 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                 const float b1 = q1.y * dx;
 #pragma unroll
                 for (int P = 0; P < NP; ++P) {
+#if S3R_RASTER_CLIST && S3R_RASTER_PMASK
+                    if (!(pm & (1u << P))) continue;     // the pair block is all flushed
+#endif
                     const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
                     const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
                     const float2 e2r = __ffma2_rn(dy, c1, f2(a2));

@@ -38,7 +38,7 @@ VARIANT_SETS = {
     },
     "clist": {
         "base": [],
-        "noclist": ["S3R_RASTER_CLIST=0"],
+        "nopmask": ["S3R_RASTER_PMASK=0"],
     },
     "bex": {
         "base": [],
