@@ -62,7 +62,7 @@ class Stats(C.Structure):
 class Out(C.Structure):
     _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("final_T", C.c_void_p),
                 ("visible", C.c_void_p), ("temporal_idx", C.c_void_p), ("keys", C.c_void_p),
-                ("splat_mz", C.c_void_p), ("flags", C.c_void_p), ("rect", C.c_void_p), ("pair_tile", C.c_void_p),
+                ("splat_keys", C.c_void_p), ("flags", C.c_void_p), ("rect", C.c_void_p), ("pair_tile", C.c_void_p),
                 ("pair_gauss", C.c_void_p), ("pair_capacity", C.c_int64),
                 ("ranges", C.c_void_p), ("stats", Stats)]
 
@@ -168,7 +168,7 @@ def render_view(scene, view, precision: str = "f32", table: Optional[np.ndarray]
     TX, TY = (W + TILE - 1) // TILE, (H + TILE - 1) // TILE
     o = {
         "visible": np.zeros(N, np.uint8), "temporal_idx": np.zeros(max(N, 1), np.int32),
-        "keys": np.zeros((N, 6), real), "splat_mz": np.full((N, 3), np.nan, real),
+        "keys": np.zeros((N, 6), real), "splat_keys": np.full((N, 6), np.nan, real),
         "flags": np.zeros(N, np.uint8),
         "rect": np.zeros((N, 4), np.int16), "ranges": np.zeros((TX * TY, 2), np.int32),
     }
@@ -176,7 +176,7 @@ def render_view(scene, view, precision: str = "f32", table: Optional[np.ndarray]
         o.update(rgb=np.zeros((H, W, 3), real), depth=np.zeros((H, W), real),
                  final_T=np.zeros((H, W), real))
     out = Out()
-    for k in ("rgb", "depth", "final_T", "visible", "temporal_idx", "keys", "splat_mz", "flags",
+    for k in ("rgb", "depth", "final_T", "visible", "temporal_idx", "keys", "splat_keys", "flags",
               "rect", "ranges"):
         if k in o:
             setattr(out, k, _ptr(o[k]))

@@ -83,7 +83,7 @@ typedef struct {
         uint8_t* visible;     /* [n]  M_t  */                                   \
         int32_t* temporal_idx;/* [n]  ascending indices passing the filter */   \
         REAL* keys;           /* [n][6] mx,my,z,a,b,c (only temporal ones) */   \
-        REAL* splat_mz;       /* [n][3] mx,my,z of the rendered splat      */   \
+        REAL* splat_keys;     /* [n][6] keys of the rendered splat (moved) */   \
         uint8_t* flags;       /* [n]  SO_F_* */                                 \
         int16_t* rect;        /* [n][4] tx0,tx1,ty0,ty1 (visible ones) */       \
         int32_t* pair_tile;   /* [pair_capacity] sorted pairs: tile id */       \

@@ -61,7 +61,7 @@ static void rotmat(double w, double x, double y, double z, double R[9])
 /* Projection adjoint of Gaussian g in view v: from the splat's accumulated
  * (gmx, gmy, gz, gA, gB, gC) to mean, scales and quaternion. */
 static void project_adjoint(const so_scene* s, const so_view* v, int64_t g, const bw_splat* sp,
-                            double* out, double* gtab)
+                            const double* key, int jittered, double* out, double* gtab)
 {
     const int32_t id = s->instance_ids[g];
     const float* Mf = v->instance_w2c + 12 * (int64_t)id;
@@ -70,8 +70,18 @@ static void project_adjoint(const so_scene* s, const so_view* v, int64_t g, cons
         for (int c = 0; c < 3; ++c) Wr[3 * r + c] = Mf[4 * r + c];
         t[r] = Mf[4 * r + 3];
     }
-    const double mu[3] = {s->means_opacity[4 * g], s->means_opacity[4 * g + 1],
-                          s->means_opacity[4 * g + 2]};
+    double mu[3] = {s->means_opacity[4 * g], s->means_opacity[4 * g + 1],
+                    s->means_opacity[4 * g + 2]};
+    if (jittered) {
+        /* the splat was rendered from the mean moved by the LOD noisy offset
+         * (NEXT-3, as in the forward); reading R23: the offset is a constant of
+         * the backward (stop-gradient through the noise and its depth scale), so
+         * dL/dmu = dL/dmu_moved and the projection adjoint runs at mu_moved */
+        float nz[3];
+        so_lod_normal3(v->lod_seed, g, nz);
+        const double nd = fmin(1.0, key[2] / (double)v->lod_D);
+        for (int a = 0; a < 3; ++a) mu[a] = fma((double)v->lod_jitter[a] * nd, (double)nz[a], mu[a]);
+    }
     double p[3];
     for (int r = 0; r < 3; ++r) p[r] = Wr[3 * r] * mu[0] + Wr[3 * r + 1] * mu[1] + Wr[3 * r + 2] * mu[2] + t[r];
     const double qr[4] = {s->rotations[4 * g], s->rotations[4 * g + 1], s->rotations[4 * g + 2],
@@ -195,9 +205,11 @@ int so_backward_f64(const so_scene* s, const so_view* v, const double* g_rgb,
     so_out_f64 o;
     memset(&o, 0, sizeof(o));
     double* keys = (double*)malloc((size_t)(n > 0 ? n : 1) * 6 * sizeof(double));
+    double* skeys = (double*)malloc((size_t)(n > 0 ? n : 1) * 6 * sizeof(double));
     uint8_t* flags = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
     int16_t* rect = (int16_t*)calloc((size_t)(n > 0 ? n : 1) * 4, sizeof(int16_t));
     o.keys = keys;
+    o.splat_keys = skeys;
     o.flags = flags;
     o.rect = rect;
     so_render_view_f64(s, v, &o);            /* forward decisions (f64 shadow) */
@@ -206,7 +218,7 @@ int so_backward_f64(const so_scene* s, const so_view* v, const double* g_rgb,
     int64_t npairs = 0;
     for (int64_t g = 0; g < n; ++g) {
         if (!(flags[g] & SO_F_RENDERED)) continue;
-        const double* k = keys + 6 * g;
+        const double* k = skeys + 6 * g;            /* the rendered splat (moved mean) */
         const double ad = k[3] + 0.3, cd = k[5] + 0.3, det = ad * cd - k[4] * k[4];
         bw_splat* q = &sp[g];
         q->mx = k[0]; q->my = k[1]; q->z = k[2];
@@ -284,9 +296,11 @@ int so_backward_f64(const so_scene* s, const so_view* v, const double* g_rgb,
         }
     }
     for (int64_t g = 0; g < n; ++g)
-        if (flags[g] & SO_F_RENDERED) project_adjoint(s, v, g, &sp[g], grads + 16 * g, g_table);
+        if (flags[g] & SO_F_RENDERED)
+            project_adjoint(s, v, g, &sp[g], keys + 6 * g, (flags[g] & SO_F_JITTERED) != 0,
+                            grads + 16 * g, g_table);
 
     free(pw); free(Tk); free(al); free(start); free(pairs); free(sp);
-    free(rect); free(flags); free(keys);
+    free(rect); free(flags); free(keys); free(skeys);
     return 0;
 }

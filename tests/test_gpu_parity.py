@@ -64,7 +64,7 @@ def check_view(ctx, scene, view, table, out, vi, exact=True, o=None, img_tol=IMG
         assert np.array_equal(out["visible"].cpu().numpy(), o["visible"])
     # depth order of rendered Gaussians: (z, index)
     rend = np.nonzero(o["flags"] & oracle.F_RENDERED)[0]
-    want_order = rend[np.lexsort((rend, o["splat_mz"][rend, 2]))]
+    want_order = rend[np.lexsort((rend, o["splat_keys"][rend, 2]))]
     assert np.array_equal(d["depth_order"], want_order)
     # K3-K6: pair list and ranges
     assert np.array_equal(d["pair_tile"], o["pair_tile"])
