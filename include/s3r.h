@@ -273,8 +273,9 @@ int s3r_set_pipeline(s3r_ctx* ctx, int pipeline);
  * projected again: its splat, depth key and tile rectangle come from the moved
  * mean (it is not rendered if that leaves the frustum); M_t, the small set and
  * the drop set come from the original one.  (0, 0, 0) = off (the default).
- * Ignored by the conventional pipeline (no LOD); s3r_render_backward refuses
- * (S3R_ESTATE) a render made with it.  S3R_EINVAL if non-finite.            */
+ * Ignored by the conventional pipeline (no LOD).  s3r_render_backward of a
+ * training render made with it differentiates at the moved means, the offset
+ * being a constant (reading R23).  S3R_EINVAL if non-finite.                */
 int s3r_set_lod_jitter(s3r_ctx* ctx, float dx, float dy, float dz);
 
 /* NeurF colour query (Eq.7 rows 5-6; NEXT-4): with it enabled the

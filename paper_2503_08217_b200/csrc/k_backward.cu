@@ -379,7 +379,15 @@ __device__ __forceinline__ int project_bwd_one(const BackwardArgs& a, const DevV
     const long long g = (long long)(a.dkey_sorted[V.cap_off + r] & a.gmask);
     const int id = a.ids[g];
     const float* M = V.table + 12 * id;
-    const float4 mo = a.means_opacity[g], sc = a.scales[g], qq = a.rotations[g];
+    float4 mo = a.means_opacity[g];
+    const float4 sc = a.scales[g], qq = a.rotations[g];
+    if (a.rec_mu) {
+        // rendered from the mean moved by the LOD noisy offset (NEXT-3): the
+        // adjoint runs there; the offset is a constant (reading R23), so the
+        // mean gradient is the moved mean's
+        const float4 m = a.rec_mu[V.cap_off + a.order[V.cap_off + r]];
+        mo.x = m.x; mo.y = m.y; mo.z = m.z;
+    }
     float p[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) p[i] = M[4 * i] * mo.x + M[4 * i + 1] * mo.y + M[4 * i + 2] * mo.z + M[4 * i + 3];

@@ -236,7 +236,9 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
             for (int jj = 0; jj < nk; ++jj) {
                 const unsigned ent = s_cl[warp][jj];
                 const int j = ent & 0xff;
+#if S3R_RASTER_PMASK
                 const unsigned pm = ent >> 8;
+#endif
 #else
             for (int j = 0; j < nb; ++j) {
 #endif

@@ -44,7 +44,7 @@ struct s3r_ctx {
     bool debug = false, timing = false, counters = false, training = false;
     int pipeline = S3R_PIPELINE_STREAMLINED, last_pipeline = S3R_PIPELINE_STREAMLINED;
     float lod_jitter[3] = {0.0f, 0.0f, 0.0f};   // NEXT-3 noisy offset scale
-    bool last_jitter = false;
+    bool last_jitter = false, last_recmu = false;
     // NEXT-4 NeurF colour query
     bool neurf = false, last_neurf = false;
     Buf d_nw, d_nb, d_temb, d_cemb, d_recmu, d_toff;
@@ -384,7 +384,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if ((rc = ensure(c, c->d_rec, (size_t)capS * 48))) return rc;
     if ((rc = ensure(c, c->d_dkey, (size_t)capS * 8))) return rc;
     if (c->debug && (rc = ensure(c, c->d_gidx, (size_t)capS * 4))) return rc;
-    if (neurf && (rc = ensure(c, c->d_recmu, (size_t)capS * 16))) return rc;
+    // per-record own-frame means: the NeurF query, and the backward of a
+    // training render under the noisy offset (the projection adjoint runs at the
+    // moved mean)
+    const bool want_mu = neurf || (c->training && c->last_jitter);
+    c->last_recmu = want_mu;
+    if (want_mu && (rc = ensure(c, c->d_recmu, (size_t)capS * 16))) return rc;
     if (c->debug) {
         if ((rc = ensure(c, c->d_dbg_keys, (size_t)capS * 24))) return rc;
         if ((rc = ensure(c, c->d_dbg_flags, (size_t)capS))) return rc;
@@ -416,7 +421,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         ProjectArgs a{};
         a.world_mo = conv ? P<float4>(c->d_wmo) : nullptr;
         a.world_rot = conv ? P<float4>(c->d_wrot) : nullptr;
-        a.rec_mu = neurf ? P<float4>(c->d_recmu) : nullptr;
+        a.rec_mu = want_mu ? P<float4>(c->d_recmu) : nullptr;
         a.means_opacity = reinterpret_cast<const float4*>(sc->means_opacity);
         a.scales = reinterpret_cast<const float4*>(sc->scales);
         a.rotations = reinterpret_cast<const float4*>(sc->rotations);
@@ -1075,8 +1080,6 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
         return fail(c, S3R_ESTATE, "backward: no training forward (s3r_set_training(1) + render)");
     if (c->last_pipeline != S3R_PIPELINE_STREAMLINED)
         return fail(c, S3R_ESTATE, "backward: the last render used the conventional pipeline");
-    if (c->last_jitter)
-        return fail(c, S3R_ESTATE, "backward: the last render used the LOD noisy offset");
     if (c->last_neurf)
         return fail(c, S3R_ESTATE, "backward: the last render used NeurF colours");
     if (nv != c->last_nviews || sc->n != c->last_N)
@@ -1115,6 +1118,9 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
     a.train_n = P<int>(c->d_train_n);
     a.splat_grads = P<float>(c->d_sgrads);
     a.dkey_sorted = P<unsigned long long>(c->d_sortk[c->final_order]);
+    // noisy offset: the splats' moved means by compacted slot, and rank -> slot
+    a.rec_mu = c->last_jitter && c->last_recmu ? P<float4>(c->d_recmu) : nullptr;
+    a.order = P<uint32_t>(c->d_sortv[c->final_order]);
     a.gmask = (1ull << c->gbits) - 1ull;
     a.ids = sc->instance_ids;
     a.means_opacity = reinterpret_cast<const float4*>(sc->means_opacity);

@@ -315,6 +315,8 @@ struct BackwardArgs {
     int num_instances;
     int smem_table;                      // accumulate g_table per CTA in shared memory
     int has_depth_cot, has_T_cot;        // some view has a depth / final_T cotangent
+    const float4* rec_mu;                // [cap] moved own-frame means (noisy offset) or NULL
+    const uint32_t* order;               // [cap] depth rank -> compacted slot
 };
 void launch_backward(const BackwardArgs& a, int max_tiles, long long max_rendered, cudaStream_t st);
 void launch_mse(const float* x, const float* y, long long n, float scale, float* grad,

@@ -394,17 +394,17 @@ def test_invalid_arguments(ctx):
                 ctx.render_batch(ds, views, list(tabs), outs)
         finally:
             ctx.set_neural_colors(None)
-    # backward is refused after a render that used the noisy offset / NeurF
+    # backward is refused after a render that used NeurF colours
     ctx.set_training(True)
     try:
-        ctx.set_lod_jitter(0.1, 0.1, 0.1)
+        ctx.set_neural_colors(dict(dev, pos_scale=10.0))
         ctx.render_batch(ds, views, list(tabs), outs)
         cots = [{"rgb": torch.zeros_like(outs[0]["rgb"])}]
         with pytest.raises(s3r.S3RError) as e:
             ctx.render_backward(ds, views, list(tabs), cots, _grads_like(ds))
         assert e.value.code == s3r.S3R_ESTATE
     finally:
-        ctx.set_lod_jitter(0.0, 0.0, 0.0)
+        ctx.set_neural_colors(None)
         ctx.set_training(False)
 
 
@@ -504,6 +504,31 @@ def test_mse_ragged(ctx, n, off):
     assert torch.equal(grad.cpu(), (2 * s * (x - y)).cpu())
     want = 0.5 + s * float(((xd - yd) ** 2).sum())
     assert abs(float(loss) - want) <= 1e-5 * want
+
+
+def test_backward_with_noisy_offset(ctx):
+    """Backward of a training render with the LOD noisy offset on (the splats of
+    kept small Gaussians moved; reading R23: the offset is a constant of the
+    backward) vs the oracle's adjoint, 1e-3 gate."""
+    scene, views = sg.make_random_dynamic(4, 1500, 3, 150, 131, 97, 3, lod=(6.0, 0.4, 8.0))
+    rng = np.random.default_rng(4)
+    cot = [{"rgb": rng.standard_normal((v.height, v.width, 3))} for v in views]
+    jit = (0.05, 0.05, 0.1)
+    ctx.set_lod_jitter(*jit)
+    try:
+        g_gpu, tabs = _gpu_backward(ctx, scene, views, cot)
+    finally:
+        ctx.set_lod_jitter(0.0, 0.0, 0.0)
+    import dataclasses
+    g_ref = np.zeros((scene.n, 16))
+    n_jit = 0
+    for v, t, c in zip(views, tabs, cot):
+        vj = dataclasses.replace(v, lod_jitter=jit)
+        oracle.backward(scene, vj, c["rgb"], table=t.cpu().numpy(), grads=g_ref)
+        o = oracle.render_view(scene, vj, "f32", table=t.cpu().numpy(), pairs=False, image=False)
+        n_jit += int(np.count_nonzero(o["flags"] & oracle.F_JITTERED))
+    assert n_jit > 50
+    _check_grads(g_gpu, g_ref)
 
 
 def test_training_step_mse_street(ctx):
