@@ -746,15 +746,18 @@ int s3r_get_stage_times(s3r_ctx* c, double* out_ms, int64_t* out_count)
 {
     if (!c) return S3R_EINVAL;
     CU(cudaSetDevice(c->device));
-    for (auto& e : c->ev) {
-        CU(cudaEventSynchronize(e.b));
+    cudaError_t err = cudaSuccess;
+    for (auto& e : c->ev) {       // every event is consumed (and destroyed) once
         float ms = 0;
-        CU(cudaEventElapsedTime(&ms, e.a, e.b));
-        c->stage_ms[e.stage] += ms;
+        if (err == cudaSuccess) err = cudaEventSynchronize(e.b);
+        if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, e.a, e.b);
+        if (err == cudaSuccess) c->stage_ms[e.stage] += ms;
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
     }
     c->ev.clear();
+    if (err != cudaSuccess)
+        return fail(c, S3R_ECUDA, "get_stage_times: %s", cudaGetErrorString(err));
     if (out_ms)
         for (int i = 0; i < S3R_NUM_STAGES; ++i) out_ms[i] = c->stage_ms[i];
     if (out_count) *out_count = c->timed_renders;
