@@ -14,9 +14,15 @@
  *   point-life update with M_t (Eq.5)    -> stage K2 (atomics)
  *   visibility commit / reset (Eq.6)     -> s3r_commit_visibility,
  *                                                      s3r_reset_visibility
+ * and the rows SURVEY.md §8(f) marks next:
+ *   backward of blend + projection, pose gradient   -> s3r_render_backward,
+ *     (config 5)                            s3r_mse, s3r_set_training
+ *   conventional pipeline (Fig.1a)             -> s3r_set_pipeline
+ *   LOD noisy offset (Eq.7 row 4)            -> s3r_set_lod_jitter
+ *   NeurF colour query (Eq.7 rows 5-6)       -> s3r_set_neural_colors
  *
  * "P:n" = line n of /root/reference/PAPER.md.  The arithmetic is the fp32
- * contract "R-ARITH" of DESIGN.md; readings of the paper (R1-R19) are listed
+ * contract "R-ARITH" of DESIGN.md; readings of the paper (R1-R23) are listed
  * there.
  *
  * Conventions for every call:
@@ -70,7 +76,7 @@ typedef struct s3r_ctx s3r_ctx;
  * l ... dynamic Gaussian is associated with an instance ID").  Structure of
  * arrays, one element per Gaussian, all DEVICE pointers, 16-byte aligned.   */
 typedef struct {
-    int64_t n;                   /* number of Gaussians, 0 <= n < 2^31          */
+    int64_t n;                   /* number of Gaussians, 0 <= n < 2^30          */
     int32_t num_instances;       /* K+1: id 0 = static background, 1..K objects */
     const float* means_opacity;  /* float4[n]: mu (x,y,z) in the local frame of
                                     its instance (world frame for id 0), opacity
