@@ -38,9 +38,10 @@ from paper_2503_08217_b200 import scenegen as sg  # noqa: E402
 METRIC = "rendered views/sec and Gaussians/sec at 1/2/4/8 B200; % HBM/FP32 roofline"
 UNIT = "views/s"
 # FP32 operations per blend evaluation of the R-ARITH exp2-form step (FMA = 2,
-# min / compare = 1): dx, dy 2; a1, a2, b1 3; c1, e2 4; clamp 1; s3r_exp2 14
-# (3 add, 5 fma, scale); alpha 2; w 1; colour + depth 8; T 1; termination 1.
-FLOPS_PER_EVAL = 37
+# min / compare = 1): dx, dy 2; a1, a2, b1 3; c1, e2 4; clamp 1; o * s3r_exp2
+# 14 (3 add, 5 fma, one multiply by o 2^n); alpha clamp 1; w 1; colour + depth
+# 8; T 1; termination 1.
+FLOPS_PER_EVAL = 36
 SM_COUNT_B200 = 148
 
 

@@ -24,7 +24,7 @@ namespace s3r {
 namespace {
 
 // R-ARITH s3r_exp2 for -24 <= x <= 0 (the caller handles the flush x < -24 -> 0),
-// evaluated on pixel pairs by s3r_exp2_x2 below: n = rint(x) by the 1.5*2^23
+// evaluated on pixel pairs (times the opacity) by o_exp2_x2 below: n = rint(x) by the 1.5*2^23
 // shifter (full-rate FADDs, no F2I/FRND), r = x - n exact, 2^r by the Cephes
 // degree-4 P of DESIGN.md R-ARITH, times 2^n built from the shifter's bits: bits(t) =
 // 0x4B400000 + n, so (bits(t) << 23) + 0x3F800000 = bits(2^n).
@@ -78,7 +78,11 @@ __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 __device__ __forceinline__ float2 neg2(float2 x) { return make_float2(-x.x, -x.y); }
 
 // s3r_exp2 on a pair (same operations as s3r_exp2, component-wise)
-__device__ __forceinline__ float2 s3r_exp2_x2(float2 x, float c0)
+// o * s3r_exp2(x) on a pair, as y * (o 2^n): o 2^n is exact (an exponent add on
+// o's bits, no under/overflow for o in (0, 1], n in [-24, 0]), so the one
+// rounding is that of the exact product o y 2^n — bit-identical to
+// o * (y * 2^n), one multiply less
+__device__ __forceinline__ float2 o_exp2_x2(float2 x, float o, float c0)
 {
     const float2 t = __fadd2_rn(x, f2(12582912.0f));
     const float2 n = __fadd2_rn(t, f2(-12582912.0f));
@@ -88,9 +92,11 @@ __device__ __forceinline__ float2 s3r_exp2_x2(float2 x, float c0)
     p = __ffma2_rn(p, r, f2(2.4022243916988373e-1f));
     p = __ffma2_rn(p, r, f2(6.931470036506653e-1f));
     const float2 y = __ffma2_rn(p, r, f2(1.0f));
-    const float2 sc = make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + 0x3F800000u),
-                                  __uint_as_float((__float_as_uint(t.y) << 23) + 0x3F800000u));
-    return __fmul2_rn(y, sc);
+    // bits(t) << 23 == n << 23 (mod 2^32): the shifter's 0x4B400000 part shifts out
+    const uint32_t ob = __float_as_uint(o);
+    const float2 osc = make_float2(__uint_as_float(ob + (__float_as_uint(t.x) << 23)),
+                                   __uint_as_float(ob + (__float_as_uint(t.y) << 23)));
+    return __fmul2_rn(y, osc);
 }
 
 template <bool COUNT, bool TRAIN>
@@ -276,7 +282,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                     const bool onx = (e2.x >= S3R_FLUSH_E2) && (T[P].x >= 1e-4f);
                     const bool ony = (e2.y >= S3R_FLUSH_E2) && (T[P].y >= 1e-4f);
                     if (onx || ony) {
-                        const float2 og = __fmul2_rn(f2(q0.w), s3r_exp2_x2(e2, c0));
+                        const float2 og = o_exp2_x2(e2, q0.w, c0);
                         const float2 alpha = make_float2(onx ? fminf(0.99f, og.x) : 0.0f,
                                                          ony ? fminf(0.99f, og.y) : 0.0f);
                         const float2 w = __fmul2_rn(alpha, T[P]);
