@@ -318,6 +318,7 @@ def scene_instances(ds):
 
 
 def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
+    from paper_2503_08217_b200 import parallel
     """Config 5: one step = training forward of the batch, MSE against noisy
     targets (s3r_mse), backward of blend + projection (s3r_render_backward)
     and, for N > 1, an NCCL all-reduce (SUM) of the per-Gaussian gradients."""
@@ -354,9 +355,7 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
         if world > 1:
             # per-Gaussian gradients are summed over ranks; the pose gradient is
             # per view (each rank owns its views' poses) and stays local
-            for k_, g in grads.items():
-                if k_ != "table":
-                    dist.all_reduce(g, op=dist.ReduceOp.SUM)
+            parallel.allreduce_grads(grads)
 
     for _ in range(2):
         step()

@@ -39,3 +39,14 @@ def merge_life(life: torch.Tensor, flip: Callable[[torch.Tensor], None],
     flip(life)
     dist.all_reduce(life, op=dist.ReduceOp.MAX, group=group)
     flip(life)
+
+
+def allreduce_grads(grads: dict, group: Optional[dist.ProcessGroup] = None) -> None:
+    """Config 5 with views sharded: sum the per-Gaussian gradients of every
+    rank's views (one all-reduce SUM per tensor; fp32 summation order differs
+    from one process, so the result agrees to rounding, not bit for bit).
+    The pose gradient ("table": per view) belongs to the rank owning the view
+    and is not reduced."""
+    for k, g in grads.items():
+        if k != "table":
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)

@@ -86,3 +86,45 @@ def test_world2_life_merge_matches_single_process(tmp_path):
         assert np.array_equal(got, want_life)
         assert np.array_equal(np.load(tmp_path / f"vis_{r}.npy"), scene.visibility)
     assert (want_life[:, 0] <= want_life[:, 1]).sum() > 100     # observed Gaussians exist
+
+
+def _grad_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        scene, views = _scene()
+        g = np.zeros((scene.n, 16))
+        for v in parallel.shard_views(views, rank, world):
+            cot = np.random.default_rng(int(1000 * (v.t + 2))).standard_normal(
+                (v.height, v.width, 3))
+            oracle.backward(scene, v, cot, grads=g)
+        grads = {"means_opacity": torch.from_numpy(g[:, 0:4].copy()),
+                 "colors": torch.from_numpy(g[:, 12:16].copy()),
+                 "table": torch.full((2, 12), float(rank))}
+        parallel.allreduce_grads(grads)
+        np.save(os.path.join(out_dir, f"g_{rank}.npy"),
+                np.concatenate([grads["means_opacity"].numpy(), grads["colors"].numpy()], 1))
+        np.save(os.path.join(out_dir, f"t_{rank}.npy"), grads["table"].numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_gradient_allreduce_matches_single_process(tmp_path):
+    """Config 5 sharded over 2 ranks: after parallel.allreduce_grads every rank
+    holds the gradient of the whole batch (the single-process sum, to fp64
+    rounding); the per-view pose gradient stays rank-local."""
+    world = 2
+    port = _free_port()
+    mp.spawn(_grad_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    scene, views = _scene()
+    g = np.zeros((scene.n, 16))
+    for v in views:
+        cot = np.random.default_rng(int(1000 * (v.t + 2))).standard_normal((v.height, v.width, 3))
+        oracle.backward(scene, v, cot, grads=g)
+    want = np.concatenate([g[:, 0:4], g[:, 12:16]], 1)
+    assert np.abs(want).max() > 0
+    for r in range(world):
+        got = np.load(tmp_path / f"g_{r}.npy")
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+        assert np.all(np.load(tmp_path / f"t_{r}.npy") == r)
