@@ -45,6 +45,9 @@ constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 #ifndef S3R_RASTER_CLIST
 #define S3R_RASTER_CLIST 1
 #endif
+#ifndef S3R_RASTER_NOBR
+#define S3R_RASTER_NOBR 0
+#endif
 #ifndef S3R_RASTER_PMASK
 #define S3R_RASTER_PMASK 0   // per-pair-block skip (A/B: 15.59 vs 15.14 ms without)
 #endif
@@ -281,7 +284,11 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                     // (both of the pair) or get alpha = 0 (one of the pair).
                     const bool onx = (e2.x >= S3R_FLUSH_E2) && (T[P].x >= 1e-4f);
                     const bool ony = (e2.y >= S3R_FLUSH_E2) && (T[P].y >= 1e-4f);
+#if S3R_RASTER_NOBR
+                    {   // branch-free: both pixels always evaluated, alpha selected
+#else
                     if (onx || ony) {
+#endif
                         const float2 og = o_exp2_x2(e2, q0.w, c0);
                         const float2 alpha = make_float2(onx ? fminf(0.99f, og.x) : 0.0f,
                                                          ony ? fminf(0.99f, og.y) : 0.0f);

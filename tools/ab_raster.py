@@ -38,7 +38,7 @@ VARIANT_SETS = {
     },
     "clist": {
         "base": [],
-        "nopmask": ["S3R_RASTER_PMASK=0"],
+        "nobr": ["S3R_RASTER_NOBR=1"],
     },
     "bex": {
         "base": [],
