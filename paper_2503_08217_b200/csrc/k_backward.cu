@@ -286,12 +286,13 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
 #else
                 // the exact R-ARITH exp2 on the pair (the forward's values)
                 const float2 G = s3r_exp2_pair(e2);
-                const float2 og = __fmul2_rn(f2(q0.w), G);
 #endif
-                // a pixel of the pair that is not ok gets alpha = 0: T, R and the
-                // sums are then unchanged, and its o / power gradients are masked
-                const float2 alpha = make_float2(okx ? fminf(0.99f, og.x) : 0.0f,
-                                                 oky ? fminf(0.99f, og.y) : 0.0f);
+                // a pixel of the pair that is not ok gets G = 0, hence o G = 0,
+                // alpha = 0: T, R and the sums are unchanged, and its o / power
+                // gradients (go G, go alpha) vanish — one select per pixel
+                const float2 Gm = make_float2(okx ? G.x : 0.0f, oky ? G.y : 0.0f);
+                const float2 ogm = __fmul2_rn(f2(q0.w), Gm);
+                const float2 alpha = make_float2(fminf(0.99f, ogm.x), fminf(0.99f, ogm.y));
                 const float2 om = __fadd2_rn(f2(1.0f), neg2(alpha));
                 const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
                 const float2 Tb = __fmul2_rn(Tc[P], inv);        // T before this splat
@@ -312,9 +313,9 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 if (HAS_D) s_z = __ffma2_rn(w, gd[P], s_z);
                 // alpha clamped at 0.99: no gradient to o or the power;
                 // power clamped at 0 (e2raw > 0): no gradient to the power
-                const float2 go = make_float2(okx && og.x < 0.99f ? galpha.x : 0.0f,
-                                              oky && og.y < 0.99f ? galpha.y : 0.0f);
-                s_o = __ffma2_rn(go, G, s_o);
+                const float2 go = make_float2(ogm.x < 0.99f ? galpha.x : 0.0f,
+                                              ogm.y < 0.99f ? galpha.y : 0.0f);
+                s_o = __ffma2_rn(go, Gm, s_o);
                 float2 gP = __fmul2_rn(go, alpha);
                 gP.x = e2raw.x <= 0.0f ? gP.x : 0.0f;
                 gP.y = e2raw.y <= 0.0f ? gP.y : 0.0f;
