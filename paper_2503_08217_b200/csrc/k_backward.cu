@@ -38,6 +38,9 @@ namespace {
 #ifndef S3R_BWD_MINB
 #define S3R_BWD_MINB 20     // 96 registers at RPIX 8 (A/B: 37.1 ms; 16: 37.3, 24: 45.0)
 #endif
+#ifndef S3R_BWD_RPR
+#define S3R_BWD_RPR 1   // records per warp reduction (1 or 2)
+#endif
 #ifndef S3R_BWD_EX2
 #define S3R_BWD_EX2 0   // 0: exact R-ARITH exp2 on pairs (A/B 35.9 ms); 1, 2: ex2.approx + re-decision (37.0, 36.6)
 #endif
@@ -233,8 +236,10 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
             }
             __syncthreads();
         }
-        for (int kk = run[warp] - 1; kk >= 0; --kk) {
-            const int jj = s_cl[warp][kk];
+        // one record (by staged index jj): per-pixel recurrences (T, R) and the
+        // thread's partial sums -> v10 (the splat's 10 gradient values before the
+        // warp reduction); returns whether any pixel of the thread contributed
+        auto eval_record = [&](int jj, float* v10) -> bool {
             const int j = lo + jj;
             const float4 q0 = s_rec[3 * jj], q1 = s_rec[3 * jj + 1], q2 = s_rec[3 * jj + 2];
             const float dx = q0.x - fpx;
@@ -324,18 +329,69 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 S1 = __fadd2_rn(S1, t);
                 S2 = __ffma2_rn(t, dy, S2);
             }
-            if (__any_sync(0xffffffffu, any)) {
-                // 10-value warp reduction by halving exchanges: at xor-distance
-                // 16 / 8 / 4 / 2 each lane keeps the lower or upper half of its
-                // (zero-padded) values and adds its partner's copy of that half:
-                // 10 -> 5 -> 3 -> 2 -> 1, then one xor-1 step; 12 shuffles. The
-                // lane pair (u16, u8, u4, u2) ends with value 5 u16 + 3 u8 + 2 u4 + u2
-                // (valid when 2 u4 + u2 <= 2 and 3 u8 + 2 u4 + u2 <= 4).
                 const float S0s = S0.x + S0.y, S1s = S1.x + S1.y, S2s = S2.x + S2.y;
                 const float dS0 = dx * S0s;
-                const float v10[10] = {-(A * dS0 + B * S1s), -(B * dS0 + Cc * S1s), s_z.x + s_z.y,
+                const float vv[10] = {-(A * dS0 + B * S1s), -(B * dS0 + Cc * S1s), s_z.x + s_z.y,
                                        -0.5f * dx * dS0, -dx * S1s, -0.5f * S2s,
                                        s_o.x + s_o.y, s_r.x + s_r.y, s_g.x + s_g.y, s_b.x + s_b.y};
+#pragma unroll
+            for (int i = 0; i < 10; ++i) v10[i] = vv[i];
+            return any;
+        };
+#if S3R_BWD_RPR == 2
+        // two records per warp reduction: 20 values, 21 shuffles (10 at distance
+        // 16 separate the records, then the 10-value scheme below per record)
+        for (int kk = run[warp] - 1; kk >= 0; kk -= 2) {
+            const int jjA = s_cl[warp][kk];
+            float vA[10], vB[10];
+            const bool anyA = eval_record(jjA, vA);
+            const bool hasB = kk >= 1;                      // warp-uniform
+            int jjB = 0;
+            bool anyB = false;
+            if (hasB) {
+                jjB = s_cl[warp][kk - 1];
+                anyB = eval_record(jjB, vB);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 10; ++i) vB[i] = 0.0f;
+            }
+            if (__any_sync(0xffffffffu, anyA || anyB)) {
+                const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2, u1 = lane & 1;
+                float v10[10], v5[5], v3[3], v2[2];
+#pragma unroll
+                for (int i = 0; i < 10; ++i)
+                    v10[i] = (u16 ? vB[i] : vA[i]) +
+                             __shfl_xor_sync(0xffffffffu, u16 ? vA[i] : vB[i], 16);
+#pragma unroll
+                for (int i = 0; i < 5; ++i)
+                    v5[i] = (u8 ? v10[5 + i] : v10[i]) +
+                            __shfl_xor_sync(0xffffffffu, u8 ? v10[i] : v10[5 + i], 8);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const float hiv = i < 2 ? v5[3 + i] : 0.0f;
+                    v3[i] = (u4 ? hiv : v5[i]) + __shfl_xor_sync(0xffffffffu, u4 ? v5[i] : hiv, 4);
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float hiv = i < 1 ? v3[2 + i] : 0.0f;
+                    v2[i] = (u2 ? hiv : v3[i]) + __shfl_xor_sync(0xffffffffu, u2 ? v3[i] : hiv, 2);
+                }
+                const float v1 = (u1 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, u1 ? v2[0] : v2[1], 1);
+                const int inner = 5 * u8 + 3 * u4 + 2 * u2 + u1;
+                if (2 * u2 + u1 <= 2 && 3 * u4 + 2 * u2 + u1 <= 4 && (!u16 || hasB)) {
+                    const int jjR = u16 ? jjB : jjA;
+                    const uint32_t g = __float_as_uint(s_rec[3 * jjR + 1].w);   // list entry
+                    atomicAdd(acc + 10ll * g + inner, v1);
+                }
+            }
+        }
+#else
+        for (int kk = run[warp] - 1; kk >= 0; --kk) {
+            const int jj = s_cl[warp][kk];
+            const float4 q1 = s_rec[3 * jj + 1];
+            float v10[10];
+            const bool any = eval_record(jj, v10);
+            if (__any_sync(0xffffffffu, any)) {
                 const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
                 float v5[5], v3[3], v2[2];
 #pragma unroll
@@ -361,6 +417,7 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 }
             }
         }
+#endif
         hi = lo;
     }
 }

@@ -40,6 +40,11 @@ VARIANT_SETS = {
         "base": [],
         "nobr": ["S3R_RASTER_NOBR=1"],
     },
+    "rpr": {
+        "base": [],
+        "rpr2": ["S3R_BWD_RPR=2"],
+        "rpr2m18": ["S3R_BWD_RPR=2", "S3R_BWD_MINB=18"],
+    },
     "bex": {
         "base": [],
         "ex2pair": ["S3R_BWD_EX2=2"],
