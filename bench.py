@@ -42,6 +42,10 @@ UNIT = "views/s"
 # 14 (3 add, 5 fma, one multiply by o 2^n); alpha clamp 1; w 1; colour + depth
 # 8; T 1; termination 1.
 FLOPS_PER_EVAL = 36
+# ... and of its adjoint (k_raster_bwd): dy, e2 6; clamp 1; exp2 14; o G 1;
+# alpha 1; 1 - alpha 1; rcp 1; T_before 1; w 1; c.gC 6; rest 2; dL/dalpha 2;
+# R 2; colour sums 6; opacity 2; power 1; dy moments 5; flush test 1.
+BWD_FLOPS_PER_EVAL = 54
 SM_COUNT_B200 = 148
 
 
@@ -550,6 +554,15 @@ def main():
     train = None
     if not args.no_train and args.config != "toy":
         train = run_train(args, ctx, ds, pools[0], tables[0], outs, world, dev, stream)
+        # the backward rasterizer revisits the forward's evaluations (same E_alg)
+        # back to front: FP32 roofline of the whole backward against them
+        bw_s = train["backward_ms"] / 1e3
+        train["roofline"] = {
+            "kernel": "k_raster_bwd (+ k_project_bwd)", "bound": "alu",
+            "achieved": BWD_FLOPS_PER_EVAL * E_alg / bw_s / 1e12, "peak": alu_peak,
+            "unit": "TFLOP/s", "frac": BWD_FLOPS_PER_EVAL * E_alg / bw_s / 1e12 / alu_peak,
+            "alg_flops_per_launch": BWD_FLOPS_PER_EVAL * E_alg,
+            "note": f"{BWD_FLOPS_PER_EVAL} FLOP per evaluation (bench.py BWD_FLOPS_PER_EVAL)"}
 
     # ---------------- NEXT-2: the conventional pipeline on the same views
     conventional = None
