@@ -457,9 +457,15 @@ def main():
     import torch.distributed as dist
     from paper_2503_08217_b200 import s3r
 
+    if os.environ.get("S3R_DIST_BACKEND") and torch.cuda.device_count():
+        local = local % torch.cuda.device_count()    # functional multi-rank test on fewer GPUs
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("S3R_DIST_BACKEND", "nccl")   # gloo: functional test on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     # ---------------- workload (identical scene on every rank; views sharded)
     if args.config == "toy":
