@@ -7,10 +7,11 @@
 // below is shared by 256 pixels (A/B: 37.1 ms vs 40.7 ms with the forward's
 // 64-thread, 4-pixel layout).
 // Every pixel knows from the forward its final transmittance and how many list
-// entries it blended; the CTA walks its tile list BACK TO FRONT in batches of
-// 256 staged records, recomputes alpha with the forward's R-ARITH ops (so the
-// flush / clamps / skips are the forward's), recovers T before each splat as
-// T / (1 - alpha), and forms
+// entries it blended; the warp walks its tile list BACK TO FRONT in batches of
+// 256 staged records (only those whose flush ellipse reaches the tile, from a
+// compacted list built while staging), recomputes alpha with the forward's
+// R-ARITH ops on packed pairs (so the flush / clamps / skips are the
+// forward's), recovers T before each splat as T / (1 - alpha), and forms
 //     dL/dc = w gC,  dL/dz = w gD,
 //     dL/dalpha = T (c.gC + z gD) - (R + gT T_final) / (1 - alpha),
 //     R += (c.gC + z gD) w,

@@ -24,12 +24,12 @@ namespace s3r {
 namespace {
 
 // R-ARITH s3r_exp2 for -24 <= x <= 0 (the caller handles the flush x < -24 -> 0),
-// evaluated on pixel pairs (times the opacity) by o_exp2_x2 below: n = rint(x) by the 1.5*2^23
-// shifter (full-rate FADDs, no F2I/FRND), r = x - n exact, 2^r by the Cephes
-// degree-4 P of DESIGN.md R-ARITH, times 2^n built from the shifter's bits: bits(t) =
-// 0x4B400000 + n, so (bits(t) << 23) + 0x3F800000 = bits(2^n).
-// c0 = 1.3264695880934596e-3f (the leading coefficient of the degree-4 P of
-// DESIGN.md R-ARITH) is passed in a register (see k_raster).
+// evaluated on pixel pairs, times the opacity, by o_exp2_x2 below: n = rint(x)
+// by the 1.5*2^23 shifter (full-rate FADDs, no F2I/FRND), r = x - n exact, 2^r
+// as 1 + r P(r) with the degree-4 P of DESIGN.md R-ARITH, times 2^n built from
+// the shifter's bits: bits(t) = 0x4B400000 + n, so bits(t) << 23 == n << 23.
+// c0 = 1.3264695880934596e-3f (the leading coefficient of P) is passed in a
+// register (see k_raster).
 
 #ifndef S3R_RASTER_RPIX
 #define S3R_RASTER_RPIX 4
