@@ -215,15 +215,22 @@ __global__ void __launch_bounds__(NT) k_neurf(NeurfArgs a)
             }
             const float mu[3] = {m4.x * inv_s, m4.y * inv_s, m4.z * inv_s};
             f[0] = mu[0]; f[1] = mu[1]; f[2] = mu[2];
+            // octave 0 by sincospif, octaves 1-3 by the double-angle identities
+            // sin 2a = 2 sin a cos a, cos 2a = 1 - 2 sin^2 a (absolute error grows
+            // ~2x per octave, ~1e-6 at octave 3, far below the features' bf16 step)
 #pragma unroll
-            for (int l = 0; l < 4; ++l)
+            for (int ax = 0; ax < 3; ++ax) {
+                float sn, cs;
+                sincospif(mu[ax], &sn, &cs);
 #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    float sn, cs;
-                    sincospif((float)(1 << l) * mu[ax], &sn, &cs);
+                for (int l = 0; l < 4; ++l) {
                     f[3 + 6 * l + 2 * ax] = sn;
                     f[4 + 6 * l + 2 * ax] = cs;
+                    const float s2 = 2.0f * sn * cs;
+                    cs = fmaf(-2.0f * sn, sn, 1.0f);
+                    sn = s2;
                 }
+            }
             f[27] = fminf(1.0f, p[2] / V.lod_D);
             const float rn = rsqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
             const float ph[3] = {p[0] * rn, p[1] * rn, p[2] * rn};
