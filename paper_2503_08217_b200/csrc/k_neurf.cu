@@ -35,7 +35,8 @@ constexpr int A_BYTES = NT * KF * 2;             // 16 KB
 constexpr int W12_BYTES = 128 * KF * 2;          // 16 KB each (sta | dyn)
 constexpr int W3_BYTES = 32 * KF * 2;            // 4 KB
 constexpr int NB = 128 + 128 + 32;               // fp32 biases b1 | b2 | b3
-constexpr size_t SMEM = (size_t)A_BYTES + 2 * W12_BYTES + W3_BYTES + NB * 4 + 64;
+constexpr int MAXV = 256;      // views whose tile offsets fit in smem (keeps 4 CTAs per SM)
+constexpr size_t SMEM = (size_t)A_BYTES + 2 * W12_BYTES + W3_BYTES + NB * 4 + 64 + MAXV * 4;
 
 // byte offset of element (row, k) in a K-major no-swizzle core-matrix tile
 // with 64 columns: core matrix (row / 8, k / 8) at ((row/8) * 8 + k/8) * 128
@@ -90,9 +91,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase)
         : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r)
 {
-    uint32_t r[16];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
         "%14,%15}, [%16];\n"
@@ -100,9 +100,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v)
           "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
           "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
+}
+
+// the sta and dyn halves of 16 columns, one wait for both loads
+__device__ __forceinline__ void tmem_ld16x2(uint32_t ta, uint32_t tb, float* va, float* vb)
+{
+    uint32_t ra[16], rb[16];
+    tmem_ld16_nowait(ta, ra);
+    tmem_ld16_nowait(tb, rb);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 16; ++i) {
+        va[i] = __uint_as_float(ra[i]);
+        vb[i] = __uint_as_float(rb[i]);
+    }
 }
 
 __device__ __forceinline__ void fence_async_smem()
@@ -150,6 +161,7 @@ __global__ void __launch_bounds__(NT) k_neurf(NeurfArgs a)
     float* sB = reinterpret_cast<float*>(sW3 + W3_BYTES);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sB + NB);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+    int* s_toff = reinterpret_cast<int*>(smem + A_BYTES + 2 * W12_BYTES + W3_BYTES + NB * 4 + 64);
     const int tid = threadIdx.x, warp = tid >> 5;
 
     // ---- weights and biases (pre-packed bf16 core-matrix layout) ----
@@ -182,26 +194,52 @@ __global__ void __launch_bounds__(NT) k_neurf(NeurfArgs a)
     uint32_t phase = 0;
     const float inv_s = 1.0f / a.pos_scale;
 
-    for (int T = blockIdx.x; T < a.total_tiles; T += gridDim.x) {
-        // view of tile T: the last v with tile_off[v] <= T
-        int lo = 0, hi = a.n_views - 1;
+    // first tile of each view in shared memory (the per-tile view lookup is a
+    // binary search there), and the next tile's per-row mean prefetched into a
+    // register while the current tile is in the MMA / epilogue phases
+    const int nv = a.n_views;
+    const bool toff_smem = nv <= MAXV;
+    if (toff_smem)
+        for (int i = tid; i < nv; i += NT) s_toff[i] = a.tile_off[i];
+    __syncthreads();
+    auto view_of = [&](int T) -> int {
+        int lo = 0, hi = nv - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (a.tile_off[mid] <= T) lo = mid;
+            if ((toff_smem ? s_toff[mid] : a.tile_off[mid]) <= T) lo = mid;
             else hi = mid - 1;
         }
+        return lo;
+    };
+    auto row_of = [&](int T, int v, long long& o) -> bool {
+        const DevView& W = a.views[v];
+        const long long rr = (long long)(T - (toff_smem ? s_toff[v] : a.tile_off[v])) * NT + tid;
+        o = W.cap_off + rr;
+        return rr < W.n_rendered;
+    };
+    int Tn = blockIdx.x, vn = 0;
+    long long on = 0;
+    bool validn = false;
+    float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (Tn < a.total_tiles) {
+        vn = view_of(Tn);
+        validn = row_of(Tn, vn, on);
+        if (validn) m4n = a.rec_mu[on];
+    }
+    for (int T = blockIdx.x; T < a.total_tiles; T += gridDim.x) {
+        const int lo = vn;
         const DevView& V = a.views[lo];
-        const long long r0 = (long long)(T - a.tile_off[lo]) * NT;
         const int r = tid;
-        const bool valid = r0 + r < V.n_rendered;
-        const long long o = V.cap_off + r0 + r;
+        const bool valid = validn;
+        const long long o = on;
+        const float4 m4c = m4n;
         bool dyn = false;
         // ---- features of row r (zero rows past the view's records) ----
         float f[KF];
 #pragma unroll
         for (int k = 0; k < KF; ++k) f[k] = 0.0f;
         if (valid) {
-            const float4 m4 = a.rec_mu[o];
+            const float4 m4 = m4c;
             const int id = __float_as_int(m4.w);
             dyn = id > 0;
             const float* M = V.table + 12 * id;
@@ -258,6 +296,14 @@ __global__ void __launch_bounds__(NT) k_neurf(NeurfArgs a)
         for (int k0 = 0; k0 < KF; k0 += 8) st_row8(sA, r, k0, f + k0);
         fence_async_smem();
         __syncthreads();
+        // prefetch the next tile's row (lands during this tile's three layers)
+        Tn = T + gridDim.x;
+        validn = false;
+        if (Tn < a.total_tiles) {
+            vn = view_of(Tn);
+            validn = row_of(Tn, vn, on);
+            if (validn) m4n = a.rec_mu[on];
+        }
 
         // ---- layers 1 and 2 (N = 128: sta | dyn), layer 3 (N = 32) ----
 #pragma unroll 1
@@ -275,8 +321,7 @@ __global__ void __launch_bounds__(NT) k_neurf(NeurfArgs a)
 #pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 16) {
                     float vs[16], vd[16];
-                    tmem_ld16(trow + c0, vs);             // NeurF_sta columns
-                    tmem_ld16(trow + 64 + c0, vd);        // NeurF_dyn columns
+                    tmem_ld16x2(trow + c0, trow + 64 + c0, vs, vd);   // NeurF_sta | NeurF_dyn
                     float h[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) h[i] = fmaxf((dyn ? vd[i] : vs[i]) + bias[c0 + i], 0.0f);
@@ -285,8 +330,7 @@ __global__ void __launch_bounds__(NT) k_neurf(NeurfArgs a)
                 }
             } else {
                 float v[16], w[16];
-                tmem_ld16(trow, v);                       // sta outputs in columns 0-2
-                tmem_ld16(trow + 16, w);                  // dyn outputs in columns 16-18
+                tmem_ld16x2(trow, trow + 16, v, w);       // sta outputs in columns 0-2, dyn 16-18
                 if (valid) {
                     const float* b3 = sB + 256 + (dyn ? 16 : 0);
                     float c[3];
