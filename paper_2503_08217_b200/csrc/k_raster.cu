@@ -45,6 +45,9 @@ constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 #ifndef S3R_RASTER_CLIST
 #define S3R_RASTER_CLIST 1
 #endif
+#ifndef S3R_RASTER_ADJ
+#define S3R_RASTER_ADJ 1     // vertically adjacent pixel pairs (A/B: 14.65 vs 15.01 ms)
+#endif
 #ifndef S3R_RASTER_NOBR
 #define S3R_RASTER_NOBR 0
 #endif
@@ -121,6 +124,13 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     // compact BW x RS block (rows RS k .. RS k + RS - 1)
     const int px = tx * TILE + (tid >> 5) * BW + (lane % BW);
     const int py0 = ty * TILE + (lane / BW);
+#if S3R_RASTER_ADJ
+    // pixel k of the thread at row 2 RS (k >> 1) + 2 (lane / BW) + (k & 1): the
+    // two pixels of a pair are vertically adjacent
+    auto prow = [&](int k) { return ty * TILE + 2 * RS * (k >> 1) + 2 * (lane / BW) + (k & 1); };
+#else
+    auto prow = [&](int k) { return py0 + RS * k; };
+#endif
     const float fpx = (float)px;
     // centre of the warp's BW x 16 pixel block (flush-ellipse culling; the
     // stored extents include the 8 x 16 block's half size)
@@ -138,7 +148,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     unsigned inside = 0;
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
-        const int py = py0 + RS * k;
+        const int py = prow(k);
         stop[k] = -1;
         const bool in = px < V.W && py < V.H;
         inside |= (in ? 1u : 0u) << k;
@@ -146,7 +156,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     }
 #pragma unroll
     for (int P = 0; P < NP; ++P) {
-        nfpy[P] = make_float2(-(float)(py0 + RS * 2 * P), -(float)(py0 + RS * (2 * P + 1)));
+        nfpy[P] = make_float2(-(float)prow(2 * P), -(float)prow(2 * P + 1));
         // a pixel outside the image starts "terminated" (T = 0 is never written)
         T[P] = make_float2((inside >> (2 * P)) & 1 ? 1.0f : 0.0f,
                            (inside >> (2 * P + 1)) & 1 ? 1.0f : 0.0f);
@@ -332,7 +342,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
         if (!(inside & (1u << k))) continue;
         const int P = k >> 1;
         const bool hi = k & 1;
-        const long long pix = (long long)(py0 + RS * k) * V.W + px;
+        const long long pix = (long long)prow(k) * V.W + px;
         float* o = V.rgb + 3 * pix;
         o[0] = hi ? cr[P].y : cr[P].x;
         o[1] = hi ? cg[P].y : cg[P].x;

@@ -38,7 +38,7 @@ VARIANT_SETS = {
     },
     "clist": {
         "base": [],
-        "nobr": ["S3R_RASTER_NOBR=1"],
+        "adj": ["S3R_RASTER_ADJ=1"],
     },
     "rpr": {
         "base": [],
