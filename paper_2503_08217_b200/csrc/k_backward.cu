@@ -39,6 +39,9 @@ namespace {
 #ifndef S3R_BWD_MINB
 #define S3R_BWD_MINB 20     // 96 registers at RPIX 8 (A/B: 37.1 ms; 16: 37.3, 24: 45.0)
 #endif
+#ifndef S3R_BWD_ADJ
+#define S3R_BWD_ADJ 0   // adjacent-row pairs: neutral here (A/B 34.17 vs 34.15 ms)
+#endif
 #ifndef S3R_BWD_RPR
 #define S3R_BWD_RPR 1   // records per warp reduction (1 or 2)
 #endif
@@ -137,14 +140,19 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     const float bcx0 = (float)(tx * TILE) + 0.5f * (BW - 1);     // warp block 0
     const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
     const s3r_cot C = a.cots[v];
-    // the thread's 4 pixels (rows py0 + 4k) as 2 packed pairs: pair P holds
+    // the thread's RPIX pixels of one column as RPIX / 2 packed pairs: pair P holds
     // k = 2P (.x) and 2P + 1 (.y); sm_100a FADD2/FMUL2/FFMA2 work on both
     float Tk[RPIX], gtTk[RPIX], grk[RPIX], ggk[RPIX], gbk[RPIX], gdk[RPIX], nfk[RPIX];
     int last[RPIX];
     int mymax = 0;
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
+#if S3R_BWD_ADJ
+        // the two pixels of a packed pair are vertically adjacent (as in K7)
+        const int py = ty * TILE + 2 * (32 / BW) * (k >> 1) + 2 * (lane / BW) + (k & 1);
+#else
         const int py = py0 + (32 / BW) * k;
+#endif
         nfk[k] = -(float)py;
         last[k] = 0;
         Tk[k] = 1.0f;

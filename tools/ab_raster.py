@@ -42,8 +42,7 @@ VARIANT_SETS = {
     },
     "rpr": {
         "base": [],
-        "rpr2": ["S3R_BWD_RPR=2"],
-        "rpr2m18": ["S3R_BWD_RPR=2", "S3R_BWD_MINB=18"],
+        "noadj": ["S3R_BWD_ADJ=0"],
     },
     "bex": {
         "base": [],
