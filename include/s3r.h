@@ -214,6 +214,19 @@ int s3r_render(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* view,
 int s3r_render_batch(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* views,
                      int32_t n_views, const s3r_outputs* outs, void* stream);
 
+/* Overlapped batches (default off): s3r_render_batch with >= 16 views renders
+ * the second half of the batch in an internal twin context (its own scratch)
+ * on an internal stream forked from and joined back into `stream`, so that
+ * half's filter / projection / sort / binning (and their host syncs) run while
+ * the first half rasterizes.  Results are identical to one piece;
+ * s3r_get_stats covers every view; s3r_dump_intermediates returns S3R_ESTATE
+ * after such a batch.  Debug, counters, training and NeurF renders are never
+ * split.  enable = 0 (the default; S3R_OVERLAP=1 at s3r_create turns it on)
+ * renders every batch in one piece.  Measured neutral on the C3 workload
+ * (the rasterizer already fills every SM), kept as an option
+ * for workloads whose front stages dominate.                               */
+int s3r_set_overlap(s3r_ctx* ctx, int enable);
+
 /* Same as s3r_render_batch, but every pointer of scene, views (including
  * instance_w2c) and outs is a HOST pointer (page-locked memory recommended).
  * The library copies the inputs to device scratch, renders, copies the

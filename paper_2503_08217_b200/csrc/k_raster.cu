@@ -123,12 +123,12 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
     // warp w owns columns BW w .. BW w + BW - 1; for pixel k a warp covers a
     // compact BW x RS block (rows RS k .. RS k + RS - 1)
     const int px = tx * TILE + (tid >> 5) * BW + (lane % BW);
-    const int py0 = ty * TILE + (lane / BW);
 #if S3R_RASTER_ADJ
     // pixel k of the thread at row 2 RS (k >> 1) + 2 (lane / BW) + (k & 1): the
     // two pixels of a pair are vertically adjacent
     auto prow = [&](int k) { return ty * TILE + 2 * RS * (k >> 1) + 2 * (lane / BW) + (k & 1); };
 #else
+    const int py0 = ty * TILE + (lane / BW);
     auto prow = [&](int k) { return py0 + RS * k; };
 #endif
     const float fpx = (float)px;

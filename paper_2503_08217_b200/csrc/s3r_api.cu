@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -76,6 +77,13 @@ struct s3r_ctx {
     // mirrors for s3r_render_batch_host
     Buf m_scene[7];
     cudaStream_t copy_stream = nullptr;      // D2H of finished chunks (host path)
+    // overlapped batches: the second half of a batch renders in a twin context
+    // (own scratch) on its own stream, so its filter / projection / sort /
+    // binning run while the first half rasterizes
+    s3r_ctx* twin = nullptr;
+    cudaStream_t twin_stream = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    bool overlap = false;
     std::vector<cudaEvent_t> chunk_done;
     bool host_chunked = false;               // last render was a chunked host batch
     std::vector<Buf> m_tab, m_rgb, m_depth, m_T, m_vis;
@@ -665,6 +673,7 @@ int s3r_create(int device, s3r_ctx** out)
     s3r_ctx* c = new (std::nothrow) s3r_ctx();
     if (!c) return S3R_ENOMEM;
     c->device = device;
+    if (const char* e = std::getenv("S3R_OVERLAP")) c->overlap = e[0] && e[0] != '0';
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
@@ -684,6 +693,10 @@ void s3r_destroy(s3r_ctx* c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    if (c->twin) s3r_destroy(c->twin);
+    if (c->twin_stream) cudaStreamDestroy(c->twin_stream);
+    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    if (c->join_ev) cudaEventDestroy(c->join_ev);
     Buf* bufs[] = {&c->d_nw, &c->d_nb, &c->d_temb, &c->d_cemb, &c->d_recmu, &c->d_toff,
                    &c->d_wmo, &c->d_wrot, &c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
                    &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
@@ -739,6 +752,7 @@ int s3r_set_timing(s3r_ctx* c, int enable)
     for (double& m : c->stage_ms) m = 0;
     c->timed_renders = 0;
     c->timing = enable != 0;
+    if (c->twin) s3r_set_timing(c->twin, enable);
     return S3R_OK;
 }
 
@@ -758,6 +772,14 @@ int s3r_get_stage_times(s3r_ctx* c, double* out_ms, int64_t* out_count)
     c->ev.clear();
     if (err != cudaSuccess)
         return fail(c, S3R_ECUDA, "get_stage_times: %s", cudaGetErrorString(err));
+    if (c->twin) {            // the second halves of overlapped batches
+        double tw[S3R_NUM_STAGES];
+        int64_t tc = 0;
+        if (int r = s3r_get_stage_times(c->twin, tw, &tc)) return fail(c, r, "%s", c->twin->err.c_str());
+        for (int i = 0; i < S3R_NUM_STAGES; ++i) c->stage_ms[i] += tw[i];
+        c->twin->stage_ms[0] = 0;
+        for (double& m : c->twin->stage_ms) m = 0;
+    }
     if (out_ms)
         for (int i = 0; i < S3R_NUM_STAGES; ++i) out_ms[i] = c->stage_ms[i];
     if (out_count) *out_count = c->timed_renders;
@@ -781,7 +803,43 @@ int s3r_render_batch(s3r_ctx* c, const s3r_scene* scene, const s3r_view* views, 
                      const s3r_outputs* outs, void* stream)
 {
     if (!c) return S3R_EINVAL;
-    return render_impl(c, scene, views, n_views, outs, (cudaStream_t)stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    // Overlapped halves: the second half renders in the twin context on its own
+    // stream, forked from and joined back into `stream`, so its latency-bound
+    // front stages (K1-K5, with their two host syncs) overlap the first half's
+    // compute-bound rasterization.  Modes whose state must describe one batch
+    // (debug dumps, counters, training, NeurF) render in one piece.
+    const bool split = c->overlap && n_views >= 16 && !c->debug && !c->counters &&
+                       !c->training && !c->neurf;
+    if (!split) return render_impl(c, scene, views, n_views, outs, st);
+    CU(cudaSetDevice(c->device));
+    if (!c->twin) {
+        int rc = s3r_create(c->device, &c->twin);
+        if (rc) return fail(c, rc, "overlap: creating the twin context failed");
+        c->twin->overlap = false;
+        CU(cudaStreamCreateWithFlags(&c->twin_stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    }
+    s3r_ctx* t = c->twin;
+    t->pipeline = c->pipeline;
+    for (int a = 0; a < 3; ++a) t->lod_jitter[a] = c->lod_jitter[a];
+    if (t->timing != c->timing) s3r_set_timing(t, c->timing);
+    CU(cudaEventRecord(c->fork_ev, st));
+    CU(cudaStreamWaitEvent(c->twin_stream, c->fork_ev, 0));
+    const int n1 = n_views / 2;
+    int rc1 = render_impl(c, scene, views, n1, outs, st);
+    if (rc1 != S3R_OK && rc1 != S3R_EINSTANCE) return rc1;
+    int rc2 = render_impl(t, scene, views + n1, n_views - n1, outs + n1, c->twin_stream);
+    if (rc2 != S3R_OK && rc2 != S3R_EINSTANCE) {
+        cudaStreamSynchronize(c->twin_stream);
+        return fail(c, rc2, "%s", t->err.c_str());
+    }
+    CU(cudaEventRecord(c->join_ev, c->twin_stream));
+    CU(cudaStreamWaitEvent(st, c->join_ev, 0));
+    c->stats.insert(c->stats.end(), t->stats.begin(), t->stats.end());
+    c->host_chunked = true;        // per-view intermediates live in two contexts
+    return rc1 ? rc1 : rc2;
 }
 
 int s3r_render(s3r_ctx* c, const s3r_scene* scene, const s3r_view* view, const s3r_outputs* out,
@@ -1066,6 +1124,13 @@ int s3r_set_neural_colors(s3r_ctx* c, const s3r_neurf* p, void* stream)
     return S3R_OK;
 }
 
+int s3r_set_overlap(s3r_ctx* c, int enable)
+{
+    if (!c) return S3R_EINVAL;
+    c->overlap = enable != 0;
+    return S3R_OK;
+}
+
 int s3r_set_pipeline(s3r_ctx* c, int pipeline)
 {
     if (!c) return S3R_EINVAL;
@@ -1177,6 +1242,13 @@ int s3r_check(s3r_ctx* c, void* stream)
     uint32_t e = 0;
     CU(cudaMemcpy(&e, c->d_err.p, sizeof e, cudaMemcpyDeviceToHost));
     CU(cudaMemset(c->d_err.p, 0, sizeof e));
+    if (c->twin && c->twin_stream) {
+        uint32_t e2 = 0;
+        CU(cudaStreamSynchronize(c->twin_stream));
+        CU(cudaMemcpy(&e2, c->twin->d_err.p, sizeof e2, cudaMemcpyDeviceToHost));
+        CU(cudaMemset(c->twin->d_err.p, 0, sizeof e2));
+        e |= e2;
+    }
     if (e & ERR_BADID) return fail(c, S3R_EINSTANCE, "a Gaussian had an out-of-range instance id");
     return S3R_OK;
 }

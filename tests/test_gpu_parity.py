@@ -675,3 +675,34 @@ def test_training_recovers_perturbed_scene():
         assert col_err1 < col_err0
     finally:
         c.close()
+
+
+def test_overlapped_batch_halves(ctx):
+    """s3r_set_overlap: a 20-view batch rendered as two overlapped halves (twin
+    context on a second stream) equals the one-piece render bit for bit —
+    images, M_t, life and per-view stats; dumps are refused afterwards."""
+    scene, views = sg.make_random_dynamic(44, 3000, 3, 200, 120, 88, 20, lod=(3.0, 0.5, 12.0))
+    ds1, tabs, o1, _ = gpu_render(ctx, scene, views)           # debug on: one piece
+    want = [ctx.stats(i) for i in range(len(views))]
+    ctx.set_debug(False)
+    ctx.set_overlap(True)
+    try:
+        ds2 = s3r.DeviceScene.from_numpy(scene)
+        o2 = s3r.alloc_outputs(views, n_visible=scene.n)
+        rc = ctx.render_batch(ds2, views, list(tabs), o2)
+        torch.cuda.synchronize()
+        got = [ctx.stats(i) for i in range(len(views))]
+        with pytest.raises(s3r.S3RError):
+            ctx.dump(0, views[0].width, views[0].height)
+        assert ctx.check() == 0
+    finally:
+        ctx.set_debug(True)
+        ctx.set_overlap(False)
+    assert rc == 0
+    for a, b in zip(o1, o2):
+        for k in ("rgb", "depth", "final_T", "visible"):
+            assert torch.equal(a[k], b[k])
+    assert torch.equal(ds1.life, ds2.life)
+    for g, w in zip(got, want):
+        for k in ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped", "n_rendered", "n_pairs"):
+            assert g[k] == w[k], k

@@ -40,6 +40,10 @@ VARIANT_SETS = {
         "base": [],
         "adj": ["S3R_RASTER_ADJ=1"],
     },
+    "ov": {
+        "base": [],
+        "ov": [],
+    },
     "rpr": {
         "base": [],
         "noadj": ["S3R_BWD_ADJ=0"],
@@ -91,6 +95,8 @@ if __name__ == "__main__":
         for name in variants:
             env = dict(os.environ, S3R_LIB=os.path.join(ROOT, "paper_2503_08217_b200",
                                                         f"libs3r_{name}.so"))
+            if name.startswith("ov"):
+                env["S3R_OVERLAP"] = "1"
             r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3",
                                 "--no-e2e", "--no-cpu-baseline", "--pool", "1"], cwd=ROOT,
                                env=env, capture_output=True, text=True, timeout=400)
