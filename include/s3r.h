@@ -227,6 +227,18 @@ int s3r_render_batch(s3r_ctx* ctx, const s3r_scene* scene, const s3r_view* views
  * for workloads whose front stages dominate.                               */
 int s3r_set_overlap(s3r_ctx* ctx, int enable);
 
+/* Fast exponential (default off): the rasterizer (K7, Eq.2's exp) evaluates
+ * 2^x with the SFU's ex2.approx.ftz (<= 2 ulp) instead of the R-ARITH
+ * polynomial of DESIGN.md §4; the SFU runs beside the FP32 pipe that bounds
+ * the blend.  Images are then NOT bit-identical to the oracle: RGB and final T
+ * stay within 1e-4 (include-then-stop bounds a flipped termination by the
+ * remaining T < 1e-4), depth within 1e-4 * (the largest splat depth of the
+ * pixel's list) at such flips (reading R24).  Everything before K7
+ * (decisions, order, life, stats) is unaffected.  Training renders
+ * (s3r_set_training) always use the exact exponential, since the backward
+ * recomputes alpha with it.  Returns S3R_EINVAL for a NULL ctx.             */
+int s3r_set_fast_exp(s3r_ctx* ctx, int enable);
+
 /* Same as s3r_render_batch, but every pointer of scene, views (including
  * instance_w2c) and outs is a HOST pointer (page-locked memory recommended).
  * The library copies the inputs to device scratch, renders, copies the

@@ -105,7 +105,19 @@ __device__ __forceinline__ float2 o_exp2_x2(float2 x, float o, float c0)
     return __fmul2_rn(y, osc);
 }
 
-template <bool COUNT, bool TRAIN>
+// Fast-exponential mode (s3r_set_fast_exp): 2^x from the SFU's ex2.approx.ftz
+// (MUFU.EX2, <= 2 ulp) instead of the R-ARITH polynomial.  The MUFU pipe runs
+// beside the FP32 pipe, so the 8 FP32 instructions per pair of the polynomial
+// leave the blend's bottleneck (A/B, C3: raster 11.9 vs 14.6 ms).  Not
+// bit-exact with the oracle (R24).
+__device__ __forceinline__ float ex2_sfu(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <bool COUNT, bool TRAIN, bool FAST>
 __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
@@ -299,7 +311,9 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
 #else
                     if (onx || ony) {
 #endif
-                        const float2 og = o_exp2_x2(e2, q0.w, c0);
+                        const float2 og = FAST
+                            ? __fmul2_rn(make_float2(ex2_sfu(e2.x), ex2_sfu(e2.y)), f2(q0.w))
+                            : o_exp2_x2(e2, q0.w, c0);
                         const float2 alpha = make_float2(onx ? fminf(0.99f, og.x) : 0.0f,
                                                          ony ? fminf(0.99f, og.y) : 0.0f);
                         const float2 w = __fmul2_rn(alpha, T[P]);
@@ -372,12 +386,17 @@ void launch_raster(const RasterArgs& args, cudaStream_t st)
     RasterArgs a = args;
     a.exp2_c0 = 1.3264695880934596e-3f;
     dim3 grid(a.max_tiles, a.n_views);
-    if (a.evals) {
-        if (a.train_T) k_raster<true, true><<<grid, RT, 0, st>>>(a);
-        else k_raster<true, false><<<grid, RT, 0, st>>>(a);
+    // training renders always take the exact R-ARITH exponential: the backward
+    // recomputes alpha with it and relies on the forward's decisions
+    if (a.train_T) {
+        if (a.evals) k_raster<true, true, false><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, true, false><<<grid, RT, 0, st>>>(a);
+    } else if (a.fast_exp) {
+        if (a.evals) k_raster<true, false, true><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, false, true><<<grid, RT, 0, st>>>(a);
     } else {
-        if (a.train_T) k_raster<false, true><<<grid, RT, 0, st>>>(a);
-        else k_raster<false, false><<<grid, RT, 0, st>>>(a);
+        if (a.evals) k_raster<true, false, false><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, false, false><<<grid, RT, 0, st>>>(a);
     }
 }
 

@@ -84,6 +84,7 @@ struct s3r_ctx {
     cudaStream_t twin_stream = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool overlap = false;
+    bool fast_exp = false;                   // s3r_set_fast_exp: SFU ex2 in K7
     std::vector<cudaEvent_t> chunk_done;
     bool host_chunked = false;               // last render was a chunked host batch
     std::vector<Buf> m_tab, m_rgb, m_depth, m_T, m_vis;
@@ -633,6 +634,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         }
         a.train_T = c->training ? P<float>(c->d_train_T) : nullptr;
         a.train_n = c->training ? P<int>(c->d_train_n) : nullptr;
+        a.fast_exp = c->fast_exp ? 1 : 0;
         launch_raster(a, st);
         ev_end(c, st, e);
         c->last_counters = a.evals != nullptr;
@@ -823,6 +825,7 @@ int s3r_render_batch(s3r_ctx* c, const s3r_scene* scene, const s3r_view* views, 
     }
     s3r_ctx* t = c->twin;
     t->pipeline = c->pipeline;
+    t->fast_exp = c->fast_exp;
     for (int a = 0; a < 3; ++a) t->lod_jitter[a] = c->lod_jitter[a];
     if (t->timing != c->timing) s3r_set_timing(t, c->timing);
     CU(cudaEventRecord(c->fork_ev, st));
@@ -1128,6 +1131,13 @@ int s3r_set_overlap(s3r_ctx* c, int enable)
 {
     if (!c) return S3R_EINVAL;
     c->overlap = enable != 0;
+    return S3R_OK;
+}
+
+int s3r_set_fast_exp(s3r_ctx* c, int enable)
+{
+    if (!c) return S3R_EINVAL;
+    c->fast_exp = enable != 0;
     return S3R_OK;
 }
 

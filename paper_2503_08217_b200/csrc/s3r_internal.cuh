@@ -282,6 +282,7 @@ struct RasterArgs {
     float* train_T;              // per pixel final T (training) or NULL, at V.pix_off
     int* train_n;                // per pixel blended list entries (training), at V.pix_off
     float exp2_c0;               // 1.3264695880934596e-3f (set by launch_raster)
+    int fast_exp;                // 1: SFU ex2.approx instead of R-ARITH (not for training)
 };
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 

@@ -32,7 +32,7 @@ EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_se
            "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
            "s3r_life_flip", "s3r_check", "s3r_set_training", "s3r_render_backward",
            "s3r_mse", "s3r_set_pipeline", "s3r_set_lod_jitter", "s3r_set_neural_colors",
-           "s3r_set_overlap"]
+           "s3r_set_overlap", "s3r_set_fast_exp"]
 S3R_PIPELINE_STREAMLINED, S3R_PIPELINE_CONVENTIONAL = 0, 1
 
 
@@ -126,6 +126,7 @@ def lib():
                 "s3r_set_training": (I, [P, I]),
                 "s3r_set_pipeline": (I, [P, I]),
                 "s3r_set_overlap": (I, [P, I]),
+                "s3r_set_fast_exp": (I, [P, I]),
                 "s3r_set_lod_jitter": (I, [P, C.c_float, C.c_float, C.c_float]),
                 "s3r_set_neural_colors": (I, [P, P, P]),
                 "s3r_render_backward": (I, [P, P, P, C.c_int32, P, P, P]),
@@ -329,6 +330,11 @@ class Context:
     def set_overlap(self, on: bool):
         """Overlapped batch halves (s3r_set_overlap); off by default."""
         self._check(self.L.s3r_set_overlap(self.h, int(on)))
+
+    def set_fast_exp(self, on: bool):
+        """SFU ex2.approx in the rasterizer (s3r_set_fast_exp); off by default.
+        Images within 1e-4 of the oracle instead of bit-identical."""
+        self._check(self.L.s3r_set_fast_exp(self.h, int(on)))
 
     def set_lod_jitter(self, dx: float, dy: float, dz: float):
         """NEXT-3: LOD noisy offset scale [dx, dy, dz] (Eq.7 row 4); 0 = off."""

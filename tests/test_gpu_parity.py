@@ -706,3 +706,37 @@ def test_overlapped_batch_halves(ctx):
     for g, w in zip(got, want):
         for k in ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped", "n_rendered", "n_pairs"):
             assert g[k] == w[k], k
+
+
+@pytest.mark.parametrize("case", ["dynamic", "street"])
+def test_fast_exp_within_tolerance(ctx, case):
+    """s3r_set_fast_exp (SFU ex2.approx in K7, R24): everything
+    before the rasterizer stays bit-exact; RGB and final T within 1e-4 of the
+    oracle; depth within 1e-4 x the deepest rendered splat (a flipped
+    termination moves depth by at most T_min x z); flips are rare."""
+    if case == "dynamic":
+        scene, views = sg.make_random_dynamic(5, 3000, 4, 300, 203, 141, 4, lod=(3.0, 0.6, 12.0))
+    else:
+        scene, views = sg.make_config("street", scale=0.1, n_views=3)
+    ctx.set_fast_exp(True)
+    try:
+        _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    finally:
+        ctx.set_fast_exp(False)
+    assert rc == 0
+    n_px = n_off = 0
+    for vi, v in enumerate(views):
+        o = oracle.render_view(scene, v, "f32", table=tabs[vi].cpu().numpy())
+        st = ctx.stats(vi)
+        for k in ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped", "n_rendered", "n_pairs"):
+            assert st[k] == o["stats"][k]
+        assert np.array_equal(outs[vi]["visible"].cpu().numpy(), o["visible"])
+        rgb, dep, T = (outs[vi][k].cpu().numpy() for k in ("rgb", "depth", "final_T"))
+        assert np.abs(rgb - o["rgb"]).max() <= IMG_TOL
+        assert np.abs(T - o["final_T"]).max() <= IMG_TOL
+        rend = o["flags"] & oracle.F_RENDERED
+        zmax = float(np.max(o["splat_keys"][rend != 0, 2])) if rend.any() else 0.0
+        assert np.abs(dep - o["depth"]).max() <= IMG_TOL * max(zmax, 1.0)
+        n_px += rgb.shape[0] * rgb.shape[1]
+        n_off += int((np.abs(rgb - o["rgb"]).max(-1) > 1e-5).sum())
+    assert n_off <= 1e-3 * n_px, (n_off, n_px)

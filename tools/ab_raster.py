@@ -40,6 +40,10 @@ VARIANT_SETS = {
         "base": [],
         "adj": ["S3R_RASTER_ADJ=1"],
     },
+    "mufu": {
+        "base": [],
+        "mufu": ["S3R_RASTER_MUFU=1"],
+    },
     "ov": {
         "base": [],
         "ov": [],
