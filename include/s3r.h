@@ -65,8 +65,12 @@ enum {
                            ("ID in Z"); reported by s3r_check          */
     S3R_ENOMEM = -3,    /* scratch allocation failed                          */
     S3R_ECUDA = -4,     /* a CUDA runtime error; see s3r_last_error           */
-    S3R_ESTATE = -5     /* call out of order (e.g. dump without a render, or
+    S3R_ESTATE = -5,    /* call out of order (e.g. dump without a render, or
                            debug data requested without s3r_set_debug)        */
+    S3R_EINTERNAL = -6  /* an internal self-check failed (with s3r_set_debug
+                           on: K2's conservative frustum pre-test culled a
+                           Gaussian the exact test found visible); reported
+                           by s3r_check; a library bug, never expected        */
 };
 
 typedef struct s3r_ctx s3r_ctx;

@@ -324,6 +324,67 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
     s.flags |= F_RENDERED;
 }
 
+#ifndef S3R_K2_PRECULL
+#define S3R_K2_PRECULL 1
+#endif
+// Conservative frustum pre-test (changes no result): true only when the
+// Gaussian is certainly invisible, so the exact path (quaternion
+// normalisation, ~10 IEEE divisions, 3 square roots) is skipped for the
+// in-front Gaussians outside the view.  Bound (exact arithmetic):
+//   lambda'_max <= a + c + 0.3,  a + c = |J T|_F^2 <= |J|_F^2 |M3|_F^2 (sx^2+sy^2+sz^2)
+// (R_q orthonormal; Cauchy-Schwarz per entry also bounds the fp32-computed a, c
+// to within a few ulps), |J|_F^2 = (fx/z)^2 (1 + uc^2) + (fy/z)^2 (1 + vc^2), so
+// r_f = ceil(3 sqrt(lambda')) <= 3 sqrt(bound) + 1.  Approximate reciprocal /
+// sqrt are used here; the 1 % + 2 px + 1e-4 |m| slack covers their error and
+// the rounding of mx = fx u + cx.  Non-finite values never cull (every compare
+// is false), so such Gaussians take the exact path.  With debug dumps on, the
+// exact path still runs and a visible Gaussian the pre-test had culled sets
+// ERR_PRECULL (a self-check the parity tests read through s3r_check).
+__device__ __forceinline__ float rcp_apx(float x)
+{
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_apx(float x)
+{
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ bool surely_outside(const float* __restrict__ M, float4 mo, float4 sc,
+                                               const DevView& V, float lox, float hix,
+                                               float loy, float hiy)
+{
+    float p[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        float acc = __fmaf_rn(M[4 * r + 0], mo.x, M[4 * r + 3]);
+        acc = __fmaf_rn(M[4 * r + 1], mo.y, acc);
+        acc = __fmaf_rn(M[4 * r + 2], mo.z, acc);
+        p[r] = acc;
+    }
+    const float z = p[2];
+    if (!(z > V.near_plane)) return false;       // the exact path rejects it cheaply
+    const float iz = rcp_apx(z);
+    const float u = p[0] * iz, v = p[1] * iz;
+    const float uc = fminf(fmaxf(u, lox), hix), vc = fminf(fmaxf(v, loy), hiy);
+    const float fz = V.fx * iz, gz = V.fy * iz;
+    const float j2 = __fmaf_rn(fz * fz, __fmaf_rn(uc, uc, 1.0f), (gz * gz) * __fmaf_rn(vc, vc, 1.0f));
+    float m2 = 0.0f;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) m2 = __fmaf_rn(M[4 * r + c], M[4 * r + c], m2);
+    const float s2 = __fmaf_rn(sc.x, sc.x, __fmaf_rn(sc.y, sc.y, sc.z * sc.z));
+    const float lam = __fmaf_rn((j2 * m2) * s2, 1.01f, 0.31f);
+    const float mx = __fmaf_rn(V.fx, u, V.cx), my = __fmaf_rn(V.fy, v, V.cy);
+    const float rb = __fmaf_rn(3.03f, sqrt_apx(lam), 3.0f) +
+                     1e-4f * (fabsf(mx) + fabsf(my));
+    return mx - rb > (float)(V.W - 1) || mx + rb < 0.0f || my - rb > (float)(V.H - 1) ||
+           my + rb < 0.0f;
+}
+
 #ifndef S3R_K2_MINB
 #define S3R_K2_MINB 4     // 64 registers (A/B: K2 0.91 ms vs 1.03 at 3, 1.40 at 2)
 #endif
@@ -363,8 +424,92 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     const unsigned lt = (1u << lane) - 1u;
 
     unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0, c_spairs = 0;
+#if S3R_K2_PRECULL
+    // ---- pass A: the conservative pre-test over the CTA's PTILE entries; the
+    // entries it cannot reject (and, with debug dumps, all valid ones, bit 15 =
+    // "the pre-test would have culled it") are queued in shared memory, so that
+    // pass B runs the exact path on dense warps (the visible Gaussians are
+    // scattered through the index list: without the queue nearly every warp
+    // holds one and pays the full path for all 32 lanes) ----
+    __shared__ uint16_t s_q[PTILE];
+    __shared__ uint32_t s_g[PTILE];
+    __shared__ int s_qn;
+    if (tid == 0) s_qn = 0;
+    __syncthreads();
+    // all PR rounds' loads are issued before any test: two dependent load
+    // latencies per CTA instead of two per round
+    long long gA[PR];
+    int idA[PR];
+    float4 scA[PR], moA[PR];
+#pragma unroll
     for (int rd = 0; rd < PR; ++rd) {
         const long long i = i0 + rd * PT + tid;
+        gA[rd] = i < n_t ? (long long)tl[i] : -1ll;
+    }
+#pragma unroll
+    for (int rd = 0; rd < PR; ++rd) idA[rd] = gA[rd] >= 0 ? __ldg(a.ids + gA[rd]) : 0;
+#pragma unroll
+    for (int rd = 0; rd < PR; ++rd) {
+        const long long g = max(gA[rd], 0ll);
+        scA[rd] = __ldg(a.scales + g);
+        moA[rd] = a.world_mo ? __ldg(a.world_mo + (long long)vi * a.n + g)
+                             : __ldg(a.means_opacity + g);
+    }
+#pragma unroll
+    for (int rd = 0; rd < PR; ++rd) {
+        const int li = rd * PT + tid;
+        const long long i = i0 + li;
+        bool keep = false;
+        uint16_t tag = (uint16_t)li;
+        if (i < n_t) {
+            const int id = idA[rd];
+            if (id < 0 || id >= K1) {
+                c_bad++;
+                if (a.dbg_flags) {
+                    const long long di = V.dbg_off + i;
+                    a.dbg_flags[di] = F_TEMPORAL | F_BADID;
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) a.dbg_keys[6 * di + j] = __int_as_float(0x7fc00000);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) a.dbg_rect[4 * di + j] = 0;
+                }
+            } else {
+                const bool out = surely_outside(s_tab + 12 * (a.world_mo ? 0 : id), moA[rd],
+                                                scA[rd], V, lox, hix, loy, hiy);
+                keep = !out || a.dbg_flags;
+                if (out) tag |= 0x8000u;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        int qb = 0;
+        if (lane == 0 && bal) qb = atomicAdd(&s_qn, __popc(bal));
+        qb = __shfl_sync(0xffffffffu, qb, 0);
+        if (keep) {
+            s_q[qb + __popc(bal & lt)] = tag;
+            s_g[qb + __popc(bal & lt)] = (uint32_t)gA[rd];
+        }
+    }
+    __syncthreads();
+    const int qn = s_qn;
+    for (int qbase = 0; qbase < qn; qbase += PT) {
+        const int qi = qbase + tid;
+        const uint16_t tag = qi < qn ? s_q[qi] : (uint16_t)0;
+        const long long i = qi < qn ? i0 + (tag & 0x7fff) : n_t;
+        const bool culled = tag & 0x8000u;
+        Splat sp;
+        sp.flags = 0;
+        long long g = -1;
+        int gid_id = 0;
+        float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < n_t) {
+            g = s_g[qi];
+            const int id = __ldg(a.ids + g);
+            gid_id = id;
+            {
+#else
+    for (int rd = 0; rd < PR; ++rd) {
+        const long long i = i0 + rd * PT + tid;
+        const bool culled = false;
         Splat sp;
         sp.flags = 0;
         long long g = -1;
@@ -380,6 +525,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
                 for (int j = 0; j < 6; ++j) sp.k[j] = __int_as_float(0x7fc00000);
                 c_bad++;
             } else {
+#endif
                 const float4 sc = __ldg(a.scales + g);
                 float4 mo, q;
                 int slot = id;
@@ -393,6 +539,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
                     q = __ldg(a.rotations + g);
                 }
                 project_one(s_tab + 12 * slot, mo, sc, q, V, lox, hix, loy, hiy, g, sp);
+                if (culled && (sp.flags & F_VISIBLE)) atomicOr(a.err, ERR_PRECULL);
                 if (sp.flags & F_VISIBLE) {
                     c_vis++;
                     if (vis_out) vis_out[g] = 1;

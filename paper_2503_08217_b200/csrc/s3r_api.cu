@@ -1259,6 +1259,8 @@ int s3r_check(s3r_ctx* c, void* stream)
         CU(cudaMemset(c->twin->d_err.p, 0, sizeof e2));
         e |= e2;
     }
+    if (e & ERR_PRECULL)
+        return fail(c, S3R_EINTERNAL, "K2 frustum pre-test culled a visible Gaussian");
     if (e & ERR_BADID) return fail(c, S3R_EINSTANCE, "a Gaussian had an out-of-range instance id");
     return S3R_OK;
 }

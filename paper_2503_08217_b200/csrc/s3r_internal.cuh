@@ -101,6 +101,7 @@ constexpr uint8_t F_TEMPORAL = 1, F_VISIBLE = 2, F_SMALL = 4, F_DROPPED = 8,
 
 // Device error bits
 constexpr uint32_t ERR_BADID = 1;
+constexpr uint32_t ERR_PRECULL = 2;   // K2 pre-test culled a visible Gaussian (debug self-check)
 
 // Per-view descriptor in device memory (one per view of a batch).
 struct DevView {

@@ -22,7 +22,8 @@ _SO = os.environ.get("S3R_LIB") or os.path.join(_HERE, "libs3r.so")   # S3R_LIB:
 _lock = threading.Lock()
 _lib = None
 
-S3R_OK, S3R_EINVAL, S3R_EINSTANCE, S3R_ENOMEM, S3R_ECUDA, S3R_ESTATE = 0, -1, -2, -3, -4, -5
+S3R_OK, S3R_EINVAL, S3R_EINSTANCE, S3R_ENOMEM, S3R_ECUDA, S3R_ESTATE, S3R_EINTERNAL = \
+    0, -1, -2, -3, -4, -5, -6
 STAGES = ["filter", "project", "depth_sort", "bin", "raster", "color"]
 TILE = 16
 # every symbol include/s3r.h declares

@@ -580,6 +580,41 @@ def test_run_to_run_determinism(ctx):
     assert torch.equal(ds1.life, ds2.life)
 
 
+@pytest.mark.parametrize("cfg", ["street", "av2_small"])
+def test_precull_changes_nothing(ctx, cfg):
+    """K2's conservative frustum pre-test (k_project.cu surely_outside) only
+    skips Gaussians the exact test rejects: with debug dumps on the exact path
+    runs for every Gaussian and s3r_check reports S3R_EINTERNAL if the pre-test
+    would have culled a visible one; without debug the pre-test is live, and the
+    outputs (M_t, images, life, counts) must be bit-identical to the debug run."""
+    if cfg == "street":
+        scene, views = sg.make_config("street")
+        views = views[::10]
+    else:   # the C3 ring rig (7 cameras, ~1/7 of the in-front Gaussians visible)
+        scene, views = sg.make_config("av2", scale=0.1, n_views=14, width=388, height=512)
+    ds1, tabs, o1, _ = gpu_render(ctx, scene, views)
+    assert ctx.check() == 0
+    st1 = [ctx.stats(i) for i in range(len(views))]
+    c2 = s3r.Context(0)
+    try:
+        ds2 = s3r.DeviceScene.from_numpy(scene, life=True)
+        o2 = s3r.alloc_outputs(views, n_visible=scene.n)
+        c2.set_counters(True)
+        c2.render_batch(ds2, views, list(tabs), o2)
+        torch.cuda.synchronize()
+        assert c2.check() == 0
+        for i in range(len(views)):
+            st2 = c2.stats(i)
+            for k in ("n_temporal", "n_visible", "n_rendered", "n_pairs"):
+                assert st1[i][k] == st2[k], (i, k)
+    finally:
+        c2.close()
+    for a, b in zip(o1, o2):
+        for k in ("rgb", "depth", "final_T", "visible"):
+            assert torch.equal(a[k], b[k]), k
+    assert torch.equal(ds1.life, ds2.life)
+
+
 @pytest.mark.slow
 def test_scaling_acceptance():
     """S:642 / S:682 acceptance 4 (the qualitative Fig.4 claim): with

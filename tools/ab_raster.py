@@ -79,6 +79,12 @@ VARIANT_SETS = {
         "rp8m20": ["S3R_BWD_RPIX=8", "S3R_BWD_MINB=20"],
         "rp8m24": ["S3R_BWD_RPIX=8", "S3R_BWD_MINB=24"],
     },
+    "front": {
+        "base": [],
+        "noprecull": ["S3R_K2_PRECULL=0"],
+        "k2m3": ["S3R_K2_MINB=3"],
+        "k2m5": ["S3R_K2_MINB=5"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
@@ -102,7 +108,9 @@ if __name__ == "__main__":
             if name.startswith("ov"):
                 env["S3R_OVERLAP"] = "1"
             r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3",
-                                "--no-e2e", "--no-cpu-baseline", "--pool", "1"], cwd=ROOT,
+                                "--no-e2e", "--no-cpu-baseline", "--pool", "1"] +
+                               (["--no-train", "--no-neurf", "--no-conventional", "--no-fast-exp"]
+                                if os.environ.get("AB_FWD_ONLY") else []), cwd=ROOT,
                                env=env, capture_output=True, text=True, timeout=400)
             try:
                 d = json.loads(r.stdout.strip().splitlines()[-1])
