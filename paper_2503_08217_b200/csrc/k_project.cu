@@ -16,12 +16,16 @@
 // Layout: grid (CTA, view); one CTA walks 4 x 256 consecutive entries of its
 // view's temporal index list (coalesced 4-byte index loads, then 16-byte
 // gathers of the SoA float4 streams).  The view's (K+1) x 3x4 camera table is
-// staged in shared memory once per CTA.  Rendered splats are compacted with
-// ballot/popc inside the CTA and ONE atomic per CTA-round on the view's
-// counter, into 48-byte records {mx,my,z,o}{qa,qb,qc,rect.x}{r,g,b,rect.y}, a
-// 64-bit depth key (depth bits << gbits | Gaussian index).  The record order
-// is therefore not deterministic; the depth sort (K5a) on those keys restores
-// the unique (depth, index) order, so everything downstream is deterministic.
+// staged in shared memory once per CTA.  A conservative frustum pre-test
+// queues the entries it cannot reject, and the exact path runs on those in
+// dense warps.  Rendered splats are compacted with ballot/popc and ONE atomic
+// per warp-round on the view's counter, into 48-byte records
+// {mx,my,z,o}{qa,qb,qc,rect.x}{r,g,b,rect.y} and a 64-bit depth key (depth
+// bits << gbits | Gaussian index).  The record order is therefore not
+// deterministic; the depth sort (K5a) on those keys restores the unique
+// (depth, index) order, so everything downstream is deterministic.  (Equal
+// depths are common: a car face seen along a camera axis has thousands of
+// Gaussians at one fp32 depth, so the index bits cannot be left to a fix-up.)
 #include <algorithm>
 
 #include "s3r_internal.cuh"

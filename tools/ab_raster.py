@@ -85,6 +85,10 @@ VARIANT_SETS = {
         "k2m3": ["S3R_K2_MINB=3"],
         "k2m5": ["S3R_K2_MINB=5"],
     },
+    "bin": {
+        "base": [],
+        "scat0": ["S3R_SCATTER_MASK=0"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
