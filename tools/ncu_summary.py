@@ -19,7 +19,12 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
         "smsp__inst_executed.sum", "launch__grid_size", "launch__block_size",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"]
+        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "smsp__warps_active.avg.per_cycle_active", "smsp__warps_eligible.avg.per_cycle_active"] + [
+        f"smsp__average_warps_issue_stalled_{r}_per_issue_active.ratio"
+        for r in ("wait", "not_selected", "math_pipe_throttle", "long_scoreboard",
+                  "short_scoreboard", "barrier", "mio_throttle", "lg_throttle")]
 
 
 def summarise(rep):

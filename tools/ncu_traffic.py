@@ -20,7 +20,11 @@ def nbytes(s: str) -> float:
 src = sys.argv[1]
 workload = sys.argv[2] if len(sys.argv) > 2 else "av2"
 d = json.load(open(src))
-out = {}
+# kernels this capture does not cover keep their entry from an earlier capture
+try:
+    out = json.load(open("profiles/ncu_traffic.json"))
+except FileNotFoundError:
+    out = {}
 for rep, ks in d.items():
     for k in ks:
         name = k["kernel"]
