@@ -37,13 +37,16 @@ namespace {
 #define S3R_BWD_RPIX 8
 #endif
 #ifndef S3R_BWD_MINB
-#define S3R_BWD_MINB 20     // 96 registers at RPIX 8 (A/B: 37.1 ms; 16: 37.3, 24: 45.0)
+#define S3R_BWD_MINB 14     // 128 registers with NOBR (A/B: 31.7 ms; 16: 33.0, 12: 34.3, 18: 34.9)
 #endif
 #ifndef S3R_BWD_ADJ
 #define S3R_BWD_ADJ 0   // adjacent-row pairs: neutral here (A/B 34.17 vs 34.15 ms)
 #endif
 #ifndef S3R_BWD_RPR
 #define S3R_BWD_RPR 1   // records per warp reduction (1 or 2)
+#endif
+#ifndef S3R_BWD_NOBR
+#define S3R_BWD_NOBR 1  // no per-pair skip branch (A/B with MINB 14: 31.7 vs 34.1 ms)
 #endif
 #ifndef S3R_BWD_EX2
 #define S3R_BWD_EX2 0   // 0: exact R-ARITH exp2 on pairs (A/B 35.9 ms); 1, 2: ex2.approx + re-decision (37.0, 36.6)
@@ -273,7 +276,14 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 // (alpha = 0): nothing to differentiate
                 const bool okx = j < last[2 * P] && e2.x >= -24.0f;
                 const bool oky = j < last[2 * P + 1] && e2.y >= -24.0f;
+#if S3R_BWD_NOBR
+                // branch-free: a pair with neither pixel ok gets G = 0 below, which
+                // leaves T, R and every sum bit-identical; the pairs' dependency
+                // chains can then interleave
+                any = any || okx || oky;
+#else
                 if (!(okx || oky)) continue;
+#endif
 #if S3R_BWD_EX2 == 1
                 // hardware exp2 (rel. error ~2^-22); the forward's clamp decision
                 // (o G < 0.99) is re-taken with the exact R-ARITH exp2 whenever
@@ -320,7 +330,9 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 const float2 galpha = __ffma2_rn(Tb, cdot, neg2(rest));
                 Rr[P] = __ffma2_rn(cdot, w, Rr[P]);
                 Tc[P] = Tb;
+#if !S3R_BWD_NOBR
                 any = true;
+#endif
                 s_r = __ffma2_rn(w, gr[P], s_r);
                 s_g = __ffma2_rn(w, gg[P], s_g);
                 s_b = __ffma2_rn(w, gb[P], s_b);

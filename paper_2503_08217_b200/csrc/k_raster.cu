@@ -304,8 +304,16 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                     // has alpha = 0, which leaves C, D and T bit-identical
                     // (fma(c, 0, C) == C, T - 0 == T): such evaluations are skipped
                     // (both of the pair) or get alpha = 0 (one of the pair).
-                    const bool onx = (e2.x >= S3R_FLUSH_E2) && (T[P].x >= 1e-4f);
-                    const bool ony = (e2.y >= S3R_FLUSH_E2) && (T[P].y >= 1e-4f);
+                    const bool livx = T[P].x >= 1e-4f, livy = T[P].y >= 1e-4f;
+                    const bool onx = (e2.x >= S3R_FLUSH_E2) && livx;
+                    const bool ony = (e2.y >= S3R_FLUSH_E2) && livy;
+                    if (TRAIN && !COUNT) {
+                        // the backward's per-pixel bound: the last entry the pixel
+                        // was live at (its terminating one, or a later entry that
+                        // is flushed for it anyway), one select per pixel
+                        stop[2 * P] = livx ? tpos + j : stop[2 * P];
+                        stop[2 * P + 1] = livy ? tpos + j : stop[2 * P + 1];
+                    }
 #if S3R_RASTER_NOBR
                     {   // branch-free: both pixels always evaluated, alpha selected
 #else
@@ -323,7 +331,7 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                         dp[P] = __ffma2_rn(f2(q0.z), w, dp[P]);
                         const float2 Tn = __fadd2_rn(T[P], neg2(w));
                         // include-then-stop (R14): the pixel is dead once T < 1e-4
-                        if (COUNT || TRAIN) {
+                        if (COUNT) {
                             if (onx && Tn.x < 1e-4f) stop[2 * P] = tpos + j + 1;
                             if (ony && Tn.y < 1e-4f) stop[2 * P + 1] = tpos + j + 1;
                         }
@@ -366,7 +374,11 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
         if (V.finalT) V.finalT[pix] = Tk;
         if (TRAIN) {      // state the backward (k_raster_bwd) starts from
             a.train_T[V.pix_off + pix] = Tk;
-            a.train_n[V.pix_off + pix] = stop[k] >= 0 ? stop[k] : tpos;
+            // entries the backward differentiates: [0, train_n).  With COUNT the
+            // terminating entry + 1 (else every entry); otherwise the last live
+            // entry + 1 — the same derivative, since the entries between them are
+            // flushed for the pixel (culled from its warp's list)
+            a.train_n[V.pix_off + pix] = COUNT ? (stop[k] >= 0 ? stop[k] : tpos) : stop[k] + 1;
         }
     }
 }

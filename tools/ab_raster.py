@@ -89,6 +89,26 @@ VARIANT_SETS = {
         "base": [],
         "scat0": ["S3R_SCATTER_MASK=0"],
     },
+    "nobr": {
+        "base": [],
+        "bnobr": ["S3R_BWD_NOBR=1"],
+        "bnobr_m16": ["S3R_BWD_NOBR=1", "S3R_BWD_MINB=16"],
+        "fnobr": ["S3R_RASTER_NOBR=1"],
+    },
+    "nobr2": {
+        "base": [],
+        "m16": ["S3R_BWD_MINB=16"],
+        "bnobr_m16": ["S3R_BWD_NOBR=1", "S3R_BWD_MINB=16"],
+        "bnobr_m14": ["S3R_BWD_NOBR=1", "S3R_BWD_MINB=14"],
+        "bnobr_m12": ["S3R_BWD_NOBR=1", "S3R_BWD_MINB=12"],
+        "bnobr_m18": ["S3R_BWD_NOBR=1", "S3R_BWD_MINB=18"],
+    },
+    "bmb": {
+        "base": [],
+        "m13": ["S3R_BWD_MINB=13"],
+        "m15": ["S3R_BWD_MINB=15"],
+        "m16": ["S3R_BWD_MINB=16"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
