@@ -109,6 +109,19 @@ VARIANT_SETS = {
         "m15": ["S3R_BWD_MINB=15"],
         "m16": ["S3R_BWD_MINB=16"],
     },
+    "rpr2": {
+        "base": [],
+        "rpr2": ["S3R_BWD_RPR=2"],
+        "rpr2m12": ["S3R_BWD_RPR=2", "S3R_BWD_MINB=12"],
+        "rpr2m10": ["S3R_BWD_RPR=2", "S3R_BWD_MINB=10"],
+    },
+    "bin2": {
+        "base": [],
+        "xpf1": ["S3R_XPF=1"],
+        "xpf2": ["S3R_XPF=2"],
+        "scat1d": ["S3R_SCAT2D=0"],
+        "xpf1_scat1d": ["S3R_XPF=1", "S3R_SCAT2D=0"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
