@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
 #define S3R_SCAT2D 1   // scatter: 8 x 4 lane grid over a splat's bins (A/B: bin 1.06 vs 1.15 ms with k / bw, k % bw)
 #endif
 #ifndef S3R_XT
-#define S3R_XT 256     // A/B: bin 1.21 ms vs 1.27 at 512, 1.40 at 128
+#define S3R_XT 128     // A/B (mask expansion): bin 1.025 ms vs 1.059 at 256
 #endif
 constexpr int XT = S3R_XT;
 __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ views,

@@ -37,7 +37,10 @@ namespace {
 #define S3R_K2_WARP_COMPACT 1
 #endif
 constexpr int PT = 256;
-constexpr int PR = 4;                 // rounds of PT entries per CTA
+#ifndef S3R_K2_PR
+#define S3R_K2_PR 4
+#endif
+constexpr int PR = S3R_K2_PR;         // rounds of PT entries per CTA
 constexpr int PTILE = PT * PR;
 
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x)

@@ -51,9 +51,13 @@ constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 #ifndef S3R_RASTER_NOBR
 #define S3R_RASTER_NOBR 0
 #endif
+#ifndef S3R_VOTE_EVERY
+#define S3R_VOTE_EVERY 1     // records per warp-termination vote (A/B: raster 14.65 ms; 2: 15.41, 4: 15.01)
+#endif
 #ifndef S3R_RASTER_PMASK
 #define S3R_RASTER_PMASK 0   // per-pair-block skip (A/B: 15.59 vs 15.14 ms without)
 #endif
+constexpr int kVoteEvery = S3R_VOTE_EVERY;
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
 // Build-time variants (for A/B measurement; the defaults are the product):
@@ -264,6 +268,9 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
         // its warp is live) so that the votes below see the full warp
         if (__any_sync(0xffffffffu, nlive != 0)) {
 #if S3R_RASTER_CLIST
+#if S3R_VOTE_EVERY > 1
+#pragma unroll (kVoteEvery)
+#endif
             for (int jj = 0; jj < nk; ++jj) {
                 const unsigned ent = s_cl[warp][jj];
                 const int j = ent & 0xff;
@@ -338,11 +345,18 @@ __global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
                         T[P] = Tn;
                     }
                 }
+#if S3R_RASTER_CLIST && S3R_VOTE_EVERY > 1
+                // the warp-termination vote every S3R_VOTE_EVERY records (a dead
+                // pixel blends nothing, so later votes only cost evaluations)
+                if ((jj % S3R_VOTE_EVERY) == S3R_VOTE_EVERY - 1 || jj + 1 == nk)
+#endif
+                {
                 float tmax = fmaxf(T[0].x, T[0].y);
 #pragma unroll
                 for (int P = 1; P < NP; ++P) tmax = fmaxf(tmax, fmaxf(T[P].x, T[P].y));
                 nlive = tmax >= 1e-4f ? 1 : 0;
                 if (!__any_sync(0xffffffffu, nlive != 0)) break;   // whole warp done
+                }
             }
         }
         tpos += nb;

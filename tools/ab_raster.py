@@ -122,6 +122,18 @@ VARIANT_SETS = {
         "scat1d": ["S3R_SCAT2D=0"],
         "xpf1_scat1d": ["S3R_XPF=1", "S3R_SCAT2D=0"],
     },
+    "vote": {
+        "base": [],
+        "vote2": ["S3R_VOTE_EVERY=2"],
+        "vote4": ["S3R_VOTE_EVERY=4"],
+        "xt128": ["S3R_XT=128"],
+    },
+    "k2pr": {
+        "base": [],
+        "pr2": ["S3R_K2_PR=2"],
+        "pr8": ["S3R_K2_PR=8"],
+        "pr2m6": ["S3R_K2_PR=2", "S3R_K2_MINB=6"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
