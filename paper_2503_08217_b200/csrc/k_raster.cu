@@ -69,6 +69,9 @@ constexpr int RB = 256;     // splat records staged in shared memory per batch
 #ifndef S3R_RASTER_MINB
 #define S3R_RASTER_MINB 16    // 64 registers, 32 resident warps per SM (A/B: 16.6 vs 17.2 ms)
 #endif
+#ifndef S3R_RASTER_TRAIN_MINB
+#define S3R_RASTER_TRAIN_MINB S3R_RASTER_MINB   // the training forward's bound
+#endif
 #ifndef S3R_FLUSH_E2
 #define S3R_FLUSH_E2 FLUSH_E2
 #endif
@@ -122,7 +125,8 @@ __device__ __forceinline__ float ex2_sfu(float x)
 }
 
 template <bool COUNT, bool TRAIN, bool FAST>
-__global__ void S3R_RASTER_BOUNDS k_raster(RasterArgs a)
+__global__ void __launch_bounds__(RT, TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER_MINB)
+    k_raster(RasterArgs a)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
 #if S3R_RASTER_CLIST

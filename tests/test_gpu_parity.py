@@ -38,6 +38,10 @@ def gpu_render(ctx, scene, views, life=True, visible=True):
     outs = s3r.alloc_outputs(views, n_visible=scene.n if visible else 0)
     rc = ctx.render_batch(ds, views, list(tabs), outs)
     torch.cuda.synchronize()
+    if rc == 0:
+        # the device error word: with debug dumps on (the module's context) this
+        # includes K2's pre-cull self-check (S3R_EINTERNAL raises here)
+        assert ctx.check() == 0
     return ds, tabs, outs, rc
 
 

@@ -134,6 +134,11 @@ VARIANT_SETS = {
         "pr8": ["S3R_K2_PR=8"],
         "pr2m6": ["S3R_K2_PR=2", "S3R_K2_MINB=6"],
     },
+    "trainmb": {
+        "base": [],
+        "tmb14": ["S3R_RASTER_TRAIN_MINB=14"],
+        "tmb12": ["S3R_RASTER_TRAIN_MINB=12"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
