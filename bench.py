@@ -375,10 +375,19 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
     import torch.distributed as dist
     gen = torch.Generator(device=dev)
     gen.manual_seed(5)
+    # the batch's images, targets and image gradients each live in one flat
+    # buffer (per-view slices), so that the MSE is ONE s3r_mse call per step
+    sizes = [v.height * v.width * 3 for v in views]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    rgb_all = torch.empty(int(offs[-1]), device=dev)
+    outs = [dict(o, rgb=rgb_all[offs[i]:offs[i + 1]].view(v.height, v.width, 3))
+            for i, (o, v) in enumerate(zip(outs, views))]
     ctx.render_batch(ds, views, tables, outs)
-    targets = [torch.clamp(o["rgb"] + 0.05 * torch.randn(o["rgb"].shape, generator=gen,
-                                                          device=dev), 0, 1) for o in outs]
-    gimg = [torch.empty_like(o["rgb"]) for o in outs]
+    targets_all = torch.clamp(rgb_all + 0.05 * torch.randn(rgb_all.shape, generator=gen,
+                                                           device=dev), 0, 1)
+    gimg_all = torch.empty_like(rgb_all)
+    gimg = [gimg_all[offs[i]:offs[i + 1]].view(v.height, v.width, 3)
+            for i, v in enumerate(views)]
     grads = {k: torch.zeros_like(getattr(ds, k)) for k in
              ("means_opacity", "scales", "rotations", "colors")}
     # NEXT-1 pose gradient: dL/d(instance camera table) per view and instance
@@ -396,8 +405,7 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
         e_fwd[0].record(stream)
         ctx.render_batch(ds, views, tables, outs)
         e_fwd[1].record(stream)
-        for o, t, g in zip(outs, targets, gimg):
-            ctx.mse(o["rgb"], t, 1.0 / npix, g, loss)
+        ctx.mse(rgb_all, targets_all, 1.0 / npix, gimg_all, loss)
         e_fwd[2].record(stream)
         ctx.render_backward(ds, views, tables, cots, grads)
         e_fwd[3].record(stream)
