@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(KT) k_bin_count(const DevView* __restrict__ vi
 // Thread i owns the contiguous run [i per, (i+1) per): it sums the run, the
 // 1024 run sums are scanned in shared memory, and the run is rewritten from
 // its base (two L1-resident passes instead of one barrier round per 1024
-// elements: A/B 0.31 -> see DESIGN.md §12).
+// elements: 0.31 -> 0.12 ms on C3, then 8 loads in flight per thread).
 __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ views,
                                                    uint32_t* __restrict__ cnt,
                                                    int2* __restrict__ ranges)
@@ -99,8 +99,18 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long per = (n + 1023) / 1024;
     const long long i0 = min(n, (long long)tid * per), i1 = min(n, i0 + per);
+    // loads issued 8 at a time (the run is strided across the warp: each load
+    // is its own L2 transaction, so the latency, not the bytes, is the cost)
     uint32_t x = 0;
-    for (long long i = i0; i < i1; ++i) x += a[i];
+    long long i = i0;
+    for (; i + 8 <= i1; i += 8) {
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c[k] = a[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x += c[k];
+    }
+    for (; i < i1; ++i) x += a[i];
     uint32_t v = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -122,7 +132,17 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
     }
     __syncthreads();
     uint32_t run = s_warp[warp] + v - x;
-    for (long long i = i0; i < i1; ++i) {
+    for (i = i0; i + 8 <= i1; i += 8) {
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c[k] = a[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a[i + k] = run;
+            run += c[k];
+        }
+    }
+    for (; i < i1; ++i) {
         const uint32_t c = a[i];
         a[i] = run;
         run += c;

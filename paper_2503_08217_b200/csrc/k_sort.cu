@@ -21,9 +21,15 @@ namespace s3r {
 namespace {
 constexpr int ST = 256;
 constexpr int SW = ST / 32;
-constexpr int ITEMS32 = 8;
-constexpr int ITEMS64 = 8;
-constexpr int HITEMS = 8;      // histogram tiles == onesweep tiles (2048 keys)
+#ifndef S3R_SORT_ITEMS
+#define S3R_SORT_ITEMS 8
+#endif
+#ifndef S3R_SORT_MINB
+#define S3R_SORT_MINB 4   // 64 registers, 4 CTAs/SM (A/B: depth sort 0.446 ms; 3 (80 regs): 0.481, none (96): 0.564)
+#endif
+constexpr int ITEMS32 = S3R_SORT_ITEMS;
+constexpr int ITEMS64 = S3R_SORT_ITEMS;
+constexpr int HITEMS = S3R_SORT_ITEMS;   // histogram tiles == onesweep tiles (ST * ITEMS keys)
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p)
 {
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(ST) k_hist_scan(uint32_t* __restrict__ hist)
 
 // ------------------------------------------------------------------ onesweep
 template <typename K, bool KV, int ITEMS>
-__global__ void __launch_bounds__(ST) k_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(ST, S3R_SORT_MINB) k_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                  K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                  const Seg* __restrict__ segs, int nsegs,
                                                  const int* __restrict__ seg_tile0,

@@ -139,6 +139,13 @@ VARIANT_SETS = {
         "tmb14": ["S3R_RASTER_TRAIN_MINB=14"],
         "tmb12": ["S3R_RASTER_TRAIN_MINB=12"],
     },
+    "sort": {
+        "base": [],
+        "it4": ["S3R_SORT_ITEMS=4"],
+        "mb3": ["S3R_SORT_MINB=3"],
+        "mb4": ["S3R_SORT_MINB=4"],
+        "it4mb6": ["S3R_SORT_ITEMS=4", "S3R_SORT_MINB=6"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
