@@ -392,59 +392,24 @@ __device__ __forceinline__ bool surely_outside(const float* __restrict__ M, floa
            my + rb < 0.0f;
 }
 
-#ifndef S3R_K2_MINB
-#define S3R_K2_MINB 4     // 64 registers (A/B: K2 0.91 ms vs 1.03 at 3, 1.40 at 2)
-#endif
-__global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
+// Pass A of K2 over one CTA chunk of PTILE temporal-list entries: all PR
+// rounds' loads are issued before any test (two dependent load latencies per
+// chunk instead of two per round); the conservative pre-test (surely_outside)
+// runs on each valid entry, and the entries it cannot reject (and, with debug
+// dumps, all valid ones; tag bit 15 = "the pre-test would have culled it") are
+// appended to (qt, qg) — shared memory, or the chunk's slice of the global
+// survivor list in the split form — through the counter *qn (shared).  Bad
+// instance ids are counted into c_bad (and dumped) here.
+__device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevView& V, int vi,
+                                              long long i0, long long n_t,
+                                              const int32_t* __restrict__ tl,
+                                              const float* __restrict__ s_tab, float lox,
+                                              float hix, float loy, float hiy, uint16_t* qt,
+                                              uint32_t* qg, int* qn, unsigned long long& c_bad)
 {
-    extern __shared__ float s_tab[];          // [K1][12]
-    __shared__ float s_bounds[4];
-#if !S3R_K2_WARP_COMPACT
-    __shared__ uint32_t s_wcnt[PT / 32];
-    __shared__ uint32_t s_base;
-#endif
-    __shared__ unsigned long long s_red[6][PT / 32];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int vi = blockIdx.y;
-    const DevView& V = a.views[vi];
-    const long long n_t = V.n_temporal;
-    const long long i0 = (long long)blockIdx.x * PTILE;
-    if (i0 >= n_t) return;                    // uniform for the CTA
-    const int K1 = a.num_instances;
-    for (int i = tid; i < K1 * 12; i += PT) s_tab[i] = V.table[i];
-    if (tid == 0) {
-        // tangent-plane clamp bounds (reading R5), per view, in R-ARITH order
-        const float Wf = (float)V.W, Hf = (float)V.H;
-        s_bounds[0] = (-(0.15f * Wf) - V.cx) / V.fx;
-        s_bounds[1] = ((1.15f * Wf) - V.cx) / V.fx;
-        s_bounds[2] = (-(0.15f * Hf) - V.cy) / V.fy;
-        s_bounds[3] = ((1.15f * Hf) - V.cy) / V.fy;
-    }
-    __syncthreads();
-    const float lox = s_bounds[0], hix = s_bounds[1], loy = s_bounds[2], hiy = s_bounds[3];
-    const int32_t* tl = a.tidx + (long long)V.tslot * a.idx_stride;
-    const long long cap_off = V.cap_off;
-    const float t = V.t;
-    uint8_t* vis_out = V.visible;
-    ViewCounters* ctr = a.counters + vi;
+    const int tid = threadIdx.x, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
-
-    unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0, c_spairs = 0;
-#if S3R_K2_PRECULL
-    // ---- pass A: the conservative pre-test over the CTA's PTILE entries; the
-    // entries it cannot reject (and, with debug dumps, all valid ones, bit 15 =
-    // "the pre-test would have culled it") are queued in shared memory, so that
-    // pass B runs the exact path on dense warps (the visible Gaussians are
-    // scattered through the index list: without the queue nearly every warp
-    // holds one and pays the full path for all 32 lanes) ----
-    __shared__ uint16_t s_q[PTILE];
-    __shared__ uint32_t s_g[PTILE];
-    __shared__ int s_qn;
-    if (tid == 0) s_qn = 0;
-    __syncthreads();
-    // all PR rounds' loads are issued before any test: two dependent load
-    // latencies per CTA instead of two per round
+    const int K1 = a.num_instances;
     long long gA[PR];
     int idA[PR];
     float4 scA[PR], moA[PR];
@@ -489,18 +454,131 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         int qb = 0;
-        if (lane == 0 && bal) qb = atomicAdd(&s_qn, __popc(bal));
+        if (lane == 0 && bal) qb = atomicAdd(qn, __popc(bal));
         qb = __shfl_sync(0xffffffffu, qb, 0);
         if (keep) {
-            s_q[qb + __popc(bal & lt)] = tag;
-            s_g[qb + __popc(bal & lt)] = (uint32_t)gA[rd];
+            qt[qb + __popc(bal & lt)] = tag;
+            qg[qb + __popc(bal & lt)] = (uint32_t)gA[rd];
         }
     }
+}
+
+// K2 prologue shared by k_precull and k_project: the view's camera table into
+// shared memory and the tangent-plane clamp bounds (reading R5, R-ARITH order)
+__device__ __forceinline__ void stage_view(const ProjectArgs& a, const DevView& V, float* s_tab,
+                                           float* s_bounds)
+{
+    const int tid = threadIdx.x;
+    for (int i = tid; i < a.num_instances * 12; i += PT) s_tab[i] = V.table[i];
+    if (tid == 0) {
+        const float Wf = (float)V.W, Hf = (float)V.H;
+        s_bounds[0] = (-(0.15f * Wf) - V.cx) / V.fx;
+        s_bounds[1] = ((1.15f * Wf) - V.cx) / V.fx;
+        s_bounds[2] = (-(0.15f * Hf) - V.cy) / V.fy;
+        s_bounds[3] = ((1.15f * Hf) - V.cy) / V.fy;
+    }
+}
+
+#ifndef S3R_K2_SPLIT
+#define S3R_K2_SPLIT 0   // 1: K2a + K2b (A/B: project 0.94 vs 0.75 ms on C3, 2.23 vs 1.67 on C4; off)
+#endif
+// K2a (split form): pass A alone, at the occupancy its ~40 registers allow;
+// the survivors of chunk c of view vi go to a.surv_t / a.surv_g at
+// [cap_off + c PTILE, + a.surv_cnt[vi max_tiles + c]).
+#if S3R_K2_SPLIT
+#ifndef S3R_K2A_MINB
+#define S3R_K2A_MINB 6
+#endif
+__global__ void __launch_bounds__(PT, S3R_K2A_MINB) k_precull(ProjectArgs a)
+{
+    extern __shared__ float s_tab[];
+    __shared__ float s_bounds[4];
+    __shared__ int s_qn;
+    __shared__ unsigned long long s_bad;
+    const int vi = blockIdx.y;
+    const DevView& V = a.views[vi];
+    const long long n_t = V.n_temporal;
+    const long long i0 = (long long)blockIdx.x * PTILE;
+    if (i0 >= n_t) return;
+    stage_view(a, V, s_tab, s_bounds);
+    if (threadIdx.x == 0) {
+        s_qn = 0;
+        s_bad = 0;
+    }
+    __syncthreads();
+    const long long off = V.cap_off + i0;
+    unsigned long long c_bad = 0;
+    precull_chunk(a, V, vi, i0, n_t, a.tidx + (long long)V.tslot * a.idx_stride, s_tab,
+                  s_bounds[0], s_bounds[1], s_bounds[2], s_bounds[3], a.surv_t + off,
+                  a.surv_g + off, &s_qn, c_bad);
+    if (c_bad) atomicAdd(&s_bad, c_bad);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.surv_cnt[(long long)vi * a.max_tiles + blockIdx.x] = s_qn;
+        if (s_bad) {
+            atomicAdd(&a.counters[vi].n_bad, s_bad);
+            atomicOr(a.err, ERR_BADID);
+        }
+    }
+}
+#endif
+
+#ifndef S3R_K2_MINB
+#define S3R_K2_MINB 4     // 64 registers (A/B: K2 0.91 ms vs 1.03 at 3, 1.40 at 2)
+#endif
+__global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
+{
+    extern __shared__ float s_tab[];          // [K1][12]
+    __shared__ float s_bounds[4];
+#if !S3R_K2_WARP_COMPACT
+    __shared__ uint32_t s_wcnt[PT / 32];
+    __shared__ uint32_t s_base;
+#endif
+    __shared__ unsigned long long s_red[6][PT / 32];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int vi = blockIdx.y;
+    const DevView& V = a.views[vi];
+    const long long n_t = V.n_temporal;
+    const long long i0 = (long long)blockIdx.x * PTILE;
+    if (i0 >= n_t) return;                    // uniform for the CTA
+    [[maybe_unused]] const int K1 = a.num_instances;
+    stage_view(a, V, s_tab, s_bounds);
+    __syncthreads();
+    const float lox = s_bounds[0], hix = s_bounds[1], loy = s_bounds[2], hiy = s_bounds[3];
+    [[maybe_unused]] const int32_t* tl = a.tidx + (long long)V.tslot * a.idx_stride;
+    const long long cap_off = V.cap_off;
+    const float t = V.t;
+    uint8_t* vis_out = V.visible;
+    ViewCounters* ctr = a.counters + vi;
+    const unsigned lt = (1u << lane) - 1u;
+
+    unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0, c_spairs = 0;
+#if S3R_K2_PRECULL
+    // ---- pass A (precull_chunk) queues the entries the conservative pre-test
+    // cannot reject, so that pass B runs the exact path on dense warps (the
+    // visible Gaussians are scattered through the index list: without the queue
+    // nearly every warp holds one and pays the full path for all 32 lanes).
+    // In the split form K2a (k_precull) has already done it into global memory.
+    __shared__ int s_qn;
+#if S3R_K2_SPLIT
+    const uint16_t* qt = a.surv_t + cap_off + i0;
+    const uint32_t* qg = a.surv_g + cap_off + i0;
+    if (tid == 0) s_qn = a.surv_cnt[(long long)vi * a.max_tiles + blockIdx.x];
+#else
+    __shared__ uint16_t s_q[PTILE];
+    __shared__ uint32_t s_g[PTILE];
+    const uint16_t* qt = s_q;
+    const uint32_t* qg = s_g;
+    if (tid == 0) s_qn = 0;
+    __syncthreads();
+    precull_chunk(a, V, vi, i0, n_t, tl, s_tab, lox, hix, loy, hiy, s_q, s_g, &s_qn, c_bad);
+#endif
     __syncthreads();
     const int qn = s_qn;
     for (int qbase = 0; qbase < qn; qbase += PT) {
         const int qi = qbase + tid;
-        const uint16_t tag = qi < qn ? s_q[qi] : (uint16_t)0;
+        const uint16_t tag = qi < qn ? qt[qi] : (uint16_t)0;
         const long long i = qi < qn ? i0 + (tag & 0x7fff) : n_t;
         const bool culled = tag & 0x8000u;
         Splat sp;
@@ -509,7 +587,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
         int gid_id = 0;
         float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < n_t) {
-            g = s_g[qi];
+            g = qg[qi];
             const int id = __ldg(a.ids + g);
             gid_id = id;
             {
@@ -859,10 +937,16 @@ void launch_project(const ProjectArgs& a, cudaStream_t st)
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(a.max_tiles, a.n_views);
+#if S3R_K2_SPLIT
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_precull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_precull<<<grid, PT, smem, st>>>(a);
+#endif
     k_project<<<grid, PT, smem, st>>>(a);
 }
 
 int project_tile() { return PTILE; }
+bool project_split() { return S3R_K2_PRECULL && S3R_K2_SPLIT; }
 
 void launch_compose(const float* w2c, const float* i2g, int n_views, int K, float* out,
                     cudaStream_t st)

@@ -146,6 +146,12 @@ VARIANT_SETS = {
         "mb4": ["S3R_SORT_MINB=4"],
         "it4mb6": ["S3R_SORT_ITEMS=4", "S3R_SORT_MINB=6"],
     },
+    "split": {
+        "base": [],
+        "nosplit": ["S3R_K2_SPLIT=0"],
+        "k2a4": ["S3R_K2A_MINB=4"],
+        "k2a8": ["S3R_K2A_MINB=8"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
