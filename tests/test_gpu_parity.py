@@ -619,6 +619,17 @@ def test_precull_changes_nothing(ctx, cfg):
     assert torch.equal(ds1.life, ds2.life)
 
 
+def test_large_image_wide_supertiles(ctx):
+    """An image with more than MAX_BINS 4x4 supertiles (4100 x 2100: 257 x 132
+    tiles) bins with 8 x 8 supertiles: the general expansion path and the
+    scatter over wider supertiles, against the oracle element by element."""
+    scene, views = sg.make_config("street", scale=0.05, n_views=2, width=4100, height=2100)
+    _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    assert rc == 0
+    for vi, v in enumerate(views):
+        check_view(ctx, scene, v, tabs[vi], outs[vi], vi)
+
+
 @pytest.mark.slow
 def test_scaling_acceptance():
     """S:642 / S:682 acceptance 4 (the qualitative Fig.4 claim): with
