@@ -152,6 +152,11 @@ VARIANT_SETS = {
         "k2a4": ["S3R_K2A_MINB=4"],
         "k2a8": ["S3R_K2A_MINB=8"],
     },
+    "bex2": {
+        "base": [],
+        "ex2a": ["S3R_BWD_EX2=1"],
+        "ex2b": ["S3R_BWD_EX2=2"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
