@@ -397,8 +397,7 @@ __device__ __forceinline__ bool surely_outside(const float* __restrict__ M, floa
 // chunk instead of two per round); the conservative pre-test (surely_outside)
 // runs on each valid entry, and the entries it cannot reject (and, with debug
 // dumps, all valid ones; tag bit 15 = "the pre-test would have culled it") are
-// appended to (qt, qg) — shared memory, or the chunk's slice of the global
-// survivor list in the split form — through the counter *qn (shared).  Bad
+// appended to the shared-memory queue (qt, qg) through the counter *qn.  Bad
 // instance ids are counted into c_bad (and dumped) here.
 __device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevView& V, int vi,
                                               long long i0, long long n_t,
@@ -463,7 +462,7 @@ __device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevVie
     }
 }
 
-// K2 prologue shared by k_precull and k_project: the view's camera table into
+// K2 prologue: the view's camera table into
 // shared memory and the tangent-plane clamp bounds (reading R5, R-ARITH order)
 __device__ __forceinline__ void stage_view(const ProjectArgs& a, const DevView& V, float* s_tab,
                                            float* s_bounds)
@@ -478,50 +477,6 @@ __device__ __forceinline__ void stage_view(const ProjectArgs& a, const DevView& 
         s_bounds[3] = ((1.15f * Hf) - V.cy) / V.fy;
     }
 }
-
-#ifndef S3R_K2_SPLIT
-#define S3R_K2_SPLIT 0   // 1: K2a + K2b (A/B: project 0.94 vs 0.75 ms on C3, 2.23 vs 1.67 on C4; off)
-#endif
-// K2a (split form): pass A alone, at the occupancy its ~40 registers allow;
-// the survivors of chunk c of view vi go to a.surv_t / a.surv_g at
-// [cap_off + c PTILE, + a.surv_cnt[vi max_tiles + c]).
-#if S3R_K2_SPLIT
-#ifndef S3R_K2A_MINB
-#define S3R_K2A_MINB 6
-#endif
-__global__ void __launch_bounds__(PT, S3R_K2A_MINB) k_precull(ProjectArgs a)
-{
-    extern __shared__ float s_tab[];
-    __shared__ float s_bounds[4];
-    __shared__ int s_qn;
-    __shared__ unsigned long long s_bad;
-    const int vi = blockIdx.y;
-    const DevView& V = a.views[vi];
-    const long long n_t = V.n_temporal;
-    const long long i0 = (long long)blockIdx.x * PTILE;
-    if (i0 >= n_t) return;
-    stage_view(a, V, s_tab, s_bounds);
-    if (threadIdx.x == 0) {
-        s_qn = 0;
-        s_bad = 0;
-    }
-    __syncthreads();
-    const long long off = V.cap_off + i0;
-    unsigned long long c_bad = 0;
-    precull_chunk(a, V, vi, i0, n_t, a.tidx + (long long)V.tslot * a.idx_stride, s_tab,
-                  s_bounds[0], s_bounds[1], s_bounds[2], s_bounds[3], a.surv_t + off,
-                  a.surv_g + off, &s_qn, c_bad);
-    if (c_bad) atomicAdd(&s_bad, c_bad);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        a.surv_cnt[(long long)vi * a.max_tiles + blockIdx.x] = s_qn;
-        if (s_bad) {
-            atomicAdd(&a.counters[vi].n_bad, s_bad);
-            atomicOr(a.err, ERR_BADID);
-        }
-    }
-}
-#endif
 
 #ifndef S3R_K2_MINB
 #define S3R_K2_MINB 4     // 64 registers (A/B: K2 0.91 ms vs 1.03 at 3, 1.40 at 2)
@@ -546,7 +501,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     stage_view(a, V, s_tab, s_bounds);
     __syncthreads();
     const float lox = s_bounds[0], hix = s_bounds[1], loy = s_bounds[2], hiy = s_bounds[3];
-    [[maybe_unused]] const int32_t* tl = a.tidx + (long long)V.tslot * a.idx_stride;
+    const int32_t* tl = a.tidx + (long long)V.tslot * a.idx_stride;
     const long long cap_off = V.cap_off;
     const float t = V.t;
     uint8_t* vis_out = V.visible;
@@ -559,13 +514,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     // cannot reject, so that pass B runs the exact path on dense warps (the
     // visible Gaussians are scattered through the index list: without the queue
     // nearly every warp holds one and pays the full path for all 32 lanes).
-    // In the split form K2a (k_precull) has already done it into global memory.
     __shared__ int s_qn;
-#if S3R_K2_SPLIT
-    const uint16_t* qt = a.surv_t + cap_off + i0;
-    const uint32_t* qg = a.surv_g + cap_off + i0;
-    if (tid == 0) s_qn = a.surv_cnt[(long long)vi * a.max_tiles + blockIdx.x];
-#else
     __shared__ uint16_t s_q[PTILE];
     __shared__ uint32_t s_g[PTILE];
     const uint16_t* qt = s_q;
@@ -573,7 +522,6 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     if (tid == 0) s_qn = 0;
     __syncthreads();
     precull_chunk(a, V, vi, i0, n_t, tl, s_tab, lox, hix, loy, hiy, s_q, s_g, &s_qn, c_bad);
-#endif
     __syncthreads();
     const int qn = s_qn;
     for (int qbase = 0; qbase < qn; qbase += PT) {
@@ -937,16 +885,10 @@ void launch_project(const ProjectArgs& a, cudaStream_t st)
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(a.max_tiles, a.n_views);
-#if S3R_K2_SPLIT
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_precull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_precull<<<grid, PT, smem, st>>>(a);
-#endif
     k_project<<<grid, PT, smem, st>>>(a);
 }
 
 int project_tile() { return PTILE; }
-bool project_split() { return S3R_K2_PRECULL && S3R_K2_SPLIT; }
 
 void launch_compose(const float* w2c, const float* i2g, int n_views, int K, float* out,
                     cudaStream_t st)

@@ -57,7 +57,7 @@ constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 #ifndef S3R_RASTER_PMASK
 #define S3R_RASTER_PMASK 0   // per-pair-block skip (A/B: 15.59 vs 15.14 ms without)
 #endif
-constexpr int kVoteEvery = S3R_VOTE_EVERY;
+[[maybe_unused]] constexpr int kVoteEvery = S3R_VOTE_EVERY;
 constexpr int RB = 256;     // splat records staged in shared memory per batch
 
 // Build-time variants (for A/B measurement; the defaults are the product):

@@ -23,7 +23,6 @@ using namespace s3r;
 namespace s3r {
 int filter_tile();
 int project_tile();
-bool project_split();
 }
 
 namespace {
@@ -70,7 +69,6 @@ struct s3r_ctx {
     cudaStream_t last_stream = nullptr;
     // device scratch
     Buf d_views, d_times, d_tidx, d_counts, d_lb, d_ticket, d_ctr, d_rec, d_dkey, d_gidx,
-        d_surv_t, d_surv_g, d_surv_cnt,
         d_sortk[2], d_sortv[2], d_recs, d_rects, d_lists, d_tlists, d_tranges, d_cnt, d_hist,
         d_dsegs, d_dtile0,
         d_ranges, d_err, d_dbg_keys, d_dbg_flags, d_dbg_rect, d_dbg_tcnt;
@@ -455,14 +453,6 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.dbg_keys = c->debug ? P<float>(c->d_dbg_keys) : nullptr;
         a.dbg_flags = c->debug ? P<uint8_t>(c->d_dbg_flags) : nullptr;
         a.dbg_rect = c->debug ? P<int16_t>(c->d_dbg_rect) : nullptr;
-        if (project_split()) {
-            if ((rc = ensure(c, c->d_surv_t, (size_t)capS * 2))) return rc;
-            if ((rc = ensure(c, c->d_surv_g, (size_t)capS * 4))) return rc;
-            if ((rc = ensure(c, c->d_surv_cnt, (size_t)std::max(nv * k2_tiles, 1) * 4))) return rc;
-            a.surv_t = P<uint16_t>(c->d_surv_t);
-            a.surv_g = P<uint32_t>(c->d_surv_g);
-            a.surv_cnt = P<int>(c->d_surv_cnt);
-        }
         StageEvent e;
         ev_begin(c, S3R_STAGE_PROJECT, st, e);
         launch_project(a, st);
@@ -711,7 +701,7 @@ void s3r_destroy(s3r_ctx* c)
     if (c->join_ev) cudaEventDestroy(c->join_ev);
     Buf* bufs[] = {&c->d_nw, &c->d_nb, &c->d_temb, &c->d_cemb, &c->d_recmu, &c->d_toff,
                    &c->d_wmo, &c->d_wrot, &c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
-                   &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_surv_t, &c->d_surv_g, &c->d_surv_cnt, &c->d_sortk[0], &c->d_sortk[1],
+                   &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
                    &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_rects, &c->d_lists,
                    &c->d_tlists, &c->d_tranges, &c->d_train_T, &c->d_train_n, &c->d_sgrads,
                    &c->d_cots,

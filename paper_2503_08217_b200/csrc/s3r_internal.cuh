@@ -188,11 +188,6 @@ struct ProjectArgs {
     int32_t* gidx;               // [cap] Gaussian index (debug dumps) or NULL
     ViewCounters* counters;      // [n_views]; n_rendered is the compaction cursor
     uint32_t* err;
-    // split K2 (project_split()): K2a's survivors per (view, chunk), laid out
-    // like the temporal lists ([cap_off + chunk PTILE, + count)); NULL: one kernel
-    uint16_t* surv_t;
-    uint32_t* surv_g;
-    int* surv_cnt;               // [n_views][max_tiles]
     // debug (NULL when off)
     float* dbg_keys;
     uint8_t* dbg_flags;
@@ -200,7 +195,6 @@ struct ProjectArgs {
 };
 void launch_project(const ProjectArgs& a, cudaStream_t st);
 int project_tile();
-bool project_split();   // K2 runs as K2a (k_precull) + K2b: a.surv_* are required
 
 // Conventional pipeline (NEXT-2): K0 moves every Gaussian to the world frame
 // of each view's time (views[v].table slot i >= 1 = local->world pose of
