@@ -30,6 +30,17 @@ __device__ __forceinline__ void rect_of(uint2 rr, int& tx0, int& tx1, int& ty0, 
     tx0 = rr.x & 0xffff; tx1 = rr.x >> 16; ty0 = rr.y & 0xffff; ty1 = rr.y >> 16;
 }
 
+// 16-bit mask of the tiles of 4 x 4 supertile (sbx, sby) that the tile
+// rectangle [tx0, tx1] x [ty0, ty1] contains (bit 4 ly + lx)
+__device__ __forceinline__ uint32_t tile_mask4(int tx0, int tx1, int ty0, int ty1, int sbx, int sby)
+{
+    const int lx0 = max(tx0 - 4 * sbx, 0), lx1 = min(tx1 - 4 * sbx, 3);
+    const int ly0 = max(ty0 - 4 * sby, 0), ly1 = min(ty1 - 4 * sby, 3);
+    const uint32_t xm = (2u << lx1) - (1u << lx0);                    // bits lx0..lx1
+    const uint32_t ym = ((1u << (4 * ly1 + 4)) - (1u << (4 * ly0))) & 0x1111u;
+    return xm * ym;                                                   // no carries: xm < 16
+}
+
 // ------------------------------------------------------------------ K3 permute
 // rec_sorted[r] = rec[order[r]] and rect_sorted[r] = its tile rectangle.
 __global__ void __launch_bounds__(256) k_permute(const DevView* __restrict__ views,
@@ -175,9 +186,6 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
 #ifndef S3R_XMASK
 #define S3R_XMASK 1    // 4 x 4 supertiles: per-entry tile masks + 16 ballots
 #endif
-#ifndef S3R_XPF
-#define S3R_XPF 1      // chunks per load batch in the mask expansion (A/B: 1.06 ms; 2: 1.12, 4: 1.41)
-#endif
 #ifndef S3R_SCAT2D
 #define S3R_SCAT2D 1   // scatter: 8 x 4 lane grid over a splat's bins (A/B: bin 1.06 vs 1.15 ms with k / bw, k % bw)
 #endif
@@ -217,35 +225,14 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
         // and per-warp counts exchanged through shared memory order the warps.
         __shared__ int s_wc[XT / 32][16];
         const unsigned lt = (1u << lane) - 1u;
-        constexpr int XPF = S3R_XPF;   // chunks whose loads are issued together
-        for (int base0 = rg.x; base0 < rg.y; base0 += XPF * XT) {
-        uint32_t rr[XPF];
-        uint2 rc[XPF];
-#pragma unroll
-        for (int p = 0; p < XPF; ++p) {
-            const int e = base0 + p * XT + tid;
-            rr[p] = e < rg.y ? lst[e] : 0u;
-        }
-#pragma unroll
-        for (int p = 0; p < XPF; ++p) {
-            const int e = base0 + p * XT + tid;
-            rc[p] = e < rg.y ? rects[rr[p]] : make_uint2(0u, 0u);
-        }
-#pragma unroll
-        for (int p = 0; p < XPF; ++p) {
-            const int base = base0 + p * XT;
-            if (base >= rg.y) break;                  // uniform
+        for (int base = rg.x; base < rg.y; base += XT) {
             const int e = base + tid;
             uint32_t r = 0, m = 0;
             if (e < rg.y) {
-                r = rr[p];
+                r = lst[e];
                 int tx0, tx1, ty0, ty1;
-                rect_of(rc[p], tx0, tx1, ty0, ty1);
-                const int lx0 = max(tx0 - 4 * bx, 0), lx1 = min(tx1 - 4 * bx, 3);
-                const int ly0 = max(ty0 - 4 * by, 0), ly1 = min(ty1 - 4 * by, 3);
-                const uint32_t xm = (2u << lx1) - (1u << lx0);            // bits lx0..lx1
-                const uint32_t ym = ((1u << (4 * ly1 + 4)) - (1u << (4 * ly0))) & 0x1111u;
-                m = xm * ym;                                            // no carries: xm < 16
+                rect_of(rects[r], tx0, tx1, ty0, ty1);
+                m = tile_mask4(tx0, tx1, ty0, ty1, bx, by);
             }
             unsigned bal[16];
 #pragma unroll
@@ -272,7 +259,6 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
             __syncthreads();
             if (warp == 0 && lane < 16) s_tcnt[lane] += mytot;
             __syncthreads();
-        }
         }
     } else
 #endif

@@ -157,6 +157,10 @@ VARIANT_SETS = {
         "ex2a": ["S3R_BWD_EX2=1"],
         "ex2b": ["S3R_BWD_EX2=2"],
     },
+    "lmask": {
+        "base": [],
+        "lmask0": ["S3R_LMASK=0"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
