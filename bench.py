@@ -436,7 +436,8 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
         ms = float(t.item())
     k = args.train_steps
     return {"metric": "training views/s (forward + MSE + backward"
-                      + (" + NCCL grad all-reduce" if world > 1 else "") + ")",
+                      + (f" + {dist.get_backend().upper()} grad all-reduce" if world > 1 else "")
+                      + ")",
             "value": len(views) * world * k / (ms / 1e3), "unit": "views/s",
             "ms_per_step": ms / k, "forward_ms": fwd_ms / k, "backward_ms": bwd_ms / k,
             "loss": float(loss.item()), "views_per_gpu_per_step": len(views), "steps": k,
