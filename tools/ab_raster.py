@@ -161,6 +161,12 @@ VARIANT_SETS = {
         "base": [],
         "lmask0": ["S3R_LMASK=0"],
     },
+    "fnobr": {
+        "base": [],
+        "fnobr": ["S3R_RASTER_NOBR=1"],
+        "fnobr14": ["S3R_RASTER_NOBR=1", "S3R_RASTER_MINB=14"],
+        "fnobr12": ["S3R_RASTER_NOBR=1", "S3R_RASTER_MINB=12"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],

@@ -45,6 +45,8 @@ def summarise(rep):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) < 3 or sys.argv[1].startswith("-"):
+        sys.exit(__doc__)
     res = {r.split("/")[-1]: summarise(r) for r in sys.argv[2:]}
     json.dump(res, open(sys.argv[1], "w"), indent=1)
     print(json.dumps(res, indent=1))
