@@ -391,7 +391,8 @@ int s3r_mse(s3r_ctx* ctx, const float* x, const float* y, int64_t n, float scale
 int s3r_life_flip(s3r_ctx* ctx, float* life, int64_t n, void* stream);
 
 /* Synchronise `stream` and return the device error state accumulated since
- * the last check: S3R_EINSTANCE, S3R_ECUDA or S3R_OK.                      */
+ * the last check: S3R_EINTERNAL (a failed self-check, see the enum),
+ * S3R_EINSTANCE, S3R_ECUDA or S3R_OK.                                      */
 int s3r_check(s3r_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
