@@ -17,6 +17,8 @@
 // the 48-byte records at a time in shared memory; every pixel then blends the
 // batch.  A pixel stops at its termination; the CTA stops when all its pixels
 // have (__syncthreads_count).
+#include <algorithm>
+
 #include "s3r_internal.cuh"
 
 namespace s3r {
@@ -50,6 +52,9 @@ constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 #endif
 #ifndef S3R_RASTER_NOBR
 #define S3R_RASTER_NOBR 0
+#endif
+#ifndef S3R_RASTER_PERSIST
+#define S3R_RASTER_PERSIST 0  // 1: persistent CTAs over an atomic (view, tile) counter (A/B: raster 15.31 vs 14.68 ms on C3, 1.97 vs 1.82 on C2; off)
 #endif
 #ifndef S3R_VOTE_EVERY
 #define S3R_VOTE_EVERY 1     // records per warp-termination vote (A/B: raster 14.65 ms; 2: 15.41, 4: 15.01)
@@ -124,9 +129,9 @@ __device__ __forceinline__ float ex2_sfu(float x)
     return y;
 }
 
+// One (view, tile): the whole K7 computation of the tile's 256 pixels.
 template <bool COUNT, bool TRAIN, bool FAST>
-__global__ void __launch_bounds__(RT, TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER_MINB)
-    k_raster(RasterArgs a)
+__device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, const int tile)
 {
     __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
 #if S3R_RASTER_CLIST
@@ -134,9 +139,7 @@ __global__ void __launch_bounds__(RT, TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER
                                        // (index | pair-block mask << 8)
     __shared__ int s_wc[NW][NW];       // [staging warp][warp block] kept counts
 #endif
-    const int v = blockIdx.y;
     const DevView& V = a.views[v];
-    const int tile = blockIdx.x;
     if (tile >= V.ntiles) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tx = tile % V.TX, ty = tile / V.TX;
@@ -401,6 +404,30 @@ __global__ void __launch_bounds__(RT, TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER
     }
 }
 
+// K7: one CTA per (tile, view) — or, with a.work (S3R_RASTER_PERSIST), a
+// persistent grid whose CTAs take (view, tile) work items from an atomic
+// counter in (view, tile) order
+template <bool COUNT, bool TRAIN, bool FAST>
+__global__ void __launch_bounds__(RT, TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER_MINB)
+    k_raster(RasterArgs a)
+{
+#if !S3R_RASTER_PERSIST
+    raster_tile<COUNT, TRAIN, FAST>(a, blockIdx.y, blockIdx.x);
+#else
+    __shared__ int s_item;
+    const int total = a.max_tiles * a.n_views;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(a.work, 1);
+        __syncthreads();
+        const int w = s_item;
+        __syncthreads();
+        if (w >= total) break;
+        raster_tile<COUNT, TRAIN, FAST>(a, w / a.max_tiles, w % a.max_tiles);
+        __syncthreads();          // shared staging buffers are reused by the next item
+    }
+#endif
+}
+
 // ------------------------------------------------------------------ dumps
 __global__ void k_dump_order(const uint32_t* __restrict__ order, const int32_t* __restrict__ gidx,
                              long long base, long long count, int32_t* __restrict__ out)
@@ -416,6 +443,18 @@ void launch_raster(const RasterArgs& args, cudaStream_t st)
     RasterArgs a = args;
     a.exp2_c0 = 1.3264695880934596e-3f;
     dim3 grid(a.max_tiles, a.n_views);
+#if S3R_RASTER_PERSIST
+    {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (a.train_T) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster<false, true, false>, RT, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster<false, false, false>, RT, 0);
+        grid = dim3((unsigned)std::max(1, sms * per_sm), 1);
+    }
+#else
+    a.work = nullptr;
+#endif
     // training renders always take the exact R-ARITH exponential: the backward
     // recomputes alpha with it and relies on the forward's decisions
     if (a.train_T) {

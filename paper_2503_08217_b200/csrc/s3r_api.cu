@@ -635,6 +635,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.train_T = c->training ? P<float>(c->d_train_T) : nullptr;
         a.train_n = c->training ? P<int>(c->d_train_n) : nullptr;
         a.fast_exp = c->fast_exp ? 1 : 0;
+        a.work = next_ticket(c);          // zeroed per batch; used by the persistent form
         launch_raster(a, st);
         ev_end(c, st, e);
         c->last_counters = a.evals != nullptr;

@@ -284,6 +284,7 @@ struct RasterArgs {
     int* train_n;                // per pixel blended list entries (training), at V.pix_off
     float exp2_c0;               // 1.3264695880934596e-3f (set by launch_raster)
     int fast_exp;                // 1: SFU ex2.approx instead of R-ARITH (not for training)
+    int* work;                   // zeroed work counter (persistent form) or NULL
 };
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 

@@ -167,6 +167,10 @@ VARIANT_SETS = {
         "fnobr14": ["S3R_RASTER_NOBR=1", "S3R_RASTER_MINB=14"],
         "fnobr12": ["S3R_RASTER_NOBR=1", "S3R_RASTER_MINB=12"],
     },
+    "persist": {
+        "base": [],
+        "persist": ["S3R_RASTER_PERSIST=1"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
