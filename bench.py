@@ -697,6 +697,29 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": k_e2e, "api": "s3r_render_batch_host (pinned host buffers)"}
 
+    # ---------------- end of a sweep (Eq.5 merge across ranks, Eq.6 commit): once per
+    # pass over the trajectory, not per step, so timed separately (last: it
+    # changes the scene's intervals)
+    from paper_2503_08217_b200 import parallel
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    if world > 1:
+        parallel.merge_life(ds.life, ctx.life_flip)
+    ctx.commit_visibility(ds, 0.1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sweep_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([sweep_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sweep_ms = float(t.item())
+    sweep_end = {"ms": sweep_ms, "ops": ("life merge: " + dist.get_backend().upper() +
+                                         " all-reduce MAX over 2N floats + " if world > 1 else "")
+                 + "commit (Eq.6, k_commit)", "allreduce_bytes": 8 * scene.n if world > 1 else 0}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "toy":
         cpu = cpu_baseline(args.config)
@@ -737,6 +760,7 @@ def main():
             "conventional": conventional,
             "neurf": neurf_line,
             "fast_exp": fast_exp,
+            "sweep_end": sweep_end,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
