@@ -171,6 +171,10 @@ VARIANT_SETS = {
         "base": [],
         "persist": ["S3R_RASTER_PERSIST=1"],
     },
+    "frange": {
+        "base": [],
+        "frange0": ["S3R_FILTER_RANGE=0"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
