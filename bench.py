@@ -380,8 +380,9 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
     sizes = [v.height * v.width * 3 for v in views]
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     rgb_all = torch.empty(int(offs[-1]), device=dev)
-    outs = [dict(o, rgb=rgb_all[offs[i]:offs[i + 1]].view(v.height, v.width, 3))
-            for i, (o, v) in enumerate(zip(outs, views))]
+    # (the loss is on RGB: the training render writes no depth / final-T images)
+    outs = [{"rgb": rgb_all[offs[i]:offs[i + 1]].view(v.height, v.width, 3)}
+            for i, v in enumerate(views)]
     ctx.render_batch(ds, views, tables, outs)
     targets_all = torch.clamp(rgb_all + 0.05 * torch.randn(rgb_all.shape, generator=gen,
                                                            device=dev), 0, 1)
