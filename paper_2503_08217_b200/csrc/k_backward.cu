@@ -45,6 +45,9 @@ namespace {
 #ifndef S3R_BWD_RPR
 #define S3R_BWD_RPR 1   // records per warp reduction (1 or 2)
 #endif
+#ifndef S3R_BWD_ROWSKIP
+#define S3R_BWD_ROWSKIP 0   // 1: skip a pair whose 4-row band is beyond the flush extent (A/B: 33.7 vs 31.7 ms: the branches stop the pairs interleaving; off)
+#endif
 #ifndef S3R_BWD_NOBR
 #define S3R_BWD_NOBR 1  // no per-pair skip branch (A/B with MINB 14: 31.7 vs 34.1 ms)
 #endif
@@ -142,6 +145,10 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     constexpr float XPAD = 0.5f * (BW - 1) - CULL_HALF_BX;
     const float bcx0 = (float)(tx * TILE) + 0.5f * (BW - 1);     // warp block 0
     const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
+#if S3R_BWD_ROWSKIP
+    static_assert(!S3R_BWD_ADJ && RPIX == 8 && BW == 16, "row bands assume rows py0 + 2k");
+    const float band_c0 = (float)(ty * TILE) + 1.5f;     // centre of pair 0's row band
+#endif
     const s3r_cot C = a.cots[v];
     // the thread's RPIX pixels of one column as RPIX / 2 packed pairs: pair P holds
     // k = 2P (.x) and 2P + 1 (.y); sm_100a FADD2/FMUL2/FFMA2 work on both
@@ -266,8 +273,19 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
             float2 S0 = f2(0.f), S1 = f2(0.f), S2 = f2(0.f), s_z = f2(0.f), s_o = f2(0.f),
                    s_r = f2(0.f), s_g = f2(0.f), s_b = f2(0.f);
             bool any = false;
+#if S3R_BWD_ROWSKIP
+            // pair P of every lane covers the 4-row band [4P, 4P + 3] of the tile:
+            // a band beyond the record's flush-ellipse y extent (q2.w minus the
+            // 16-row block half size, s3r_internal.cuh flush_extent) is flushed
+            // for all its pixels — skipped warp-uniformly
+            const float thr = q2.w - (CULL_HALF_BY - 1.5f);
+            const float dyc = q0.y - band_c0;
+#endif
 #pragma unroll
             for (int P = 0; P < NP; ++P) {
+#if S3R_BWD_ROWSKIP
+                if (fabsf(dyc - 4.0f * P) > thr) continue;
+#endif
                 const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
                 const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
                 const float2 e2raw = __ffma2_rn(dy, c1, f2(a2));

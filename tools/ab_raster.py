@@ -175,6 +175,10 @@ VARIANT_SETS = {
         "base": [],
         "frange0": ["S3R_FILTER_RANGE=0"],
     },
+    "rowskip": {
+        "base": [],
+        "rowskip": ["S3R_BWD_ROWSKIP=1"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
