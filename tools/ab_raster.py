@@ -57,11 +57,6 @@ VARIANT_SETS = {
         "ex2pair": ["S3R_BWD_EX2=2"],
         "exact": ["S3R_BWD_EX2=0"],
     },
-    "xt": {
-        "base": [],
-        "xt256": ["S3R_XT=256"],
-        "xt128": ["S3R_XT=128"],
-    },
     "k2": {
         "base": [],
         "k2m5": ["S3R_K2_MINB=5"],
@@ -178,6 +173,11 @@ VARIANT_SETS = {
     "rowskip": {
         "base": [],
         "rowskip": ["S3R_BWD_ROWSKIP=1"],
+    },
+    "xt": {
+        "base": [],
+        "xt32": ["S3R_XT=32"],
+        "xt64": ["S3R_XT=64"],
     },
     "bwd": {
         "base": [],
