@@ -623,7 +623,9 @@ def test_large_image_wide_supertiles(ctx):
     """An image with more than MAX_BINS 4x4 supertiles (4100 x 2100: 257 x 132
     tiles) bins with 8 x 8 supertiles: the general expansion path and the
     scatter over wider supertiles, against the oracle element by element."""
-    scene, views = sg.make_config("street", scale=0.05, n_views=2, width=4100, height=2100)
+    scene, views = sg.make_config("street", scale=0.05, n_views=3, width=4100, height=2100)
+    # one batch mixing both supertile sizes: the third view is small (4 x 4 supertiles)
+    views[2].width, views[2].height, views[2].cx, views[2].cy = 300, 200, 150.0, 100.0
     _, tabs, outs, rc = gpu_render(ctx, scene, views)
     assert rc == 0
     for vi, v in enumerate(views):
