@@ -179,6 +179,11 @@ VARIANT_SETS = {
         "xt32": ["S3R_XT=32"],
         "xt64": ["S3R_XT=64"],
     },
+    "rmb": {
+        "base": [],
+        "rm14": ["S3R_RASTER_MINB=14"],
+        "rm12": ["S3R_RASTER_MINB=12"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
