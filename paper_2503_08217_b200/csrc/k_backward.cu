@@ -45,6 +45,9 @@ namespace {
 #ifndef S3R_BWD_RPR
 #define S3R_BWD_RPR 1   // records per warp reduction (1 or 2)
 #endif
+#ifndef S3R_POSE_GROUPS
+#define S3R_POSE_GROUPS 4   // instances per warp reduced in registers in k_project_bwd
+#endif
 #ifndef S3R_BWD_ROWSKIP
 #define S3R_BWD_ROWSKIP 0   // 1: skip a pair whose 4-row band is beyond the flush extent (A/B: 33.7 vs 31.7 ms: the branches stop the pairs interleaving; off)
 #endif
@@ -649,16 +652,24 @@ __global__ void __launch_bounds__(256) k_project_bwd(BackwardArgs a)
     const bool act = id >= 0;
     const unsigned am = __ballot_sync(0xffffffffu, act);
     if (am) {
-        const int leader = __ffs(am) - 1;
-        const int idl = __shfl_sync(0xffffffffu, id, leader);
         float* dst = use_smem ? s_gt : gt_view;
-        if (__all_sync(0xffffffffu, !act || id == idl)) {
+        // segmented by instance: up to S3R_POSE_GROUPS instances of the warp are
+        // reduced in registers (one warp sum per value, one atomic by the group's
+        // first lane); splats of further instances add their own values (depth
+        // order mixes instances, but a warp rarely holds more than a few)
+        unsigned rem = am;
+        for (int it = 0; it < S3R_POSE_GROUPS && rem; ++it) {
+            const int leader = __ffs(rem) - 1;
+            const int idl = __shfl_sync(0xffffffffu, id, leader);
+            const bool mine = act && id == idl;
+            rem &= ~__ballot_sync(0xffffffffu, mine);
 #pragma unroll
             for (int j = 0; j < 12; ++j) {
-                const float v = warp_sum(gm12[j]);
+                const float v = warp_sum(mine ? gm12[j] : 0.0f);
                 if (lane == leader) atomicAdd(dst + 12 * idl + j, v);
             }
-        } else if (act) {
+        }
+        if ((rem >> lane) & 1u) {
 #pragma unroll
             for (int j = 0; j < 12; ++j) atomicAdd(dst + 12 * id + j, gm12[j]);
         }

@@ -184,6 +184,11 @@ VARIANT_SETS = {
         "rm14": ["S3R_RASTER_MINB=14"],
         "rm12": ["S3R_RASTER_MINB=12"],
     },
+    "pose": {
+        "base": [],
+        "pg1": ["S3R_POSE_GROUPS=1"],
+        "pg8": ["S3R_POSE_GROUPS=8"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
