@@ -184,3 +184,129 @@ def test_adjoint_with_noisy_offset_matches_central_differences():
     # and the offset matters: the gradient differs from the unmoved render's
     g0 = oracle.backward(s, dataclasses.replace(v, lod_jitter=(0.0, 0.0, 0.0)), wr)
     assert not np.allclose(g0, g)
+
+
+# --------------------------------------------------------------------------
+# The adjoint's piecewise branches (reading R14): pixels where the front splat's
+# alpha is clamped at 0.99 and pixels whose list terminates at T < 1e-4.
+# Central differences of the fp64 forward are valid there as long as the
+# perturbation crosses no branch boundary; the cotangent is restricted to
+# pixels whose margins to every boundary (clamp, termination) exceed the
+# perturbation's effect by orders of magnitude.  The margins are evaluated
+# from the oracle's exported keys with a plain numpy loop (pixel selection
+# only; the pin itself is the finite difference).
+# --------------------------------------------------------------------------
+
+def _stack_scene(seed):
+    """Six near-concentric, mildly anisotropic Gaussians around the non-integer
+    pixel (24.4, 23.7) of a 64x48 view (f = 80): the front one has o = 0.999
+    (alpha clamped near the centre), the others o in [0.90, 0.96] so the centre
+    pixels terminate after 4-5 of them; two low-opacity ones elsewhere."""
+    rng = np.random.default_rng(seed)
+    f, cx, cy = 80.0, 32.0, 24.0
+    zs = [2.0, 2.6, 3.1, 3.7, 4.4, 5.2]
+    ops = [0.999, 0.95, 0.93, 0.96, 0.90, 0.94]
+    pts, sig = [], []
+    for i, z in enumerate(zs):
+        if i == 0:      # the clamped front splat: within 0.1 px of pixel (24, 24)
+            px, py = 24.05 + rng.uniform(-0.04, 0.04), 23.95 + rng.uniform(-0.04, 0.04)
+        else:
+            px, py = 24.4 + rng.uniform(-0.3, 0.3), 23.7 + rng.uniform(-0.3, 0.3)
+        pts.append([(px - cx) * z / f, (py - cy) * z / f, z])
+        sig.append(0.045 * z * rng.uniform(0.85, 1.15, 3))
+    for (px, py, z) in [(50.5, 10.2, 3.0), (44.1, 38.6, 4.0)]:
+        pts.append([(px - cx) * z / f, (py - cy) * z / f, z])
+        sig.append(0.02 * z * np.ones(3))
+        ops.append(0.4)
+    n = len(pts)
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    s = make_scene(np.array(pts), np.array(sig), quats=q, opacity=np.array(ops),
+                   rgb=rng.random((n, 3)))
+    return s, make_view(f, cx, 64, 48, cy=cy), rng
+
+
+def _pixel_margins(s, v):
+    """Per pixel: (clamped anywhere, terminated, min relative margin to the 0.99
+    clamp, min relative margin of T_k to 1e-4) from the f64 keys, in the oracle's
+    depth order (the stack's z are distinct)."""
+    o = oracle.render_view(s, v, "f64")
+    k = o["keys"]
+    rend = np.nonzero(o["flags"] & oracle.F_RENDERED)[0]
+    rend = rend[np.argsort(k[rend, 2])]
+    H, W = v.height, v.width
+    clamp = np.zeros((H, W), bool)
+    term = np.zeros((H, W), bool)
+    mc = np.full((H, W), np.inf)
+    mt = np.full((H, W), np.inf)
+    rect = o["rect"]
+    for py in range(H):
+        for px in range(W):
+            T = 1.0
+            for g in rend:
+                x0, x1, y0, y1 = rect[g]
+                if not (x0 <= px // 16 <= x1 and y0 <= py // 16 <= y1):
+                    continue
+                mx, my, z, a, b, c = k[g]
+                ad, cd = a + 0.3, c + 0.3
+                det = ad * cd - b * b
+                A, B, C = cd / det, -b / det, ad / det
+                dx, dy = mx - px, my - py
+                pw = min(0.0, -0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy)
+                og = float(s.means_opacity[g, 3]) * np.exp(pw)
+                mc[py, px] = min(mc[py, px], abs(og / 0.99 - 1.0))
+                clamp[py, px] |= og >= 0.99
+                T = T * (1.0 - min(0.99, og))
+                mt[py, px] = min(mt[py, px], abs(T / 1e-4 - 1.0))
+                if T < 1e-4:
+                    term[py, px] = True
+                    break
+    return clamp, term, mc, mt
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_adjoint_at_clamped_and_terminated_pixels(seed):
+    s, v, rng = _stack_scene(seed)
+    H, W = v.height, v.width
+    clamp, term, mc, mt = _pixel_margins(s, v)
+    safe = (mc > 2e-3) & (mt > 2e-2)
+    assert (safe & clamp).sum() >= 1 and (safe & term).sum() >= 4
+    mask = safe & (clamp | term)
+    wr = rng.standard_normal((H, W, 3)) * mask[..., None]
+    wd = rng.standard_normal((H, W)) * 0.1 * mask
+    wt = rng.standard_normal((H, W)) * mask * 100.0      # final T ~ 1e-5 there
+    g = oracle.backward(s, v, wr, wd, wt)
+    fd = np.zeros_like(g)
+    for gi in range(s.n):
+        for cols in ATTR.values():
+            for col in cols:
+                arr, c = _field(s, col)
+                x0 = arr[gi, c]
+                h = np.float32(max(abs(float(x0)) * 2e-5, 2e-6))
+                arr[gi, c] = x0 + h
+                xp = float(arr[gi, c])
+                lp = _loss(s, v, wr, wd, wt)
+                arr[gi, c] = x0 - h
+                xm = float(arr[gi, c])
+                lm = _loss(s, v, wr, wd, wt)
+                arr[gi, c] = x0
+                fd[gi, col] = (lp - lm) / (xp - xm)
+    for name, cols in ATTR.items():
+        d = np.abs(g[:, cols] - fd[:, cols]).max()
+        ref = np.abs(fd[:, cols]).max()
+        assert ref > 0
+        assert d <= 1e-3 * ref, (name, d, ref)
+    # the clamped front splat passes no opacity gradient through its clamped
+    # pixels: with the cotangent on those pixels only, dL/do_0 == 0 (FD agrees)
+    only = safe & clamp
+    wr0 = rng.standard_normal((H, W, 3)) * only[..., None]
+    g0 = oracle.backward(s, v, wr0)
+    arr = s.means_opacity
+    x0 = arr[0, 3]
+    h = np.float32(1e-4)
+    arr[0, 3] = x0 + h
+    lp = _loss(s, v, wr0, 0, 0)
+    arr[0, 3] = x0 - h
+    lm = _loss(s, v, wr0, 0, 0)
+    arr[0, 3] = x0
+    assert g0[0, 3] == 0.0 and abs(lp - lm) < 1e-12

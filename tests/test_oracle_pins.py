@@ -639,3 +639,89 @@ def test_exp2_contract():
     for k in range(25):
         assert oracle.exp2_32(-float(k)) == 2.0 ** -k
     assert oracle.exp2_32(-24.01) == 0.0 and oracle.exp2_32(-1e30) == 0.0
+
+
+# --------------------------------------------------------------------------
+# Eq.2 edge rules of reading R14: the 0.99
+# clamp on alpha and include-then-stop at T < 1e-4.  Each expectation is a
+# closed form of the concentric-Gaussian stack at its common centre pixel,
+# where power = 0 and exp(power) = 1 exactly.
+# --------------------------------------------------------------------------
+
+def _concentric(zs, opac, rgb):
+    """Gaussians on the optical axis with the same 3.2-px footprint (sigma
+    proportional to z), so every one of them covers the centre pixel (32, 32)
+    of a 64x64 view (f = 64, c = 32) with power = 0 there."""
+    return make_scene([[0, 0, z] for z in zs], [[0.05 * z] * 3 for z in zs],
+                      opacity=opac, rgb=rgb)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_early_termination_include_then_stop(prec):
+    """Five concentric o = 0.95 Gaussians: T = (1 - o)^k after k of them.
+    0.05^3 = 1.25e-4 >= 1e-4, so the 4th is blended; 0.05^4 = 6.25e-6 < 1e-4,
+    so blending stops and the 5th is not.  Discriminates: a threshold of 1e-3
+    (would stop after the 3rd: no blue), stop-before-include (would refuse the
+    4th because T would fall below: no blue), no termination at all (green >
+    0).  Expectations use the fp32-stored opacity (the scene is fp32)."""
+    zs = [2.0, 3.0, 4.0, 5.0, 6.0]
+    rgb = np.zeros((5, 3))
+    rgb[3] = [0, 0, 1]          # only the 4th carries blue
+    rgb[4] = [0, 1, 0]          # only the 5th carries green
+    o = oracle.render_view(_concentric(zs, 0.95, rgb), make_view(64.0, 32.0, 64, 64), prec)
+    a = float(np.float32(0.95))
+    q = 1.0 - a
+    tol = 1e-4 if prec == "f32" else 1e-12          # relative; fp32: the T - w chain
+    T = float(o["final_T"][32, 32])
+    assert abs(T - q ** 4) <= tol * q ** 4
+    blue = float(o["rgb"][32, 32, 2])
+    assert abs(blue - a * q ** 3) <= tol * a * q ** 3
+    assert o["rgb"][32, 32, 1] == 0.0 and o["rgb"][32, 32, 0] == 0.0
+    want_d = sum(a * q ** k * z for k, z in enumerate(zs[:4]))
+    assert abs(o["depth"][32, 32] - want_d) <= tol * want_d
+    # the neighbouring pixel (power < 0) is not terminated after 4: T stays larger
+    assert o["final_T"][32, 34] > 1e-4
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_termination_threshold_is_strict_1e4(prec):
+    """o chosen so that T after two Gaussians is 1.2e-4 (>= 1e-4, continue) and
+    after three is 2.4e-6 (< 1e-4, stop): alpha_1 = 0.99 (clamped from 0.995),
+    alpha_2 = 0.988, alpha_3 = 0.98.  A 4th Gaussian must not contribute and a
+    threshold of 2e-4 or 1e-3 would drop the 3rd's red."""
+    zs = [2.0, 3.0, 4.0, 5.0]
+    rgb = np.array([[0, 0, 0], [0, 0, 0], [1, 0, 0], [0, 1, 0]], float)
+    o = oracle.render_view(_concentric(zs, [0.995, 0.988, 0.98, 0.9], rgb),
+                           make_view(64.0, 32.0, 64, 64), prec)
+    a2, a3 = float(np.float32(0.988)), float(np.float32(0.98))
+    T2 = (1 - 0.99) * (1 - a2)
+    tol = 1e-4 if prec == "f32" else 1e-12
+    assert T2 > 1e-4 and T2 * (1 - a3) < 1e-4
+    assert abs(o["rgb"][32, 32, 0] - a3 * T2) <= tol * a3 * T2
+    assert o["rgb"][32, 32, 1] == 0.0
+    assert abs(o["final_T"][32, 32] - (1 - a3) * T2) <= tol * (1 - a3) * T2
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_alpha_clamp_at_099(prec):
+    """alpha = min(0.99, o exp(power)) (reading R14): a front Gaussian of
+    opacity 0.999 blends with weight 0.99 at its centre (not 0.999) and leaves
+    T = 0.01 for the one behind it (o = 0.5 -> weight 0.005); away from the
+    centre, where o exp(power) < 0.99, the clamp is inactive and alpha is the
+    closed form o exp(-r^2 / (2 s^2)) of the isotropic splat."""
+    zs = [2.0, 4.0]
+    rgb = np.array([[1, 0, 0], [0, 1, 0]], float)
+    s = _concentric(zs, [0.999, 0.5], rgb)
+    o = oracle.render_view(s, make_view(64.0, 32.0, 64, 64), prec)
+    tol = 2e-6 if prec == "f32" else 1e-12
+    assert abs(o["rgb"][32, 32, 0] - 0.99) <= tol
+    assert abs(o["final_T"][32, 32] - 0.01 * 0.5) <= tol * 0.01
+    assert abs(o["rgb"][32, 32, 1] - 0.005) <= tol * 0.01
+    # off centre: the front splat's Sigma' = (64 sigma / z)^2 I (+0.3 dilation),
+    # sigma = fp32(0.1) as stored
+    op = float(np.float32(0.999))
+    s2 = (64.0 * float(np.float32(0.1)) / 2.0) ** 2 + 0.3
+    for dx in (3, 5):
+        a = op * math.exp(-0.5 * dx * dx / s2)
+        assert a < 0.99
+        assert abs(o["rgb"][32, 32 + dx, 0] - a) <= (4e-6 if prec == "f32" else 1e-12)

@@ -1,0 +1,94 @@
+"""Mutation check of the oracle's pins: each mutant below
+is a plausible mistake in the Eq.2 edge rules (reading R14: alpha clamp 0.99,
+include-then-stop at T < 1e-4) or in their adjoint.  For each one the repo is
+copied to a scratch directory, the mutation applied to oracle/, liboracle.so
+rebuilt, and the CPU oracle pins run; a mutant must make at least one pin fail (all failing pins are recorded).
+
+    python tools/mutate_oracle.py [--out profiles/r02_oracle_mutants.json]
+"""
+import argparse
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+IMPL = "oracle/s3r_oracle_impl.inc"
+BWD = "oracle/s3r_oracle_bwd.c"
+
+EXP2_W = "        REAL w = alpha * T;\n        Cr = FMA(q->r, w, Cr);"
+MUTANTS = {
+    # forward (both precisions: the f32 contract and the f64 shadow)
+    "fwd_threshold_1e-3": [(IMPL, "if (T < R(1e-4)) break;", "if (T < R(1e-3)) break;", 2)],
+    "fwd_threshold_2e-4": [(IMPL, "if (T < R(1e-4)) break;", "if (T < R(2e-4)) break;", 2)],
+    "fwd_stop_before_include": [
+        (IMPL, "        REAL alpha = FMIN(R(0.99), q->o * so_exp2_f32(e2));\n        REAL w = alpha * T;\n",
+         "        REAL alpha = FMIN(R(0.99), q->o * so_exp2_f32(e2));\n        REAL w = alpha * T;\n"
+         "        if (T - w < R(1e-4)) break;\n", 1),
+        (IMPL, "        REAL alpha = FMIN(R(0.99), q->o * EXPF(power));\n        REAL w = alpha * T;\n",
+         "        REAL alpha = FMIN(R(0.99), q->o * EXPF(power));\n        REAL w = alpha * T;\n"
+         "        if (T * (R(1.0) - alpha) < R(1e-4)) break;\n", 1)],
+    "fwd_no_termination": [(IMPL, "if (T < R(1e-4)) break;", "if (T < R(0.0)) break;", 2)],
+    "fwd_no_alpha_clamp": [
+        (IMPL, "FMIN(R(0.99), q->o * so_exp2_f32(e2))", "(q->o * so_exp2_f32(e2))", 1),
+        (IMPL, "FMIN(R(0.99), q->o * EXPF(power))", "(q->o * EXPF(power))", 1)],
+    "fwd_alpha_clamp_0.999": [
+        (IMPL, "FMIN(R(0.99), q->o * so_exp2_f32(e2))", "FMIN(R(0.999), q->o * so_exp2_f32(e2))", 1),
+        (IMPL, "FMIN(R(0.99), q->o * EXPF(power))", "FMIN(R(0.999), q->o * EXPF(power))", 1)],
+    "fwd_flush_below_-20": [(IMPL.replace("impl.inc", "f32.c"), "if (!(x >= -24.0f)) return 0.0f;",
+                              "if (!(x >= -20.0f)) return 0.0f;", 1)],
+    # adjoint (fp64)
+    "bwd_clamp_passes_gradient": [(BWD, "if (q->o * G >= 0.99) continue;", "if (0) continue;", 1)],
+    "bwd_threshold_1e-3": [(BWD, "if (T < 1e-4) break;", "if (T < 1e-3) break;", 1)],
+    "bwd_stop_before_include": [
+        (BWD, "                T = T * (1.0 - a);\n                last = i + 1;\n",
+         "                if (T * (1.0 - a) < 1e-4) break;\n                T = T * (1.0 - a);\n"
+         "                last = i + 1;\n", 1)],
+    "bwd_no_termination": [(BWD, "if (T < 1e-4) break;", "if (T < 0.0) break;", 1)],
+}
+TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_backward.py"]
+
+
+def run_mutant(name, edits):
+    tmp = tempfile.mkdtemp(prefix="s3r_mut_")
+    try:
+        for d in ("oracle", "tests", "paper_2503_08217_b200"):
+            shutil.copytree(os.path.join(ROOT, d), os.path.join(tmp, d),
+                            ignore=shutil.ignore_patterns("*.so", "__pycache__", "build"))
+        for path, old, new, count in edits:
+            p = os.path.join(tmp, path)
+            src = open(p).read()
+            assert src.count(old) == count, (name, path, src.count(old))
+            open(p, "w").write(src.replace(old, new))
+        subprocess.run(["make", "-s", "-B", "liboracle.so"], cwd=os.path.join(tmp, "oracle"),
+                       check=True)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "not gpu",
+                            "-p", "no:cacheprovider", *TESTS], cwd=tmp, capture_output=True,
+                           text=True, timeout=3000)
+        failed = [ln.split(" ")[1] for ln in r.stdout.splitlines() if ln.startswith("FAILED")]
+        return {"killed": r.returncode != 0, "failures": failed, "rc": r.returncode}
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_oracle_mutants.json"))
+    ap.add_argument("--only", default=None)
+    a = ap.parse_args()
+    res = {}
+    for name, edits in MUTANTS.items():
+        if a.only and a.only not in name:
+            continue
+        res[name] = run_mutant(name, edits)
+        print(name, res[name], flush=True)
+    json.dump({"tests": TESTS, "mutants": res}, open(a.out, "w"), indent=1)
+    survivors = [k for k, v in res.items() if not v["killed"]]
+    print("survivors:", survivors)
+    sys.exit(1 if survivors else 0)
+
+
+if __name__ == "__main__":
+    main()
