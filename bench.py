@@ -3,14 +3,22 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config av2] [--impl s3r|reference]
 
-One step = one s3r_render_batch of this rank's views (default 64) of the
-config's scene: temporal filter -> instance projection + LOD + life update ->
-depth sort -> key emission -> tile sort -> ranges -> alpha blend (every row of
-SURVEY.md §8(a)).  Inputs are resident in HBM before the timed region (scene
-168 MB at C3, larger than the 126 MB L2; each step also writes ~4 GB of
-images), so no L2 flush is needed between steps.  Under torchrun each rank
-renders its own 64 views (weak scaling, views sharded, Gaussians replicated, no
-data-path collective: views are independent).  Rank 0 prints one JSON line.
+One step = one s3r_render_batch of this rank's views of the config's scene:
+temporal filter -> instance projection + LOD + life update -> depth sort ->
+supertile binning -> alpha blend (every row of SURVEY.md §8(a)).  Inputs are
+resident in HBM before the timed region (scene 168 MB at C3, larger than the
+126 MB L2; each step also writes ~4 GB of images), so no L2 flush is needed
+between steps (smaller scenes are flushed).
+
+Multi-GPU (BASELINE configs C3/C4): the configured global batch (C3 64 views,
+C4 256, C2 100) is split into contiguous shards of the (frame, camera)-sorted
+views, one per rank (strong scaling, the default; --scaling weak keeps
+--views per rank instead).  Gaussians are replicated; views are independent,
+so there is no data-path collective.  `python bench.py --gpus N` without a
+torchrun environment re-launches itself under torch.distributed.run with N
+ranks (S3R_DIST_BACKEND=gloo runs the ranks on fewer GPUs as a functional
+test); under torchrun WORLD_SIZE must equal --gpus.  Rank 0 prints one JSON
+line.
 
 --impl reference times the CPU oracle (oracle/, single-threaded C) on host
 cores: one view of the same workload per step.
@@ -37,16 +45,20 @@ from paper_2503_08217_b200 import scenegen as sg  # noqa: E402
 
 METRIC = "rendered views/sec and Gaussians/sec at 1/2/4/8 B200; % HBM/FP32 roofline"
 UNIT = "views/s"
-# FP32 operations per blend evaluation of the R-ARITH exp2-form step (FMA = 2,
-# min / compare = 1): dx, dy 2; a1, a2, b1 3; c1, e2 4; clamp 1; o * s3r_exp2
-# 14 (3 add, 5 fma, one multiply by o 2^n); alpha clamp 1; w 1; colour + depth
-# 8; T 1; termination 1.
-FLOPS_PER_EVAL = 36
+# FP32 operations per blend evaluation for the roofline: SURVEY.md §8(d)'s
+# algorithmic count for Eq.2 with an exact exponential, ~28 per E_alg (FMA = 2):
+# dx, dy 2; power 5; clamp 1; exp 10; alpha clamp 1; w 1; colour + depth 6;
+# T 1; termination 1.  The R-ARITH step as the kernel executes it costs 36
+# (exp2 polynomial 14 instead of 10, the o 2^n multiply, the exp2 scaling)
+# and is reported beside it (EXEC_FLOPS_PER_EVAL) but is not the roofline's.
+FLOPS_PER_EVAL = 28
+EXEC_FLOPS_PER_EVAL = 36
 # ... and of its adjoint (k_raster_bwd): dy, e2 6; clamp 1; exp2 14; o G 1;
 # alpha 1; 1 - alpha 1; rcp 1; T_before 1; w 1; c.gC 6; rest 2; dL/dalpha 2;
 # R 2; colour sums 6; opacity 2; power 1; dy moments 5; flush test 1.
 BWD_FLOPS_PER_EVAL = 54
 SM_COUNT_B200 = 148
+GLOBAL = {"views": 0}        # views of one step over all ranks (set in main)
 
 
 def env_int(k, d):
@@ -174,7 +186,7 @@ def run_reference(args, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": K, "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg_name, "n_gaussians": scene.n,
                    "image": f"{views[0].width}x{views[0].height}", "views_per_step": 1},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -223,7 +235,7 @@ def run_conventional(args, ctx, ds, views, outs, world, dev, stream, streamlined
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = len(views) * world * k / (ms / 1e3)
+    value = GLOBAL["views"] * k / (ms / 1e3)
     renders = max(st["renders"], 1)
     return {"metric": "conventional-pipeline views/s (world transform + project all, no "
                       "temporal filter, no LOD)", "value": value, "unit": UNIT,
@@ -291,7 +303,7 @@ def run_neurf(args, ctx, ds, scene, views, tables, outs, world, dev, stream, pea
     alg_flops = rows * 2 * (64 * 64 + 64 * 64 + 64 * 3)      # one network per Gaussian
     peak = float(peaks.get("bf16_tflops", 1695.8))
     return {"metric": "views/s with the NeurF colour query (tcgen05 bf16 MLP, NEXT-4)",
-            "value": len(views) * world * k / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / k,
+            "value": GLOBAL["views"] * k / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / k,
             "color_stage_ms": color_ms, "rows_per_step": rows,
             "roofline": {"kernel": "k_neurf", "bound": "tensor",
                          "achieved": exec_flops / (color_ms / 1e3) / 1e12 if color_ms else None,
@@ -333,7 +345,7 @@ def run_fast_exp(args, ctx, ds, views, tables, outs, world, dev, stream, exact_v
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = len(views) * world * k / (ms / 1e3)
+    value = GLOBAL["views"] * k / (ms / 1e3)
     raster_ms = st["raster"] / max(st["renders"], 1)
     return {"metric": "views/s with the SFU exponential in the rasterizer (s3r_set_fast_exp)",
             "value": value, "unit": UNIT, "ms_per_step": ms / k, "steps": k,
@@ -439,7 +451,7 @@ def run_train(args, ctx, ds, views, tables, outs, world, dev, stream):
     return {"metric": "training views/s (forward + MSE + backward"
                       + (f" + {dist.get_backend().upper()} grad all-reduce" if world > 1 else "")
                       + ")",
-            "value": len(views) * world * k / (ms / 1e3), "unit": "views/s",
+            "value": GLOBAL["views"] * k / (ms / 1e3), "unit": "views/s",
             "ms_per_step": ms / k, "forward_ms": fwd_ms / k, "backward_ms": bwd_ms / k,
             "loss": float(loss.item()), "views_per_gpu_per_step": len(views), "steps": k,
             "grads": "mean, opacity, scales, quaternion, colour (14 fp32 per Gaussian) + "
@@ -481,6 +493,19 @@ def cpu_baseline(cfg_name, procs=None):
                       f"{dt:.1f} s wall"}
 
 
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: run this command again as N ranks
+    under torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -488,7 +513,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="s3r", choices=["s3r", "reference"])
     ap.add_argument("--config", default="av2", choices=["toy", "street", "av2", "drive"])
-    ap.add_argument("--views", type=int, default=None, help="views per GPU per step")
+    ap.add_argument("--views", type=int, default=None,
+                    help="views per GPU per step (implies --scaling weak)")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="strong (default): the config's global batch split over the ranks")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool", type=int, default=4, help="distinct view batches cycled per step")
@@ -501,14 +529,41 @@ def main():
                     help="skip the conventional-pipeline comparison (NEXT-2)")
     ap.add_argument("--train-steps", type=int, default=5)
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "s3r":
+        sys.exit(relaunch(args.gpus))
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     args.warmup = max(args.warmup, 3)
-    if args.views is None:
-        args.views = 1 if args.config == "toy" else sg.CONFIGS[args.config].n_views if \
-            args.config in ("street",) else 64
+    if args.scaling is None:
+        args.scaling = "weak" if args.views is not None else "strong"
     if args.impl == "reference":
+        if args.views is None:
+            args.views = 1
         run_reference(args, rank)
         return
+    # global batch of the config (BASELINE: C3 64 views, C4 256, C2 all 100 frames)
+    global_views = {"toy": 1, "street": sg.CONFIGS["street"].n_views, "av2": 64,
+                    "drive": sg.CONFIGS["drive"].n_views}[args.config]
+    if args.scaling == "weak":
+        per = args.views if args.views is not None else global_views
+        shards = [(r * per, per) for r in range(world)]
+        global_views = per * world
+    else:
+        # contiguous shards of the (frame, camera)-sorted batch: same-t views co-locate
+        base, extra = divmod(global_views, world)
+        shards, off = [], 0
+        for r in range(world):
+            cnt = base + (1 if r < extra else 0)
+            shards.append((off, cnt))
+            off += cnt
+    args.views = shards[rank][1]
+    GLOBAL["views"] = global_views
+    if args.views < 1:
+        print(f"bench.py: {global_views} views cannot be split over {world} ranks",
+              file=sys.stderr)
+        sys.exit(2)
 
     import torch
     import torch.distributed as dist
@@ -532,9 +587,10 @@ def main():
         cfg = sg.CONFIGS[args.config]
         scene, traj = sg.make_street_scene(cfg)
         pools = []
+        s0, sn = shards[rank]
         for p in range(args.pool):
-            allv = sg.make_views(cfg, traj, n_views=args.views * world, seed=cfg.seed + 101 * p)
-            pools.append(allv[rank * args.views:(rank + 1) * args.views])
+            allv = sg.make_views(cfg, traj, n_views=global_views, seed=cfg.seed + 101 * p)
+            pools.append(allv[s0:s0 + sn])
     ctx = s3r.Context(local)
     ds = s3r.DeviceScene.from_numpy(scene, device=dev)
     tables = [list(s3r.view_tables(ctx, vs, device=dev)) for vs in pools]
@@ -587,7 +643,7 @@ def main():
         ms = max(per) * args.steps
         dist.barrier()
     views_per_step = len(pools[0])
-    value = views_per_step * world * args.steps / (ms / 1e3)
+    value = global_views * args.steps / (ms / 1e3)
 
     # ---------------- workload statistics + roofline (untimed render with counters)
     ctx.set_counters(True)
@@ -614,13 +670,19 @@ def main():
                      "GBps": bytes_[k] / t_s / 1e9 if t_s > 0 else None}
     stages["raster"]["TFLOPs"] = FLOPS_PER_EVAL * E_alg / (stage_ms["raster"] / 1e3) / 1e12 \
         if stage_ms["raster"] > 0 else None
+    stages["raster"]["TFLOPs_executed_form"] = EXEC_FLOPS_PER_EVAL * E_alg / \
+        (stage_ms["raster"] / 1e3) / 1e12 if stage_ms["raster"] > 0 else None
     dom = max(s3r.STAGES, key=lambda k: stage_ms[k])
     if dom == "raster":
         ach = stages["raster"]["TFLOPs"]
         roof = {"kernel": "k_raster", "bound": "alu", "achieved": ach, "peak": alu_peak,
                 "unit": "TFLOP/s", "frac": ach / alu_peak,
                 "peak_source": f"148 SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (B200_PROFILING.md unit counts)",
-                "alg_flops_per_launch": FLOPS_PER_EVAL * E_alg, "traffic": None}
+                "alg_flops_per_launch": FLOPS_PER_EVAL * E_alg, "traffic": None,
+                "flops_per_eval": f"{FLOPS_PER_EVAL} (SURVEY.md §8(d), exact-exp Eq.2) x E_alg "
+                                  f"{E_alg} per launch; the executed R-ARITH form is "
+                                  f"{EXEC_FLOPS_PER_EVAL} (frac "
+                                  f"{EXEC_FLOPS_PER_EVAL / FLOPS_PER_EVAL * ach / alu_peak:.3f})"}
         tr, tr_src = load_traffic(("k_raster<0,0,0>", "k_raster<0,0>"), args.config)
         if tr is not None:
             roof["traffic"] = tr
@@ -694,7 +756,7 @@ def main():
                                                    "instance_ids", "visibility", "life"))
         h2d += sum(t.nbytes for t in htabs[0])
         d2h = sum(o["rgb"].nbytes for o in hout) + hs.life.nbytes
-        e2e = {"value": views_per_step * world * k_e2e / dt, "unit": UNIT,
+        e2e = {"value": global_views * k_e2e / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": k_e2e, "api": "s3r_render_batch_host (pinned host buffers)"}
 
@@ -734,18 +796,21 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "n_gaussians": n_scene,
                        "instances": scene.num_instances - 1,
                        "image": f"{pools[0][0].width}x{pools[0][0].height}",
                        "views_per_gpu_per_step": views_per_step, "global_views_per_step":
-                       views_per_step * world, "parallelism": f"views sharded x{world}, Gaussians replicated",
+                       global_views, "views_per_rank": [n for _, n in shards],
+                       "parallelism": f"views sharded x{world}, Gaussians replicated",
+                       "dist": ({"backend": dist.get_backend(), "ranks": dist.get_world_size()}
+                                if world > 1 else None),
                        "l2": ("L2 flushed between timed steps (256 MiB write outside the "
                               "per-step CUDA-event pairs): scene smaller than L2") if flush else
                              f"inputs larger than L2 (scene {scene.n * 84 / 1e6:.0f} MB > 126 MB; "
                              "images written every step)"},
             "gaussians_per_s": n_scene * value,
-            "processed_gaussians_per_s": sum(s["n_temporal"] for s in stats) * world * value / views_per_step,
+            "processed_gaussians_per_s": sum(s["n_temporal"] for s in stats) / views_per_step * value,
             "clocks": clocks,
             "rank_ms_per_step": rank_ms,
             "gpu_launches": launches_per_step * args.steps,

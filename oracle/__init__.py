@@ -20,6 +20,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
+# S3R_ORACLE_SO selects another build of the same sources, e.g. the ASan/UBSan
+# one (Makefile target liboracle_san.so, tools/oracle_sanitize.sh)
+_SO_ALT = os.environ.get("S3R_ORACLE_SO")
 _SRCS = ["s3r_oracle_f32.c", "s3r_oracle_f64.c", "s3r_oracle_bwd.c", "s3r_oracle_impl.inc",
          "s3r_oracle.h", "Makefile"]
 _lock = threading.Lock()
@@ -71,8 +74,11 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            build()
-            L = C.CDLL(_SO)
+            if _SO_ALT:
+                L = C.CDLL(os.path.abspath(_SO_ALT))
+            else:
+                build()
+                L = C.CDLL(_SO)
             P = C.c_void_p
             sig = {
                 "so_normalize_time": (C.c_double, [C.c_int64, C.c_int64]),

@@ -1,12 +1,13 @@
-// k_sort.cu — K5: segmented, stable LSD radix sort (onesweep with decoupled
-// look-back), used twice per batch:
-//   depth sort  : 32-bit keys = bits(z) (z > near > 0, so bit order == numeric
-//                 order), values = local index j (ascending Gaussian index),
-//                 4 passes of 8 bits -> order by (depth, index) (reading R11);
-//   tile sort   : 64-bit words (tile << 32) | rank, keys only, digits taken
-//                 from bits 32.. -> stable order by (tile, rank).
-// Segments are views: every view has its own digit histograms and its own
-// look-back chain, so one launch sorts the whole batch.
+// k_sort.cu — K5: the depth sort of a batch: a segmented, stable LSD radix
+// sort (onesweep with decoupled look-back) of 64-bit keys
+// (bits(z) << gbits | Gaussian index) with the compacted slot as the value.
+// z > near > 0, so the IEEE bit order of z is its numeric order, and the
+// index bits make every key unique: the result is the (depth, index) order of
+// reading R11 whatever order K2 compacted the records in.  8-bit digits,
+// ceil((32 + gbits) / 8) passes (7 at C3's 2 M Gaussians).
+// Segments are views: every view has its own digit histograms (k_hist, one
+// read of the keys for all passes) and its own look-back chain, so one launch
+// per pass sorts the whole batch.  Tile binning does not sort (k_bin.cu).
 //
 // Per pass each CTA takes a tile of 256*ITEMS keys (warp-striped, coalesced),
 // ranks them with __match_any_sync per warp (stable: lane order within a
@@ -27,7 +28,6 @@ constexpr int SW = ST / 32;
 #ifndef S3R_SORT_MINB
 #define S3R_SORT_MINB 4   // 64 registers, 4 CTAs/SM (A/B: depth sort 0.446 ms; 3 (80 regs): 0.481, none (96): 0.564)
 #endif
-constexpr int ITEMS32 = S3R_SORT_ITEMS;
 constexpr int ITEMS64 = S3R_SORT_ITEMS;
 constexpr int HITEMS = S3R_SORT_ITEMS;   // histogram tiles == onesweep tiles (ST * ITEMS keys)
 
@@ -227,16 +227,8 @@ __global__ void __launch_bounds__(ST, S3R_SORT_MINB) k_onesweep(const K* __restr
 }
 }  // namespace
 
-int onesweep32_tile() { return ST * ITEMS32; }
 int onesweep64_tile() { return ST * ITEMS64; }
 int hist_tile() { return ST * HITEMS; }
-
-void launch_hist32(const uint32_t* keys, const Seg* segs, int nsegs, const int* seg_tile0,
-                   int total_tiles, int npasses, uint32_t* hist, cudaStream_t st)
-{
-    if (total_tiles == 0) return;
-    k_hist<uint32_t><<<total_tiles, ST, 0, st>>>(keys, segs, nsegs, seg_tile0, 0, npasses, hist);
-}
 
 void launch_hist64(const unsigned long long* keys, const Seg* segs, int nsegs,
                    const int* seg_tile0, int total_tiles, int shift0, int npasses, uint32_t* hist,
@@ -253,17 +245,6 @@ void launch_hist_scan(uint32_t* hist, int nsegs, int npasses, cudaStream_t st)
     k_hist_scan<<<nsegs * npasses, ST, 0, st>>>(hist);
 }
 
-void launch_onesweep32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
-                       const Seg* segs, int nsegs, const int* seg_tile0, int total_tiles,
-                       const uint32_t* digit_base, int pass, int npasses, uint32_t* lookback,
-                       int* ticket, int shift, cudaStream_t st)
-{
-    if (total_tiles == 0) return;
-    k_onesweep<uint32_t, true, ITEMS32><<<total_tiles, ST, 0, st>>>(
-        kin, vin, kout, vout, segs, nsegs, seg_tile0, digit_base, pass, npasses, lookback, ticket,
-        shift);
-}
-
 void launch_onesweep64kv(const unsigned long long* kin, const uint32_t* vin,
                          unsigned long long* kout, uint32_t* vout, const Seg* segs, int nsegs,
                          const int* seg_tile0, int total_tiles, const uint32_t* digit_base,
@@ -274,17 +255,6 @@ void launch_onesweep64kv(const unsigned long long* kin, const uint32_t* vin,
     k_onesweep<unsigned long long, true, ITEMS64><<<total_tiles, ST, 0, st>>>(
         kin, vin, kout, vout, segs, nsegs, seg_tile0, digit_base, pass, npasses, lookback, ticket,
         shift);
-}
-
-void launch_onesweep64(const unsigned long long* kin, unsigned long long* kout, const Seg* segs,
-                       int nsegs, const int* seg_tile0, int total_tiles,
-                       const uint32_t* digit_base, int pass, int npasses, uint32_t* lookback,
-                       int* ticket, int shift, cudaStream_t st)
-{
-    if (total_tiles == 0) return;
-    k_onesweep<unsigned long long, false, ITEMS64><<<total_tiles, ST, 0, st>>>(
-        kin, nullptr, kout, nullptr, segs, nsegs, seg_tile0, digit_base, pass, npasses, lookback,
-        ticket, shift);
 }
 
 }  // namespace s3r

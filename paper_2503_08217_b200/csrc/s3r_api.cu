@@ -72,7 +72,8 @@ struct s3r_ctx {
         d_sortk[2], d_sortv[2], d_recs, d_rects, d_lists, d_tlists, d_tranges, d_cnt, d_hist,
         d_dsegs, d_dtile0,
         d_ranges, d_err, d_dbg_keys, d_dbg_flags, d_dbg_rect, d_dbg_tcnt;
-    int ticket_slot = 0;
+    int ticket_slot = 0, ticket_cap = 0;
+    bool ticket_overflow = false;
     int gbits = 1;
     // mirrors for s3r_render_batch_host
     Buf m_scene[7];
@@ -180,7 +181,16 @@ void* stage_alloc(s3r_ctx* c, size_t bytes)
     return c->h_stage + off;
 }
 
-int* next_ticket(s3r_ctx* c) { return P<int>(c->d_ticket) + (c->ticket_slot++); }
+int* next_ticket(s3r_ctx* c)
+{
+    // sized per batch by construction; running out is an internal error that
+    // render_impl reports (S3R_EINTERNAL) instead of writing past the buffer
+    if (c->ticket_slot >= c->ticket_cap) {
+        c->ticket_overflow = true;
+        return P<int>(c->d_ticket);
+    }
+    return P<int>(c->d_ticket) + (c->ticket_slot++);
+}
 
 // NVTX range per stage (host-side enqueue span; free without a tool attached)
 const char* const kStageName[S3R_NUM_STAGES] = {"s3r.filter", "s3r.project", "s3r.depth_sort",
@@ -271,6 +281,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     const long long N = sc->n;
     c->N_last = N;
     c->ticket_slot = 0;
+    c->ticket_overflow = false;
     c->last_debug = c->debug;
     c->gbits = bits_for(std::max<long long>(N, 2));   // Gaussian-index bits of the depth key
     const bool conv = c->pipeline == S3R_PIPELINE_CONVENTIONAL;
@@ -337,9 +348,14 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
                                (size_t)(nv + 1) * 64;
     if ((rc = stage_reserve(c, stage_bytes))) return rc;
     c->h_stage_top = 0;
-    if ((rc = ensure(c, c->d_ticket, 256 * sizeof(int)))) return rc;
+    // one zeroed work counter per launch that takes tickets: the filter chunks,
+    // the depth-sort passes and the rasterizer
+    const int n_tickets = (T + MAX_TSLOTS - 1) / MAX_TSLOTS +
+                          (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS + 1;
+    c->ticket_cap = n_tickets;
+    if ((rc = ensure(c, c->d_ticket, (size_t)n_tickets * sizeof(int)))) return rc;
     if ((rc = ensure(c, c->d_err, sizeof(uint32_t)))) return rc;
-    CU(cudaMemsetAsync(c->d_ticket.p, 0, 256 * sizeof(int), st));
+    CU(cudaMemsetAsync(c->d_ticket.p, 0, (size_t)n_tickets * sizeof(int), st));
 
     // ================= K1: temporal filter + compaction
     const long long Ns = std::max<long long>(N, 1);
@@ -651,6 +667,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     CU(cudaEventRecord(c->staging_free, st));
     c->staging_recorded = true;
     c->have_render = true;
+    if (c->ticket_overflow) return fail(c, S3R_EINTERNAL, "work-counter slots exhausted");
     if (bad) return fail(c, S3R_EINSTANCE, "a Gaussian had an instance id outside [0, %d]",
                          sc->num_instances - 1);
     c->err.clear();

@@ -228,29 +228,18 @@ void launch_neurf_pack(const float* w1, const float* b1, const float* w2, const 
                        cudaStream_t st);
 void launch_neurf(const NeurfArgs& a, cudaStream_t st);
 
-// Segmented LSD radix sort helpers (onesweep with decoupled look-back).
-// keys: u32 (depth) or u64 (pair words).  digit = (key >> shift) & 255.
-void launch_hist32(const uint32_t* keys, const Seg* segs, int nsegs, const int* seg_tile0,
-                   int total_tiles, int npasses, uint32_t* hist, cudaStream_t st);
+// K5 depth sort: segmented LSD radix sort of 64-bit keys (onesweep with
+// decoupled look-back), digit = (key >> shift) & 255.
 void launch_hist64(const unsigned long long* keys, const Seg* segs, int nsegs,
                    const int* seg_tile0, int total_tiles, int shift0, int npasses,
                    uint32_t* hist, cudaStream_t st);
 void launch_hist_scan(uint32_t* hist, int nsegs, int npasses, cudaStream_t st);
-void launch_onesweep32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
-                       uint32_t* vout, const Seg* segs, int nsegs, const int* seg_tile0,
-                       int total_tiles, const uint32_t* digit_base, int pass, int npasses,
-                       uint32_t* lookback, int* ticket, int shift, cudaStream_t st);
-// 64-bit keys with 32-bit values (vin == NULL: value = index in the segment).
+// 32-bit values (vin == NULL: value = index in the segment).
 void launch_onesweep64kv(const unsigned long long* kin, const uint32_t* vin,
                          unsigned long long* kout, uint32_t* vout, const Seg* segs, int nsegs,
                          const int* seg_tile0, int total_tiles, const uint32_t* digit_base,
                          int pass, int npasses, uint32_t* lookback, int* ticket, int shift,
                          cudaStream_t st);
-void launch_onesweep64(const unsigned long long* kin, unsigned long long* kout,
-                       const Seg* segs, int nsegs, const int* seg_tile0, int total_tiles,
-                       const uint32_t* digit_base, int pass, int npasses, uint32_t* lookback,
-                       int* ticket, int shift, cudaStream_t st);
-int onesweep32_tile();
 int onesweep64_tile();
 int hist_tile();
 

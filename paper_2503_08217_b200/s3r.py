@@ -148,6 +148,34 @@ def _ptr(t: Optional[torch.Tensor]):
     return C.c_void_p(t.data_ptr())
 
 
+def _req(t, name: str, dtype, shape, device=None, optional: bool = False):
+    """Argument check before a pointer crosses the ABI: the kernels index these
+    buffers by the sizes in the structs, so a wrong dtype / shape / device or a
+    non-contiguous view would make them read or write out of bounds.  Raises
+    ValueError (never stripped, unlike assert)."""
+    if t is None:
+        if optional:
+            return
+        raise ValueError(f"{name}: required tensor is None")
+    if not torch.is_tensor(t):
+        raise ValueError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if device is not None and (not t.is_cuda or t.device.index != device):
+        raise ValueError(f"{name}: on {t.device}, expected cuda:{device}")
+
+
+def _req_table(t, name: str, K1: int, device):
+    if not (torch.is_tensor(t) and t.dtype == torch.float32 and t.numel() == 12 * K1
+            and t.is_contiguous() and t.is_cuda and t.device.index == device):
+        raise ValueError(f"{name}: expected a contiguous float32 cuda:{device} tensor of "
+                         f"{K1} x 12 floats (per-instance 3x4 local->camera)")
+
+
 def _stream(stream=None):
     s = torch.cuda.current_stream() if stream is None else stream
     return C.c_void_p(s.cuda_stream)
@@ -177,10 +205,16 @@ class DeviceScene:
                            f(scene.visibility), f(scene.life) if life else None,
                            int(scene.num_instances))
 
-    def struct(self) -> Scene_:
-        for t in (self.means_opacity, self.scales, self.rotations, self.colors,
-                  self.instance_ids, self.visibility):
-            assert t.is_cuda and t.is_contiguous()
+    def check(self, device: Optional[int] = None):
+        n = self.n
+        for k in ("means_opacity", "scales", "rotations", "colors"):
+            _req(getattr(self, k), f"scene.{k}", torch.float32, (n, 4), device)
+        _req(self.instance_ids, "scene.instance_ids", torch.int32, (n,), device)
+        _req(self.visibility, "scene.visibility", torch.float32, (n, 2), device)
+        _req(self.life, "scene.life", torch.float32, (n, 2), device, optional=True)
+
+    def struct(self, device: Optional[int] = None) -> Scene_:
+        self.check(device)
         return Scene_(self.n, self.num_instances, _ptr(self.means_opacity), _ptr(self.scales),
                       _ptr(self.rotations), _ptr(self.colors), _ptr(self.instance_ids),
                       _ptr(self.visibility), _ptr(self.life))
@@ -253,14 +287,28 @@ class Context:
                                                         _ptr(out), _stream(stream)))
         return out
 
+    def _check_views(self, scene: DeviceScene, views, tables, outs):
+        if not (len(views) == len(tables) == len(outs)):
+            raise ValueError(f"{len(views)} views, {len(tables)} tables, {len(outs)} outputs")
+        for i, (v, t, o) in enumerate(zip(views, tables, outs)):
+            _req_table(t, f"tables[{i}]", scene.num_instances, self.device)
+            H, W = int(v.height), int(v.width)
+            _req(o.get("rgb"), f"outs[{i}]['rgb']", torch.float32, (H, W, 3), self.device)
+            _req(o.get("depth"), f"outs[{i}]['depth']", torch.float32, (H, W), self.device, True)
+            _req(o.get("final_T"), f"outs[{i}]['final_T']", torch.float32, (H, W), self.device,
+                 True)
+            _req(o.get("visible"), f"outs[{i}]['visible']", torch.uint8, (scene.n,), self.device,
+                 True)
+
     def render_batch(self, scene: DeviceScene, views: Sequence, tables: Sequence[torch.Tensor],
                      outs: Sequence[Dict[str, torch.Tensor]], stream=None) -> int:
         n = len(views)
+        self._check_views(scene, views, tables, outs)
         vs = (View_ * max(n, 1))(*[view_struct(v, t) for v, t in zip(views, tables)])
         os_ = (Outputs_ * max(n, 1))(*[Outputs_(_ptr(o["rgb"]), _ptr(o.get("depth")),
                                                 _ptr(o.get("final_T")), _ptr(o.get("visible")))
                                        for o in outs])
-        sc = scene.struct()
+        sc = scene.struct(self.device)
         return self._check(self.L.s3r_render_batch(self.h, C.byref(sc), vs, n, os_,
                                                    _stream(stream)),
                            allow=(S3R_OK, S3R_EINSTANCE))
@@ -313,11 +361,11 @@ class Context:
         return d
 
     def commit_visibility(self, scene: DeviceScene, margin: float = 0.1, stream=None):
-        sc = scene.struct()
+        sc = scene.struct(self.device)
         self._check(self.L.s3r_commit_visibility(self.h, C.byref(sc), margin, _stream(stream)))
 
     def reset_visibility(self, scene: DeviceScene, stream=None):
-        sc = scene.struct()
+        sc = scene.struct(self.device)
         self._check(self.L.s3r_reset_visibility(self.h, C.byref(sc), _stream(stream)))
 
     def set_pipeline(self, conventional: bool):
@@ -350,8 +398,9 @@ class Context:
             self._check(self.L.s3r_set_neural_colors(self.h, None, _stream(stream)))
             return
         t = {k: v.contiguous() for k, v in params.items() if torch.is_tensor(v)}
-        for v in t.values():
-            assert v.is_cuda and v.dtype == torch.float32
+        for k, v in t.items():
+            if not (v.is_cuda and v.dtype == torch.float32 and v.device.index == self.device):
+                raise ValueError(f"neural colours: {k} must be float32 on cuda:{self.device}")
         self._neurf_keep = t
         p = Neurf_(_ptr(t["w1"]), _ptr(t["b1"]), _ptr(t["w2"]), _ptr(t["b2"]), _ptr(t["w3"]),
                    _ptr(t["b3"]), _ptr(t["time_emb"]), int(t["time_emb"].shape[0]),
@@ -370,24 +419,42 @@ class Context:
         """Accumulate dL/d(scene params) of the last (training) forward into grads
         (keys means_opacity, scales, rotations, colors: (N,4) float32 tensors)."""
         n = len(views)
+        if not (len(views) == len(tables) == len(cots)):
+            raise ValueError(f"{len(views)} views, {len(tables)} tables, {len(cots)} cotangents")
+        N, dv = scene.n, self.device
+        for i, (v, t, c) in enumerate(zip(views, tables, cots)):
+            _req_table(t, f"tables[{i}]", scene.num_instances, dv)
+            H, W = int(v.height), int(v.width)
+            _req(c.get("rgb"), f"cots[{i}]['rgb']", torch.float32, (H, W, 3), dv, True)
+            _req(c.get("depth"), f"cots[{i}]['depth']", torch.float32, (H, W), dv, True)
+            _req(c.get("final_T"), f"cots[{i}]['final_T']", torch.float32, (H, W), dv, True)
+        for k in ("means_opacity", "scales", "rotations", "colors"):
+            _req(grads.get(k), f"grads['{k}']", torch.float32, (N, 4), dv)
+        _req(grads.get("table"), "grads['table']", torch.float32, (n, scene.num_instances, 12),
+             dv, True)
         vs = (View_ * max(n, 1))(*[view_struct(v, t) for v, t in zip(views, tables)])
         cs = (Cot_ * max(n, 1))(*[Cot_(_ptr(c["rgb"]), _ptr(c.get("depth")),
                                        _ptr(c.get("final_T"))) for c in cots])
         g = Grads_(_ptr(grads["means_opacity"]), _ptr(grads["scales"]),
                    _ptr(grads["rotations"]), _ptr(grads["colors"]), _ptr(grads.get("table")))
-        sc = scene.struct()
+        sc = scene.struct(self.device)
         self._check(self.L.s3r_render_backward(self.h, C.byref(sc), vs, n, cs, C.byref(g),
                                                _stream(stream)))
 
     def mse(self, x: torch.Tensor, y: torch.Tensor, scale: float, grad: torch.Tensor,
             loss: torch.Tensor, stream=None):
         """grad = 2 scale (x - y); loss += scale sum (x - y)^2 (device scalar)."""
+        _req(x, "x", torch.float32, tuple(x.shape), self.device)
+        _req(y, "y", torch.float32, tuple(x.shape), self.device)
+        _req(grad, "grad", torch.float32, tuple(x.shape), self.device)
+        _req(loss, "loss", torch.float32, (1,), self.device)
         self._check(self.L.s3r_mse(self.h, _ptr(x), _ptr(y), int(x.numel()), float(scale),
                                    _ptr(grad), _ptr(loss), _stream(stream)))
 
     def life_flip(self, life: torch.Tensor, stream=None):
         """Negate l_s in place (see s3r_life_flip): brackets an all-reduce MAX."""
-        assert life.is_cuda and life.is_contiguous() and life.dtype == torch.float32
+        _req(life, "life", torch.float32, (life.shape[0], 2) if life.dim() == 2 else (-1,),
+             self.device)
         self._check(self.L.s3r_life_flip(self.h, _ptr(life), int(life.shape[0]),
                                          _stream(stream)))
 

@@ -93,8 +93,10 @@ class Config:
 
 CONFIGS = {
     # C2 small street: 150k + 10x5k, 1 forward camera 960x640, ~40 % temporal pass
+    # (window -38/+108 m: the realised mean pass over the 100 views is 40.0 %;
+    # the survey's -20/+80 m gives 28.5 % once the street's ends clip the window)
     "street": Config("street", 150_000, 10, 5_000, 960, 640, 600.0, (0.0,), 250.0, 100,
-                     20.0, 80.0, (4.0, 0.5, 50.0), 100, 2),
+                     38.0, 108.0, (4.0, 0.5, 50.0), 100, 2),
     # C3 Argoverse2-shaped: 1.7M + 30x10k, 7 ring cameras 1550x2048, ~25 % pass
     "av2": Config("av2", 1_700_000, 30, 10_000, 1550, 2048, 1700.0,
                   (0.0, 45.0, -45.0, 99.0, -99.0, 153.0, -153.0), 400.0, 150,
