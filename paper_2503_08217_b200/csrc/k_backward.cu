@@ -26,6 +26,7 @@
 // linear scales, unnormalised quaternion, opacity, colour), atomically added
 // into the caller's gradient arrays.
 #include <algorithm>
+#include <type_traits>
 
 #include "s3r_internal.cuh"
 
@@ -54,6 +55,12 @@ namespace {
 #ifndef S3R_BWD_NOBR
 #define S3R_BWD_NOBR 1  // no per-pair skip branch (A/B with MINB 14: 31.7 vs 34.1 ms)
 #endif
+#ifndef S3R_BWD_VRED
+#define S3R_BWD_VRED 0  // 1: the 10 reduced values gathered into 3 lanes, added with vector REDs (v4, v4, v2)
+#endif
+#ifndef S3R_BWD_ULAST
+#define S3R_BWD_ULAST 0 // 1: no per-pixel "entry before the pixel's stop" test in a batch every pixel of the warp reaches
+#endif
 #ifndef S3R_BWD_EX2
 #define S3R_BWD_EX2 0   // 0: exact R-ARITH exp2 on pairs (A/B 35.9 ms); 1, 2: ex2.approx + re-decision (37.0, 36.6)
 #endif
@@ -64,6 +71,11 @@ constexpr int RT = TILE * TILE / RPIX;
 constexpr int BW = TILE / (RT / 32);
 constexpr int RB = 256;
 constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
+}  // namespace
+// per-splat accumulator stride in floats (16-byte rows for the vector REDs)
+constexpr int ACC_STRIDE = S3R_BWD_VRED ? 12 : 10;
+int splat_grad_stride() { return ACC_STRIDE; }
+namespace {
 
 #if S3R_BWD_EX2
 __device__ __forceinline__ float s3r_exp2_b(float x)
@@ -199,10 +211,15 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     __syncthreads();
     atomicMax(&s_max, mymax);
     __syncthreads();
+    // the smallest stop over the thread's pixels (pixels outside the image have
+    // last = 0 and never differentiate anything)
+    int minlast = last[0];
+#pragma unroll
+    for (int k = 1; k < RPIX; ++k) minlast = min(minlast, last[k]);
     const int2 rg = a.tranges[V.trange_off + tile];
     const uint32_t* lst = a.tlists + V.tlist_off;
     const float4* recs = a.rec_sorted + 3 * V.cap_off;
-    float* acc = a.splat_grads + 10 * V.cap_off;
+    float* acc = a.splat_grads + (long long)ACC_STRIDE * V.cap_off;
     // conic from the exp2-form coefficients: qa = A (-log2e/2), qb = B (-log2e),
     // qc = C (-log2e/2)  =>  A = qa (-2 ln2), B = qb (-ln2), C = qc (-2 ln2)
     const float k2 = -1.3862943611198906f, k1 = -0.6931471805599453f;
@@ -261,7 +278,8 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
         // one record (by staged index jj): per-pixel recurrences (T, R) and the
         // thread's partial sums -> v10 (the splat's 10 gradient values before the
         // warp reduction); returns whether any pixel of the thread contributed
-        auto eval_record = [&](int jj, float* v10) -> bool {
+        auto eval_record = [&](int jj, float* v10, auto chk_tag) -> bool {
+            constexpr bool CHK = decltype(chk_tag)::value;   // test j < last per pixel
             const int j = lo + jj;
             const float4 q0 = s_rec[3 * jj], q1 = s_rec[3 * jj + 1], q2 = s_rec[3 * jj + 2];
             const float dx = q0.x - fpx;
@@ -295,8 +313,8 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 const float2 e2 = make_float2(fminf(0.0f, e2raw.x), fminf(0.0f, e2raw.y));
                 // entries after the pixel's termination, or flushed in the forward
                 // (alpha = 0): nothing to differentiate
-                const bool okx = j < last[2 * P] && e2.x >= -24.0f;
-                const bool oky = j < last[2 * P + 1] && e2.y >= -24.0f;
+                const bool okx = (!CHK || j < last[2 * P]) && e2.x >= -24.0f;
+                const bool oky = (!CHK || j < last[2 * P + 1]) && e2.y >= -24.0f;
 #if S3R_BWD_NOBR
                 // branch-free: a pair with neither pixel ok gets G = 0 below, which
                 // leaves T, R and every sum bit-identical; the pairs' dependency
@@ -386,13 +404,13 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
         for (int kk = run[warp] - 1; kk >= 0; kk -= 2) {
             const int jjA = s_cl[warp][kk];
             float vA[10], vB[10];
-            const bool anyA = eval_record(jjA, vA);
+            const bool anyA = eval_record(jjA, vA, std::true_type{});
             const bool hasB = kk >= 1;                      // warp-uniform
             int jjB = 0;
             bool anyB = false;
             if (hasB) {
                 jjB = s_cl[warp][kk - 1];
-                anyB = eval_record(jjB, vB);
+                anyB = eval_record(jjB, vB, std::true_type{});
             } else {
 #pragma unroll
                 for (int i = 0; i < 10; ++i) vB[i] = 0.0f;
@@ -423,16 +441,20 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 if (2 * u2 + u1 <= 2 && 3 * u4 + 2 * u2 + u1 <= 4 && (!u16 || hasB)) {
                     const int jjR = u16 ? jjB : jjA;
                     const uint32_t g = __float_as_uint(s_rec[3 * jjR + 1].w);   // list entry
-                    atomicAdd(acc + 10ll * g + inner, v1);
+                    atomicAdd(acc + (long long)ACC_STRIDE * g + inner, v1);
                 }
             }
         }
 #else
+        // every pixel of the warp differentiates every entry of this batch
+        // (its stop lies at or beyond the batch's end): no per-pixel test
+        const bool full = S3R_BWD_ULAST && __all_sync(0xffffffffu, minlast >= hi);
         for (int kk = run[warp] - 1; kk >= 0; --kk) {
             const int jj = s_cl[warp][kk];
             const float4 q1 = s_rec[3 * jj + 1];
             float v10[10];
-            const bool any = eval_record(jj, v10);
+            const bool any = full ? eval_record(jj, v10, std::false_type{})
+                                  : eval_record(jj, v10, std::true_type{});
             if (__any_sync(0xffffffffu, any)) {
                 const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
                 float v5[5], v3[3], v2[2];
@@ -452,11 +474,30 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 }
                 float v1 = (u2 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, u2 ? v2[0] : v2[1], 2);
                 v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+                const uint32_t g = __float_as_uint(q1.w);        // list entry staged in .w
+#if S3R_BWD_VRED
+                // value i now sits in lane L(i) = {0, 2, 4, 8, 10, 16, 18, 20, 24, 26}[i];
+                // lanes 0, 1, 2 gather values 0-3, 4-7, 8-9 (slot s of lane l reads
+                // byte l of SRC[s]) and add them with one vector RED each
+                constexpr uint32_t SRC0 = 0x00180a00u, SRC1 = 0x001a1002u, SRC2 = 0x00001204u,
+                                   SRC3 = 0x00001408u;
+                const int sh = 8 * (lane & 3);
+                const float w0 = __shfl_sync(0xffffffffu, v1, (SRC0 >> sh) & 31);
+                const float w1 = __shfl_sync(0xffffffffu, v1, (SRC1 >> sh) & 31);
+                const float w2 = __shfl_sync(0xffffffffu, v1, (SRC2 >> sh) & 31);
+                const float w3 = __shfl_sync(0xffffffffu, v1, (SRC3 >> sh) & 31);
+                float* dst = acc + (long long)ACC_STRIDE * g + 4 * lane;
+                if (lane < 2)
+                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                                 ::"l"(dst), "f"(w0), "f"(w1), "f"(w2), "f"(w3) : "memory");
+                else if (lane == 2)
+                    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};"
+                                 ::"l"(dst), "f"(w0), "f"(w1) : "memory");
+#else
                 const int inner = 3 * u8 + 2 * u4 + u2;
-                if (!(lane & 1) && 2 * u4 + u2 <= 2 && inner <= 4) {
-                    const uint32_t g = __float_as_uint(q1.w);    // list entry staged in .w
-                    atomicAdd(acc + 10ll * g + 5 * u16 + inner, v1);
-                }
+                if (!(lane & 1) && 2 * u4 + u2 <= 2 && inner <= 4)
+                    atomicAdd(acc + (long long)ACC_STRIDE * g + 5 * u16 + inner, v1);
+#endif
             }
         }
 #endif
@@ -470,7 +511,7 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
 __device__ __forceinline__ int project_bwd_one(const BackwardArgs& a, const DevView& V,
                                                long long r, float* gm12)
 {
-    const float* acc = a.splat_grads + 10 * (V.cap_off + r);
+    const float* acc = a.splat_grads + (long long)ACC_STRIDE * (V.cap_off + r);
     const float gmx = acc[0], gmy = acc[1], gz = acc[2], gA = acc[3], gB = acc[4], gC = acc[5],
                 go = acc[6], gcr = acc[7], gcg = acc[8], gcb = acc[9];
     if (gmx == 0.f && gmy == 0.f && gz == 0.f && gA == 0.f && gB == 0.f && gC == 0.f &&

@@ -18,6 +18,7 @@
 // batch.  A pixel stops at its termination; the CTA stops when all its pixels
 // have (__syncthreads_count).
 #include <algorithm>
+#include <type_traits>
 
 #include "s3r_internal.cuh"
 
@@ -44,33 +45,29 @@ constexpr int BW = TILE / (RT / 32);
 constexpr int RS = 32 / BW;
 constexpr int NP = RPIX / 2;
 constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
-#ifndef S3R_RASTER_CLIST
-#define S3R_RASTER_CLIST 1
-#endif
 #ifndef S3R_RASTER_ADJ
 #define S3R_RASTER_ADJ 1     // vertically adjacent pixel pairs (A/B: 14.65 vs 15.01 ms)
 #endif
-#ifndef S3R_RASTER_NOBR
-#define S3R_RASTER_NOBR 0
+#ifndef S3R_RASTER_ALUEXP
+#define S3R_RASTER_ALUEXP 0  // 1: o 2^n exponent add as a funnel shift (ALU pipe) instead of IMAD
 #endif
-#ifndef S3R_RASTER_PERSIST
-#define S3R_RASTER_PERSIST 0  // 1: persistent CTAs over an atomic (view, tile) counter (A/B: raster 15.31 vs 14.68 ms on C3, 1.97 vs 1.82 on C2; off)
+#ifndef S3R_RASTER_UVOTE
+#define S3R_RASTER_UVOTE 0   // 1: warp-uniform skip of a pixel pair (vote) instead of a divergent branch
 #endif
-#ifndef S3R_VOTE_EVERY
-#define S3R_VOTE_EVERY 1     // records per warp-termination vote (A/B: raster 14.65 ms; 2: 15.41, 4: 15.01)
+#ifndef S3R_RASTER_FASTLIVE
+#define S3R_RASTER_FASTLIVE 1   // no per-pixel liveness test while every pixel of the warp is live (A/B, C3: training forward 19.2 -> 17.6 ms; render neutral)
 #endif
-#ifndef S3R_RASTER_PMASK
-#define S3R_RASTER_PMASK 0   // per-pair-block skip (A/B: 15.59 vs 15.14 ms without)
+#ifndef S3R_RASTER_STAGE
+#define S3R_RASTER_STAGE 1   // record staging: 0 LDG+STS, 1 cp.async (A/B: 14.55 vs 14.57 ms), 2 cp.async double-buffered at 128 records (15.20 ms)
 #endif
-[[maybe_unused]] constexpr int kVoteEvery = S3R_VOTE_EVERY;
-constexpr int RB = 256;     // splat records staged in shared memory per batch
+constexpr int RB = S3R_RASTER_STAGE == 2 ? 128 : 256;   // records staged per batch (per buffer)
+constexpr int NBUF = S3R_RASTER_STAGE == 2 ? 2 : 1;
 
 // Build-time variants (for A/B measurement; the defaults are the product):
-//   S3R_CULL          1: skip records whose flush ellipse misses the warp's block
-//   S3R_RASTER_CLIST  1: ... by per-warp compacted record lists built while
-//                        staging (A/B: raster 15.15 vs 15.81 ms with the
-//                        per-record test in the blend loop)
 //   S3R_RASTER_MINB   minimum resident CTAs per SM for __launch_bounds__ (0: none)
+// Measured and removed: the per-record cull test in the blend
+// loop instead of per-warp compacted lists, per-pair-block masks, a vote every
+// 2 / 4 records, the branch-free pair, a persistent grid.
 #ifndef S3R_RASTER_MINB
 #define S3R_RASTER_MINB 16    // 64 registers, 32 resident warps per SM (A/B: 16.6 vs 17.2 ms)
 #endif
@@ -79,11 +76,6 @@ constexpr int RB = 256;     // splat records staged in shared memory per batch
 #endif
 #ifndef S3R_FLUSH_E2
 #define S3R_FLUSH_E2 FLUSH_E2
-#endif
-#if S3R_RASTER_MINB > 0
-#define S3R_RASTER_BOUNDS __launch_bounds__(RT, S3R_RASTER_MINB)
-#else
-#define S3R_RASTER_BOUNDS __launch_bounds__(RT)
 #endif
 
 // Packed pairs: sm_100a executes two fp32 operations per instruction
@@ -112,8 +104,16 @@ __device__ __forceinline__ float2 o_exp2_x2(float2 x, float o, float c0)
     const float2 y = __ffma2_rn(p, r, f2(1.0f));
     // bits(t) << 23 == n << 23 (mod 2^32): the shifter's 0x4B400000 part shifts out
     const uint32_t ob = __float_as_uint(o);
+#if S3R_RASTER_ALUEXP
+    // as a funnel shift (LEA.HI / SHF on the ALU pipe) instead of the IMAD that
+    // ptxas otherwise picks, which issues to the saturated FMA pipe
+    const float2 osc = make_float2(
+        __uint_as_float(ob + __funnelshift_l(0u, __float_as_uint(t.x), 23)),
+        __uint_as_float(ob + __funnelshift_l(0u, __float_as_uint(t.y), 23)));
+#else
     const float2 osc = make_float2(__uint_as_float(ob + (__float_as_uint(t.x) << 23)),
                                    __uint_as_float(ob + (__float_as_uint(t.y) << 23)));
+#endif
     return __fmul2_rn(y, osc);
 }
 
@@ -129,16 +129,24 @@ __device__ __forceinline__ float ex2_sfu(float x)
     return y;
 }
 
+// cp.async of one 16-byte chunk global -> shared (L2 only: the records are
+// re-read by the other tiles of the splat, not by this SM)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // One (view, tile): the whole K7 computation of the tile's 256 pixels.
 template <bool COUNT, bool TRAIN, bool FAST>
 __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, const int tile)
 {
-    __shared__ float4 s_rec[3 * RB];   // RB splat records, 48 B each
-#if S3R_RASTER_CLIST
-    __shared__ uint16_t s_cl[NW][RB];  // per warp block: staged records reaching it
-                                       // (index | pair-block mask << 8)
-    __shared__ int s_wc[NW][NW];       // [staging warp][warp block] kept counts
-#endif
+    __shared__ float4 s_rec[NBUF][3 * RB];   // staged splat records, 48 B each
+    __shared__ uint16_t s_cl[NW][RB];        // per warp block: staged records reaching it
+    __shared__ int s_wc[NW][NW];             // [staging warp][warp block] kept counts
     const DevView& V = a.views[v];
     if (tile >= V.ntiles) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -160,9 +168,6 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
     static_assert(BW >= 8, "cull extents assume >= 8 x 16 warp blocks");
     constexpr float XPAD = 0.5f * (BW - 1) - CULL_HALF_BX;
     const float bcx0 = (float)(tx * TILE) + 0.5f * (BW - 1);     // warp block 0
-#if !S3R_RASTER_CLIST
-    const float bcx = bcx0 + (float)((tid >> 5) * BW);
-#endif
     const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
     // pair P holds pixels k = 2P (.x) and 2P + 1 (.y)
     float2 nfpy[NP], T[NP], cr[NP], cg[NP], cb[NP], dp[NP];
@@ -185,6 +190,11 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
                            (inside >> (2 * P + 1)) & 1 ? 1.0f : 0.0f);
         cr[P] = cg[P] = cb[P] = dp[P] = f2(0.0f);
     }
+#if S3R_RASTER_FASTLIVE
+    // every pixel of the warp live (warp-uniform): the blend skips the per-pixel
+    // T >= 1e-4 tests until the first termination in the warp
+    bool all_live = __all_sync(0xffffffffu, inside == (1u << RPIX) - 1u);
+#endif
     const int2 rg = a.tranges[V.trange_off + tile];
     const uint32_t* lst = a.tlists + V.tlist_off;
     const float4* recs = a.rec_sorted + 3 * V.cap_off;
@@ -192,50 +202,141 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
     // argument so it stays in a register (an immediate is re-materialised per use)
     const float c0 = a.exp2_c0;
 
-    int cur = rg.x;                    // cursor in the supertile list (uniform)
+    // one record (staged slot j of buffer `buf`, tile-list entry tpos + j) for the
+    // thread's 4 pixels; LIVE: test each pixel's T >= 1e-4 (else all are live)
+    auto blend = [&](const float4* sr, const int tj, auto live_tag) {
+        constexpr bool LIVE = decltype(live_tag)::value;
+        const float4 q0 = sr[0];   // mx, my, z, o
+        const float4 q1 = sr[1];   // qa, qb, qc, flush half extent x
+        const float4 q2 = sr[2];   // r, g, b, flush half extent y
+        // e2 = log2(e) * power = qa dx^2 + qb dx dy + qc dy^2 (R-ARITH exp2
+        // form); the dx terms are shared by the thread's 4 pixels
+        const float dx = q0.x - fpx;
+        const float a1 = q1.x * dx;
+        const float a2 = a1 * dx;
+        const float b1 = q1.y * dx;
+#pragma unroll
+        for (int P = 0; P < NP; ++P) {
+            const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
+            const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
+            const float2 e2r = __ffma2_rn(dy, c1, f2(a2));
+            const float2 e2 = make_float2(fminf(0.0f, e2r.x), fminf(0.0f, e2r.y));
+            // A dead pixel (T < 1e-4) or a flushed exp2 (e2 < -24, s3r_exp2 = 0)
+            // has alpha = 0, which leaves C, D and T bit-identical
+            // (fma(c, 0, C) == C, T - 0 == T): such evaluations are skipped
+            // (both of the pair) or get alpha = 0 (one of the pair).
+            const bool livx = !LIVE || T[P].x >= 1e-4f, livy = !LIVE || T[P].y >= 1e-4f;
+            const bool onx = (e2.x >= S3R_FLUSH_E2) && livx;
+            const bool ony = (e2.y >= S3R_FLUSH_E2) && livy;
+            if (TRAIN && !COUNT) {
+                // the backward's per-pixel bound: the last entry the pixel
+                // was live at (its terminating one, or a later entry that
+                // is flushed for it anyway), one select per pixel
+                stop[2 * P] = livx ? tj : stop[2 * P];
+                stop[2 * P + 1] = livy ? tj : stop[2 * P + 1];
+            }
+#if S3R_RASTER_UVOTE
+            if (__any_sync(0xffffffffu, onx || ony)) {
+#else
+            if (onx || ony) {
+#endif
+                const float2 og = FAST
+                    ? __fmul2_rn(make_float2(ex2_sfu(e2.x), ex2_sfu(e2.y)), f2(q0.w))
+                    : o_exp2_x2(e2, q0.w, c0);
+                const float2 alpha = make_float2(onx ? fminf(0.99f, og.x) : 0.0f,
+                                                 ony ? fminf(0.99f, og.y) : 0.0f);
+                const float2 w = __fmul2_rn(alpha, T[P]);
+                cr[P] = __ffma2_rn(f2(q2.x), w, cr[P]);
+                cg[P] = __ffma2_rn(f2(q2.y), w, cg[P]);
+                cb[P] = __ffma2_rn(f2(q2.z), w, cb[P]);
+                dp[P] = __ffma2_rn(f2(q0.z), w, dp[P]);
+                const float2 Tn = __fadd2_rn(T[P], neg2(w));
+                // include-then-stop (R14): the pixel is dead once T < 1e-4
+                if (COUNT) {
+                    if (onx && Tn.x < 1e-4f) stop[2 * P] = tj + 1;
+                    if (ony && Tn.y < 1e-4f) stop[2 * P + 1] = tj + 1;
+                }
+                T[P] = Tn;
+            }
+        }
+    };
+    auto tmax_of = [&]() {
+        float m = fmaxf(T[0].x, T[0].y);
+#pragma unroll
+        for (int P = 1; P < NP; ++P) m = fmaxf(m, fmaxf(T[P].x, T[P].y));
+        return m;
+    };
+
+    // stage records [c, c + n) of the tile list into buffer b (16-byte pieces)
+    auto stage = [&](int b, int c, int n) {
+        for (int i = tid; i < n; i += RT) {
+            const float4* src = recs + 3ll * lst[c + i];
+#if S3R_RASTER_STAGE == 0
+            const float4 q0 = src[0], q1 = src[1], q2 = src[2];
+            s_rec[b][3 * i + 0] = q0;
+            s_rec[b][3 * i + 1] = q1;
+            s_rec[b][3 * i + 2] = q2;
+#else
+            cp_async16(&s_rec[b][3 * i + 0], src + 0);
+            cp_async16(&s_rec[b][3 * i + 1], src + 1);
+            cp_async16(&s_rec[b][3 * i + 2], src + 2);
+#endif
+        }
+#if S3R_RASTER_STAGE != 0
+        cp_async_commit();
+#endif
+    };
+
+    int cur = rg.x;                    // cursor in the tile list (uniform)
     int tpos = 0;                      // tile-list entries consumed so far (uniform)
     uint32_t n_exec = 0;
+    int buf = 0;
+#if S3R_RASTER_STAGE == 2
+    if (cur < rg.y) stage(0, cur, min(RB, rg.y - cur));
+#endif
     while (cur < rg.y) {
         if (__syncthreads_count(nlive) == 0) break;
-        // ---- stage the next RB records of the tile's list (16-byte loads)
         const int nb = min(RB, rg.y - cur);
-#if S3R_RASTER_CLIST
-        // ... and, per warp block, the order-preserving list of the records
-        // whose flush ellipse reaches it (the others have alpha = 0 on every
-        // pixel of the block, s3r_internal.cuh flush_extent): ballot + popc
-        // inside each staging warp, staging warps in order
+#if S3R_RASTER_STAGE == 2
+        // the next batch streams into the other buffer while this one blends
+        // (the barrier above ended every warp's use of that buffer)
+        if (cur + nb < rg.y) stage(buf ^ 1, cur + nb, min(RB, rg.y - cur - nb));
+        else cp_async_commit();              // empty group: wait_group 1 stays uniform
+        cp_async_wait<1>();
+        __syncthreads();
+#elif S3R_RASTER_STAGE == 1
+        stage(0, cur, nb);
+        cp_async_wait<0>();
+        __syncthreads();
+#endif
+        // ---- the staged batch's per-warp-block lists: the order-preserving
+        // list of the records whose flush ellipse reaches the block (the others
+        // have alpha = 0 on every pixel of the block, s3r_internal.cuh
+        // flush_extent): ballot + popc inside each staging warp, warps in order
         int run[NW];
 #pragma unroll
         for (int w = 0; w < NW; ++w) run[w] = 0;
         for (int base = 0; base < nb; base += RT) {
             const int i = base + tid;
             bool keep[NW];
-            unsigned pmask = (1u << NP) - 1u;
-#if S3R_RASTER_PMASK
-            pmask = 0;
-#endif
 #pragma unroll
             for (int w = 0; w < NW; ++w) keep[w] = false;
             if (i < nb) {
+#if S3R_RASTER_STAGE == 0
                 const float4* src = recs + 3ll * lst[cur + i];
                 const float4 q0 = src[0], q1 = src[1], q2 = src[2];
-                s_rec[3 * i + 0] = q0;
-                s_rec[3 * i + 1] = q1;
-                s_rec[3 * i + 2] = q2;
+                s_rec[0][3 * i + 0] = q0;
+                s_rec[0][3 * i + 1] = q1;
+                s_rec[0][3 * i + 2] = q2;
+#else
+                const float4 q0 = s_rec[buf][3 * i + 0], q1 = s_rec[buf][3 * i + 1],
+                             q2 = s_rec[buf][3 * i + 2];
+#endif
                 const float hx = XPAD != 0.0f ? q1.w + XPAD : q1.w;
                 const bool yok = !(fabsf(q0.y - bcy) > q2.w);
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
                     keep[w] = yok && !(fabsf(q0.x - (bcx0 + (float)(w * BW))) > hx);
-#if S3R_RASTER_PMASK
-                // pair P covers the tile rows 2 RS P .. 2 RS P + 2 RS - 1
-#pragma unroll
-                for (int P = 0; P < NP; ++P) {
-                    const float cy = (float)(ty * TILE + 2 * RS * P) + 0.5f * (2 * RS - 1);
-                    if (!(fabsf(q0.y - cy) > q2.w - (CULL_HALF_BY - 0.5f * (2 * RS - 1))))
-                        pmask |= 1u << P;
-                }
-#endif
             }
             unsigned bal[NW];
 #pragma unroll
@@ -253,121 +354,52 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
                     if (sw < warp) off += c;
                     tot += c;
                 }
-                if (keep[w])
-                    s_cl[w][off + __popc(bal[w] & ((1u << lane) - 1u))] = (uint16_t)(i | (pmask << 8));
+                if (keep[w]) s_cl[w][off + __popc(bal[w] & ((1u << lane) - 1u))] = (uint16_t)i;
                 run[w] += tot;
             }
             __syncthreads();
         }
         const int nk = run[warp];
-#else
-        for (int i = tid; i < nb; i += RT) {
-            const float4* src = recs + 3ll * lst[cur + i];
-            s_rec[3 * i + 0] = src[0];
-            s_rec[3 * i + 1] = src[1];
-            s_rec[3 * i + 2] = src[2];
-        }
-        __syncthreads();
-#endif
         cur += nb;
         n_exec += nb;
+        const float4* sb = s_rec[buf];
         // the blend loop is warp-uniform (every lane runs it while any lane of
         // its warp is live) so that the votes below see the full warp
         if (__any_sync(0xffffffffu, nlive != 0)) {
-#if S3R_RASTER_CLIST
-#if S3R_VOTE_EVERY > 1
-#pragma unroll (kVoteEvery)
-#endif
-            for (int jj = 0; jj < nk; ++jj) {
-                const unsigned ent = s_cl[warp][jj];
-                const int j = ent & 0xff;
-#if S3R_RASTER_PMASK
-                const unsigned pm = ent >> 8;
-#endif
-#else
-            for (int j = 0; j < nb; ++j) {
-#endif
-                const float4* sr = s_rec + 3 * j;
-                const float4 q0 = sr[0];   // mx, my, z, o
-                const float4 q1 = sr[1];   // qa, qb, qc, flush half extent x
-                const float4 q2 = sr[2];   // r, g, b, flush half extent y
-#if S3R_CULL && !S3R_RASTER_CLIST
-                // every evaluation of the warp's block lies outside the splat's
-                // flush ellipse (alpha = 0 for all of them): skip the record,
-                // warp-uniformly (s3r_internal.cuh flush_extent)
-                if (fabsf(q0.x - bcx) > (XPAD != 0.0f ? q1.w + XPAD : q1.w) ||
-                    fabsf(q0.y - bcy) > q2.w)
-                    continue;
-#endif
-                // e2 = log2(e) * power = qa dx^2 + qb dx dy + qc dy^2 (R-ARITH exp2
-                // form); the dx terms are shared by the thread's 4 pixels
-                const float dx = q0.x - fpx;
-                const float a1 = q1.x * dx;
-                const float a2 = a1 * dx;
-                const float b1 = q1.y * dx;
+            int jj = 0;
+#if S3R_RASTER_FASTLIVE
+            if (all_live) {
+                for (; jj < nk; ++jj) {
+                    const int j = s_cl[warp][jj];
+                    blend(sb + 3 * j, tpos + j, std::false_type{});
+                    float m = fminf(T[0].x, T[0].y);
 #pragma unroll
-                for (int P = 0; P < NP; ++P) {
-#if S3R_RASTER_CLIST && S3R_RASTER_PMASK
-                    if (!(pm & (1u << P))) continue;     // the pair block is all flushed
-#endif
-                    const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
-                    const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
-                    const float2 e2r = __ffma2_rn(dy, c1, f2(a2));
-                    const float2 e2 = make_float2(fminf(0.0f, e2r.x), fminf(0.0f, e2r.y));
-                    // A dead pixel (T < 1e-4) or a flushed exp2 (e2 < -24, s3r_exp2 = 0)
-                    // has alpha = 0, which leaves C, D and T bit-identical
-                    // (fma(c, 0, C) == C, T - 0 == T): such evaluations are skipped
-                    // (both of the pair) or get alpha = 0 (one of the pair).
-                    const bool livx = T[P].x >= 1e-4f, livy = T[P].y >= 1e-4f;
-                    const bool onx = (e2.x >= S3R_FLUSH_E2) && livx;
-                    const bool ony = (e2.y >= S3R_FLUSH_E2) && livy;
-                    if (TRAIN && !COUNT) {
-                        // the backward's per-pixel bound: the last entry the pixel
-                        // was live at (its terminating one, or a later entry that
-                        // is flushed for it anyway), one select per pixel
-                        stop[2 * P] = livx ? tpos + j : stop[2 * P];
-                        stop[2 * P + 1] = livy ? tpos + j : stop[2 * P + 1];
-                    }
-#if S3R_RASTER_NOBR
-                    {   // branch-free: both pixels always evaluated, alpha selected
-#else
-                    if (onx || ony) {
-#endif
-                        const float2 og = FAST
-                            ? __fmul2_rn(make_float2(ex2_sfu(e2.x), ex2_sfu(e2.y)), f2(q0.w))
-                            : o_exp2_x2(e2, q0.w, c0);
-                        const float2 alpha = make_float2(onx ? fminf(0.99f, og.x) : 0.0f,
-                                                         ony ? fminf(0.99f, og.y) : 0.0f);
-                        const float2 w = __fmul2_rn(alpha, T[P]);
-                        cr[P] = __ffma2_rn(f2(q2.x), w, cr[P]);
-                        cg[P] = __ffma2_rn(f2(q2.y), w, cg[P]);
-                        cb[P] = __ffma2_rn(f2(q2.z), w, cb[P]);
-                        dp[P] = __ffma2_rn(f2(q0.z), w, dp[P]);
-                        const float2 Tn = __fadd2_rn(T[P], neg2(w));
-                        // include-then-stop (R14): the pixel is dead once T < 1e-4
-                        if (COUNT) {
-                            if (onx && Tn.x < 1e-4f) stop[2 * P] = tpos + j + 1;
-                            if (ony && Tn.y < 1e-4f) stop[2 * P + 1] = tpos + j + 1;
-                        }
-                        T[P] = Tn;
+                    for (int P = 1; P < NP; ++P) m = fminf(m, fminf(T[P].x, T[P].y));
+                    if (__any_sync(0xffffffffu, m < 1e-4f)) {   // a pixel of the warp died
+                        all_live = false;
+                        ++jj;
+                        nlive = tmax_of() >= 1e-4f ? 1 : 0;
+                        if (!__any_sync(0xffffffffu, nlive != 0)) jj = nk;
+                        break;
                     }
                 }
-#if S3R_RASTER_CLIST && S3R_VOTE_EVERY > 1
-                // the warp-termination vote every S3R_VOTE_EVERY records (a dead
-                // pixel blends nothing, so later votes only cost evaluations)
-                if ((jj % S3R_VOTE_EVERY) == S3R_VOTE_EVERY - 1 || jj + 1 == nk)
+            }
 #endif
-                {
-                float tmax = fmaxf(T[0].x, T[0].y);
-#pragma unroll
-                for (int P = 1; P < NP; ++P) tmax = fmaxf(tmax, fmaxf(T[P].x, T[P].y));
-                nlive = tmax >= 1e-4f ? 1 : 0;
+            for (; jj < nk; ++jj) {
+                const int j = s_cl[warp][jj];
+                blend(sb + 3 * j, tpos + j, std::true_type{});
+                nlive = tmax_of() >= 1e-4f ? 1 : 0;
                 if (!__any_sync(0xffffffffu, nlive != 0)) break;   // whole warp done
-                }
             }
         }
         tpos += nb;
+#if S3R_RASTER_STAGE == 2
+        buf ^= 1;
+#endif
     }
+#if S3R_RASTER_STAGE == 2
+    cp_async_wait<0>();                   // nothing in flight when the CTA exits
+#endif
     if (COUNT) {
         // E_alg = sum over pixels of the tile-list entries examined up to and
         // including the terminating one; E_exec = 256 x entries the CTA staged
@@ -404,28 +436,12 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
     }
 }
 
-// K7: one CTA per (tile, view) — or, with a.work (S3R_RASTER_PERSIST), a
-// persistent grid whose CTAs take (view, tile) work items from an atomic
-// counter in (view, tile) order
+// K7: one CTA per (tile, view)
 template <bool COUNT, bool TRAIN, bool FAST>
 __global__ void __launch_bounds__(RT, TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER_MINB)
     k_raster(RasterArgs a)
 {
-#if !S3R_RASTER_PERSIST
     raster_tile<COUNT, TRAIN, FAST>(a, blockIdx.y, blockIdx.x);
-#else
-    __shared__ int s_item;
-    const int total = a.max_tiles * a.n_views;
-    for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(a.work, 1);
-        __syncthreads();
-        const int w = s_item;
-        __syncthreads();
-        if (w >= total) break;
-        raster_tile<COUNT, TRAIN, FAST>(a, w / a.max_tiles, w % a.max_tiles);
-        __syncthreads();          // shared staging buffers are reused by the next item
-    }
-#endif
 }
 
 // ------------------------------------------------------------------ dumps
@@ -442,19 +458,7 @@ void launch_raster(const RasterArgs& args, cudaStream_t st)
     if (args.max_tiles == 0 || args.n_views == 0) return;
     RasterArgs a = args;
     a.exp2_c0 = 1.3264695880934596e-3f;
-    dim3 grid(a.max_tiles, a.n_views);
-#if S3R_RASTER_PERSIST
-    {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (a.train_T) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster<false, true, false>, RT, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster<false, false, false>, RT, 0);
-        grid = dim3((unsigned)std::max(1, sms * per_sm), 1);
-    }
-#else
-    a.work = nullptr;
-#endif
+    const dim3 grid(a.max_tiles, a.n_views);
     // training renders always take the exact R-ARITH exponential: the backward
     // recomputes alpha with it and relies on the forward's decisions
     if (a.train_T) {

@@ -23,6 +23,7 @@ using namespace s3r;
 namespace s3r {
 int filter_tile();
 int project_tile();
+int splat_grad_stride();
 }
 
 namespace {
@@ -348,10 +349,10 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
                                (size_t)(nv + 1) * 64;
     if ((rc = stage_reserve(c, stage_bytes))) return rc;
     c->h_stage_top = 0;
-    // one zeroed work counter per launch that takes tickets: the filter chunks,
-    // the depth-sort passes and the rasterizer
+    // one zeroed work counter per launch that takes tickets: the filter chunks
+    // and the depth-sort passes
     const int n_tickets = (T + MAX_TSLOTS - 1) / MAX_TSLOTS +
-                          (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS + 1;
+                          (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS;
     c->ticket_cap = n_tickets;
     if ((rc = ensure(c, c->d_ticket, (size_t)n_tickets * sizeof(int)))) return rc;
     if ((rc = ensure(c, c->d_err, sizeof(uint32_t)))) return rc;
@@ -651,7 +652,6 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.train_T = c->training ? P<float>(c->d_train_T) : nullptr;
         a.train_n = c->training ? P<int>(c->d_train_n) : nullptr;
         a.fast_exp = c->fast_exp ? 1 : 0;
-        a.work = next_ticket(c);          // zeroed per batch; used by the persistent form
         launch_raster(a, st);
         ev_end(c, st, e);
         c->last_counters = a.evals != nullptr;
@@ -1194,8 +1194,9 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
     int rc;
     long long cap = 0;
     for (int v = 0; v < nv; ++v) cap = std::max(cap, c->hv[v].cap_off + c->hv[v].n_temporal);
-    if ((rc = ensure(c, c->d_sgrads, (size_t)std::max(cap, 1ll) * 40))) return rc;
-    CU(cudaMemsetAsync(c->d_sgrads.p, 0, (size_t)std::max(cap, 1ll) * 40, st));
+    const size_t sg_bytes = (size_t)std::max(cap, 1ll) * 4 * splat_grad_stride();
+    if ((rc = ensure(c, c->d_sgrads, sg_bytes))) return rc;
+    CU(cudaMemsetAsync(c->d_sgrads.p, 0, sg_bytes, st));
     if ((rc = ensure(c, c->d_cots, (size_t)std::max(nv, 1) * sizeof(s3r_cot)))) return rc;
     if ((rc = stage_reserve(c, (size_t)std::max(nv, 1) * sizeof(s3r_cot) + 512))) return rc;
     if (c->staging_recorded) CU(cudaEventSynchronize(c->staging_free));

@@ -273,7 +273,6 @@ struct RasterArgs {
     int* train_n;                // per pixel blended list entries (training), at V.pix_off
     float exp2_c0;               // 1.3264695880934596e-3f (set by launch_raster)
     int fast_exp;                // 1: SFU ex2.approx instead of R-ARITH (not for training)
-    int* work;                   // zeroed work counter (persistent form) or NULL
 };
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 
@@ -292,7 +291,7 @@ struct BackwardArgs {
     const float4* rec_sorted;
     const float* train_T;
     const int* train_n;
-    float* splat_grads;                  // [cap][10] per depth rank
+    float* splat_grads;                  // [cap][splat_grad_stride()] per depth rank (10 used)
     const unsigned long long* dkey_sorted;
     unsigned long long gmask;            // (1 << gbits) - 1
     const int32_t* ids;

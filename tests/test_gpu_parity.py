@@ -6,6 +6,7 @@ pair order, tile ranges, life update; RGB and depth within 1e-4 max abs.  Under
 the R-ARITH contract the fp32 keys and images are in fact
 bit-identical, which is asserted separately.
 """
+import ctypes as C
 import math
 
 import numpy as np
@@ -45,12 +46,21 @@ def gpu_render(ctx, scene, views, life=True, visible=True):
     return ds, tabs, outs, rc
 
 
-def check_view(ctx, scene, view, table, out, vi, exact=True, o=None, img_tol=IMG_TOL):
-    """Compare view `vi` of the last GPU render with the oracle (f32 contract)."""
-    if o is None:
-        o = oracle.render_view(scene, view, "f32", table=table.cpu().numpy())
-    st = ctx.stats(vi)
+def gpu_dump(ctx, view, vi, out):
+    """Everything the parity check compares, for view `vi` of the last GPU render,
+    as numpy arrays (stats, debug dumps, images, M_t)."""
     d = {k: v.cpu().numpy() for k, v in ctx.dump(vi, view.width, view.height).items()}
+    d["stats"] = ctx.stats(vi)
+    for k in ("rgb", "depth", "final_T", "visible"):
+        if k in out:
+            d[k] = out[k].cpu().numpy()
+    return d
+
+
+def compare_dump(d, o, exact=True, img_tol=IMG_TOL):
+    """GPU dump `d` vs oracle render `o` (f32 contract): integer outputs
+    bit-exact, images within img_tol (bit-identical when exact)."""
+    st = d["stats"]
     # counts
     for k in ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped", "n_rendered", "n_pairs",
               "n_bad_instance"):
@@ -64,8 +74,8 @@ def check_view(ctx, scene, view, table, out, vi, exact=True, o=None, img_tol=IMG
         np.nanmax(np.abs(d["keys"] - ok))
     assert np.array_equal(d["flags"], o["flags"][ti])
     assert np.array_equal(d["rect"], o["rect"][ti])
-    if "visible" in out:
-        assert np.array_equal(out["visible"].cpu().numpy(), o["visible"])
+    if "visible" in d:
+        assert np.array_equal(d["visible"], o["visible"])
     # depth order of rendered Gaussians: (z, index)
     rend = np.nonzero(o["flags"] & oracle.F_RENDERED)[0]
     want_order = rend[np.lexsort((rend, o["splat_keys"][rend, 2]))]
@@ -81,7 +91,7 @@ def check_view(ctx, scene, view, table, out, vi, exact=True, o=None, img_tol=IMG
     ne = cnt_o > 0
     assert np.array_equal(d["ranges"][ne], o["ranges"][ne])
     # K7: images
-    rgb, dep, T = (out[k].cpu().numpy() for k in ("rgb", "depth", "final_T"))
+    rgb, dep, T = d["rgb"], d["depth"], d["final_T"]
     assert np.abs(rgb - o["rgb"]).max() <= img_tol
     assert np.abs(dep - o["depth"]).max() <= img_tol
     assert np.abs(T - o["final_T"]).max() <= img_tol
@@ -89,6 +99,14 @@ def check_view(ctx, scene, view, table, out, vi, exact=True, o=None, img_tol=IMG
         assert np.array_equal(rgb, o["rgb"]) and np.array_equal(dep, o["depth"])
         assert np.array_equal(T, o["final_T"])
     return o
+
+
+def check_view(ctx, scene, view, table, out, vi, exact=True, o=None, img_tol=IMG_TOL):
+    """Compare view `vi` of the last GPU render with the oracle (f32 contract;
+    the oracle composes its own instance camera table from the view)."""
+    if o is None:
+        o = oracle.render_view(scene, view, "f32")
+    return compare_dump(gpu_dump(ctx, view, vi, out), o, exact, img_tol)
 
 
 def test_compose_matches_oracle(ctx):
@@ -131,7 +149,7 @@ def test_life_update_and_commit(ctx):
     ds, tabs, outs, rc = gpu_render(ctx, scene, views)
     ref = scene.copy()
     for vi, v in enumerate(views):
-        o = oracle.render_view(ref, v, "f32", table=tabs[vi].cpu().numpy(), pairs=False,
+        o = oracle.render_view(ref, v, "f32", pairs=False,
                                image=False)
         oracle.update_life(ref, o["visible"], v.t)
     assert np.array_equal(ds.life.cpu().numpy(), ref.life)
@@ -242,7 +260,7 @@ def test_lod_noisy_offset(ctx, seed):
     n_jit = 0
     for vi, v in enumerate(views):
         vj = dataclasses.replace(v, lod_jitter=jit)
-        o = oracle.render_view(scene, vj, "f32", table=tabs[vi].cpu().numpy())
+        o = oracle.render_view(scene, vj, "f32")
         check_view(ctx, scene, vj, tabs[vi], outs[vi], vi, o=o)
         n_jit += int(np.count_nonzero(o["flags"] & oracle.F_JITTERED))
     assert n_jit > 100
@@ -280,14 +298,14 @@ def test_neurf_colors(ctx, seed):
         d = {k: t.cpu().numpy() for k, t in dumps[vi].items()}
         order = d["depth_order"]
         assert len(order) == stats[vi]["n_rendered"] > 200
-        want = neurf.query_colors(scene, v, tabs[vi].cpu().numpy(), order, prm)
+        want = neurf.query_colors(scene, v, oracle.compose(v), order, prm)
         err = np.abs(d["splat_rgb"].astype(np.float64) - want).max()
         worst = max(worst, err)
         assert err <= NEURF_TOL, (vi, err)
         # the rest of the pipeline on the oracle's colours
         sc = scene.copy()
         sc.colors[order, :3] = want.astype(np.float32)
-        o = oracle.render_view(sc, v, "f32", table=tabs[vi].cpu().numpy())
+        o = oracle.render_view(sc, v, "f32")
         # check_view dumps again: render once more with the query on
     print("max NeurF colour error", worst)
     ctx.set_neural_colors(dev)
@@ -296,9 +314,8 @@ def test_neurf_colors(ctx, seed):
         for vi, v in enumerate(views):
             order = ctx.dump(vi, v.width, v.height)["depth_order"].cpu().numpy()
             sc = scene.copy()
-            sc.colors[order, :3] = neurf.query_colors(scene, v, tabs[vi].cpu().numpy(), order,
-                                                      prm).astype(np.float32)
-            o = oracle.render_view(sc, v, "f32", table=tabs[vi].cpu().numpy())
+            sc.colors[order, :3] = neurf.query_colors(scene, v, oracle.compose(v), order, prm).astype(np.float32)
+            o = oracle.render_view(sc, v, "f32")
             check_view(ctx, sc, v, tabs[vi], outs[vi], vi, exact=False, o=o, img_tol=NEURF_TOL)
     finally:
         ctx.set_neural_colors(None)
@@ -375,8 +392,13 @@ def test_invalid_arguments(ctx):
     with pytest.raises(s3r.S3RError):
         ctx.render_batch(ds, [bad], [tabs[0]], outs)
     bad = sg.View(**{**views[0].__dict__, "width": 0})
-    with pytest.raises(s3r.S3RError):
+    with pytest.raises((s3r.S3RError, ValueError)):      # the binding's shape check first
         ctx.render_batch(ds, [bad], [tabs[0]], outs)
+    with pytest.raises(s3r.S3RError) as e:             # the C ABI's own check
+        ctx._check(ctx.L.s3r_render_batch(ctx.h, C.byref(ds.struct()), (s3r.View_ * 1)(
+            s3r.view_struct(bad, tabs[0])), 1, (s3r.Outputs_ * 1)(s3r.Outputs_(
+                s3r._ptr(outs[0]["rgb"]), None, None, None)), s3r._stream()))
+    assert e.value.code == s3r.S3R_EINVAL
     # mode setters: unknown pipeline, non-finite offset, bad NeurF parameters
     with pytest.raises(s3r.S3RError) as e:
         ctx._check(ctx.L.s3r_set_pipeline(ctx.h, 7))
@@ -460,12 +482,27 @@ GRAD_ATTR = {"mean": [0, 1, 2], "opacity": [3], "scale": [4, 5, 6], "rot": [8, 9
              "color": [12, 13, 14]}
 
 
-def _check_grads(g_gpu, g_ref, tol=1e-3):
+def _check_grads(g_gpu, g_ref, tol=1e-3, floor=1e-2):
+    """north_star's 1e-3 gate, two ways: per attribute max|g_gpu - g_oracle| <=
+    1e-3 max|g_oracle|; and element by element, relative to the entry itself for
+    the entries above `floor` x the attribute's max (so that small per-Gaussian
+    gradients are checked relative to themselves, not only to the largest)."""
     for name, cols in GRAD_ATTR.items():
         ref = np.abs(g_ref[:, cols]).max()
         d = np.abs(g_gpu[:, cols] - g_ref[:, cols]).max()
         assert ref > 0, name
         assert d <= tol * ref, (name, d, ref)
+        a, b = g_gpu[:, cols], g_ref[:, cols]
+        big = np.abs(b) > floor * ref
+        rel = np.abs(a[big] - b[big]) / np.abs(b[big])
+        # every entry above 10 % of the max within 1e-3; above 1 %: 99.9 % of the
+        # entries within 1e-3 and all within 1e-2 (a world-frame mean / scale
+        # gradient can be a cancelling sum of camera-frame terms ~10x larger;
+        # measured on a full C3 view: p99.9 3.9e-4, max 1.5e-3, DESIGN.md §4)
+        top = np.abs(b[big]) > 0.1 * ref
+        assert rel[top].max() <= tol, (name, float(rel[top].max()), int(top.sum()))
+        assert np.quantile(rel, 0.999) <= tol and rel.max() <= 10 * tol, \
+            (name, float(np.quantile(rel, 0.999)), float(rel.max()), int(big.sum()))
 
 
 @pytest.mark.parametrize("seed", [1, 2])
@@ -481,7 +518,7 @@ def test_backward_matches_oracle(ctx, seed):
     g_ref = np.zeros((scene.n, 16))
     for vi, (v, t, c) in enumerate(zip(views, tabs, cot)):
         gt_ref = np.zeros((scene.num_instances, 12))
-        oracle.backward(scene, v, c["rgb"], c["depth"], c["final_T"], table=t.cpu().numpy(),
+        oracle.backward(scene, v, c["rgb"], c["depth"], c["final_T"],
                         grads=g_ref, g_table=gt_ref)
         # NEXT-1 pose gradient per view and instance, same 1e-3 gate
         got = gt[vi].cpu().numpy().astype(np.float64)
@@ -528,8 +565,8 @@ def test_backward_with_noisy_offset(ctx):
     n_jit = 0
     for v, t, c in zip(views, tabs, cot):
         vj = dataclasses.replace(v, lod_jitter=jit)
-        oracle.backward(scene, vj, c["rgb"], table=t.cpu().numpy(), grads=g_ref)
-        o = oracle.render_view(scene, vj, "f32", table=t.cpu().numpy(), pairs=False, image=False)
+        oracle.backward(scene, vj, c["rgb"], grads=g_ref)
+        o = oracle.render_view(scene, vj, "f32", pairs=False, image=False)
         n_jit += int(np.count_nonzero(o["flags"] & oracle.F_JITTERED))
     assert n_jit > 50
     _check_grads(g_gpu, g_ref)
@@ -567,7 +604,7 @@ def test_training_step_mse_street(ctx):
                             ("means_opacity", "scales", "rotations", "colors")], 1)
     g_ref = np.zeros((scene.n, 16))
     for v, t, c in zip(views, tabs, cots):
-        oracle.backward(scene, v, c["rgb"].cpu().numpy().astype(np.float64), table=t.cpu().numpy(),
+        oracle.backward(scene, v, c["rgb"].cpu().numpy().astype(np.float64),
                         grads=g_ref)
     _check_grads(g_gpu, g_ref)
 
@@ -778,7 +815,7 @@ def test_fast_exp_within_tolerance(ctx, case):
     assert rc == 0
     n_px = n_off = 0
     for vi, v in enumerate(views):
-        o = oracle.render_view(scene, v, "f32", table=tabs[vi].cpu().numpy())
+        o = oracle.render_view(scene, v, "f32")
         st = ctx.stats(vi)
         for k in ("n_temporal", "n_visible", "n_lod_small", "n_lod_dropped", "n_rendered", "n_pairs"):
             assert st[k] == o["stats"][k]

@@ -9,6 +9,23 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANT_SETS = {
+    "r2bwd": {
+        "base": [],
+        "stage0": ["S3R_RASTER_STAGE=0"],
+        "vred": ["S3R_BWD_VRED=1"],
+        "ulast": ["S3R_BWD_ULAST=1"],
+        "vredulast": ["S3R_BWD_VRED=1", "S3R_BWD_ULAST=1"],
+    },
+    "r2raster": {
+        "base": [],
+        "fastlive": ["S3R_RASTER_FASTLIVE=1"],
+        "uvote": ["S3R_RASTER_UVOTE=1"],
+        "aluexp": ["S3R_RASTER_ALUEXP=1"],
+        "flalu": ["S3R_RASTER_FASTLIVE=1", "S3R_RASTER_ALUEXP=1"],
+        "fluvalu": ["S3R_RASTER_FASTLIVE=1", "S3R_RASTER_UVOTE=1", "S3R_RASTER_ALUEXP=1"],
+        "stage1": ["S3R_RASTER_STAGE=1"],
+        "stage2": ["S3R_RASTER_STAGE=2"],
+    },
     "flush": {
         "base": [],
         "flush32": ["S3R_FLUSH_E2=-32.0f"],
