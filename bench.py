@@ -528,6 +528,11 @@ def main():
     ap.add_argument("--no-conventional", action="store_true",
                     help="skip the conventional-pipeline comparison (NEXT-2)")
     ap.add_argument("--train-steps", type=int, default=5)
+    ap.add_argument("--mode", default="graph", choices=["graph", "sync"],
+                    help="graph: capacity mode (s3r_set_capacity, sized from a warm-up batch "
+                         "x 1.1) with each view batch captured once in a CUDA graph and "
+                         "replayed; sync: the default synchronous sizing (two host readbacks "
+                         "per batch)")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "s3r":
         sys.exit(relaunch(args.gpus))
@@ -597,13 +602,45 @@ def main():
     outs = s3r.alloc_outputs(pools[0], device=dev)
     torch.cuda.synchronize()
 
-    def step(i):
+    def step_eager(i):
         p = i % len(pools)
         ctx.render_batch(ds, pools[p], tables[p], outs)
 
+    step = step_eager
     for i in range(args.warmup):
-        step(i)
+        step_eager(i)
     torch.cuda.synchronize()
+    graphs = None
+    if args.mode == "graph":
+        # capacities: what every batch of the pool needed, x 1.1 (any overflow is
+        # reported by s3r_check after the timed region and fails the run)
+        need = None
+        for p in range(len(pools)):
+            step_eager(p)
+            c_p = ctx.capacity_from_last(1.1)
+            need = c_p if need is None else {k: max(need[k], c_p[k]) for k in need}
+        ctx.set_capacity(need)
+        graphs = []
+        side = torch.cuda.Stream(device=dev)
+        for p in range(len(pools)):
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step_eager(p)                 # capacity-mode scratch + staging in place
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step_eager(p)
+            graphs.append(g)
+        for g in graphs:
+            g.replay()
+        torch.cuda.synchronize()
+        if ctx.check() != 0:
+            raise RuntimeError("capacity mode overflowed during the warm-up")
+
+        def step(i):
+            graphs[i % len(graphs)].replay()
+    capacity = ctx.capacity_from_last(1.0) if args.mode == "graph" else None
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local)
@@ -630,8 +667,24 @@ def main():
     torch.cuda.synchronize()
     clocks = sampler.stop()
     ms = sum(a.elapsed_time(b) for a, b in evs)
+    stage_src = "CUDA events per stage inside the timed steps"
+    if graphs is not None:
+        # graph replays carry no per-stage events: the stage breakdown (and the
+        # roofline's rasterizer time) comes from the same K steps rendered eagerly
+        # in the capacity mode right after the timed region
+        if ctx.check() != 0:
+            raise RuntimeError("capacity mode overflowed during the timed steps")
+        ctx.set_timing(True)
+        for i in range(args.steps):
+            if flush:
+                flush_buf.fill_(float(i))
+            step_eager(args.warmup + i)
+        torch.cuda.synchronize()
+        stage_src = ("CUDA events per stage of the same K steps rendered eagerly in the capacity "
+                     "mode after the timed graph replays")
     st_times = ctx.stage_times()
     ctx.set_timing(False)
+    ctx.set_capacity(None)
     rank_ms = {"max": ms / args.steps, "mean": ms / args.steps, "min": ms / args.steps}
     if world > 1:
         # load balance over ranks (front vs side cameras, near vs far content):
@@ -814,6 +867,10 @@ def main():
             "clocks": clocks,
             "rank_ms_per_step": rank_ms,
             "gpu_launches": launches_per_step * args.steps,
+            "mode": ("capacity mode + one CUDA graph per view batch (no host sync in a step; "
+                     f"capacities {capacity})" if graphs is not None else
+                     "synchronous sizing (two host readbacks per batch)"),
+            "stage_times_source": stage_src,
             "roofline": roof,
             "stages": stages,
             "workload_per_view": {k: sum(s[k] for s in stats) / views_per_step for k in

@@ -32,8 +32,10 @@
  *    scratch, grown on demand and reused; no caller pointer is retained after a
  *    call returns.
  *  - Calls enqueue work on `stream` (a cudaStream_t, NULL = legacy default
- *    stream) and return.  s3r_render / s3r_render_batch synchronise the stream
- *    twice internally to size scratch (after K1 and after K2); s3r_check,
+ *    stream) and return.  By default s3r_render / s3r_render_batch synchronise
+ *    the stream twice internally to size scratch exactly (after K1 and after
+ *    K2); in the capacity mode (s3r_set_capacity) they do not synchronise at
+ *    all and can be captured in a CUDA graph.  s3r_check,
  *    s3r_get_stage_times and s3r_render_batch_host synchronise it fully.
  *  - Return value: S3R_OK (0) or a negative S3R_E* code; the message is in
  *    s3r_last_error(ctx).  Nothing throws or aborts across the ABI.
@@ -49,7 +51,7 @@
 extern "C" {
 #endif
 
-#define S3R_VERSION 10000 /* 1.0.0 */
+#define S3R_VERSION 10100 /* 1.1.0 */
 #define S3R_TILE 16       /* tile edge in pixels (reading R12) */
 
 enum {
@@ -67,10 +69,13 @@ enum {
     S3R_ECUDA = -4,     /* a CUDA runtime error; see s3r_last_error           */
     S3R_ESTATE = -5,    /* call out of order (e.g. dump without a render, or
                            debug data requested without s3r_set_debug)        */
-    S3R_EINTERNAL = -6  /* an internal self-check failed (with s3r_set_debug
+    S3R_EINTERNAL = -6, /* an internal self-check failed (with s3r_set_debug
                            on: K2's conservative frustum pre-test culled a
                            Gaussian the exact test found visible); reported
                            by s3r_check; a library bug, never expected        */
+    S3R_ECAPACITY = -7  /* capacity mode (s3r_set_capacity): a view of a batch
+                           did not fit the reserved scratch and was rendered
+                           empty (black, final T = 1); reported by s3r_check */
 };
 
 typedef struct s3r_ctx s3r_ctx;
@@ -243,6 +248,41 @@ int s3r_set_overlap(s3r_ctx* ctx, int enable);
  * recomputes alpha with it.  Returns S3R_EINVAL for a NULL ctx.             */
 int s3r_set_fast_exp(s3r_ctx* ctx, int enable);
 
+/* Capacity mode (PAPER.md P:155 runs the per-view pipeline once per training
+ * view; SURVEY.md §7 "hard parts" 4 and 7: a per-view host readback of the
+ * splat / pair counts serialises small views).  With a reservation in place,
+ * s3r_render / s3r_render_batch size every step of a batch on the device
+ * (k_plan.cu) from the reserved capacities instead of reading counts back:
+ * the call enqueues the whole batch without a host synchronisation and may be
+ * captured in a CUDA graph (cudaStreamBeginCapture on `stream`; replaying the
+ * graph re-renders the same views and outputs).  Results are bit-identical to
+ * the default mode.  Scratch is allocated at reservation size on the next
+ * render.  A view whose counts exceed a capacity is rendered empty and
+ * s3r_check then returns S3R_ECAPACITY: check it (once per many batches is
+ * enough, it accumulates) or reserve from s3r_capacity_from_last with a
+ * margin.  Debug dumps, training, NeurF and the conventional pipeline keep the
+ * synchronous sizing (their renders ignore the reservation); s3r_get_stats
+ * synchronises on the batch.
+ *   records        rendered-candidate records over a batch: the sum over views
+ *                  of n_temporal (Gaussians passing the temporal filter)
+ *   rendered_view  splats rendered (after LOD) in any one view
+ *   bin_pairs      supertile pairs over a batch (s3r_stats.n_bin_pairs summed)
+ *   tile_entries   tile-list entries over a batch: sum of S*S x bin pairs
+ *                  (S = 4, or 8 above 4096 supertiles of 4 x 4 tiles)
+ *   temporal_view  largest n_temporal of a view (grid hint only; any count
+ *                  is processed)
+ * cap == NULL switches the mode off.  S3R_EINVAL for a NULL ctx or a
+ * negative / zero capacity.                                                */
+typedef struct s3r_capacity {
+    int64_t records, rendered_view, bin_pairs, tile_entries, temporal_view;
+} s3r_capacity;
+int s3r_set_capacity(s3r_ctx* ctx, const s3r_capacity* cap);
+
+/* The capacities the last batch needed, each multiplied by `margin` (>= 1),
+ * for s3r_set_capacity.  Synchronises on the last batch.  S3R_ESTATE
+ * without a previous render.                                               */
+int s3r_capacity_from_last(s3r_ctx* ctx, float margin, s3r_capacity* out);
+
 /* Same as s3r_render_batch, but every pointer of scene, views (including
  * instance_w2c) and outs is a HOST pointer (page-locked memory recommended).
  * The library copies the inputs to device scratch, renders, copies the
@@ -392,7 +432,7 @@ int s3r_life_flip(s3r_ctx* ctx, float* life, int64_t n, void* stream);
 
 /* Synchronise `stream` and return the device error state accumulated since
  * the last check: S3R_EINTERNAL (a failed self-check, see the enum),
- * S3R_EINSTANCE, S3R_ECUDA or S3R_OK.                                      */
+ * S3R_ECAPACITY, S3R_EINSTANCE, S3R_ECUDA or S3R_OK.                       */
 int s3r_check(s3r_ctx* ctx, void* stream);
 
 #ifdef __cplusplus

@@ -331,9 +331,6 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
     s.flags |= F_RENDERED;
 }
 
-#ifndef S3R_K2_PRECULL
-#define S3R_K2_PRECULL 1
-#endif
 // Conservative frustum pre-test (changes no result): true only when the
 // Gaussian is certainly invisible, so the exact path (quaternion
 // normalisation, ~10 IEEE divisions, 3 square roots) is skipped for the
@@ -495,8 +492,9 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     const int vi = blockIdx.y;
     const DevView& V = a.views[vi];
     const long long n_t = V.n_temporal;
-    const long long i0 = (long long)blockIdx.x * PTILE;
-    if (i0 >= n_t) return;                    // uniform for the CTA
+    // grid-stride over the view's chunks of PTILE list entries: any n_temporal
+    // is covered whatever grid.x (the capacity-mode launch sizes it from a hint)
+    if ((long long)blockIdx.x * PTILE >= n_t) return;      // uniform for the CTA
     [[maybe_unused]] const int K1 = a.num_instances;
     stage_view(a, V, s_tab, s_bounds);
     __syncthreads();
@@ -509,7 +507,6 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     const unsigned lt = (1u << lane) - 1u;
 
     unsigned long long c_vis = 0, c_small = 0, c_drop = 0, c_pairs = 0, c_bad = 0, c_spairs = 0;
-#if S3R_K2_PRECULL
     // ---- pass A (precull_chunk) queues the entries the conservative pre-test
     // cannot reject, so that pass B runs the exact path on dense warps (the
     // visible Gaussians are scattered through the index list: without the queue
@@ -519,6 +516,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     __shared__ uint32_t s_g[PTILE];
     const uint16_t* qt = s_q;
     const uint32_t* qg = s_g;
+    for (long long i0 = (long long)blockIdx.x * PTILE; i0 < n_t; i0 += (long long)gridDim.x * PTILE) {
     if (tid == 0) s_qn = 0;
     __syncthreads();
     precull_chunk(a, V, vi, i0, n_t, tl, s_tab, lox, hix, loy, hiy, s_q, s_g, &s_qn, c_bad);
@@ -539,26 +537,6 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
             const int id = __ldg(a.ids + g);
             gid_id = id;
             {
-#else
-    for (int rd = 0; rd < PR; ++rd) {
-        const long long i = i0 + rd * PT + tid;
-        const bool culled = false;
-        Splat sp;
-        sp.flags = 0;
-        long long g = -1;
-        int gid_id = 0;
-        float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < n_t) {
-            g = tl[i];
-            const int id = __ldg(a.ids + g);
-            gid_id = id;
-            if (id < 0 || id >= K1) {
-                sp.flags = F_TEMPORAL | F_BADID;
-#pragma unroll
-                for (int j = 0; j < 6; ++j) sp.k[j] = __int_as_float(0x7fc00000);
-                c_bad++;
-            } else {
-#endif
                 const float4 sc = __ldg(a.scales + g);
                 float4 mo, q;
                 int slot = id;
@@ -657,6 +635,8 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
             if (a.gidx) a.gidx[o] = (int32_t)g;
             if (a.rec_mu) a.rec_mu[o] = make_float4(sp.mu[0], sp.mu[1], sp.mu[2], __int_as_float(gid_id));
         }
+    }
+    __syncthreads();                          // the queue is refilled by the next chunk
     }
     // ---- per-view counters: one set of atomics per CTA ----
     unsigned long long cv[6] = {c_vis, c_small, c_drop, c_pairs, c_bad, c_spairs};

@@ -7,7 +7,8 @@
 // ceil((32 + gbits) / 8) passes (7 at C3's 2 M Gaussians).
 // Segments are views: every view has its own digit histograms (k_hist, one
 // read of the keys for all passes) and its own look-back chain, so one launch
-// per pass sorts the whole batch.  Tile binning does not sort (k_bin.cu).
+// per pass sorts the whole batch.  seg_tile0[nsegs] = the batch's tiles; a grid
+// larger than that (sized from a capacity, no host readback) is allowed.  Tile binning does not sort (k_bin.cu).
 //
 // Per pass each CTA takes a tile of 256*ITEMS keys (warp-striped, coalesced),
 // ranks them with __match_any_sync per warp (stable: lane order within a
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(ST) k_hist(const K* __restrict__ keys, const S
 {
     __shared__ uint32_t s_h[8][RADIX];
     const int gt = blockIdx.x;
+    if (gt >= seg_tile0[nsegs]) return;       // capacity-sized grid: beyond the batch's tiles
     const int sg = find_seg(seg_tile0, nsegs, gt);
     const Seg S = segs[sg];
     const long long lbase = (long long)(gt - seg_tile0[sg]) * (ST * HITEMS);
@@ -148,6 +150,9 @@ __global__ void __launch_bounds__(ST, S3R_SORT_MINB) k_onesweep(const K* __restr
     for (int i = tid; i < SW * RADIX; i += ST) (&s_whist[0][0])[i] = 0;
     __syncthreads();
     const int gt = s_gt, sg = s_sg;
+    // capacity-sized grid: tickets past the batch's tiles have nothing to sort
+    // (they come after every real tile, so no look-back chain waits on them)
+    if (gt >= seg_tile0[nsegs]) return;
     const Seg S = segs[sg];
     const int ltile = gt - seg_tile0[sg];
     const long long tbase = (long long)ltile * TI;

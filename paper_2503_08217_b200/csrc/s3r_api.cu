@@ -60,13 +60,38 @@ struct s3r_ctx {
     bool last_counters = false, evals_fetched = false;
     Buf d_evals;
     bool last_debug = false;
-    // pinned staging
-    char* h_stage = nullptr;
+    // pinned (mapped) staging: a ring of NSTAGE areas, so that a call waits only
+    // for the call that used its area NSTAGE calls earlier; a call captured in
+    // a CUDA graph gets an area of its own (kept until s3r_destroy)
+    struct Stage {
+        char* h = nullptr;
+        char* d = nullptr;
+        size_t cap = 0;
+        cudaEvent_t ev = nullptr;
+        bool rec = false;
+    };
+    static constexpr int NSTAGE = 3;
+    Stage ring[NSTAGE];
+    int ring_i = 0, cur_slot = -1;
+    std::vector<char*> graph_blocks;
+    char* graph_spare = nullptr;             // pinned area for the next captured call
+    size_t graph_spare_cap = 0;
+    char* h_stage = nullptr;                 // the current call's area
     char* h_stage_dev = nullptr;             // its device address (mapped)
     size_t h_stage_cap = 0;
     size_t h_stage_top = 0;
-    cudaEvent_t staging_free = nullptr;
-    bool staging_recorded = false;
+    bool capture_now = false;                // the current call is being graph-captured
+    // capacity mode (s3r_set_capacity)
+    bool cap_on = false;
+    s3r_capacity cap{};
+    bool cap_pending = false;                // stats of the last batch still on the device side
+    bool cap_suspend = false;                // s3r_render_batch_host: per-chunk stats on the host
+    bool last_capm = false;                  // the last render was planned on the device
+    long long* cap_h_ntemp = nullptr;        // mapped per-view n_temporal of that batch
+    ViewCounters* cap_h_ctr = nullptr;       // mapped per-view K2 counters of that batch
+    // the last batch's needs (for s3r_capacity_from_last)
+    s3r_capacity last_need{};
+    bool last_need_valid = false;
     cudaStream_t last_stream = nullptr;
     // device scratch
     Buf d_views, d_times, d_tidx, d_counts, d_lb, d_ticket, d_ctr, d_rec, d_dkey, d_gidx,
@@ -150,25 +175,91 @@ T* P(const Buf& b) { return reinterpret_cast<T*>(b.p); }
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-// pinned staging: a bump allocator reset at the start of each batch
-int stage_reserve(s3r_ctx* c, size_t bytes)
+// pinned staging: the next area of the ring (or, while the stream is being
+// captured, a fresh area owned by the graph), at least `bytes` large; a bump
+// allocator over it (stage_alloc) for the call
+int stage_begin(s3r_ctx* c, size_t bytes, cudaStream_t st)
 {
-    if (bytes <= c->h_stage_cap) return S3R_OK;
-    if (c->h_stage) {
-        cudaDeviceSynchronize();
-        cudaFreeHost(c->h_stage);
-        c->h_stage = nullptr;
-    }
-    size_t want = std::max<size_t>(bytes * 2, 1 << 16);
-    if (cudaHostAlloc((void**)&c->h_stage, want, cudaHostAllocMapped) != cudaSuccess ||
-        cudaHostGetDevicePointer((void**)&c->h_stage_dev, c->h_stage, 0) != cudaSuccess) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
         cudaGetLastError();
-        if (c->h_stage) cudaFreeHost(c->h_stage);
-        c->h_stage = nullptr;
-        c->h_stage_cap = 0;
-        return fail(c, S3R_ENOMEM, "cudaHostAlloc (mapped) of %zu bytes failed", want);
+        cs = cudaStreamCaptureStatusNone;
     }
-    c->h_stage_cap = want;
+    c->capture_now = cs != cudaStreamCaptureStatusNone;
+    const size_t want = std::max<size_t>(bytes * 2, 1 << 16);
+    char *h = nullptr, *d = nullptr;
+    if (c->capture_now) {
+        // no allocation or synchronisation may happen while capturing: the spare
+        // area (made outside the capture) becomes the graph's, for good
+        if (!c->graph_spare || c->graph_spare_cap < bytes)
+            return fail(c, S3R_ESTATE, "graph capture: no staging area of %zu bytes reserved "
+                                       "(render once outside the capture first)", bytes);
+        h = c->graph_spare;
+        if (cudaHostGetDevicePointer((void**)&d, h, 0) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, S3R_ECUDA, "cudaHostGetDevicePointer failed");
+        }
+        c->graph_blocks.push_back(h);
+        c->graph_spare = nullptr;
+        c->cur_slot = -1;
+        c->h_stage = h;
+        c->h_stage_dev = d;
+        c->h_stage_cap = want;
+        c->h_stage_top = 0;
+        return S3R_OK;
+    }
+    if (c->cap_on && (!c->graph_spare || c->graph_spare_cap < want)) {
+        // capacity mode: keep a spare area for a later captured call
+        if (c->graph_spare) cudaFreeHost(c->graph_spare);
+        c->graph_spare = nullptr;
+        c->graph_spare_cap = 0;
+        const size_t gw = std::max<size_t>(want * 2, 1 << 20);
+        if (cudaHostAlloc((void**)&c->graph_spare, gw, cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            c->graph_spare = nullptr;
+            return fail(c, S3R_ENOMEM, "cudaHostAlloc (mapped) of %zu bytes failed", gw);
+        }
+        c->graph_spare_cap = gw;
+    }
+    c->ring_i = (c->ring_i + 1) % s3r_ctx::NSTAGE;
+    s3r_ctx::Stage& S = c->ring[c->ring_i];
+    if (!S.ev && cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, S3R_ECUDA, "cudaEventCreate failed");
+    }
+    if (S.rec) {            // the call that used this area NSTAGE calls ago
+        if (cudaEventSynchronize(S.ev) != cudaSuccess)
+            return fail(c, S3R_ECUDA, "staging: %s", cudaGetErrorString(cudaGetLastError()));
+        S.rec = false;
+    }
+    if (bytes > S.cap) {
+        if (S.h) cudaFreeHost(S.h);
+        S.h = S.d = nullptr;
+        S.cap = 0;
+        if (cudaHostAlloc((void**)&S.h, want, cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer((void**)&S.d, S.h, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (S.h) cudaFreeHost(S.h);
+            S.h = nullptr;
+            return fail(c, S3R_ENOMEM, "cudaHostAlloc (mapped) of %zu bytes failed", want);
+        }
+        S.cap = want;
+    }
+    c->cur_slot = c->ring_i;
+    c->h_stage = S.h;
+    c->h_stage_dev = S.d;
+    c->h_stage_cap = S.cap;
+    c->h_stage_top = 0;
+    return S3R_OK;
+}
+
+// the current call's staging area is free again once `st` reaches this point
+int stage_end(s3r_ctx* c, cudaStream_t st)
+{
+    if (c->cur_slot < 0) return S3R_OK;
+    s3r_ctx::Stage& S = c->ring[c->cur_slot];
+    CU(cudaEventRecord(S.ev, st));
+    S.rec = true;
     return S3R_OK;
 }
 
@@ -201,7 +292,7 @@ void ev_begin(s3r_ctx* c, int stage, cudaStream_t st, StageEvent& e)
 {
     nvtxRangePushA(kStageName[stage]);
     e.stage = -1;
-    if (!c->timing) return;
+    if (!c->timing || c->capture_now) return;
     if (c->ev.size() > 200000) return;
     e.stage = stage;
     cudaEventCreate(&e.a);
@@ -278,7 +369,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->last_stream = st;
     c->have_render = false;
     c->host_chunked = false;
-    if (c->staging_recorded) CU(cudaEventSynchronize(c->staging_free));
+    c->cap_pending = false;
     const long long N = sc->n;
     c->N_last = N;
     c->ticket_slot = 0;
@@ -294,6 +385,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if (neurf && sc->num_instances > c->neurf_ninst)
         return fail(c, S3R_EINVAL, "NeurF: class table has %d rows, scene has %d instances",
                     c->neurf_ninst, sc->num_instances);
+    // capacity mode: every size below comes from the reservation and the device
+    // plans the batch (k_plan.cu); the modes that need the per-view layout on
+    // the host (dumps, training, NeurF, the conventional world copies) keep the
+    // synchronous sizing
+    const bool capm = c->cap_on && !c->cap_suspend && !c->debug && !c->training && !neurf && !conv;
+    c->last_capm = capm;
 
     // ---- distinct times (views sharing t share K1's compaction); the
     // conventional pipeline has no temporal filter: one identity list
@@ -311,6 +408,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
 
     c->hv.assign(nv, DevView{});
     long long total_px = 0;
+    int total_bins = 0, total_tiles = 0, max_bins = 0, max_tiles = 0;
     for (int v = 0; v < nv; ++v) {
         const s3r_view& V = views[v];
         DevView& d = c->hv[v];
@@ -334,6 +432,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         d.STX = (d.TX + (1 << d.sshift) - 1) >> d.sshift;
         d.STY = (d.TY + (1 << d.sshift) - 1) >> d.sshift;
         d.nbins = d.STX * d.STY;
+        d.range_off = total_bins;             // supertile ranges / tile ranges: image sizes only
+        d.trange_off = total_tiles;
+        total_bins += d.nbins;
+        total_tiles += d.ntiles;
+        max_bins = std::max(max_bins, d.nbins);
+        max_tiles = std::max(max_tiles, d.ntiles);
         d.rgb = outs[v].rgb; d.depth = outs[v].depth; d.finalT = outs[v].final_T;
         d.visible = outs[v].visible;
         d.pix_off = total_px;
@@ -347,8 +451,13 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     // staging layout for this batch
     const size_t stage_bytes = 8192 + (size_t)T * 16 + (size_t)nv * (3 * sizeof(DevView) + 256) +
                                (size_t)(nv + 1) * 64;
-    if ((rc = stage_reserve(c, stage_bytes))) return rc;
-    c->h_stage_top = 0;
+    if ((rc = stage_begin(c, stage_bytes + (capm ? (size_t)nv * (sizeof(ViewCounters) + 8) + 512 : 0),
+                          st)))
+        return rc;
+    if (c->capture_now && !capm)
+        return fail(c, S3R_ESTATE, "graph capture of a render needs the capacity mode "
+                                   "(s3r_set_capacity) and no debug / training / NeurF / "
+                                   "conventional pipeline");
     // one zeroed work counter per launch that takes tickets: the filter chunks
     // and the depth-sort passes
     const int n_tickets = (T + MAX_TSLOTS - 1) / MAX_TSLOTS +
@@ -391,20 +500,27 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         }
         ev_end(c, st, e);
         CU(cudaGetLastError());
-        if (T) launch_readback(mapped(c, h_counts), c->d_counts.p, T * sizeof(unsigned long long), st);
-        CU(cudaStreamSynchronize(st));
+        if (!capm) {
+            if (T) launch_readback(mapped(c, h_counts), c->d_counts.p, T * sizeof(unsigned long long), st);
+            CU(cudaStreamSynchronize(st));
+        }
     }
 
     // ================= K2: projection + LOD + life + compaction
     long long cap = 0;
-    int k2_tiles = 0;          // grid.x of K2 (grid.y = views)
-    for (int v = 0; v < nv; ++v) {
-        DevView& d = c->hv[v];
-        d.n_temporal = (long long)h_counts[d.tslot];
-        d.cap_off = cap;
-        d.dbg_off = cap;
-        cap += d.n_temporal;
-        k2_tiles = std::max(k2_tiles, (int)((d.n_temporal + project_tile() - 1) / project_tile()));
+    int k2_tiles = 0;          // grid.x of K2 (grid.y = views; K2 strides over any count)
+    if (capm) {
+        cap = c->cap.records;
+        k2_tiles = (int)std::max<long long>(1, (c->cap.temporal_view + project_tile() - 1) / project_tile());
+    } else {
+        for (int v = 0; v < nv; ++v) {
+            DevView& d = c->hv[v];
+            d.n_temporal = (long long)h_counts[d.tslot];
+            d.cap_off = cap;
+            d.dbg_off = cap;
+            cap += d.n_temporal;
+            k2_tiles = std::max(k2_tiles, (int)((d.n_temporal + project_tile() - 1) / project_tile()));
+        }
     }
     const long long capS = std::max<long long>(cap, 1);
     if ((rc = ensure(c, c->d_rec, (size_t)capS * 48))) return rc;
@@ -431,6 +547,13 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     }
     for (int v = 0; v < nv; ++v)
         if (outs[v].visible && N > 0) CU(cudaMemsetAsync(outs[v].visible, 0, (size_t)N, st));
+    if (capm) {
+        // record segments on the device from K1's counts
+        c->cap_h_ntemp = (long long*)stage_alloc(c, (size_t)std::max(nv, 1) * 8);
+        launch_plan_records(P<DevView>(c->d_views), nv, P<unsigned long long>(c->d_counts),
+                            c->cap.records, (long long*)mapped(c, c->cap_h_ntemp),
+                            P<uint32_t>(c->d_err), st);
+    }
     if (conv && N > 0 && nv > 0) {
         // ---- C0: local-to-world transformation of every view's Gaussians
         if ((rc = ensure(c, c->d_wmo, (size_t)nv * N * 16))) return rc;
@@ -477,75 +600,103 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     }
     CU(cudaGetLastError());
     ViewCounters* h_ctr = (ViewCounters*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(ViewCounters));
-    if (nv) launch_readback(mapped(c, h_ctr), c->d_ctr.p, nv * sizeof(ViewCounters), st);
-    CU(cudaStreamSynchronize(st));
-
     // ================= sizes of the sort / emit / raster phase
     c->stats.assign(nv, s3r_stats{});
     std::vector<int> dt0(nv + 1, 0);
     long long total_pairs = 0, total_cnt = 0, max_r = 0;
-    int total_bins = 0, max_chunks = 0, max_bins = 0, total_tiles = 0;
+    int max_chunks = 0;
     long long total_tlist = 0;
-    int max_tiles = 0;
     bool bad = false;
     const int stile = onesweep64_tile();
-    for (int v = 0; v < nv; ++v) {
-        DevView& d = c->hv[v];
-        const ViewCounters& k = h_ctr[v];
-        d.n_rendered = (long long)k.n_rendered;
-        d.n_pairs = (long long)k.n_pairs;
-        if (d.n_pairs >= (1ll << 31))
-            return fail(c, S3R_EINVAL, "view %d: %lld tile pairs exceed 2^31", v, d.n_pairs);
-        d.nchunks = (int)((d.n_rendered + bin_chunk() - 1) / bin_chunk());
-        d.range_off = total_bins;
-        d.cnt_off = total_cnt;
-        d.pair_off = total_pairs;
-        d.tlist_off = total_tlist;
-        d.trange_off = total_tiles;
-        const long long SS = 1ll << (2 * d.sshift);
-        if (SS * (long long)k.n_spairs >= (1ll << 31))
-            return fail(c, S3R_EINVAL, "view %d: tile-list area exceeds 2^31 entries", v);
-        total_tlist += SS * (long long)k.n_spairs;
-        total_tiles += d.ntiles;
-        total_bins += d.nbins;
-        total_cnt += (long long)d.nbins * d.nchunks;
-        total_pairs += (long long)k.n_spairs;
-        max_chunks = std::max(max_chunks, d.nchunks);
-        max_bins = std::max(max_bins, d.nbins);
-        max_r = std::max(max_r, d.n_rendered);
-        dt0[v + 1] = dt0[v] + (int)((d.n_rendered + stile - 1) / stile);
-        max_tiles = std::max(max_tiles, d.ntiles);
-        s3r_stats& s = c->stats[v];
-        s.n_scene = N;
-        s.n_temporal = d.n_temporal;
-        s.n_visible = (long long)k.n_visible;
-        s.n_lod_small = (long long)k.n_small;
-        s.n_lod_dropped = (long long)k.n_dropped;
-        s.n_rendered = d.n_rendered;
-        s.n_pairs = d.n_pairs;
-        s.n_bin_pairs = (long long)k.n_spairs;
-        s.n_bad_instance = (long long)k.n_bad;
-        if (k.n_bad) bad = true;
-    }
-    const int dtiles = dt0[nv];
-
-    // device-side metadata for the rest of the batch
-    Seg* h_dsegs = (Seg*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(Seg));
-    int* h_dt0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
-    DevView* h_views2 = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
-    for (int v = 0; v < nv; ++v) {
-        const DevView& d = c->hv[v];
-        h_dsegs[v] = Seg{d.cap_off, d.n_rendered, dt0[v], dt0[v + 1] - dt0[v]};
-    }
-    std::memcpy(h_dt0, dt0.data(), (nv + 1) * sizeof(int));
-    std::memcpy(h_views2, c->hv.data(), (size_t)nv * sizeof(DevView));
-
+    int dtiles = 0;
     if ((rc = ensure(c, c->d_dsegs, (size_t)std::max(nv, 1) * sizeof(Seg)))) return rc;
     if ((rc = ensure(c, c->d_dtile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
-    if (nv) {
-        CU(cudaMemcpyAsync(c->d_dsegs.p, h_dsegs, nv * sizeof(Seg), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_dtile0.p, h_dt0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(c->d_views.p, h_views2, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
+    if (capm) {
+        // the device plans the rest (k_plan_bins); the host sizes every buffer and
+        // grid from the reservation
+        max_r = c->cap.rendered_view;
+        max_chunks = (int)((max_r + bin_chunk() - 1) / bin_chunk());
+        for (int v = 0; v < nv; ++v) total_cnt += (long long)c->hv[v].nbins * max_chunks;
+        total_pairs = c->cap.bin_pairs;
+        total_tlist = c->cap.tile_entries;
+        // sort tiles: sum over views of ceil(n_rendered / stile), bounded by both
+        // the records and the per-view rendered capacity
+        dtiles = (int)std::min<long long>((cap + stile - 1) / stile + nv,
+                                          (long long)nv * ((max_r + stile - 1) / stile));
+        PlanCaps pc;
+        pc.rendered_view = max_r;
+        pc.bin_pairs = total_pairs;
+        pc.tile_entries = total_tlist;
+        pc.counts = total_cnt;
+        pc.bin_chunk = bin_chunk();
+        pc.sort_tile = stile;
+        c->cap_h_ctr = h_ctr;
+        launch_plan_bins(P<DevView>(c->d_views), nv, P<ViewCounters>(c->d_ctr), P<Seg>(c->d_dsegs),
+                         P<int>(c->d_dtile0), pc, (ViewCounters*)mapped(c, h_ctr),
+                         P<uint32_t>(c->d_err), st);
+        c->cap_pending = true;
+    } else {
+        if (nv) launch_readback(mapped(c, h_ctr), c->d_ctr.p, nv * sizeof(ViewCounters), st);
+        CU(cudaStreamSynchronize(st));
+        for (int v = 0; v < nv; ++v) {
+            DevView& d = c->hv[v];
+            const ViewCounters& k = h_ctr[v];
+            d.n_rendered = (long long)k.n_rendered;
+            d.n_pairs = (long long)k.n_pairs;
+            if (d.n_pairs >= (1ll << 31))
+                return fail(c, S3R_EINVAL, "view %d: %lld tile pairs exceed 2^31", v, d.n_pairs);
+            d.nchunks = (int)((d.n_rendered + bin_chunk() - 1) / bin_chunk());
+            d.cnt_off = total_cnt;
+            d.pair_off = total_pairs;
+            d.tlist_off = total_tlist;
+            const long long SS = 1ll << (2 * d.sshift);
+            if (SS * (long long)k.n_spairs >= (1ll << 31))
+                return fail(c, S3R_EINVAL, "view %d: tile-list area exceeds 2^31 entries", v);
+            total_tlist += SS * (long long)k.n_spairs;
+            total_cnt += (long long)d.nbins * d.nchunks;
+            total_pairs += (long long)k.n_spairs;
+            max_chunks = std::max(max_chunks, d.nchunks);
+            max_r = std::max(max_r, d.n_rendered);
+            dt0[v + 1] = dt0[v] + (int)((d.n_rendered + stile - 1) / stile);
+            s3r_stats& s = c->stats[v];
+            s.n_scene = N;
+            s.n_temporal = d.n_temporal;
+            s.n_visible = (long long)k.n_visible;
+            s.n_lod_small = (long long)k.n_small;
+            s.n_lod_dropped = (long long)k.n_dropped;
+            s.n_rendered = d.n_rendered;
+            s.n_pairs = d.n_pairs;
+            s.n_bin_pairs = (long long)k.n_spairs;
+            s.n_bad_instance = (long long)k.n_bad;
+            if (k.n_bad) bad = true;
+        }
+        dtiles = dt0[nv];
+        // device-side metadata for the rest of the batch
+        Seg* h_dsegs = (Seg*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(Seg));
+        int* h_dt0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
+        DevView* h_views2 = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
+        for (int v = 0; v < nv; ++v) {
+            const DevView& d = c->hv[v];
+            h_dsegs[v] = Seg{d.cap_off, d.n_rendered, dt0[v], dt0[v + 1] - dt0[v]};
+        }
+        std::memcpy(h_dt0, dt0.data(), (nv + 1) * sizeof(int));
+        std::memcpy(h_views2, c->hv.data(), (size_t)nv * sizeof(DevView));
+        if (nv) {
+            CU(cudaMemcpyAsync(c->d_dsegs.p, h_dsegs, nv * sizeof(Seg), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(c->d_dtile0.p, h_dt0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(c->d_views.p, h_views2, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
+        }
+        // what this batch needed (s3r_capacity_from_last)
+        s3r_capacity need{};
+        need.records = cap;
+        need.bin_pairs = total_pairs;
+        need.tile_entries = total_tlist;
+        for (int v = 0; v < nv; ++v) {
+            need.rendered_view = std::max<long long>(need.rendered_view, c->hv[v].n_rendered);
+            need.temporal_view = std::max<long long>(need.temporal_view, c->hv[v].n_temporal);
+        }
+        c->last_need = need;
+        c->last_need_valid = true;
     }
     for (int i = 0; i < 2; ++i) {
         if ((rc = ensure(c, c->d_sortk[i], (size_t)capS * 8))) return rc;
@@ -663,9 +814,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     c->last_max_tiles = max_tiles;
     c->last_max_r = max_r;
     c->last_N = N;
-    if (c->timing) c->timed_renders++;
-    CU(cudaEventRecord(c->staging_free, st));
-    c->staging_recorded = true;
+    if (c->timing && !c->capture_now) c->timed_renders++;
+    if ((rc = stage_end(c, st))) return rc;
     c->have_render = true;
     if (c->ticket_overflow) return fail(c, S3R_EINTERNAL, "work-counter slots exhausted");
     if (bad) return fail(c, S3R_EINSTANCE, "a Gaussian had an instance id outside [0, %d]",
@@ -694,8 +844,7 @@ int s3r_create(int device, s3r_ctx** out)
     if (!c) return S3R_ENOMEM;
     c->device = device;
     if (const char* e = std::getenv("S3R_OVERLAP")) c->overlap = e[0] && e[0] != '0';
-    if (cudaSetDevice(device) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming) != cudaSuccess) {
+    if (cudaSetDevice(device) != cudaSuccess) {
         cudaGetLastError();
         delete c;
         return S3R_ECUDA;
@@ -736,8 +885,12 @@ void s3r_destroy(s3r_ctx* c)
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
     }
-    if (c->h_stage) cudaFreeHost(c->h_stage);
-    if (c->staging_free) cudaEventDestroy(c->staging_free);
+    for (auto& S : c->ring) {
+        if (S.h) cudaFreeHost(S.h);
+        if (S.ev) cudaEventDestroy(S.ev);
+    }
+    for (char* h : c->graph_blocks) cudaFreeHost(h);
+    if (c->graph_spare) cudaFreeHost(c->graph_spare);
     for (cudaEvent_t e : c->chunk_done) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
@@ -880,6 +1033,13 @@ int s3r_render_batch_host(s3r_ctx* c, const s3r_scene* hs, const s3r_view* hview
     CU(cudaSetDevice(c->device));
     const long long N = hs->n;
     if (N < 0 || N >= (1ll << 30)) return fail(c, S3R_EINVAL, "n out of range");
+    // this entry point synchronises anyway and collects per-chunk stats on the
+    // host: it keeps the synchronous sizing
+    struct Suspend {
+        s3r_ctx* c;
+        ~Suspend() { c->cap_suspend = false; }
+    } suspend_{c};
+    c->cap_suspend = true;
     int rc;
     const size_t sz[7] = {16, 16, 16, 16, 4, 8, 8};
     const void* src[7] = {hs->means_opacity, hs->scales, hs->rotations, hs->colors,
@@ -994,6 +1154,26 @@ int s3r_get_stats(const s3r_ctx* c, int32_t view_index, s3r_stats* out)
     if (!c->have_render || view_index < 0 || view_index >= (int)c->stats.size())
         return S3R_ESTATE;
     s3r_ctx* m = const_cast<s3r_ctx*>(c);
+    if (m->cap_pending) {
+        // capacity mode: the planner wrote the counts into mapped staging memory
+        cudaSetDevice(m->device);
+        if (cudaDeviceSynchronize() != cudaSuccess)
+            return fail(m, S3R_ECUDA, "get_stats: %s", cudaGetErrorString(cudaGetLastError()));
+        for (size_t v = 0; v < m->stats.size(); ++v) {
+            const ViewCounters& k = m->cap_h_ctr[v];
+            s3r_stats& s = m->stats[v];
+            s.n_scene = m->N_last;
+            s.n_temporal = m->cap_h_ntemp[v];
+            s.n_visible = (long long)k.n_visible;
+            s.n_lod_small = (long long)k.n_small;
+            s.n_lod_dropped = (long long)k.n_dropped;
+            s.n_rendered = (long long)k.n_rendered;
+            s.n_pairs = (long long)k.n_pairs;
+            s.n_bin_pairs = (long long)k.n_spairs;
+            s.n_bad_instance = (long long)k.n_bad;
+        }
+        m->cap_pending = false;
+    }
     if (m->last_counters && !m->evals_fetched) {
         // E_alg / E_exec are produced by the rasterizer: fetch them once
         const size_t nv = m->stats.size();
@@ -1019,6 +1199,9 @@ int s3r_dump_intermediates(s3r_ctx* c, int32_t vi, const s3r_debug* dbg, void* s
     if (c->host_chunked)
         return fail(c, S3R_ESTATE, "dump: the last render was a chunked s3r_render_batch_host "
                                    "batch (enable debug mode to dump it)");
+    if (c->last_capm)
+        return fail(c, S3R_ESTATE, "dump: the last render was planned on the device (capacity "
+                                   "mode); enable debug mode to dump it");
     cudaStream_t st = (cudaStream_t)stream;
     CU(cudaSetDevice(c->device));
     const DevView& d = c->hv[vi];
@@ -1198,9 +1381,7 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
     if ((rc = ensure(c, c->d_sgrads, sg_bytes))) return rc;
     CU(cudaMemsetAsync(c->d_sgrads.p, 0, sg_bytes, st));
     if ((rc = ensure(c, c->d_cots, (size_t)std::max(nv, 1) * sizeof(s3r_cot)))) return rc;
-    if ((rc = stage_reserve(c, (size_t)std::max(nv, 1) * sizeof(s3r_cot) + 512))) return rc;
-    if (c->staging_recorded) CU(cudaEventSynchronize(c->staging_free));
-    c->h_stage_top = 0;
+    if ((rc = stage_begin(c, (size_t)std::max(nv, 1) * sizeof(s3r_cot) + 512, st))) return rc;
     s3r_cot* h = (s3r_cot*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(s3r_cot));
     for (int v = 0; v < nv; ++v) h[v] = s3r_cot{cots[v].rgb, cots[v].depth, cots[v].final_T};
     if (nv) CU(cudaMemcpyAsync(c->d_cots.p, h, nv * sizeof(s3r_cot), cudaMemcpyHostToDevice, st));
@@ -1235,7 +1416,7 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
         if (cots[v].final_T) a.has_T_cot = 1;
     }
     launch_backward(a, c->last_max_tiles, c->last_max_r, st);
-    CU(cudaEventRecord(c->staging_free, st));
+    if ((rc = stage_end(c, st))) return rc;
     CU(cudaGetLastError());
     return S3R_OK;
 }
@@ -1263,6 +1444,57 @@ int s3r_life_flip(s3r_ctx* c, float* life, int64_t n, void* stream)
     return S3R_OK;
 }
 
+int s3r_set_capacity(s3r_ctx* c, const s3r_capacity* cap)
+{
+    if (!c) return S3R_EINVAL;
+    if (!cap) {
+        c->cap_on = false;
+        return S3R_OK;
+    }
+    if (cap->records < 1 || cap->rendered_view < 1 || cap->bin_pairs < 1 ||
+        cap->tile_entries < 1 || cap->temporal_view < 1)
+        return fail(c, S3R_EINVAL, "set_capacity: every capacity must be >= 1");
+    if (cap->records >= (1ll << 32) || cap->rendered_view >= (1ll << 31) ||
+        cap->bin_pairs >= (1ll << 32) || cap->tile_entries >= (1ll << 32))
+        return fail(c, S3R_EINVAL, "set_capacity: capacities must fit 32-bit list positions");
+    c->cap = *cap;
+    c->cap_on = true;
+    return S3R_OK;
+}
+
+int s3r_capacity_from_last(s3r_ctx* c, float margin, s3r_capacity* out)
+{
+    if (!c || !out || !(margin >= 1.0f) || !std::isfinite(margin)) return S3R_EINVAL;
+    if (!c->have_render) return fail(c, S3R_ESTATE, "capacity_from_last: no render yet");
+    if (c->last_capm) {
+        // planned on the device: the needs are the counters of that batch
+        s3r_stats tmp;
+        if (int r = s3r_get_stats(c, 0, &tmp)) return r;
+        s3r_capacity need{};
+        for (size_t v = 0; v < c->stats.size(); ++v) {
+            const s3r_stats& s = c->stats[v];
+            const long long SS = 1ll << (2 * c->hv[v].sshift);
+            need.records += s.n_temporal;
+            need.bin_pairs += s.n_bin_pairs;
+            need.tile_entries += SS * s.n_bin_pairs;
+            need.rendered_view = std::max<long long>(need.rendered_view, s.n_rendered);
+            need.temporal_view = std::max<long long>(need.temporal_view, s.n_temporal);
+        }
+        c->last_need = need;
+        c->last_need_valid = true;
+    }
+    if (!c->last_need_valid) return fail(c, S3R_ESTATE, "capacity_from_last: no sized render");
+    auto sc = [&](long long x) {
+        return std::max<long long>(1, (long long)std::ceil((double)x * (double)margin));
+    };
+    out->records = sc(c->last_need.records);
+    out->rendered_view = sc(c->last_need.rendered_view);
+    out->bin_pairs = sc(c->last_need.bin_pairs);
+    out->tile_entries = sc(c->last_need.tile_entries);
+    out->temporal_view = sc(c->last_need.temporal_view);
+    return S3R_OK;
+}
+
 int s3r_check(s3r_ctx* c, void* stream)
 {
     if (!c) return S3R_EINVAL;
@@ -1280,6 +1512,9 @@ int s3r_check(s3r_ctx* c, void* stream)
     }
     if (e & ERR_PRECULL)
         return fail(c, S3R_EINTERNAL, "K2 frustum pre-test culled a visible Gaussian");
+    if (e & ERR_CAPACITY)
+        return fail(c, S3R_ECAPACITY, "capacity mode: a view exceeded the reserved scratch and was "
+                                      "rendered empty (s3r_capacity_from_last / s3r_set_capacity)");
     if (e & ERR_BADID) return fail(c, S3R_EINSTANCE, "a Gaussian had an out-of-range instance id");
     return S3R_OK;
 }

@@ -102,6 +102,7 @@ constexpr uint8_t F_TEMPORAL = 1, F_VISIBLE = 2, F_SMALL = 4, F_DROPPED = 8,
 // Device error bits
 constexpr uint32_t ERR_BADID = 1;
 constexpr uint32_t ERR_PRECULL = 2;   // K2 pre-test culled a visible Gaussian (debug self-check)
+constexpr uint32_t ERR_CAPACITY = 4;  // capacity mode: a view did not fit the reserved scratch
 
 // Per-view descriptor in device memory (one per view of a batch).
 struct DevView {
@@ -147,7 +148,25 @@ struct Seg {
     int ntiles;              // tiles of the segment
 };
 
+// Capacity-mode limits for the device-side planner (k_plan.cu)
+struct PlanCaps {
+    long long rendered_view;   // splats rendered per view (count / scatter / permute grids)
+    long long bin_pairs;       // supertile pairs over the batch (list buffer)
+    long long tile_entries;    // tile-list area over the batch (S*S x supertile pairs)
+    long long counts;          // (bin, chunk) counters over the batch
+    long long bin_chunk;       // k_bin.cu KCHUNK
+    long long sort_tile;       // onesweep keys per CTA
+};
+
 // ---------------- launchers (each enqueues on `st`) ----------------------
+
+// capacity mode: device-side sizing after K1 (record segments) and after K2
+// (sort segments, binning layout); see k_plan.cu
+void launch_plan_records(DevView* views, int nv, const unsigned long long* counts,
+                         long long cap_records, long long* h_ntemp, uint32_t* err,
+                         cudaStream_t st);
+void launch_plan_bins(DevView* views, int nv, const ViewCounters* ctr, Seg* segs, int* dt0,
+                      const PlanCaps& caps, ViewCounters* h_ctr, uint32_t* err, cudaStream_t st);
 
 // K1: temporal filter + ordered compaction for up to MAX_TSLOTS distinct times.
 void launch_filter(const float2* vis, long long n, const float* d_times, int T,

@@ -22,8 +22,8 @@ _SO = os.environ.get("S3R_LIB") or os.path.join(_HERE, "libs3r.so")   # S3R_LIB:
 _lock = threading.Lock()
 _lib = None
 
-S3R_OK, S3R_EINVAL, S3R_EINSTANCE, S3R_ENOMEM, S3R_ECUDA, S3R_ESTATE, S3R_EINTERNAL = \
-    0, -1, -2, -3, -4, -5, -6
+S3R_OK, S3R_EINVAL, S3R_EINSTANCE, S3R_ENOMEM, S3R_ECUDA, S3R_ESTATE, S3R_EINTERNAL, \
+    S3R_ECAPACITY = 0, -1, -2, -3, -4, -5, -6, -7
 STAGES = ["filter", "project", "depth_sort", "bin", "raster", "color"]
 TILE = 16
 # every symbol include/s3r.h declares
@@ -33,7 +33,7 @@ EXPORTS = ["s3r_version", "s3r_create", "s3r_destroy", "s3r_last_error", "s3r_se
            "s3r_dump_intermediates", "s3r_commit_visibility", "s3r_reset_visibility",
            "s3r_life_flip", "s3r_check", "s3r_set_training", "s3r_render_backward",
            "s3r_mse", "s3r_set_pipeline", "s3r_set_lod_jitter", "s3r_set_neural_colors",
-           "s3r_set_overlap", "s3r_set_fast_exp"]
+           "s3r_set_overlap", "s3r_set_fast_exp", "s3r_set_capacity", "s3r_capacity_from_last"]
 S3R_PIPELINE_STREAMLINED, S3R_PIPELINE_CONVENTIONAL = 0, 1
 
 
@@ -68,6 +68,11 @@ class Stats_(C.Structure):
                                          "n_lod_dropped", "n_rendered", "n_pairs",
                                          "n_bad_instance", "n_bin_pairs", "n_blend_evals",
                                          "n_blend_exec")]
+
+
+class Capacity_(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("records", "rendered_view", "bin_pairs", "tile_entries",
+                                         "temporal_view")]
 
 
 class Cot_(C.Structure):
@@ -133,6 +138,8 @@ def lib():
                 "s3r_render_backward": (I, [P, P, P, C.c_int32, P, P, P]),
                 "s3r_mse": (I, [P, P, P, I64, C.c_float, P, P, P]),
                 "s3r_check": (I, [P, P]),
+                "s3r_set_capacity": (I, [P, P]),
+                "s3r_capacity_from_last": (I, [P, C.c_float, P]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -380,6 +387,23 @@ class Context:
         """Overlapped batch halves (s3r_set_overlap); off by default."""
         self._check(self.L.s3r_set_overlap(self.h, int(on)))
 
+    def set_capacity(self, cap: Optional[Dict[str, int]]):
+        """Capacity mode (s3r_set_capacity): batches are sized on the device from
+        these reservations (keys of Capacity_), without host synchronisation, so
+        a render_batch can be captured in a CUDA graph; None switches it off.
+        Overflows render the view empty and surface in check() (S3R_ECAPACITY)."""
+        if cap is None:
+            self._check(self.L.s3r_set_capacity(self.h, None))
+            return
+        c = Capacity_(*[int(cap[k]) for k, _ in Capacity_._fields_])
+        self._check(self.L.s3r_set_capacity(self.h, C.byref(c)))
+
+    def capacity_from_last(self, margin: float = 1.25) -> Dict[str, int]:
+        """What the last batch needed, times `margin` (s3r_capacity_from_last)."""
+        c = Capacity_()
+        self._check(self.L.s3r_capacity_from_last(self.h, float(margin), C.byref(c)))
+        return {k: getattr(c, k) for k, _ in Capacity_._fields_}
+
     def set_fast_exp(self, on: bool):
         """SFU ex2.approx in the rasterizer (s3r_set_fast_exp); off by default.
         Images within 1e-4 of the oracle instead of bit-identical."""
@@ -459,7 +483,8 @@ class Context:
                                          _stream(stream)))
 
     def check(self, stream=None) -> int:
-        return self._check(self.L.s3r_check(self.h, _stream(stream)), allow=(S3R_OK, S3R_EINSTANCE))
+        return self._check(self.L.s3r_check(self.h, _stream(stream)),
+                           allow=(S3R_OK, S3R_EINSTANCE, S3R_ECAPACITY))
 
 
 def alloc_outputs(views: Sequence, device="cuda", depth=True, final_T=True, n_visible: int = 0

@@ -44,12 +44,14 @@ def test_sm100a_code_present(lib):
 
 
 def test_version_and_null_handling(lib):
-    assert lib.s3r_version() == 10000
+    assert lib.s3r_version() == 10100
     assert lib.s3r_create(0, None) == s3r.S3R_EINVAL
     assert lib.s3r_render_batch(None, None, None, 0, None, None) == s3r.S3R_EINVAL
     assert lib.s3r_last_error(None) == b"null context"
     assert lib.s3r_set_debug(None, 1) == s3r.S3R_EINVAL
     assert lib.s3r_check(None, None) == s3r.S3R_EINVAL
+    assert lib.s3r_set_capacity(None, None) == s3r.S3R_EINVAL
+    assert lib.s3r_capacity_from_last(None, 1.0, None) == s3r.S3R_EINVAL
 
 
 def test_product_path_does_not_import_oracle():

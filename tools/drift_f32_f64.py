@@ -8,8 +8,8 @@ depth / final T, the number of pixels over 1e-4, the pixels whose termination
 status (final T < 1e-4) differs, and the Gaussians whose integer decisions
 (visible / small / dropped / rendered) differ; and, key-fed (the fp64 blend
 of the fp32 contract's own keys), the same image deltas, which isolate the blend
-arithmetic from the fp32 projection.  CPU only (oracle), one worker
-process per view.
+arithmetic from the fp32 projection (--keyfed; a brute-force gather, for small
+views only).  CPU only (oracle), one worker process per view.
 
     python tools/drift_f32_f64.py [--views 2] [--out profiles/r02_f32_vs_f64_drift.json]
 """
@@ -68,6 +68,9 @@ def _one(job):
     ka, kb = a["keys"][m].astype(np.float64), b["keys"][m]
     scale = np.maximum(np.abs(kb), np.abs(kb[:, 3:4]) + np.abs(kb[:, 5:6]))
     r["keys_max_rel"] = float((np.abs(ka - kb) / np.maximum(scale, 1.0)).max()) if m.any() else 0.0
+    if not _G.get("keyfed"):
+        r["oracle_s_total"] = round(time.perf_counter() - t0, 1)
+        return r
     # key-fed: the fp64 blend (Eq.2 as written) of the fp32 contract's own keys,
     # decisions and rectangles; isolates the blend arithmetic (exp2 polynomial,
     # 2^-24 flush, T - w) from the fp32 projection of world coordinates
@@ -91,9 +94,13 @@ def main():
     ap.add_argument("--views", type=int, default=2)
     ap.add_argument("--configs", default="av2,drive")
     ap.add_argument("--workers", type=int, default=min(8, os.cpu_count() or 1))
+    ap.add_argument("--keyfed", action="store_true",
+                    help="also the brute-force fp64 blend of the fp32 keys (O(pixels x N): "
+                         "small views only)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_f32_vs_f64_drift.json"))
     a = ap.parse_args()
     from paper_2503_08217_b200 import scenegen as sg
+    _G["keyfed"] = a.keyfed
     jobs = []
     for cfg in a.configs.split(","):
         scene, views = sg.make_config(cfg)
