@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libs3r.so")
 BUILD = os.path.join(HERE, "build")
-SOURCES = ["k_filter.cu", "k_project.cu", "k_sort.cu", "k_bin.cu", "k_raster.cu", "k_plan.cu",
+SOURCES = ["k_filter.cu", "k_project.cu", "k_sort.cu", "k_bin.cu", "k_raster.cu", "k_plan.cu", "k_small.cu",
            "k_backward.cu", "k_neurf.cu", "s3r_api.cu"]
 HEADERS = ["s3r_internal.cuh", os.path.join("..", "..", "include", "s3r.h")]
 # The backward (config 5) is compared with the oracle at 1e-3, not bit for bit:

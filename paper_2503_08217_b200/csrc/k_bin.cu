@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) k_permute(const DevView* __restrict__ vie
 {
     const DevView& V = views[blockIdx.y];
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= V.n_rendered) return;
+    if (V.small || r >= V.n_rendered) return;      // small views: k_small.cu
     const long long base = V.cap_off;
     const uint32_t j = order[base + r];
     const float4* src = rec + 3 * (base + j);
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(KT) k_bin_count(const DevView* __restrict__ vi
     const DevView& V = views[blockIdx.y];
     const int c = blockIdx.x;
     const long long r0 = (long long)c * KCHUNK;
-    if (r0 >= V.n_rendered || V.nbins == 0) return;
+    if (V.small || r0 >= V.n_rendered || V.nbins == 0) return;
     const int nb = V.nbins, sh = V.sshift, sx = V.STX;
     for (int b = threadIdx.x; b < nb; b += KT) s_cnt[b] = 0;
     __syncthreads();
@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_carry;
     const DevView& V = views[blockIdx.x];
+    if (V.small) return;
     const long long n = (long long)V.nbins * V.nchunks;
     uint32_t* a = cnt + V.cnt_off;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
     __shared__ uint2 s_rect[XT];
     const DevView& V = views[blockIdx.y];
     const int b = blockIdx.x;
-    if (b >= V.nbins) return;
+    if (V.small || b >= V.nbins) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = 1 << V.sshift, SS = S * S;
     const int bx = b % V.STX, by = b / V.STX;
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
     const DevView& V = views[blockIdx.y];
     const int c = blockIdx.x;
     const long long r0 = (long long)c * KCHUNK;
-    if (r0 >= V.n_rendered || V.nbins == 0) return;
+    if (V.small || r0 >= V.n_rendered || V.nbins == 0) return;
     const int nb = V.nbins, sh = V.sshift, sx = V.STX;
     uint32_t* s_base = s_dyn;                                    // [nb] chunk base per bin
     uint32_t* s_w = s_dyn + nb;                                  // [KWARPS][nb]

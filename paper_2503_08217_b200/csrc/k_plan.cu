@@ -115,9 +115,11 @@ __global__ void __launch_bounds__(PLT) k_plan_bins(DevView* __restrict__ views, 
         }
         const unsigned long long q_sp = (unsigned long long)ns;
         const unsigned long long q_tl = (unsigned long long)SS * (unsigned long long)ns;
-        const long long nch = (nr + caps.bin_chunk - 1) / caps.bin_chunk;
+        const bool sm = v < nv && small_view(nr, views[v].ntiles);
+        const long long nch = sm ? 0 : (nr + caps.bin_chunk - 1) / caps.bin_chunk;
         const unsigned long long q_cnt = (unsigned long long)nb * (unsigned long long)nch;
-        const unsigned long long q_dt = (unsigned long long)((nr + caps.sort_tile - 1) / caps.sort_tile);
+        const unsigned long long q_dt =
+            sm ? 0ull : (unsigned long long)((nr + caps.sort_tile - 1) / caps.sort_tile);
         const unsigned long long i_sp = block_incl_scan(q_sp, s_w);
         const unsigned long long i_tl = block_incl_scan(q_tl, s_w);
         const unsigned long long i_cnt = block_incl_scan(q_cnt, s_w);
@@ -138,11 +140,14 @@ __global__ void __launch_bounds__(PLT) k_plan_bins(DevView* __restrict__ views, 
             }
             V.n_rendered = nr;
             V.n_pairs = fits ? (long long)k.n_pairs : 0;
-            V.nchunks = (int)((nr + caps.bin_chunk - 1) / caps.bin_chunk);
+            // (a dropped view renders nothing: small if its tiles fit, so that
+            // its empty tile ranges are written when the big path is not run)
+            V.small = (fits ? sm : small_view(0, V.ntiles)) ? 1 : 0;
+            V.nchunks = V.small ? 0 : (int)((nr + caps.bin_chunk - 1) / caps.bin_chunk);
             V.cnt_off = (long long)o_cnt;
             V.pair_off = (long long)o_sp;
             V.tlist_off = (long long)o_tl;
-            segs[v] = Seg{V.cap_off, nr, (int)o_dt, (int)q_dt2};
+            segs[v] = Seg{V.cap_off, V.small ? 0 : nr, (int)o_dt, (int)q_dt2};
             dt0[v] = (int)o_dt;
         }
         __syncthreads();

@@ -609,6 +609,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     bool bad = false;
     const int stile = onesweep64_tile();
     int dtiles = 0;
+    bool any_small = false, all_small = true;   // views for k_small.cu / for the big path
     if ((rc = ensure(c, c->d_dsegs, (size_t)std::max(nv, 1) * sizeof(Seg)))) return rc;
     if ((rc = ensure(c, c->d_dtile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
     if (capm) {
@@ -623,6 +624,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         // the records and the per-view rendered capacity
         dtiles = (int)std::min<long long>((cap + stile - 1) / stile + nv,
                                           (long long)nv * ((max_r + stile - 1) / stile));
+        // which views the device will mark small is not known here: launch the
+        // one-CTA path whenever a view may be small, the big path unless all are
+        any_small = false;
+        for (int v = 0; v < nv; ++v) any_small = any_small || small_view(0, c->hv[v].ntiles);
+        all_small = small_view(max_r, max_tiles);
+        if (all_small) dtiles = 0;
         PlanCaps pc;
         pc.rendered_view = max_r;
         pc.bin_pairs = total_pairs;
@@ -645,7 +652,10 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
             d.n_pairs = (long long)k.n_pairs;
             if (d.n_pairs >= (1ll << 31))
                 return fail(c, S3R_EINVAL, "view %d: %lld tile pairs exceed 2^31", v, d.n_pairs);
-            d.nchunks = (int)((d.n_rendered + bin_chunk() - 1) / bin_chunk());
+            d.small = small_view(d.n_rendered, d.ntiles) ? 1 : 0;
+            any_small = any_small || d.small;
+            all_small = all_small && d.small;
+            d.nchunks = d.small ? 0 : (int)((d.n_rendered + bin_chunk() - 1) / bin_chunk());
             d.cnt_off = total_cnt;
             d.pair_off = total_pairs;
             d.tlist_off = total_tlist;
@@ -657,7 +667,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
             total_pairs += (long long)k.n_spairs;
             max_chunks = std::max(max_chunks, d.nchunks);
             max_r = std::max(max_r, d.n_rendered);
-            dt0[v + 1] = dt0[v] + (int)((d.n_rendered + stile - 1) / stile);
+            dt0[v + 1] = dt0[v] + (d.small ? 0 : (int)((d.n_rendered + stile - 1) / stile));
             s3r_stats& s = c->stats[v];
             s.n_scene = N;
             s.n_temporal = d.n_temporal;
@@ -677,7 +687,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         DevView* h_views2 = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
         for (int v = 0; v < nv; ++v) {
             const DevView& d = c->hv[v];
-            h_dsegs[v] = Seg{d.cap_off, d.n_rendered, dt0[v], dt0[v + 1] - dt0[v]};
+            h_dsegs[v] = Seg{d.cap_off, d.small ? 0 : d.n_rendered, dt0[v], dt0[v + 1] - dt0[v]};
         }
         std::memcpy(h_dt0, dt0.data(), (nv + 1) * sizeof(int));
         std::memcpy(h_views2, c->hv.data(), (size_t)nv * sizeof(DevView));
@@ -744,9 +754,22 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         CU(cudaGetLastError());
     }
 
+    const int dpasses_run = all_small ? 0 : dpasses;
+    c->final_order = (dpasses - 1) & 1;
+    // ================= a4 of the small views: one CTA each (k_small.cu)
+    if (any_small && nv) {
+        StageEvent e;
+        ev_begin(c, S3R_STAGE_DEPTH_SORT, st, e);
+        launch_small_sortbin(P<DevView>(c->d_views), nv, P<unsigned long long>(c->d_dkey),
+                             P<float4>(c->d_rec), P<unsigned long long>(c->d_sortk[c->final_order]),
+                             P<uint32_t>(c->d_sortv[c->final_order]), P<float4>(c->d_recs),
+                             P<uint2>(c->d_rects), P<uint32_t>(c->d_tlists),
+                             P<int2>(c->d_tranges), st);
+        ev_end(c, st, e);
+    }
     // ================= K5a: depth sort: 8-bit LSD passes over (depth << gbits | index),
     // values = compacted slot j; gives the unique (depth, index) order (R11)
-    {
+    if (!all_small) {
         StageEvent e;
         ev_begin(c, S3R_STAGE_DEPTH_SORT, st, e);
         CU(cudaMemsetAsync(c->d_hist.p, 0, (size_t)std::max(nv, 1) * dpasses * RADIX * 4, st));
@@ -755,7 +778,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         launch_hist_scan(P<uint32_t>(c->d_hist), nv, dpasses, st);
         const unsigned long long* kin = P<unsigned long long>(c->d_dkey);
         const uint32_t* vin = nullptr;
-        for (int pass = 0; pass < dpasses; ++pass) {
+        for (int pass = 0; pass < dpasses_run; ++pass) {
             const int o = pass & 1;
             if (dtiles) CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)dtiles * RADIX * 4, st));
             launch_onesweep64kv(kin, vin, P<unsigned long long>(c->d_sortk[o]),
@@ -765,13 +788,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
             kin = P<unsigned long long>(c->d_sortk[o]);
             vin = P<uint32_t>(c->d_sortv[o]);
         }
-        c->final_order = (dpasses - 1) & 1;
         ev_end(c, st, e);
     }
     CU(cudaGetLastError());
 
     // ================= K3/K4: depth-ordered permute + supertile counting sort
-    {
+    if (!all_small) {
         StageEvent e;
         ev_begin(c, S3R_STAGE_BIN, st, e);
         launch_permute(P<DevView>(c->d_views), nv, max_r, P<uint32_t>(c->d_sortv[c->final_order]),

@@ -133,7 +133,19 @@ struct DevView {
     long long tlist_off;     // offset of the view's tile-list area (S*S * supertile pairs)
     int trange_off;          // offset of the view's tile ranges (ntiles entries)
     long long pix_off;       // offset of the view's pixels in the training buffers
+    int small;               // a4 in one CTA (k_small.cu) instead of the sort + binning kernels
 };
+
+// Views small enough for the one-CTA depth order + tile binning (k_small.cu):
+// at most SMALL_MAX rendered splats, SMALL_TILES tiles, and SMALL_WORK
+// (splat, tile) containment tests.
+constexpr int SMALL_MAX = 2048;
+constexpr int SMALL_TILES = 1024;
+constexpr long long SMALL_WORK = 1ll << 18;
+__host__ __device__ inline bool small_view(long long n_rendered, int ntiles)
+{
+    return n_rendered <= SMALL_MAX && ntiles <= SMALL_TILES && n_rendered * ntiles <= SMALL_WORK;
+}
 
 // Per-view counters written by K2 (device, zeroed per batch)
 struct ViewCounters {
@@ -274,6 +286,11 @@ void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
                 const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
                 uint32_t* tlists, int2* tranges, cudaStream_t st);
 // Debug: the per-tile lists of view vi as (tile, Gaussian) pairs + [start,end) ranges.
+// a4 of the small views of a batch in one CTA each (k_small.cu)
+void launch_small_sortbin(const DevView* views, int n_views, const unsigned long long* dkey,
+                          const float4* rec, unsigned long long* keys_out, uint32_t* order_out,
+                          float4* rec_sorted, uint2* rect_sorted, uint32_t* tlists,
+                          int2* tranges, cudaStream_t st);
 void launch_dbg_tile_pairs(const DevView* views, int vi, int ntiles, const uint32_t* tlists,
                            const int2* tranges, const uint32_t* toff, const uint32_t* order,
                            const int32_t* gidx, int32_t* tile_out, int32_t* gauss_out,

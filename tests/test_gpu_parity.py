@@ -124,6 +124,41 @@ def test_c1_toy(ctx):
     assert o["stats"]["n_lod_dropped"] > 0
 
 
+def test_small_and_big_views_one_batch(ctx):
+    """One batch mixing views whose depth order + tile binning run in one CTA
+    (k_small.cu: <= 2048 splats, <= 1024 tiles) with views that take the sort
+    and binning kernels (640 x 480: 1200 tiles), against the oracle element by
+    element; and the same batch planned on the device (capacity mode) is
+    bit-identical."""
+    import dataclasses
+    scene, (v0,) = sg.make_toy(n=2000)
+    big = dataclasses.replace(v0, width=640, height=480, fx=640.0, fy=640.0, cx=320.0, cy=240.0,
+                              lod_seed=7)
+    tiny = dataclasses.replace(v0, width=33, height=17, cx=16.0, cy=8.0, lod_seed=9)
+    views = [v0, big, tiny, dataclasses.replace(v0, lod_seed=11)]
+    _, tabs, outs, rc = gpu_render(ctx, scene, views)
+    assert rc == 0
+    small = []
+    for vi, v in enumerate(views):
+        o = check_view(ctx, scene, v, tabs[vi], outs[vi], vi)
+        nt = ((v.width + 15) // 16) * ((v.height + 15) // 16)
+        n = o["stats"]["n_rendered"]
+        small.append(n <= 2048 and nt <= 1024 and n * nt <= (1 << 18))
+    assert small == [True, False, True, True]
+    c2 = s3r.Context(0)
+    try:
+        c2.set_capacity(ctx.capacity_from_last(1.0))
+        o2 = s3r.alloc_outputs(views, n_visible=scene.n)
+        c2.render_batch(s3r.DeviceScene.from_numpy(scene), views, list(tabs), o2)
+        torch.cuda.synchronize()
+        assert c2.check() == 0
+        for a, b in zip(outs, o2):
+            for k in ("rgb", "depth", "final_T", "visible"):
+                assert torch.equal(a[k], b[k]), k
+    finally:
+        c2.close()
+
+
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_random_dynamic_batch(ctx, seed):
     """Batched views of a scene with moving objects, random temporal intervals,
