@@ -269,8 +269,7 @@ int s3r_set_fast_exp(s3r_ctx* ctx, int enable);
  *   bin_pairs      supertile pairs over a batch (s3r_stats.n_bin_pairs summed)
  *   tile_entries   tile-list entries over a batch: sum of S*S x bin pairs
  *                  (S = 4, or 8 above 4096 supertiles of 4 x 4 tiles)
- *   temporal_view  largest n_temporal of a view (grid hint only; any count
- *                  is processed)
+ *   temporal_view  n_temporal of any one view (sizes the projection grid)
  * cap == NULL switches the mode off.  S3R_EINVAL for a NULL ctx or a
  * negative / zero capacity.                                                */
 typedef struct s3r_capacity {

@@ -61,6 +61,9 @@ namespace {
 #ifndef S3R_BWD_ULAST
 #define S3R_BWD_ULAST 0 // 1: no per-pixel "entry before the pixel's stop" test in a batch every pixel of the warp reaches
 #endif
+#ifndef S3R_BWD_SMEMCOT
+#define S3R_BWD_SMEMCOT 0 // 1: the per-pixel RGB cotangents and stops in shared memory (fewer registers)
+#endif
 #ifndef S3R_BWD_EX2
 #define S3R_BWD_EX2 0   // 0: exact R-ARITH exp2 on pairs (A/B 35.9 ms); 1, 2: ex2.approx + re-decision (37.0, 36.6)
 #endif
@@ -69,7 +72,10 @@ namespace {
 constexpr int RPIX = S3R_BWD_RPIX;
 constexpr int RT = TILE * TILE / RPIX;
 constexpr int BW = TILE / (RT / 32);
-constexpr int RB = 256;
+#ifndef S3R_BWD_RB
+#define S3R_BWD_RB 256
+#endif
+constexpr int RB = S3R_BWD_RB;   // records staged per batch
 constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 }  // namespace
 // per-splat accumulator stride in floats (16-byte rows for the vector REDs)
@@ -144,6 +150,12 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     __shared__ uint8_t s_cl[NW][RB];   // per warp block: staged records reaching it
     __shared__ int s_wc[NW][NW];       // [staging warp][warp block] kept counts
     __shared__ int s_max;
+#if S3R_BWD_SMEMCOT
+    // per thread (column) and pair: the RGB cotangent pairs and the stops,
+    // [P][tid] so that a warp's loads of one pair are contiguous
+    __shared__ float2 s_gr[RPIX / 2][RT], s_gg[RPIX / 2][RT], s_gb[RPIX / 2][RT];
+    __shared__ int2 s_last[RPIX / 2][RT];
+#endif
     const int v = blockIdx.y;
     const DevView& V = a.views[v];
     const int tile = blockIdx.x;
@@ -200,9 +212,16 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
     for (int P = 0; P < NP; ++P) {
         Tc[P] = make_float2(Tk[2 * P], Tk[2 * P + 1]);
         gtTf[P] = make_float2(gtTk[2 * P], gtTk[2 * P + 1]);
+#if S3R_BWD_SMEMCOT
+        s_gr[P][tid] = make_float2(grk[2 * P], grk[2 * P + 1]);
+        s_gg[P][tid] = make_float2(ggk[2 * P], ggk[2 * P + 1]);
+        s_gb[P][tid] = make_float2(gbk[2 * P], gbk[2 * P + 1]);
+        s_last[P][tid] = make_int2(last[2 * P], last[2 * P + 1]);
+#else
         gr[P] = make_float2(grk[2 * P], grk[2 * P + 1]);
         gg[P] = make_float2(ggk[2 * P], ggk[2 * P + 1]);
         gb[P] = make_float2(gbk[2 * P], gbk[2 * P + 1]);
+#endif
         gd[P] = make_float2(gdk[2 * P], gdk[2 * P + 1]);
         nfpy[P] = make_float2(nfk[2 * P], nfk[2 * P + 1]);
         Rr[P] = f2(0.0f);
@@ -313,8 +332,16 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 const float2 e2 = make_float2(fminf(0.0f, e2raw.x), fminf(0.0f, e2raw.y));
                 // entries after the pixel's termination, or flushed in the forward
                 // (alpha = 0): nothing to differentiate
+#if S3R_BWD_SMEMCOT
+                const int2 lst2 = CHK ? s_last[P][tid] : make_int2(0, 0);
+                const bool okx = (!CHK || j < lst2.x) && e2.x >= -24.0f;
+                const bool oky = (!CHK || j < lst2.y) && e2.y >= -24.0f;
+                const float2 grP = s_gr[P][tid], ggP = s_gg[P][tid], gbP = s_gb[P][tid];
+#else
                 const bool okx = (!CHK || j < last[2 * P]) && e2.x >= -24.0f;
                 const bool oky = (!CHK || j < last[2 * P + 1]) && e2.y >= -24.0f;
+                const float2 grP = gr[P], ggP = gg[P], gbP = gb[P];
+#endif
 #if S3R_BWD_NOBR
                 // branch-free: a pair with neither pixel ok gets G = 0 below, which
                 // leaves T, R and every sum bit-identical; the pairs' dependency
@@ -360,9 +387,9 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
                 const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
                 const float2 Tb = __fmul2_rn(Tc[P], inv);        // T before this splat
                 const float2 w = __fmul2_rn(alpha, Tb);
-                float2 cdot = __fmul2_rn(f2(q2.x), gr[P]);
-                cdot = __ffma2_rn(f2(q2.y), gg[P], cdot);
-                cdot = __ffma2_rn(f2(q2.z), gb[P], cdot);
+                float2 cdot = __fmul2_rn(f2(q2.x), grP);
+                cdot = __ffma2_rn(f2(q2.y), ggP, cdot);
+                cdot = __ffma2_rn(f2(q2.z), gbP, cdot);
                 if (HAS_D) cdot = __ffma2_rn(f2(q0.z), gd[P], cdot);
                 // dL/dalpha = T (c.gC + z gD) - (R + gT T_final) / (1 - alpha)
                 const float2 rest = __fmul2_rn(HAS_T ? __fadd2_rn(Rr[P], gtTf[P]) : Rr[P], inv);
@@ -372,9 +399,9 @@ __global__ void __launch_bounds__(RT, S3R_BWD_MINB) k_raster_bwd(BackwardArgs a)
 #if !S3R_BWD_NOBR
                 any = true;
 #endif
-                s_r = __ffma2_rn(w, gr[P], s_r);
-                s_g = __ffma2_rn(w, gg[P], s_g);
-                s_b = __ffma2_rn(w, gb[P], s_b);
+                s_r = __ffma2_rn(w, grP, s_r);
+                s_g = __ffma2_rn(w, ggP, s_g);
+                s_b = __ffma2_rn(w, gbP, s_b);
                 if (HAS_D) s_z = __ffma2_rn(w, gd[P], s_z);
                 // alpha clamped at 0.99: no gradient to o or the power;
                 // power clamped at 0 (e2raw > 0): no gradient to the power

@@ -20,11 +20,19 @@ namespace {
 
 constexpr int PLT = 1024;
 
-// block-wide inclusive scan of one 64-bit value per thread (1024 threads)
+// block-wide inclusive scan of one 64-bit value per thread (blockDim.x = 32 k)
 __device__ __forceinline__ unsigned long long block_incl_scan(unsigned long long x,
                                                               unsigned long long* s_w)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (nw == 1) {           // one warp (batches of <= 32 views): shuffles only
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        return x;
+    }
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
@@ -33,7 +41,7 @@ __device__ __forceinline__ unsigned long long block_incl_scan(unsigned long long
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        unsigned long long w = s_w[lane];
+        unsigned long long w = lane < nw ? s_w[lane] : 0ull;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
@@ -48,10 +56,11 @@ __device__ __forceinline__ unsigned long long block_incl_scan(unsigned long long
 }
 
 // After K1: n_temporal per view (from its distinct time's count) and the
-// view's record segment [cap_off, cap_off + n_temporal).
+// view's record segment [cap_off, cap_off + n_temporal); a view above the
+// per-view capacity (which sized K2's grid) is dropped as well.
 __global__ void __launch_bounds__(PLT) k_plan_records(DevView* __restrict__ views, int nv,
                                                       const unsigned long long* __restrict__ counts,
-                                                      long long cap_records,
+                                                      long long cap_records, long long cap_view,
                                                       long long* __restrict__ h_ntemp,
                                                       uint32_t* __restrict__ err)
 {
@@ -59,14 +68,15 @@ __global__ void __launch_bounds__(PLT) k_plan_records(DevView* __restrict__ view
     __shared__ unsigned long long s_carry;
     if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
-    for (int base = 0; base < nv; base += PLT) {
+    const int T = blockDim.x;
+    for (int base = 0; base < nv; base += T) {
         const int v = base + threadIdx.x;
         const unsigned long long n = v < nv ? counts[views[v].tslot] : 0ull;
         const unsigned long long incl = block_incl_scan(n, s_w);
         const unsigned long long off = s_carry + incl - n;
         if (v < nv) {
             DevView& V = views[v];
-            const bool fits = (long long)(off + n) <= cap_records;
+            const bool fits = (long long)(off + n) <= cap_records && (long long)n <= cap_view;
             V.cap_off = (long long)off;
             V.dbg_off = (long long)off;
             V.n_temporal = fits ? (long long)n : 0;
@@ -74,7 +84,7 @@ __global__ void __launch_bounds__(PLT) k_plan_records(DevView* __restrict__ view
             if (!fits) atomicOr(err, ERR_CAPACITY);
         }
         __syncthreads();
-        if (threadIdx.x == PLT - 1) s_carry += incl;
+        if (threadIdx.x == T - 1) s_carry += incl;
         __syncthreads();
     }
 }
@@ -91,7 +101,8 @@ __global__ void __launch_bounds__(PLT) k_plan_bins(DevView* __restrict__ views, 
     __shared__ unsigned long long s_c[4];
     if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
     __syncthreads();
-    for (int base = 0; base < nv; base += PLT) {
+    const int T = blockDim.x;
+    for (int base = 0; base < nv; base += T) {
         const int v = base + threadIdx.x;
         ViewCounters k{};
         long long nr = 0, ns = 0;
@@ -151,7 +162,7 @@ __global__ void __launch_bounds__(PLT) k_plan_bins(DevView* __restrict__ views, 
             dt0[v] = (int)o_dt;
         }
         __syncthreads();
-        if (threadIdx.x == PLT - 1) {
+        if (threadIdx.x == T - 1) {
             s_c[0] += i_sp;
             s_c[1] += i_tl;
             s_c[2] += i_cnt;
@@ -165,18 +176,20 @@ __global__ void __launch_bounds__(PLT) k_plan_bins(DevView* __restrict__ views, 
 }  // namespace
 
 void launch_plan_records(DevView* views, int nv, const unsigned long long* counts,
-                         long long cap_records, long long* h_ntemp, uint32_t* err,
-                         cudaStream_t st)
+                         long long cap_records, long long cap_view, long long* h_ntemp,
+                         uint32_t* err, cudaStream_t st)
 {
     if (nv == 0) return;
-    k_plan_records<<<1, PLT, 0, st>>>(views, nv, counts, cap_records, h_ntemp, err);
+    // one warp for a batch of <= 32 views (no block barriers), else 1024 threads
+    k_plan_records<<<1, nv <= 32 ? 32 : PLT, 0, st>>>(views, nv, counts, cap_records, cap_view,
+                                                      h_ntemp, err);
 }
 
 void launch_plan_bins(DevView* views, int nv, const ViewCounters* ctr, Seg* segs, int* dt0,
                       const PlanCaps& caps, ViewCounters* h_ctr, uint32_t* err, cudaStream_t st)
 {
     if (nv == 0) return;
-    k_plan_bins<<<1, PLT, 0, st>>>(views, nv, ctr, segs, dt0, caps, h_ctr, err);
+    k_plan_bins<<<1, nv <= 32 ? 32 : PLT, 0, st>>>(views, nv, ctr, segs, dt0, caps, h_ctr, err);
 }
 
 }  // namespace s3r

@@ -40,8 +40,10 @@ constexpr int PT = 256;
 #ifndef S3R_K2_PR
 #define S3R_K2_PR 4
 #endif
-constexpr int PR = S3R_K2_PR;         // rounds of PT entries per CTA
-constexpr int PTILE = PT * PR;
+constexpr int PR_BIG = S3R_K2_PR;     // rounds of PT entries per CTA
+constexpr int PTILE = PT * PR_BIG;
+// batches whose K2 grid would not fill the GPU (small scenes: C1) take chunks of
+// one round, 4x more CTAs on the same entries (shorter serial chains)
 
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x)
 {
@@ -389,13 +391,14 @@ __device__ __forceinline__ bool surely_outside(const float* __restrict__ M, floa
            my + rb < 0.0f;
 }
 
-// Pass A of K2 over one CTA chunk of PTILE temporal-list entries: all PR
+// Pass A of K2 over one CTA chunk of (PT * PR) temporal-list entries: all PR
 // rounds' loads are issued before any test (two dependent load latencies per
 // chunk instead of two per round); the conservative pre-test (surely_outside)
 // runs on each valid entry, and the entries it cannot reject (and, with debug
 // dumps, all valid ones; tag bit 15 = "the pre-test would have culled it") are
 // appended to the shared-memory queue (qt, qg) through the counter *qn.  Bad
 // instance ids are counted into c_bad (and dumped) here.
+template <int PR>
 __device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevView& V, int vi,
                                               long long i0, long long n_t,
                                               const int32_t* __restrict__ tl,
@@ -478,6 +481,7 @@ __device__ __forceinline__ void stage_view(const ProjectArgs& a, const DevView& 
 #ifndef S3R_K2_MINB
 #define S3R_K2_MINB 4     // 64 registers (A/B: K2 0.91 ms vs 1.03 at 3, 1.40 at 2)
 #endif
+template <int PR>
 __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
 {
     extern __shared__ float s_tab[];          // [K1][12]
@@ -492,9 +496,10 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     const int vi = blockIdx.y;
     const DevView& V = a.views[vi];
     const long long n_t = V.n_temporal;
-    // grid-stride over the view's chunks of PTILE list entries: any n_temporal
-    // is covered whatever grid.x (the capacity-mode launch sizes it from a hint)
-    if ((long long)blockIdx.x * PTILE >= n_t) return;      // uniform for the CTA
+    // one chunk of PT * PR list entries per CTA (the capacity mode bounds
+    // n_temporal by the reserved temporal_view, which sizes grid.x)
+    const long long i0 = (long long)blockIdx.x * (PT * PR);
+    if (i0 >= n_t) return;                    // uniform for the CTA
     [[maybe_unused]] const int K1 = a.num_instances;
     stage_view(a, V, s_tab, s_bounds);
     __syncthreads();
@@ -512,14 +517,13 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     // visible Gaussians are scattered through the index list: without the queue
     // nearly every warp holds one and pays the full path for all 32 lanes).
     __shared__ int s_qn;
-    __shared__ uint16_t s_q[PTILE];
-    __shared__ uint32_t s_g[PTILE];
+    __shared__ uint16_t s_q[(PT * PR)];
+    __shared__ uint32_t s_g[(PT * PR)];
     const uint16_t* qt = s_q;
     const uint32_t* qg = s_g;
-    for (long long i0 = (long long)blockIdx.x * PTILE; i0 < n_t; i0 += (long long)gridDim.x * PTILE) {
     if (tid == 0) s_qn = 0;
     __syncthreads();
-    precull_chunk(a, V, vi, i0, n_t, tl, s_tab, lox, hix, loy, hiy, s_q, s_g, &s_qn, c_bad);
+    precull_chunk<PR>(a, V, vi, i0, n_t, tl, s_tab, lox, hix, loy, hiy, s_q, s_g, &s_qn, c_bad);
     __syncthreads();
     const int qn = s_qn;
     for (int qbase = 0; qbase < qn; qbase += PT) {
@@ -635,8 +639,6 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
             if (a.gidx) a.gidx[o] = (int32_t)g;
             if (a.rec_mu) a.rec_mu[o] = make_float4(sp.mu[0], sp.mu[1], sp.mu[2], __int_as_float(gid_id));
         }
-    }
-    __syncthreads();                          // the queue is refilled by the next chunk
     }
     // ---- per-view counters: one set of atomics per CTA ----
     unsigned long long cv[6] = {c_vis, c_small, c_drop, c_pairs, c_bad, c_spairs};
@@ -863,9 +865,15 @@ void launch_project(const ProjectArgs& a, cudaStream_t st)
     if (a.max_tiles == 0 || a.n_views == 0) return;
     const size_t smem = (size_t)a.num_instances * 12 * sizeof(float);
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_project<PR_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if ((long long)a.max_tiles * a.n_views < 2 * 148) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_project<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_project<1><<<dim3(a.max_tiles * PR_BIG, a.n_views), PT, smem, st>>>(a);
+        return;
+    }
     dim3 grid(a.max_tiles, a.n_views);
-    k_project<<<grid, PT, smem, st>>>(a);
+    k_project<PR_BIG><<<grid, PT, smem, st>>>(a);
 }
 
 int project_tile() { return PTILE; }

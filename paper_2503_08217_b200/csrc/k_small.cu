@@ -3,7 +3,7 @@
 // tiles, the depth sort (K5: hist, scan, ~6 onesweep passes), the permute (K3)
 // and the supertile binning (K4: count, scan, scatter, expand) — a dozen
 // launches that each do almost nothing at this size — are replaced by one CTA
-// that keeps the view in shared memory (SURVEY.md §7 hard part 7: C1 is
+// that keeps the view on chip (SURVEY.md §7 hard part 7: C1 is
 // launch-bound).  The outputs are the big path's, bit for bit: the sorted
 // (depth << gbits | index) keys and slot order, the records and rectangles by
 // rank (with the flush-ellipse extents), and per-tile lists of ranks in rank
@@ -29,6 +29,80 @@ __device__ __forceinline__ bool rect_has(uint2 rr, int tx, int ty)
            ty <= (int)(rr.y >> 16);
 }
 
+// Bitonic sort of (key, slot) over E * SMT elements in registers (thread t
+// holds positions t and t + SMT): partners within a warp by shuffles, farther
+// ones through shared memory, SMT apart inside the thread; padding keys (~0)
+// sort last.  The result is left in s_key / s_idx by position.
+template <int E>
+__device__ __forceinline__ void bitonic_sort(const unsigned long long* __restrict__ dkey,
+                                             long long base, int n,
+                                             unsigned long long* s_key, uint16_t* s_idx)
+{
+    const int tid = threadIdx.x;
+    unsigned long long key[E];
+    uint32_t idx[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int p = tid + e * SMT;
+        key[e] = p < n ? dkey[base + p] : ~0ull;
+        idx[e] = (uint32_t)p;
+    }
+    for (int k = 2; k <= E * SMT; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (E == 2 && j == SMT) {   // k = 2 SMT: ascending, partner in the thread
+                if (key[E - 1] < key[0]) {
+                    const unsigned long long tk = key[0];
+                    key[0] = key[E - 1];
+                    key[E - 1] = tk;
+                    const uint32_t ti = idx[0];
+                    idx[0] = idx[E - 1];
+                    idx[E - 1] = ti;
+                }
+                continue;
+            }
+            unsigned long long pk[E];
+            uint32_t pi[E];
+            if (j >= 32) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    s_key[tid + e * SMT] = key[e];
+                    s_idx[tid + e * SMT] = (uint16_t)idx[e];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    pk[e] = s_key[(tid ^ j) + e * SMT];
+                    pi[e] = s_idx[(tid ^ j) + e * SMT];
+                }
+                __syncthreads();
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    pk[e] = __shfl_xor_sync(0xffffffffu, key[e], j);
+                    pi[e] = __shfl_xor_sync(0xffffffffu, idx[e], j);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                // the pair's lower position keeps the min in an ascending block
+                // (the max in a descending one), the upper position the other
+                const int p = tid + e * SMT;
+                const bool keep_min = ((p & j) == 0) == ((p & k) == 0);
+                if (keep_min ? pk[e] < key[e] : pk[e] > key[e]) {
+                    key[e] = pk[e];
+                    idx[e] = pi[e];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        s_key[tid + e * SMT] = key[e];
+        s_idx[tid + e * SMT] = (uint16_t)idx[e];
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict__ views,
                                                        const unsigned long long* __restrict__ dkey,
                                                        const float4* __restrict__ rec,
@@ -39,6 +113,7 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
                                                        uint32_t* __restrict__ tlists,
                                                        int2* __restrict__ tranges)
 {
+    static_assert(SMALL_MAX == 2 * SMT, "two elements per thread");
     __shared__ unsigned long long s_key[SMALL_MAX];
     __shared__ uint16_t s_idx[SMALL_MAX];
     __shared__ uint2 s_rect[SMALL_MAX];
@@ -49,33 +124,9 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = (int)V.n_rendered;
     const long long base = V.cap_off;
-    int n2 = 1;
-    while (n2 < n) n2 <<= 1;
-    // ---- bitonic sort of (key, slot); padding keys sort last
-    for (int i = tid; i < n2; i += SMT) {
-        s_key[i] = i < n ? dkey[base + i] : ~0ull;
-        s_idx[i] = (uint16_t)i;
-    }
-    __syncthreads();
-    for (int k = 2; k <= n2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < n2; i += SMT) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const unsigned long long a = s_key[i], b = s_key[l];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        s_key[i] = b;
-                        s_key[l] = a;
-                        const uint16_t t = s_idx[i];
-                        s_idx[i] = s_idx[l];
-                        s_idx[l] = t;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
+    // ---- depth order: (key, slot) sorted in registers / shared memory
+    if (n <= SMT) bitonic_sort<1>(dkey, base, n, s_key, s_idx);
+    else bitonic_sort<2>(dkey, base, n, s_key, s_idx);
     // ---- permute (K3): records and rectangles by rank
     for (int r = tid; r < n; r += SMT) {
         const uint32_t j = s_idx[r];

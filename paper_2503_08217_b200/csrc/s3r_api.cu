@@ -508,7 +508,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
 
     // ================= K2: projection + LOD + life + compaction
     long long cap = 0;
-    int k2_tiles = 0;          // grid.x of K2 (grid.y = views; K2 strides over any count)
+    int k2_tiles = 0;          // grid.x of K2 (grid.y = views)
     if (capm) {
         cap = c->cap.records;
         k2_tiles = (int)std::max<long long>(1, (c->cap.temporal_view + project_tile() - 1) / project_tile());
@@ -551,7 +551,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         // record segments on the device from K1's counts
         c->cap_h_ntemp = (long long*)stage_alloc(c, (size_t)std::max(nv, 1) * 8);
         launch_plan_records(P<DevView>(c->d_views), nv, P<unsigned long long>(c->d_counts),
-                            c->cap.records, (long long*)mapped(c, c->cap_h_ntemp),
+                            c->cap.records, c->cap.temporal_view,
+                            (long long*)mapped(c, c->cap_h_ntemp),
                             P<uint32_t>(c->d_err), st);
     }
     if (conv && N > 0 && nv > 0) {

@@ -175,8 +175,8 @@ struct PlanCaps {
 // capacity mode: device-side sizing after K1 (record segments) and after K2
 // (sort segments, binning layout); see k_plan.cu
 void launch_plan_records(DevView* views, int nv, const unsigned long long* counts,
-                         long long cap_records, long long* h_ntemp, uint32_t* err,
-                         cudaStream_t st);
+                         long long cap_records, long long cap_view, long long* h_ntemp,
+                         uint32_t* err, cudaStream_t st);
 void launch_plan_bins(DevView* views, int nv, const ViewCounters* ctr, Seg* segs, int* dt0,
                       const PlanCaps& caps, ViewCounters* h_ctr, uint32_t* err, cudaStream_t st);
 

@@ -9,6 +9,14 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANT_SETS = {
+    "r2smem": {
+        "base": [],
+        "scot14": ["S3R_BWD_SMEMCOT=1"],
+        "scot16": ["S3R_BWD_SMEMCOT=1", "S3R_BWD_MINB=16"],
+        "scot18": ["S3R_BWD_SMEMCOT=1", "S3R_BWD_MINB=18", "S3R_BWD_RB=128"],
+        "scot20": ["S3R_BWD_SMEMCOT=1", "S3R_BWD_MINB=20", "S3R_BWD_RB=128"],
+        "rb128": ["S3R_BWD_RB=128"],
+    },
     "r2bwd": {
         "base": [],
         "stage0": ["S3R_RASTER_STAGE=0"],
