@@ -28,6 +28,57 @@ sys.path.insert(0, ROOT)
 _G = {}
 
 
+def keyfed_np(scene, view, o):
+    """fp64 Eq.2 (alpha = min(0.99, o exp(power)), include-then-stop
+    at T < 1e-4, no flush) over the oracle's fp32 tile lists and splat keys
+    (mx, my, z, a, b, c; conic from the dilated 2D covariance, reading R5),
+    all tiles at once, one list position at a time."""
+    W, H = view.width, view.height
+    TX, TY = (W + 15) // 16, (H + 15) // 16
+    nt = TX * TY
+    rg = o["ranges"].astype(np.int64)
+    cnt = rg[:, 1] - rg[:, 0]
+    L = int(cnt.max()) if nt else 0
+    k = o["splat_keys"].astype(np.float64)
+    op = scene.means_opacity[:, 3].astype(np.float64)
+    col = scene.colors[:, :3].astype(np.float64)
+    a_, b_, c_ = k[:, 3] + 0.3, k[:, 4], k[:, 5] + 0.3
+    det = a_ * c_ - b_ * b_
+    with np.errstate(all="ignore"):
+        A, B, Cc = c_ / det, -b_ / det, a_ / det
+    # pixel coordinates of every tile's 256 pixels
+    ly, lx = np.divmod(np.arange(256), 16)
+    tx, ty = np.arange(nt) % TX, np.arange(nt) // TX
+    px = (tx[:, None] * 16 + lx[None, :]).astype(np.float64)
+    py = (ty[:, None] * 16 + ly[None, :]).astype(np.float64)
+    T = np.ones((nt, 256))
+    C = np.zeros((nt, 256, 3))
+    D = np.zeros((nt, 256))
+    live = np.ones((nt, 256), bool)
+    pg = o["pair_gauss"]
+    for j in range(L):
+        has = cnt > j
+        g = np.where(has, pg[np.minimum(rg[:, 0] + j, len(pg) - 1)], 0)
+        dx = k[g, 0][:, None] - px
+        dy = k[g, 1][:, None] - py
+        power = np.minimum(0.0, -0.5 * (A[g][:, None] * dx * dx + Cc[g][:, None] * dy * dy)
+                           - B[g][:, None] * dx * dy)
+        alpha = np.minimum(0.99, op[g][:, None] * np.exp(power))
+        m = live & has[:, None]
+        w = np.where(m, alpha * T, 0.0)
+        C += w[:, :, None] * col[g][:, None, :]
+        D += w * k[g, 2][:, None]
+        T = np.where(m, T * (1.0 - alpha), T)
+        live &= ~(m & (T < 1e-4))
+    img = np.zeros((TY * 16, TX * 16, 3))
+    dep = np.zeros((TY * 16, TX * 16))
+    Ti = np.ones((TY * 16, TX * 16))
+    for arr, out in ((C, img), (D, dep), (T, Ti)):
+        v = arr.reshape(TY, TX, 16, 16, *arr.shape[2:]).swapaxes(1, 2)
+        out[...] = v.reshape(TY * 16, TX * 16, *arr.shape[2:])
+    return img[:H, :W], dep[:H, :W], Ti[:H, :W]
+
+
 def _one(job):
     import oracle
     cfg, vi = job
@@ -68,6 +119,20 @@ def _one(job):
     ka, kb = a["keys"][m].astype(np.float64), b["keys"][m]
     scale = np.maximum(np.abs(kb), np.abs(kb[:, 3:4]) + np.abs(kb[:, 5:6]))
     r["keys_max_rel"] = float((np.abs(ka - kb) / np.maximum(scale, 1.0)).max()) if m.any() else 0.0
+    # key-fed (numpy, float64): Eq.2 as written, blended over the fp32 contract's
+    # own tile lists and splat keys, so only the blend arithmetic differs
+    # (exp2 polynomial + 2^-24 flush + T - w vs exp + T (1 - alpha))
+    rgb, dep, T = keyfed_np(scene, view, a)
+    krgb = np.abs(a["rgb"].astype(np.float64) - rgb).max(-1)
+    kdep = np.abs(a["depth"].astype(np.float64) - dep)
+    kflip = (a["final_T"] < 1e-4) != (T < 1e-4)
+    r["keyfed_np"] = {"rgb_max_abs": float(krgb.max()), "depth_max_abs": float(kdep.max()),
+                      "final_T_max_abs": float(np.abs(a["final_T"] - T).max()),
+                      "rgb_px_over_1e-4": int((krgb > 1e-4).sum()),
+                      "depth_px_over_1e-4": int((kdep > 1e-4).sum()),
+                      "depth_max_rel": float((kdep / np.maximum(dep, 1e-30)).max()),
+                      "termination_status_flips": int(kflip.sum()),
+                      "rgb_max_abs_no_flip": float(krgb[~kflip].max())}
     if not _G.get("keyfed"):
         r["oracle_s_total"] = round(time.perf_counter() - t0, 1)
         return r
