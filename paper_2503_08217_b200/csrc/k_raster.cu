@@ -60,7 +60,10 @@ constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
 #ifndef S3R_RASTER_STAGE
 #define S3R_RASTER_STAGE 1   // record staging: 0 LDG+STS, 1 cp.async (A/B: 14.55 vs 14.57 ms), 2 cp.async double-buffered at 128 records (15.20 ms)
 #endif
-constexpr int RB = S3R_RASTER_STAGE == 2 ? 128 : 256;   // records staged per batch (per buffer)
+#ifndef S3R_RASTER_RB
+#define S3R_RASTER_RB (S3R_RASTER_STAGE == 2 ? 128 : 256)
+#endif
+constexpr int RB = S3R_RASTER_RB;   // records staged per batch (per buffer)
 constexpr int NBUF = S3R_RASTER_STAGE == 2 ? 2 : 1;
 
 // Build-time variants (for A/B measurement; the defaults are the product):

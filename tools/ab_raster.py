@@ -9,6 +9,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANT_SETS = {
+    "r2occ": {
+        "base": [],
+        "m18rb192": ["S3R_RASTER_MINB=18", "S3R_RASTER_RB=192"],
+        "m20rb160": ["S3R_RASTER_MINB=20", "S3R_RASTER_RB=160"],
+        "m20rb128": ["S3R_RASTER_MINB=20", "S3R_RASTER_RB=128"],
+        "m16rb192": ["S3R_RASTER_RB=192"],
+    },
     "r2smem": {
         "base": [],
         "scot14": ["S3R_BWD_SMEMCOT=1"],
