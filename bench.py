@@ -736,7 +736,8 @@ def main():
                                   f"{E_alg} per launch; the executed R-ARITH form is "
                                   f"{EXEC_FLOPS_PER_EVAL} (frac "
                                   f"{EXEC_FLOPS_PER_EVAL / FLOPS_PER_EVAL * ach / alu_peak:.3f})"}
-        tr, tr_src = load_traffic(("k_raster<0,0,0>", "k_raster<0,0>"), args.config)
+        tr, tr_src = load_traffic(("k_raster<0,0,0,4>", "k_raster<0,0,0>", "k_raster<0,0>"),
+                                  args.config)
         if tr is not None:
             roof["traffic"] = tr
             roof["traffic_source"] = f"{tr_src} (ncu --set full, one launch of this command)"

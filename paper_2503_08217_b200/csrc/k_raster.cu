@@ -38,13 +38,20 @@ namespace {
 #define S3R_RASTER_RPIX 4
 #endif
 // pixels per thread (RPIX rows of one column, RS rows apart); a tile's 256
-// pixels take RT = 256 / RPIX threads, each warp owning BW columns
-constexpr int RPIX = S3R_RASTER_RPIX;
-constexpr int RT = TILE * TILE / RPIX;
-constexpr int BW = TILE / (RT / 32);
-constexpr int RS = 32 / BW;
-constexpr int NP = RPIX / 2;
-constexpr int NW = RT / 32;        // warps (= pixel blocks) per tile CTA
+// pixels take RT = 256 / RPIX threads, each warp owning BW columns.  The
+// product layout is RPIX = 4 (2 packed pairs per thread, 64-thread CTAs); a
+// batch whose grid cannot fill the GPU (C1: 16 tiles) takes RPIX = 2 (one pair
+// per thread, 128-thread CTAs): twice the warps on the few busy SMs.
+template <int RP>
+struct Geo {
+    static constexpr int RPIX = RP;
+    static constexpr int RT = TILE * TILE / RPIX;
+    static constexpr int BW = TILE / (RT / 32);
+    static constexpr int RS = 32 / BW;
+    static constexpr int NP = RPIX / 2;
+    static constexpr int NW = RT / 32;   // warps (= pixel blocks) per tile CTA
+};
+constexpr int RPIX_BIG = S3R_RASTER_RPIX;
 #ifndef S3R_RASTER_ADJ
 #define S3R_RASTER_ADJ 1     // vertically adjacent pixel pairs (A/B: 14.65 vs 15.01 ms)
 #endif
@@ -144,9 +151,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // One (view, tile): the whole K7 computation of the tile's 256 pixels.
-template <bool COUNT, bool TRAIN, bool FAST>
+template <bool COUNT, bool TRAIN, bool FAST, int RP>
 __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, const int tile)
 {
+    constexpr int RPIX = Geo<RP>::RPIX, RT = Geo<RP>::RT, BW = Geo<RP>::BW, RS = Geo<RP>::RS,
+                  NP = Geo<RP>::NP, NW = Geo<RP>::NW;
     __shared__ float4 s_rec[NBUF][3 * RB];   // staged splat records, 48 B each
     __shared__ uint16_t s_cl[NW][RB];        // per warp block: staged records reaching it
     __shared__ int s_wc[NW][NW];             // [staging warp][warp block] kept counts
@@ -168,7 +177,9 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
     const float fpx = (float)px;
     // centre of the warp's BW x 16 pixel block (flush-ellipse culling; the
     // stored extents include the 8 x 16 block's half size)
-    static_assert(BW >= 8, "cull extents assume >= 8 x 16 warp blocks");
+    // (the stored extents include an 8 x 16 block's half size; XPAD corrects
+    // for another block width, negative for BW < 8)
+    static_assert(BW >= 1 && RS * 2 * NP == TILE, "warp blocks span the tile's 16 rows");
     constexpr float XPAD = 0.5f * (BW - 1) - CULL_HALF_BX;
     const float bcx0 = (float)(tx * TILE) + 0.5f * (BW - 1);     // warp block 0
     const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
@@ -440,11 +451,30 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
 }
 
 // K7: one CTA per (tile, view)
-template <bool COUNT, bool TRAIN, bool FAST>
-__global__ void __launch_bounds__(RT, TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER_MINB)
+template <bool COUNT, bool TRAIN, bool FAST, int RP>
+__global__ void __launch_bounds__(Geo<RP>::RT,
+                                  RP == RPIX_BIG ? (TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER_MINB) : 8)
     k_raster(RasterArgs a)
 {
-    raster_tile<COUNT, TRAIN, FAST>(a, blockIdx.y, blockIdx.x);
+    raster_tile<COUNT, TRAIN, FAST, RP>(a, blockIdx.y, blockIdx.x);
+}
+
+template <int RP>
+void launch_raster_rp(const RasterArgs& a, dim3 grid, cudaStream_t st)
+{
+    constexpr int RT = Geo<RP>::RT;
+    // training renders always take the exact R-ARITH exponential: the backward
+    // recomputes alpha with it and relies on the forward's decisions
+    if (a.train_T) {
+        if (a.evals) k_raster<true, true, false, RP><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, true, false, RP><<<grid, RT, 0, st>>>(a);
+    } else if (a.fast_exp) {
+        if (a.evals) k_raster<true, false, true, RP><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, false, true, RP><<<grid, RT, 0, st>>>(a);
+    } else {
+        if (a.evals) k_raster<true, false, false, RP><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, false, false, RP><<<grid, RT, 0, st>>>(a);
+    }
 }
 
 // ------------------------------------------------------------------ dumps
@@ -462,18 +492,8 @@ void launch_raster(const RasterArgs& args, cudaStream_t st)
     RasterArgs a = args;
     a.exp2_c0 = 1.3264695880934596e-3f;
     const dim3 grid(a.max_tiles, a.n_views);
-    // training renders always take the exact R-ARITH exponential: the backward
-    // recomputes alpha with it and relies on the forward's decisions
-    if (a.train_T) {
-        if (a.evals) k_raster<true, true, false><<<grid, RT, 0, st>>>(a);
-        else k_raster<false, true, false><<<grid, RT, 0, st>>>(a);
-    } else if (a.fast_exp) {
-        if (a.evals) k_raster<true, false, true><<<grid, RT, 0, st>>>(a);
-        else k_raster<false, false, true><<<grid, RT, 0, st>>>(a);
-    } else {
-        if (a.evals) k_raster<true, false, false><<<grid, RT, 0, st>>>(a);
-        else k_raster<false, false, false><<<grid, RT, 0, st>>>(a);
-    }
+    if ((long long)a.max_tiles * a.n_views < 2 * 148) launch_raster_rp<2>(a, grid, st);
+    else launch_raster_rp<RPIX_BIG>(a, grid, st);
 }
 
 void launch_dump_order(const uint32_t* order, const int32_t* gidx, long long base,

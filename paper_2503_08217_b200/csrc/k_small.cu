@@ -10,10 +10,12 @@
 // order with their ranges — only packed without the supertile area's gaps.
 //
 // Order (reading R11): the keys are unique (the Gaussian index is in the low
-// bits), so a bitonic sort of (key, slot) gives the same order as the stable
-// radix sort.  Tile lists (R12): warp w takes tile t, walks the ranks 32 at a
-// time and keeps those whose rectangle contains t (ballot + popc keep rank
-// order); one pass counts, a block scan places the lists, a second pass writes.
+// bits), so sorting (key, slot) by key (warp bitonic runs + pairwise merges)
+// gives the same order as the stable radix sort.  Tile lists (R12): a warp takes one contiguous part of the ranks
+// of tile t (a view with few tiles splits each tile's ranks over the idle
+// warps), walks it 32 ranks at a time and keeps those whose rectangle contains
+// t (ballot + popc keep rank order); one pass counts per (tile, part), a block
+// scan in (tile, part) order places the parts, a second pass writes.
 #include "s3r_internal.cuh"
 
 namespace s3r {
@@ -29,14 +31,18 @@ __device__ __forceinline__ bool rect_has(uint2 rr, int tx, int ty)
            ty <= (int)(rr.y >> 16);
 }
 
-// Bitonic sort of (key, slot) over E * SMT elements in registers (thread t
-// holds positions t and t + SMT): partners within a warp by shuffles, farther
-// ones through shared memory, SMT apart inside the thread; padding keys (~0)
-// sort last.  The result is left in s_key / s_idx by position.
+// Sort of (key, slot) over E * SMT positions (thread t holds positions t and
+// t + SMT), padding keys (~0) last.  Each warp first sorts its 32 consecutive
+// positions with a bitonic network on shuffles; then sorted runs of L = 32, 64,
+// ... are merged pairwise in shared memory: an element's place in the merged run
+// is its rank in its own run plus the number of keys of the partner run below
+// it (a branch-free binary search; a right-run element also counts equal keys,
+// which keeps the padding duplicates apart).  The result is left in
+// s_key / s_idx by position.
 template <int E>
-__device__ __forceinline__ void bitonic_sort(const unsigned long long* __restrict__ dkey,
-                                             long long base, int n,
-                                             unsigned long long* s_key, uint16_t* s_idx)
+__device__ __forceinline__ void merge_sort(const unsigned long long* __restrict__ dkey,
+                                           long long base, int n,
+                                           unsigned long long* s_key, uint16_t* s_idx)
 {
     const int tid = threadIdx.x;
     unsigned long long key[E];
@@ -47,50 +53,19 @@ __device__ __forceinline__ void bitonic_sort(const unsigned long long* __restric
         key[e] = p < n ? dkey[base + p] : ~0ull;
         idx[e] = (uint32_t)p;
     }
-    for (int k = 2; k <= E * SMT; k <<= 1) {
+    // ---- 32-element runs, ascending, in registers
+    for (int k = 2; k <= 32; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            if (E == 2 && j == SMT) {   // k = 2 SMT: ascending, partner in the thread
-                if (key[E - 1] < key[0]) {
-                    const unsigned long long tk = key[0];
-                    key[0] = key[E - 1];
-                    key[E - 1] = tk;
-                    const uint32_t ti = idx[0];
-                    idx[0] = idx[E - 1];
-                    idx[E - 1] = ti;
-                }
-                continue;
-            }
-            unsigned long long pk[E];
-            uint32_t pi[E];
-            if (j >= 32) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    s_key[tid + e * SMT] = key[e];
-                    s_idx[tid + e * SMT] = (uint16_t)idx[e];
-                }
-                __syncthreads();
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    pk[e] = s_key[(tid ^ j) + e * SMT];
-                    pi[e] = s_idx[(tid ^ j) + e * SMT];
-                }
-                __syncthreads();
-            } else {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    pk[e] = __shfl_xor_sync(0xffffffffu, key[e], j);
-                    pi[e] = __shfl_xor_sync(0xffffffffu, idx[e], j);
-                }
-            }
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                // the pair's lower position keeps the min in an ascending block
-                // (the max in a descending one), the upper position the other
+                const unsigned long long pk = __shfl_xor_sync(0xffffffffu, key[e], j);
+                const uint32_t pi = __shfl_xor_sync(0xffffffffu, idx[e], j);
                 const int p = tid + e * SMT;
-                const bool keep_min = ((p & j) == 0) == ((p & k) == 0);
-                if (keep_min ? pk[e] < key[e] : pk[e] > key[e]) {
-                    key[e] = pk[e];
-                    idx[e] = pi[e];
+                const bool up = k == 32 || (p & k) == 0;
+                const bool keep_min = ((p & j) == 0) == up;
+                if (keep_min ? pk < key[e] : pk > key[e]) {
+                    key[e] = pk;
+                    idx[e] = pi;
                 }
             }
         }
@@ -101,6 +76,38 @@ __device__ __forceinline__ void bitonic_sort(const unsigned long long* __restric
         s_idx[tid + e * SMT] = (uint16_t)idx[e];
     }
     __syncthreads();
+    // ---- pairwise merges of sorted runs of length L
+    for (int L = 32; L < E * SMT; L <<= 1) {
+        int outp[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int p = tid + e * SMT;
+            const int r = p / L;
+            const int q0 = (r ^ 1) * L;
+            const bool right = r & 1;
+            int c = 0;
+            for (int st = L >> 1; st > 0; st >>= 1) {
+                const unsigned long long a = s_key[q0 + c + st - 1];
+                if (right ? a <= key[e] : a < key[e]) c += st;
+            }
+            const unsigned long long a = s_key[q0 + c];
+            if (right ? a <= key[e] : a < key[e]) c += 1;
+            outp[e] = (r & ~1) * L + (p % L) + c;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            s_key[outp[e]] = key[e];
+            s_idx[outp[e]] = (uint16_t)idx[e];
+        }
+        __syncthreads();
+        // the element now at position tid (+ SMT) for the next round
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            key[e] = s_key[tid + e * SMT];
+            idx[e] = s_idx[tid + e * SMT];
+        }
+    }
 }
 
 __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict__ views,
@@ -125,8 +132,8 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
     const int n = (int)V.n_rendered;
     const long long base = V.cap_off;
     // ---- depth order: (key, slot) sorted in registers / shared memory
-    if (n <= SMT) bitonic_sort<1>(dkey, base, n, s_key, s_idx);
-    else bitonic_sort<2>(dkey, base, n, s_key, s_idx);
+    if (n <= SMT) merge_sort<1>(dkey, base, n, s_key, s_idx);
+    else merge_sort<2>(dkey, base, n, s_key, s_idx);
     // ---- permute (K3): records and rectangles by rank
     for (int r = tid; r < n; r += SMT) {
         const uint32_t j = s_idx[r];
@@ -145,20 +152,27 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
         dst[2] = q2;
     }
     __syncthreads();
-    // ---- per-tile list lengths
+    // ---- per-tile list lengths: a tile's ranks are split into PP parts (all
+    // 32 warps busy when the view has few tiles); slot t PP + part
     const int nt = V.ntiles;
-    for (int t = warp; t < nt; t += SMW) {
+    int PP = 1;
+    while (PP * 2 * nt <= SMW) PP *= 2;
+    const int ns = nt * PP;                 // <= SMT slots
+    const int plen = (n + PP - 1) / PP;
+    for (int sl = warp; sl < ns; sl += SMW) {
+        const int t = sl / PP, part = sl % PP;
         const int tx = t % V.TX, ty = t / V.TX;
+        const int r0 = part * plen, r1 = min(n, r0 + plen);
         int c = 0;
-        for (int b = 0; b < n; b += 32) {
+        for (int b = r0; b < r1; b += 32) {
             const int r = b + lane;
-            c += __popc(__ballot_sync(0xffffffffu, r < n && rect_has(s_rect[r], tx, ty)));
+            c += __popc(__ballot_sync(0xffffffffu, r < r1 && rect_has(s_rect[r], tx, ty)));
         }
-        if (lane == 0) s_cnt[t] = c;
+        if (lane == 0) s_cnt[sl] = c;
     }
     __syncthreads();
-    // ---- exclusive scan of the lengths (nt <= SMALL_TILES = SMT)
-    const int x = tid < nt ? s_cnt[tid] : 0;
+    // ---- exclusive scan of the slot lengths
+    const int x = tid < ns ? s_cnt[tid] : 0;
     int v = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -180,20 +194,24 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
     __syncthreads();
     const int start = s_w[warp] + v - x;
     __syncthreads();
-    if (tid < nt) {
-        s_cnt[tid] = start;
-        tranges[V.trange_off + tid] = make_int2(start, start + x);
-    }
+    if (tid < ns) s_cnt[tid] = start;
+    if (tid == ns - 1) s_w[0] = start + x;          // the view's total (P)
     __syncthreads();
+    // tile ranges: [its first slot's start, the next tile's first slot's start)
+    if (tid < nt)
+        tranges[V.trange_off + tid] =
+            make_int2(s_cnt[tid * PP], tid + 1 < nt ? s_cnt[(tid + 1) * PP] : s_w[0]);
     // ---- the lists: ranks in rank order
     uint32_t* out = tlists + V.tlist_off;
     const unsigned lt = (1u << lane) - 1u;
-    for (int t = warp; t < nt; t += SMW) {
+    for (int sl = warp; sl < ns; sl += SMW) {
+        const int t = sl / PP, part = sl % PP;
         const int tx = t % V.TX, ty = t / V.TX;
-        int c = s_cnt[t];
-        for (int b = 0; b < n; b += 32) {
+        const int r0 = part * plen, r1 = min(n, r0 + plen);
+        int c = s_cnt[sl];
+        for (int b = r0; b < r1; b += 32) {
             const int r = b + lane;
-            const bool in = r < n && rect_has(s_rect[r], tx, ty);
+            const bool in = r < r1 && rect_has(s_rect[r], tx, ty);
             const unsigned bal = __ballot_sync(0xffffffffu, in);
             if (in) out[c + __popc(bal & lt)] = (uint32_t)r;
             c += __popc(bal);

@@ -39,7 +39,7 @@ def keyfed_np(scene, view, o):
     rg = o["ranges"].astype(np.int64)
     cnt = rg[:, 1] - rg[:, 0]
     L = int(cnt.max()) if nt else 0
-    k = o["splat_keys"].astype(np.float64)
+    k = np.nan_to_num(o["splat_keys"].astype(np.float64))   # NaN rows: not rendered (never used)
     op = scene.means_opacity[:, 3].astype(np.float64)
     col = scene.colors[:, :3].astype(np.float64)
     a_, b_, c_ = k[:, 3] + 0.3, k[:, 4], k[:, 5] + 0.3
@@ -130,7 +130,7 @@ def _one(job):
                       "final_T_max_abs": float(np.abs(a["final_T"] - T).max()),
                       "rgb_px_over_1e-4": int((krgb > 1e-4).sum()),
                       "depth_px_over_1e-4": int((kdep > 1e-4).sum()),
-                      "depth_max_rel": float((kdep / np.maximum(dep, 1e-30)).max()),
+                      "depth_max_rel": float((kdep / np.maximum(dep, 1e-3)).max()),
                       "termination_status_flips": int(kflip.sum()),
                       "rgb_max_abs_no_flip": float(krgb[~kflip].max())}
     if not _G.get("keyfed"):
