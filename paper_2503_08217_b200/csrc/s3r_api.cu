@@ -94,7 +94,17 @@ struct s3r_ctx {
     bool last_need_valid = false;
     cudaStream_t last_stream = nullptr;
     // device scratch
-    Buf d_views, d_times, d_tidx, d_counts, d_lb, d_ticket, d_ctr, d_rec, d_dkey, d_gidx,
+    // per-batch small state: one zeroed arena (work tickets, K1 counts, K1
+    // look-back words, K2 counters: ONE memset per batch) and one upload arena
+    // (distinct times, device views: one copy in the capacity mode)
+    Buf d_zero, d_up;
+    int* p_ticket = nullptr;
+    unsigned long long* p_counts = nullptr;
+    uint32_t* p_lb1 = nullptr;
+    ViewCounters* p_ctr = nullptr;
+    float* p_times = nullptr;
+    DevView* p_views = nullptr;
+    Buf d_tidx, d_lb, d_rec, d_dkey, d_gidx,
         d_sortk[2], d_sortv[2], d_recs, d_rects, d_lists, d_tlists, d_tranges, d_cnt, d_hist,
         d_dsegs, d_dtile0,
         d_ranges, d_err, d_dbg_keys, d_dbg_flags, d_dbg_rect, d_dbg_tcnt;
@@ -279,9 +289,9 @@ int* next_ticket(s3r_ctx* c)
     // render_impl reports (S3R_EINTERNAL) instead of writing past the buffer
     if (c->ticket_slot >= c->ticket_cap) {
         c->ticket_overflow = true;
-        return P<int>(c->d_ticket);
+        return c->p_ticket;
     }
-    return P<int>(c->d_ticket) + (c->ticket_slot++);
+    return c->p_ticket + (c->ticket_slot++);
 }
 
 // NVTX range per stage (host-side enqueue span; free without a tool attached)
@@ -463,19 +473,42 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     const int n_tickets = (T + MAX_TSLOTS - 1) / MAX_TSLOTS +
                           (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS;
     c->ticket_cap = n_tickets;
-    if ((rc = ensure(c, c->d_ticket, (size_t)n_tickets * sizeof(int)))) return rc;
     if ((rc = ensure(c, c->d_err, sizeof(uint32_t)))) return rc;
-    CU(cudaMemsetAsync(c->d_ticket.p, 0, (size_t)n_tickets * sizeof(int), st));
+    // the zeroed arena and the upload arena (16-byte aligned parts)
+    const long long ntf_all = conv ? 0 : (N + filter_tile() - 1) / filter_tile();
+    auto al16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t z_ticket = 0;
+    const size_t z_counts = al16(z_ticket + (size_t)n_tickets * 4);
+    const size_t z_lb1 = al16(z_counts + (size_t)std::max(T, 1) * 8);
+    const size_t z_ctr = al16(z_lb1 + (size_t)std::min(std::max(T, 1), MAX_TSLOTS) * ntf_all * 4);
+    const size_t z_end = al16(z_ctr + (size_t)std::max(nv, 1) * sizeof(ViewCounters));
+    if ((rc = ensure(c, c->d_zero, z_end))) return rc;
+    c->p_ticket = reinterpret_cast<int*>(P<char>(c->d_zero) + z_ticket);
+    c->p_counts = reinterpret_cast<unsigned long long*>(P<char>(c->d_zero) + z_counts);
+    c->p_lb1 = reinterpret_cast<uint32_t*>(P<char>(c->d_zero) + z_lb1);
+    c->p_ctr = reinterpret_cast<ViewCounters*>(P<char>(c->d_zero) + z_ctr);
+    CU(cudaMemsetAsync(c->d_zero.p, 0, z_end, st));
+    const size_t u_views = al16((size_t)std::max(T, 1) * 4);
+    const size_t u_end = u_views + (size_t)std::max(nv, 1) * sizeof(DevView);
+    if ((rc = ensure(c, c->d_up, u_end))) return rc;
+    c->p_times = P<float>(c->d_up);
+    c->p_views = reinterpret_cast<DevView*>(P<char>(c->d_up) + u_views);
 
     // ================= K1: temporal filter + compaction
     const long long Ns = std::max<long long>(N, 1);
     if ((rc = ensure(c, c->d_tidx, (size_t)std::max(T, 1) * Ns * sizeof(int32_t)))) return rc;
-    if ((rc = ensure(c, c->d_counts, (size_t)std::max(T, 1) * sizeof(unsigned long long)))) return rc;
-    if ((rc = ensure(c, c->d_times, (size_t)std::max(T, 1) * sizeof(float)))) return rc;
-    CU(cudaMemsetAsync(c->d_counts.p, 0, (size_t)std::max(T, 1) * sizeof(unsigned long long), st));
-    float* h_times = (float*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(float));
+    // the upload arena's image in staging: [times | views]; the capacity mode
+    // sends it whole now (the device fills in the per-view sizes), the
+    // synchronous mode sends the times now and the sized views after K1
+    char* h_up = (char*)stage_alloc(c, u_end);
+    float* h_times = reinterpret_cast<float*>(h_up);
     for (int i = 0; i < T; ++i) h_times[i] = tk[i];
-    if (T) CU(cudaMemcpyAsync(c->d_times.p, h_times, T * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (capm) {
+        std::memcpy(h_up + u_views, c->hv.data(), (size_t)nv * sizeof(DevView));
+        CU(cudaMemcpyAsync(c->d_up.p, h_up, u_end, cudaMemcpyHostToDevice, st));
+    } else if (T) {
+        CU(cudaMemcpyAsync(c->p_times, h_times, T * sizeof(float), cudaMemcpyHostToDevice, st));
+    }
     unsigned long long* h_counts =
         (unsigned long long*)stage_alloc(c, (size_t)std::max(T, 1) * sizeof(unsigned long long));
     if (conv) {
@@ -491,17 +524,17 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         const long long ntf = (N + filter_tile() - 1) / filter_tile();
         for (int c0 = 0; c0 < T && N > 0; c0 += MAX_TSLOTS) {
             const int Tc = std::min(MAX_TSLOTS, T - c0);
-            if ((rc = ensure(c, c->d_lb, (size_t)Tc * ntf * sizeof(uint32_t)))) return rc;
-            CU(cudaMemsetAsync(c->d_lb.p, 0, (size_t)Tc * ntf * sizeof(uint32_t), st));
+            // look-back words: zeroed with the arena for the first chunk of
+            // distinct times, re-zeroed for later ones
+            if (c0) CU(cudaMemsetAsync(c->p_lb1, 0, (size_t)Tc * ntf * sizeof(uint32_t), st));
             launch_filter(reinterpret_cast<const float2*>(sc->visibility), N,
-                          P<float>(c->d_times) + c0, Tc, P<int32_t>(c->d_tidx) + (long long)c0 * Ns,
-                          Ns, P<unsigned long long>(c->d_counts) + c0, P<uint32_t>(c->d_lb),
-                          next_ticket(c), st);
+                          c->p_times + c0, Tc, P<int32_t>(c->d_tidx) + (long long)c0 * Ns,
+                          Ns, c->p_counts + c0, c->p_lb1, next_ticket(c), st);
         }
         ev_end(c, st, e);
         CU(cudaGetLastError());
         if (!capm) {
-            if (T) launch_readback(mapped(c, h_counts), c->d_counts.p, T * sizeof(unsigned long long), st);
+            if (T) launch_readback(mapped(c, h_counts), c->p_counts, T * sizeof(unsigned long long), st);
             CU(cudaStreamSynchronize(st));
         }
     }
@@ -537,20 +570,19 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         if ((rc = ensure(c, c->d_dbg_flags, (size_t)capS))) return rc;
         if ((rc = ensure(c, c->d_dbg_rect, (size_t)capS * 8))) return rc;
     }
-    if ((rc = ensure(c, c->d_views, (size_t)std::max(nv, 1) * sizeof(DevView)))) return rc;
-    if ((rc = ensure(c, c->d_ctr, (size_t)std::max(nv, 1) * sizeof(ViewCounters)))) return rc;
-    DevView* h_views = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
-    std::memcpy(h_views, c->hv.data(), (size_t)nv * sizeof(DevView));
-    if (nv) {
-        CU(cudaMemcpyAsync(c->d_views.p, h_views, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
-        CU(cudaMemsetAsync(c->d_ctr.p, 0, nv * sizeof(ViewCounters), st));
+    if (!capm && nv) {
+        // the sized views (the K2 counters were zeroed with the arena); the
+        // capacity mode uploaded them with the times and plans them on the device
+        DevView* h_views = (DevView*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(DevView));
+        std::memcpy(h_views, c->hv.data(), (size_t)nv * sizeof(DevView));
+        CU(cudaMemcpyAsync(c->p_views, h_views, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
     }
     for (int v = 0; v < nv; ++v)
         if (outs[v].visible && N > 0) CU(cudaMemsetAsync(outs[v].visible, 0, (size_t)N, st));
     if (capm) {
         // record segments on the device from K1's counts
         c->cap_h_ntemp = (long long*)stage_alloc(c, (size_t)std::max(nv, 1) * 8);
-        launch_plan_records(P<DevView>(c->d_views), nv, P<unsigned long long>(c->d_counts),
+        launch_plan_records(c->p_views, nv, c->p_counts,
                             c->cap.records, c->cap.temporal_view,
                             (long long*)mapped(c, c->cap_h_ntemp),
                             P<uint32_t>(c->d_err), st);
@@ -563,7 +595,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         ev_begin(c, S3R_STAGE_PROJECT, st, e);
         launch_world(reinterpret_cast<const float4*>(sc->means_opacity),
                      reinterpret_cast<const float4*>(sc->rotations), sc->instance_ids,
-                     sc->num_instances, N, P<DevView>(c->d_views), nv, P<float4>(c->d_wmo),
+                     sc->num_instances, N, c->p_views, nv, P<float4>(c->d_wmo),
                      P<float4>(c->d_wrot), st);
         ev_end(c, st, e);
     }
@@ -580,7 +612,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.life = reinterpret_cast<float2*>(sc->life);
         a.num_instances = sc->num_instances;
         a.n = N;
-        a.views = P<DevView>(c->d_views);
+        a.views = c->p_views;
         a.n_views = nv;
         a.tidx = P<int32_t>(c->d_tidx);
         a.idx_stride = Ns;
@@ -589,7 +621,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.dkey = P<unsigned long long>(c->d_dkey);
         a.gbits = c->gbits;
         a.gidx = c->debug ? P<int32_t>(c->d_gidx) : nullptr;
-        a.counters = P<ViewCounters>(c->d_ctr);
+        a.counters = c->p_ctr;
         a.err = P<uint32_t>(c->d_err);
         a.dbg_keys = c->debug ? P<float>(c->d_dbg_keys) : nullptr;
         a.dbg_flags = c->debug ? P<uint8_t>(c->d_dbg_flags) : nullptr;
@@ -639,12 +671,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         pc.bin_chunk = bin_chunk();
         pc.sort_tile = stile;
         c->cap_h_ctr = h_ctr;
-        launch_plan_bins(P<DevView>(c->d_views), nv, P<ViewCounters>(c->d_ctr), P<Seg>(c->d_dsegs),
+        launch_plan_bins(c->p_views, nv, c->p_ctr, P<Seg>(c->d_dsegs),
                          P<int>(c->d_dtile0), pc, (ViewCounters*)mapped(c, h_ctr),
                          P<uint32_t>(c->d_err), st);
         c->cap_pending = true;
     } else {
-        if (nv) launch_readback(mapped(c, h_ctr), c->d_ctr.p, nv * sizeof(ViewCounters), st);
+        if (nv) launch_readback(mapped(c, h_ctr), c->p_ctr, nv * sizeof(ViewCounters), st);
         CU(cudaStreamSynchronize(st));
         for (int v = 0; v < nv; ++v) {
             DevView& d = c->hv[v];
@@ -695,7 +727,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         if (nv) {
             CU(cudaMemcpyAsync(c->d_dsegs.p, h_dsegs, nv * sizeof(Seg), cudaMemcpyHostToDevice, st));
             CU(cudaMemcpyAsync(c->d_dtile0.p, h_dt0, (nv + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-            CU(cudaMemcpyAsync(c->d_views.p, h_views2, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(c->p_views, h_views2, nv * sizeof(DevView), cudaMemcpyHostToDevice, st));
         }
         // what this batch needed (s3r_capacity_from_last)
         s3r_capacity need{};
@@ -738,7 +770,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         StageEvent e;
         ev_begin(c, S3R_STAGE_COLOR, st, e);
         NeurfArgs na{};
-        na.views = P<DevView>(c->d_views);
+        na.views = c->p_views;
         na.n_views = nv;
         na.tile_off = P<int>(c->d_toff);
         na.total_tiles = tt;
@@ -761,7 +793,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if (any_small && nv) {
         StageEvent e;
         ev_begin(c, S3R_STAGE_DEPTH_SORT, st, e);
-        launch_small_sortbin(P<DevView>(c->d_views), nv, P<unsigned long long>(c->d_dkey),
+        launch_small_sortbin(c->p_views, nv, P<unsigned long long>(c->d_dkey),
                              P<float4>(c->d_rec), P<unsigned long long>(c->d_sortk[c->final_order]),
                              P<uint32_t>(c->d_sortv[c->final_order]), P<float4>(c->d_recs),
                              P<uint2>(c->d_rects), P<uint32_t>(c->d_tlists),
@@ -797,9 +829,9 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if (!all_small) {
         StageEvent e;
         ev_begin(c, S3R_STAGE_BIN, st, e);
-        launch_permute(P<DevView>(c->d_views), nv, max_r, P<uint32_t>(c->d_sortv[c->final_order]),
+        launch_permute(c->p_views, nv, max_r, P<uint32_t>(c->d_sortv[c->final_order]),
                        P<float4>(c->d_rec), P<float4>(c->d_recs), P<uint2>(c->d_rects), st);
-        launch_bin(P<DevView>(c->d_views), nv, max_chunks, max_bins, P<uint2>(c->d_rects),
+        launch_bin(c->p_views, nv, max_chunks, max_bins, P<uint2>(c->d_rects),
                    P<uint32_t>(c->d_cnt), P<int2>(c->d_ranges), P<uint32_t>(c->d_lists),
                    P<uint32_t>(c->d_tlists), P<int2>(c->d_tranges), st);
         ev_end(c, st, e);
@@ -811,7 +843,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         StageEvent e;
         ev_begin(c, S3R_STAGE_RASTER, st, e);
         RasterArgs a{};
-        a.views = P<DevView>(c->d_views);
+        a.views = c->p_views;
         a.n_views = nv;
         a.max_tiles = max_tiles;
         a.tranges = P<int2>(c->d_tranges);
@@ -890,8 +922,8 @@ void s3r_destroy(s3r_ctx* c)
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
     Buf* bufs[] = {&c->d_nw, &c->d_nb, &c->d_temb, &c->d_cemb, &c->d_recmu, &c->d_toff,
-                   &c->d_wmo, &c->d_wrot, &c->d_views, &c->d_times, &c->d_tidx, &c->d_counts, &c->d_lb, &c->d_ticket,
-                   &c->d_ctr, &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
+                   &c->d_wmo, &c->d_wrot, &c->d_zero, &c->d_up, &c->d_tidx, &c->d_lb,
+                   &c->d_rec, &c->d_dkey, &c->d_gidx, &c->d_sortk[0], &c->d_sortk[1],
                    &c->d_sortv[0], &c->d_sortv[1], &c->d_recs, &c->d_rects, &c->d_lists,
                    &c->d_tlists, &c->d_tranges, &c->d_train_T, &c->d_train_n, &c->d_sgrads,
                    &c->d_cots,
@@ -1270,7 +1302,7 @@ int s3r_dump_intermediates(s3r_ctx* c, int32_t vi, const s3r_debug* dbg, void* s
         if ((long long)run != d.n_pairs)
             return fail(c, S3R_ECUDA, "dump: tile lists hold %u pairs, expected %lld", run, d.n_pairs);
         CU(cudaMemcpyAsync(toff, h.data(), (size_t)nt * 4, cudaMemcpyHostToDevice, st));
-        launch_dbg_tile_pairs(P<DevView>(c->d_views), vi, nt, P<uint32_t>(c->d_tlists),
+        launch_dbg_tile_pairs(c->p_views, vi, nt, P<uint32_t>(c->d_tlists),
                               P<int2>(c->d_tranges), toff, order,
                               c->last_debug ? P<int32_t>(c->d_gidx) : nullptr, dbg->pair_tile,
                               dbg->pair_gauss, dbg->ranges, st);
@@ -1409,7 +1441,7 @@ int s3r_render_backward(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, 
     for (int v = 0; v < nv; ++v) h[v] = s3r_cot{cots[v].rgb, cots[v].depth, cots[v].final_T};
     if (nv) CU(cudaMemcpyAsync(c->d_cots.p, h, nv * sizeof(s3r_cot), cudaMemcpyHostToDevice, st));
     BackwardArgs a{};
-    a.views = P<DevView>(c->d_views);
+    a.views = c->p_views;
     a.n_views = nv;
     a.cots = P<s3r_cot>(c->d_cots);
     a.tranges = P<int2>(c->d_tranges);
