@@ -110,7 +110,7 @@ __device__ __forceinline__ void merge_sort(const unsigned long long* __restrict_
     }
 }
 
-__global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict__ views,
+__global__ void __launch_bounds__(SMT) k_small_sortbin(DevView* __restrict__ views,
                                                        const unsigned long long* __restrict__ dkey,
                                                        const float4* __restrict__ rec,
                                                        unsigned long long* __restrict__ keys_out,
@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
                                                        float4* __restrict__ rec_sorted,
                                                        uint2* __restrict__ rect_sorted,
                                                        uint32_t* __restrict__ tlists,
-                                                       int2* __restrict__ tranges)
+                                                       int2* __restrict__ tranges,
+                                                       SmallPlan sp)
 {
     static_assert(SMALL_MAX == 2 * SMT, "two elements per thread");
     __shared__ unsigned long long s_key[SMALL_MAX];
@@ -126,10 +127,28 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
     __shared__ uint2 s_rect[SMALL_MAX];
     __shared__ int s_cnt[SMALL_TILES];
     __shared__ int s_w[SMW];
-    const DevView& V = views[blockIdx.x];
+    DevView& V = views[blockIdx.x];
     if (!V.small) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n = (int)V.n_rendered;
+    int n;
+    if (sp.ctr) {
+        // self-planned view (k_plan_bins' job for this view): its splat count,
+        // the capacity check, the stats copy
+        const ViewCounters k = sp.ctr[blockIdx.x];
+        long long nr = (long long)k.n_rendered;
+        if (nr > sp.cap_rendered || !small_view(nr, V.ntiles)) {
+            nr = 0;
+            if (tid == 0) atomicOr(sp.err, ERR_CAPACITY);
+        }
+        n = (int)nr;
+        if (tid == 0) {
+            sp.h_ctr[blockIdx.x] = k;
+            V.n_rendered = nr;
+            V.n_pairs = nr ? (long long)k.n_pairs : 0;
+        }
+    } else {
+        n = (int)V.n_rendered;
+    }
     const long long base = V.cap_off;
     // ---- depth order: (key, slot) sorted in registers / shared memory
     if (n <= SMT) merge_sort<1>(dkey, base, n, s_key, s_idx);
@@ -221,14 +240,14 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(const DevView* __restrict
 
 }  // namespace
 
-void launch_small_sortbin(const DevView* views, int n_views, const unsigned long long* dkey,
+void launch_small_sortbin(DevView* views, int n_views, const unsigned long long* dkey,
                           const float4* rec, unsigned long long* keys_out, uint32_t* order_out,
                           float4* rec_sorted, uint2* rect_sorted, uint32_t* tlists,
-                          int2* tranges, cudaStream_t st)
+                          int2* tranges, const SmallPlan& sp, cudaStream_t st)
 {
     if (n_views == 0) return;
     k_small_sortbin<<<n_views, SMT, 0, st>>>(views, dkey, rec, keys_out, order_out, rec_sorted,
-                                             rect_sorted, tlists, tranges);
+                                             rect_sorted, tlists, tranges, sp);
 }
 
 }  // namespace s3r

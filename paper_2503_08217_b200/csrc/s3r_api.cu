@@ -453,6 +453,15 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         d.pix_off = total_px;
         total_px += (long long)d.W * d.H;
     }
+    // capacity mode with every view small by reservation: k_small_sortbin plans
+    // its own view from K2's counters (no k_plan_bins launch); each view gets a
+    // fixed tile-list area of SMALL_WORK entries
+    const bool self_plan = capm && small_view(c->cap.rendered_view, max_tiles);
+    if (self_plan)
+        for (int v = 0; v < nv; ++v) {
+            c->hv[v].small = 1;
+            c->hv[v].tlist_off = (long long)v * SMALL_WORK;
+        }
     if (c->training) {
         if ((rc = ensure(c, c->d_train_T, (size_t)std::max(total_px, 1ll) * 4))) return rc;
         if ((rc = ensure(c, c->d_train_n, (size_t)std::max(total_px, 1ll) * 4))) return rc;
@@ -663,6 +672,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         for (int v = 0; v < nv; ++v) any_small = any_small || small_view(0, c->hv[v].ntiles);
         all_small = small_view(max_r, max_tiles);
         if (all_small) dtiles = 0;
+        if (self_plan) total_tlist = (long long)std::max(nv, 1) * SMALL_WORK;
         PlanCaps pc;
         pc.rendered_view = max_r;
         pc.bin_pairs = total_pairs;
@@ -671,9 +681,10 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         pc.bin_chunk = bin_chunk();
         pc.sort_tile = stile;
         c->cap_h_ctr = h_ctr;
-        launch_plan_bins(c->p_views, nv, c->p_ctr, P<Seg>(c->d_dsegs),
-                         P<int>(c->d_dtile0), pc, (ViewCounters*)mapped(c, h_ctr),
-                         P<uint32_t>(c->d_err), st);
+        if (!self_plan)
+            launch_plan_bins(c->p_views, nv, c->p_ctr, P<Seg>(c->d_dsegs),
+                             P<int>(c->d_dtile0), pc, (ViewCounters*)mapped(c, h_ctr),
+                             P<uint32_t>(c->d_err), st);
         c->cap_pending = true;
     } else {
         if (nv) launch_readback(mapped(c, h_ctr), c->p_ctr, nv * sizeof(ViewCounters), st);
@@ -793,11 +804,18 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     if (any_small && nv) {
         StageEvent e;
         ev_begin(c, S3R_STAGE_DEPTH_SORT, st, e);
+        SmallPlan sp{};
+        if (self_plan) {
+            sp.ctr = c->p_ctr;
+            sp.h_ctr = (ViewCounters*)mapped(c, h_ctr);
+            sp.err = P<uint32_t>(c->d_err);
+            sp.cap_rendered = c->cap.rendered_view;
+        }
         launch_small_sortbin(c->p_views, nv, P<unsigned long long>(c->d_dkey),
                              P<float4>(c->d_rec), P<unsigned long long>(c->d_sortk[c->final_order]),
                              P<uint32_t>(c->d_sortv[c->final_order]), P<float4>(c->d_recs),
                              P<uint2>(c->d_rects), P<uint32_t>(c->d_tlists),
-                             P<int2>(c->d_tranges), st);
+                             P<int2>(c->d_tranges), sp, st);
         ev_end(c, st, e);
     }
     // ================= K5a: depth sort: 8-bit LSD passes over (depth << gbits | index),

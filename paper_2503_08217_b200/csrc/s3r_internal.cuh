@@ -286,11 +286,19 @@ void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
                 const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
                 uint32_t* tlists, int2* tranges, cudaStream_t st);
 // Debug: the per-tile lists of view vi as (tile, Gaussian) pairs + [start,end) ranges.
-// a4 of the small views of a batch in one CTA each (k_small.cu)
-void launch_small_sortbin(const DevView* views, int n_views, const unsigned long long* dkey,
+// a4 of the small views of a batch in one CTA each (k_small.cu).  With
+// sp.ctr set (capacity mode, every view small by reservation) each CTA also
+// plans its view from K2's counters, in place of k_plan_bins.
+struct SmallPlan {
+    const ViewCounters* ctr = nullptr;
+    ViewCounters* h_ctr = nullptr;          // mapped copy for s3r_get_stats
+    uint32_t* err = nullptr;
+    long long cap_rendered = 0;
+};
+void launch_small_sortbin(DevView* views, int n_views, const unsigned long long* dkey,
                           const float4* rec, unsigned long long* keys_out, uint32_t* order_out,
                           float4* rec_sorted, uint2* rect_sorted, uint32_t* tlists,
-                          int2* tranges, cudaStream_t st);
+                          int2* tranges, const SmallPlan& sp, cudaStream_t st);
 void launch_dbg_tile_pairs(const DevView* views, int vi, int ntiles, const uint32_t* tlists,
                            const int2* tranges, const uint32_t* toff, const uint32_t* order,
                            const int32_t* gidx, int32_t* tile_out, int32_t* gauss_out,

@@ -103,6 +103,44 @@ def test_capacity_overflow_renders_empty_and_reports(dev):
         b.close()
 
 
+def test_self_planned_small_views(dev):
+    """Capacity mode whose reservation makes every view small (C1): the one-CTA
+    kernel plans its own view (no k_plan_bins); bit-identical to the
+    synchronous mode, and a view above the reserved splat count renders empty
+    with S3R_ECAPACITY."""
+    scene, (v0,) = sg.make_toy()
+    import dataclasses
+    views = [v0, dataclasses.replace(v0, lod_seed=5), dataclasses.replace(v0, lod_seed=9)]
+    a, b = s3r.Context(0), s3r.Context(0)
+    try:
+        tabs = list(s3r.view_tables(a, views))
+        oa = _render(a, s3r.DeviceScene.from_numpy(scene), views, tabs, scene.n)
+        sa = [a.stats(i) for i in range(len(views))]
+        need = a.capacity_from_last(1.0)
+        assert need["rendered_view"] <= 2048
+        b.set_capacity(need)
+        ob = _render(b, s3r.DeviceScene.from_numpy(scene), views, tabs, scene.n)
+        assert b.check() == 0
+        for x, y in zip(oa, ob):
+            for k in KEYS:
+                assert torch.equal(x[k], y[k]), k
+        sb = [b.stats(i) for i in range(len(views))]
+        for x, y in zip(sa, sb):
+            for k in ("n_temporal", "n_visible", "n_rendered", "n_pairs"):
+                assert x[k] == y[k], k
+        big = max(range(len(views)), key=lambda i: sa[i]["n_rendered"])
+        b.set_capacity(dict(need, rendered_view=sa[big]["n_rendered"] - 1))
+        ob = _render(b, s3r.DeviceScene.from_numpy(scene), views, tabs, scene.n)
+        assert b.check() == s3r.S3R_ECAPACITY
+        assert float(ob[big]["rgb"].abs().max()) == 0.0
+        for i in range(len(views)):
+            if sa[i]["n_rendered"] < sa[big]["n_rendered"]:
+                assert torch.equal(oa[i]["rgb"], ob[i]["rgb"]), i
+    finally:
+        a.close()
+        b.close()
+
+
 @pytest.mark.parametrize("case", ["toy", "street"])
 def test_cuda_graph_replay(dev, case):
     """A capacity-mode render captured once in a CUDA graph and replayed equals
