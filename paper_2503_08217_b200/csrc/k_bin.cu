@@ -182,9 +182,11 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
 // kept), and appends them to the tile's list.  Tile t (local index in the
 // supertile, S*S of them) owns [S*S*start + t*len, +len) of the view's tile-list
 // area, len = supertile list length, so no count pass is needed.
-#ifndef S3R_SCATTER_MASK
-#define S3R_SCATTER_MASK 0   // 1: lane-per-splat scatter with per-bin lane masks (A/B: bin 1.182 vs 1.154 ms, off)
-#endif
+// Scatter per view: a view whose splats touch few supertiles on average
+// (DevView::scat_mask, set when bin pairs < SCAT_MASK_RATIO = 2 x splats) takes the
+// lane-per-splat form with per-bin lane masks; others the warp-per-splat form
+// (A/B, bin stage: C2 (1.5 bins per splat) 0.495 -> 0.349 ms with masks, C4
+// (2.8) 5.36 -> 4.88, C3 (3.9) 0.94 -> 1.07)
 #ifndef S3R_XMASK
 #define S3R_XMASK 1    // 4 x 4 supertiles: per-entry tile masks + 16 ballots
 #endif
@@ -308,6 +310,7 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
 // chunk's pairs for one bin follow the chunk's scanned base; inside the chunk
 // warp w's pairs follow warps < w (per-warp counts, scanned in shared memory);
 // inside a warp the splats are taken one at a time in rank order.
+template <bool MASK>
 __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ views,
                                                     const uint2* __restrict__ rect_sorted,
                                                     const uint32_t* __restrict__ cnt,
@@ -317,12 +320,14 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
     const DevView& V = views[blockIdx.y];
     const int c = blockIdx.x;
     const long long r0 = (long long)c * KCHUNK;
-    if (V.small || r0 >= V.n_rendered || V.nbins == 0) return;
+    // one launch per form (its own shared-memory size); a CTA of the other
+    // form's views exits
+    if (V.small || r0 >= V.n_rendered || V.nbins == 0 || (V.scat_mask != 0) != MASK) return;
     const int nb = V.nbins, sh = V.sshift, sx = V.STX;
     uint32_t* s_base = s_dyn;                                    // [nb] chunk base per bin
     uint32_t* s_w = s_dyn + nb;                                  // [KWARPS][nb]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < (1 + S3R_SCATTER_MASK) * KWARPS * nb; i += KT) s_w[i] = 0;
+    for (int i = tid; i < (MASK ? 2 : 1) * KWARPS * nb; i += KT) s_w[i] = 0;
     for (int b = tid; b < nb; b += KT) s_base[b] = cnt[V.cnt_off + (long long)b * V.nchunks + c];
     __syncthreads();
     const long long n_r = V.n_rendered;
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
     }
     __syncthreads();
     uint32_t* out = lists + V.pair_off;
-#if S3R_SCATTER_MASK
+    if (MASK) {
     // scatter: the warp takes its splats 32 at a time, one per lane (lane order
     // = rank order).  Every lane ORs its bit into the bin mask of each bin it
     // touches; a pair's position is the bin's running count + the number of
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
             }
         __syncwarp();
     }
-#else
+    } else {
     // scatter: the warp walks its splats in rank order
     for (int i = 0; i < wn; ++i) {
         const long long r = wr0 + i;
@@ -411,7 +416,7 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
         }
         __syncwarp();
     }
-#endif
+    }
 }
 
 // ------------------------------------------------------------------ debug
@@ -457,18 +462,23 @@ void launch_permute(const DevView* views, int n_views, long long max_rendered,
 
 void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
                 const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
-                uint32_t* tlists, int2* tranges, cudaStream_t st)
+                uint32_t* tlists, int2* tranges, int scat, cudaStream_t st)
 {
     if (n_views == 0) return;
     dim3 grid(max_chunks, n_views);
     if (max_chunks) k_bin_count<<<grid, KT, (size_t)max_bins * 4, st>>>(views, rect_sorted, cnt);
     k_bin_scan<<<n_views, 1024, 0, st>>>(views, cnt, ranges);
     if (max_chunks) {
-        const size_t smem = (size_t)max_bins * 4 * (1 + (1 + S3R_SCATTER_MASK) * KWARPS);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        k_bin_scatter<<<grid, KT, smem, st>>>(views, rect_sorted, cnt, lists);
+        const size_t smem0 = (size_t)max_bins * 4 * (1 + KWARPS);
+        const size_t smem1 = (size_t)max_bins * 4 * (1 + 2 * KWARPS);
+        if (smem0 > 48 * 1024)
+            cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem0);
+        if (smem1 > 48 * 1024)
+            cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem1);
+        if (scat != 1) k_bin_scatter<false><<<grid, KT, smem0, st>>>(views, rect_sorted, cnt, lists);
+        if (scat != 0) k_bin_scatter<true><<<grid, KT, smem1, st>>>(views, rect_sorted, cnt, lists);
     }
     k_bin_expand<<<dim3(max_bins, n_views), XT, 0, st>>>(views, rect_sorted, lists, ranges, tlists,
                                                        tranges);

@@ -9,6 +9,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANT_SETS = {
+    "r2scat": {
+        "base": [],
+        "scatmask": ["S3R_SCATTER_MASK=1"],
+    },
     "r2occ": {
         "base": [],
         "m18rb192": ["S3R_RASTER_MINB=18", "S3R_RASTER_RB=192"],
@@ -244,7 +248,8 @@ if __name__ == "__main__":
             if name.startswith("ov"):
                 env["S3R_OVERLAP"] = "1"
             r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3",
-                                "--no-e2e", "--no-cpu-baseline", "--pool", "1"] +
+                                "--no-e2e", "--no-cpu-baseline", "--pool", "1",
+                                "--config", os.environ.get("AB_CONFIG", "av2")] +
                                (["--no-train", "--no-neurf", "--no-conventional", "--no-fast-exp"]
                                 if os.environ.get("AB_FWD_ONLY") else []), cwd=ROOT,
                                env=env, capture_output=True, text=True, timeout=400)
