@@ -493,6 +493,24 @@ def cpu_baseline(cfg_name, procs=None):
                       f"{dt:.1f} s wall"}
 
 
+def view_shards(global_views: int, world: int, scaling: str, per_rank=None):
+    """(offset, count) of every rank's views and the step's global view count.
+    strong: the configured global batch in contiguous shards of the (frame,
+    camera)-sorted views (same-t views co-locate; the first ranks take one
+    more when it does not divide); weak: `per_rank` (default the global batch)
+    views on every rank."""
+    if scaling == "weak":
+        per = per_rank if per_rank is not None else global_views
+        return [(r * per, per) for r in range(world)], per * world
+    base, extra = divmod(global_views, world)
+    shards, off = [], 0
+    for r in range(world):
+        cnt = base + (1 if r < extra else 0)
+        shards.append((off, cnt))
+        off += cnt
+    return shards, global_views
+
+
 def relaunch(n: int) -> int:
     """`bench.py --gpus N` outside torchrun: run this command again as N ranks
     under torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous)."""
@@ -551,18 +569,7 @@ def main():
     # global batch of the config (BASELINE: C3 64 views, C4 256, C2 all 100 frames)
     global_views = {"toy": 1, "street": sg.CONFIGS["street"].n_views, "av2": 64,
                     "drive": sg.CONFIGS["drive"].n_views}[args.config]
-    if args.scaling == "weak":
-        per = args.views if args.views is not None else global_views
-        shards = [(r * per, per) for r in range(world)]
-        global_views = per * world
-    else:
-        # contiguous shards of the (frame, camera)-sorted batch: same-t views co-locate
-        base, extra = divmod(global_views, world)
-        shards, off = [], 0
-        for r in range(world):
-            cnt = base + (1 if r < extra else 0)
-            shards.append((off, cnt))
-            off += cnt
+    shards, global_views = view_shards(global_views, world, args.scaling, args.views)
     args.views = shards[rank][1]
     GLOBAL["views"] = global_views
     if args.views < 1:

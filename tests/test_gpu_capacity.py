@@ -184,3 +184,37 @@ def test_cuda_graph_replay(dev, case):
         assert st["n_rendered"] > 0
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["jitter", "fast_exp", "counters"])
+def test_capacity_mode_with_options(dev, mode):
+    """The render options that the capacity mode keeps (LOD noisy offset, SFU
+    exponential, work counters) give the synchronous mode's outputs bit for bit
+    (and, for the counters, the same E_alg / E_exec per view)."""
+    scene, views = sg.make_random_dynamic(34, 5000, 3, 300, 190, 131, 6, lod=(6.0, 0.4, 8.0))
+    a, b = s3r.Context(0), s3r.Context(0)
+    try:
+        for c in (a, b):
+            if mode == "jitter":
+                c.set_lod_jitter(0.3, 0.2, 0.6)
+            elif mode == "fast_exp":
+                c.set_fast_exp(True)
+            else:
+                c.set_counters(True)
+        tabs = list(s3r.view_tables(a, views))
+        oa = _render(a, s3r.DeviceScene.from_numpy(scene), views, tabs, scene.n)
+        sa = [a.stats(i) for i in range(len(views))]
+        b.set_capacity(a.capacity_from_last(1.2))
+        ob = _render(b, s3r.DeviceScene.from_numpy(scene), views, tabs, scene.n)
+        assert b.check() == 0
+        sb = [b.stats(i) for i in range(len(views))]
+        for x, y in zip(oa, ob):
+            for k in KEYS:
+                assert torch.equal(x[k], y[k]), k
+        keys = STATS + (("n_blend_evals", "n_blend_exec") if mode == "counters" else ())
+        for x, y in zip(sa, sb):
+            for k in keys:
+                assert x[k] == y[k], k
+    finally:
+        a.close()
+        b.close()

@@ -128,3 +128,22 @@ def test_world2_gradient_allreduce_matches_single_process(tmp_path):
         got = np.load(tmp_path / f"g_{r}.npy")
         assert np.allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
         assert np.all(np.load(tmp_path / f"t_{r}.npy") == r)
+
+
+def test_bench_view_shards():
+    """bench.py's split of a step's views over ranks (BASELINE C3: 64 views over
+    1/2/4/8 GPUs; C4: 256 at 32 per rank): contiguous, complete, balanced."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for n, g in ((64, 1), (64, 2), (64, 4), (64, 8), (256, 8), (100, 8), (7, 3)):
+        shards, tot = bench.view_shards(n, g, "strong")
+        assert tot == n and len(shards) == g
+        assert [o for o, _ in shards] == list(np.cumsum([0] + [c for _, c in shards[:-1]]))
+        assert sum(c for _, c in shards) == n
+        assert max(c for _, c in shards) - min(c for _, c in shards) <= 1
+    assert bench.view_shards(256, 8, "strong")[0][3] == (96, 32)
+    shards, tot = bench.view_shards(64, 4, "weak", 16)
+    assert tot == 64 and shards == [(0, 16), (16, 16), (32, 16), (48, 16)]
