@@ -1061,7 +1061,7 @@ int s3r_render_batch(s3r_ctx* c, const s3r_scene* scene, const s3r_view* views, 
     // compute-bound rasterization.  Modes whose state must describe one batch
     // (debug dumps, counters, training, NeurF) render in one piece.
     const bool split = c->overlap && n_views >= 16 && !c->debug && !c->counters &&
-                       !c->training && !c->neurf;
+                       !c->training && !c->neurf && !c->cap_on;   // (the capacity mode has no host syncs to hide)
     if (!split) return render_impl(c, scene, views, n_views, outs, st);
     CU(cudaSetDevice(c->device));
     if (!c->twin) {
