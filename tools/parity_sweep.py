@@ -1,6 +1,6 @@
 """Full-size parity sweep: the bench's batches (C3 av2, C4 drive, C2 street, in
 the launch configuration bench.py times: all of a config's views in one
-s3r_render_batch) against the CPU oracle on K sampled views each, element by
+s3r_render_batch) against the CPU oracle on K sampled views each (C2: all 100), element by
 element — temporal list, fp32 keys, decisions, rectangles, M_t, depth order,
 (tile, Gaussian) pairs, tile ranges, images.  The oracle renders run in forked
 worker processes on the host cores, each comparing its view against the GPU
@@ -27,7 +27,7 @@ def _compare(vi):
     import oracle
     scene, view, table, gpu = _G["scene"], _G["views"][vi], _G["tabs"][vi], _G["gpu"][vi]
     t0 = time.perf_counter()
-    o = oracle.render_view(scene, view, "f32", table=table)
+    o = oracle.render_view(scene, view, "f32")       # the oracle composes its own table
     dt = time.perf_counter() - t0
     d, st, out = gpu["dump"], gpu["stats"], gpu["out"]
     ti = o["temporal_idx"]
@@ -65,7 +65,7 @@ def main():
     import torch
     import oracle
     from paper_2503_08217_b200 import s3r, scenegen as sg
-    out_path = os.path.join(ROOT, "profiles", "r01_parity_sweep.json")
+    out_path = os.path.join(ROOT, "profiles", "r02_parity_sweep.json")
     k_views = 8
     args = sys.argv[1:]
     if "--views" in args:
@@ -90,7 +90,8 @@ def main():
         assert ctx.check() == 0
         gpu_s = time.perf_counter() - t0
         rng = np.random.default_rng(7)
-        pick = sorted(rng.choice(len(views), min(k_views, len(views)), replace=False).tolist())
+        kv = len(views) if cfg == "street" else k_views      # C2: every view
+        pick = sorted(rng.choice(len(views), min(kv, len(views)), replace=False).tolist())
         gpu = {}
         for vi in pick:
             v = views[vi]
