@@ -218,3 +218,38 @@ def test_capacity_mode_with_options(dev, mode):
     finally:
         a.close()
         b.close()
+
+
+def test_capacity_mode_edge_cases(dev):
+    """Capacity mode on the degenerate batches of test_edge_cases: an empty
+    scene, a 1x1 view whose Gaussians are all filtered out by time, an empty
+    view list; and graph capture without the capacity mode is refused."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from helpers import make_scene, make_view
+    cap = dict(records=64, rendered_view=64, bin_pairs=64, tile_entries=1024, temporal_view=64)
+    c = s3r.Context(0)
+    try:
+        c.set_capacity(cap)
+        s0 = make_scene(np.zeros((0, 3)), 0.1)
+        v = make_view(64.0, 32.0, 40, 33)
+        tabs = list(s3r.view_tables(c, [v]))
+        o = _render(c, s3r.DeviceScene.from_numpy(s0), [v], tabs, 0)
+        assert c.check() == 0
+        assert float(o[0]["rgb"].abs().max()) == 0.0 and torch.all(o[0]["final_T"] == 1.0)
+        s1 = make_scene([[0, 0, 3.0], [0.1, 0, 4.0]], 0.2, vis=[[0.5, 0.6], [0.7, 0.9]])
+        v1 = make_view(64.0, 0.0, 1, 1, t=-0.0)
+        tabs = list(s3r.view_tables(c, [v1]))
+        o = _render(c, s3r.DeviceScene.from_numpy(s1), [v1], tabs, s1.n)
+        assert c.check() == 0 and c.stats(0)["n_temporal"] == 0
+        assert float(o[0]["final_T"].min()) == 1.0
+        assert c.render_batch(s3r.DeviceScene.from_numpy(s1), [], [], []) == 0
+        c.set_capacity(None)
+        g = torch.cuda.CUDAGraph()
+        ds = s3r.DeviceScene.from_numpy(s1)
+        outs = s3r.alloc_outputs([v1])
+        with pytest.raises(s3r.S3RError):
+            with torch.cuda.graph(g):
+                c.render_batch(ds, [v1], tabs, outs)
+    finally:
+        c.close()
