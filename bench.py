@@ -754,6 +754,10 @@ def main():
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
                 "alg_bytes_per_launch": bytes_[dom], "traffic": None}
+        if args.config == "toy":
+            roof["note"] = ("C1 (1,024 Gaussians, 16 tiles, one view per step) is latency-bound "
+                            "in every kernel; the HBM fraction of its largest stage is not a "
+                            "meaningful efficiency measure (DESIGN.md §10c)")
 
     # ---------------- config 5: training step (forward + MSE + backward [+ grad all-reduce])
     train = None
