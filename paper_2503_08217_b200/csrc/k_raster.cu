@@ -234,14 +234,16 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
             const float2 dy = __fadd2_rn(f2(q0.y), nfpy[P]);
             const float2 c1 = __ffma2_rn(f2(q1.z), dy, f2(b1));
             const float2 e2r = __ffma2_rn(dy, c1, f2(a2));
-            const float2 e2 = make_float2(fminf(0.0f, e2r.x), fminf(0.0f, e2r.y));
             // A dead pixel (T < 1e-4) or a flushed exp2 (e2 < -24, s3r_exp2 = 0)
             // has alpha = 0, which leaves C, D and T bit-identical
             // (fma(c, 0, C) == C, T - 0 == T): such evaluations are skipped
             // (both of the pair) or get alpha = 0 (one of the pair).
             const bool livx = !LIVE || T[P].x >= 1e-4f, livy = !LIVE || T[P].y >= 1e-4f;
-            const bool onx = (e2.x >= S3R_FLUSH_E2) && livx;
-            const bool ony = (e2.y >= S3R_FLUSH_E2) && livy;
+            // the flush test min(0, e2) >= F is !(e2 < F) for F < 0 (a NaN
+            // passes, as fminf(0, NaN) = 0 does), so the clamp min(0, e2) is
+            // taken inside the branch only (A/B, C3: raster 14.66 vs 14.72 ms)
+            const bool onx = !(e2r.x < S3R_FLUSH_E2) && livx;
+            const bool ony = !(e2r.y < S3R_FLUSH_E2) && livy;
             if (TRAIN && !COUNT) {
                 // the backward's per-pixel bound: the last entry the pixel
                 // was live at (its terminating one, or a later entry that
@@ -254,6 +256,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
 #else
             if (onx || ony) {
 #endif
+                const float2 e2 = make_float2(fminf(0.0f, e2r.x), fminf(0.0f, e2r.y));
                 const float2 og = FAST
                     ? __fmul2_rn(make_float2(ex2_sfu(e2.x), ex2_sfu(e2.y)), f2(q0.w))
                     : o_exp2_x2(e2, q0.w, c0);

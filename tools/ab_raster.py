@@ -225,6 +225,12 @@ VARIANT_SETS = {
         "pg1": ["S3R_POSE_GROUPS=1"],
         "pg8": ["S3R_POSE_GROUPS=8"],
     },
+    "lean": {
+        "base": [],
+        "lean1": ["S3R_RASTER_LEAN=1"],
+        "lean3": ["S3R_RASTER_LEAN=3"],
+        "lean7": ["S3R_RASTER_LEAN=7"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
