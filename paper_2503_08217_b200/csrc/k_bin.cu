@@ -188,7 +188,9 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
 // (A/B, bin stage: C2 (1.5 bins per splat) 0.495 -> 0.349 ms with masks, C4
 // (2.8) 5.36 -> 4.88, C3 (3.9) 0.94 -> 1.07)
 #ifndef S3R_XMASK
-#define S3R_XMASK 1    // 4 x 4 supertiles: per-entry tile masks + 16 ballots
+#define S3R_XMASK 1    // 4 x 4 supertiles: per-entry tile masks + 16 ballots (A/B, bin stage with the
+                       // ballots staged through shared memory and predicated stores: C3 0.957 -> 0.880 ms,
+                       // C2 0.390 -> 0.352 ms against per-tile lane-select counts and branches)
 #endif
 #ifndef S3R_SCAT2D
 #define S3R_SCAT2D 1   // scatter: 8 x 4 lane grid over a splat's bins (A/B: bin 1.06 vs 1.15 ms with k / bw, k % bw)
@@ -225,9 +227,12 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
     if (V.sshift == 2) {
         // 4 x 4 supertile: each thread takes one entry and forms the 16-bit mask
         // of the supertile's tiles its rectangle contains (tile t = 4 ty + tx
-        // local); per tile one ballot gives the warp's members in list order,
-        // and per-warp counts exchanged through shared memory order the warps.
+        // local); per tile one ballot gives the warp's members in list order.
+        // The warp's 16 ballots go to shared memory once (lane t then counts
+        // tile t), per-warp counts order the warps, and each tile's members are
+        // stored with a predicated store at base + rank within the warp.
         __shared__ int s_wc[XT / 32][16];
+        __shared__ __align__(16) unsigned s_bal[XT / 32][16];
         const unsigned lt = (1u << lane) - 1u;
         for (int base = rg.x; base < rg.y; base += XT) {
             const int e = base + tid;
@@ -240,25 +245,42 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
             }
             unsigned bal[16];
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                bal[t] = __ballot_sync(0xffffffffu, (m >> t) & 1u);
-                if (lane == t) s_wc[warp][t] = __popc(bal[t]);
+            for (int t = 0; t < 16; ++t)     // one bit test + one vote per tile
+                asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 x;\n\tand.b32 x, %1, %2;\n\t"
+                             "setp.ne.b32 p, x, 0;\n\tvote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+                             : "=r"(bal[t]) : "r"(m), "r"(1u << t));
+            if (lane == 0) {
+#pragma unroll
+                for (int t = 0; t < 16; t += 4)
+                    *reinterpret_cast<uint4*>(&s_bal[warp][t]) =
+                        make_uint4(bal[t], bal[t + 1], bal[t + 2], bal[t + 3]);
             }
+            __syncwarp();
+            if (lane < 16) s_wc[warp][lane] = __popc(s_bal[warp][lane]);
             __syncthreads();
-            int myoff = 0, mytot = 0;          // lane t < 16: tile t's base for this warp
+            // lane t < 16: tile t's list position for this warp's members
+            uint32_t myoff = 0;
+            int mytot = 0;
             if (lane < 16) {
-                myoff = s_tcnt[lane];
+                int o = s_tcnt[lane];
 #pragma unroll
                 for (int w = 0; w < XT / 32; ++w) {
                     const int c = s_wc[w][lane];
-                    if (w < warp) myoff += c;
+                    if (w < warp) o += c;
                     mytot += c;
                 }
+                myoff = (uint32_t)(lane * len + o);
             }
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-                const int off = __shfl_sync(0xffffffffu, myoff, t);
-                if ((m >> t) & 1u) out[(long long)t * len + off + __popc(bal[t] & lt)] = r;
+                const uint32_t off = __shfl_sync(0xffffffffu, myoff, t);
+                const uint32_t pos = off + __popc(bal[t] & lt);
+                // out[pos] = r if the entry has tile t (one wide multiply-add for
+                // the address, one predicated store)
+                asm volatile("{\n\t.reg .pred q;\n\t.reg .b32 x;\n\t.reg .b64 a;\n\t"
+                             "and.b32 x, %3, %4;\n\tsetp.ne.b32 q, x, 0;\n\t"
+                             "mad.wide.u32 a, %1, 4, %0;\n\t@q st.global.b32 [a], %2;\n\t}"
+                             ::"l"(out), "r"(pos), "r"(r), "r"(m), "r"(1u << t) : "memory");
             }
             __syncthreads();
             if (warp == 0 && lane < 16) s_tcnt[lane] += mytot;

@@ -231,6 +231,10 @@ VARIANT_SETS = {
         "lean3": ["S3R_RASTER_LEAN=3"],
         "lean7": ["S3R_RASTER_LEAN=7"],
     },
+    "xm": {
+        "base": [],
+        "xm2": ["S3R_XMASK=2"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
