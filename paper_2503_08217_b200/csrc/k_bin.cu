@@ -182,18 +182,14 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
 // kept), and appends them to the tile's list.  Tile t (local index in the
 // supertile, S*S of them) owns [S*S*start + t*len, +len) of the view's tile-list
 // area, len = supertile list length, so no count pass is needed.
-// Scatter per view: a view whose splats touch few supertiles on average
-// (DevView::scat_mask, set when bin pairs < SCAT_MASK_RATIO = 2 x splats) takes the
-// lane-per-splat form with per-bin lane masks; others the warp-per-splat form
-// (A/B, bin stage: C2 (1.5 bins per splat) 0.495 -> 0.349 ms with masks, C4
-// (2.8) 5.36 -> 4.88, C3 (3.9) 0.94 -> 1.07)
+#ifndef S3R_SCAT_SMALL
+#define S3R_SCAT_SMALL 16   // scatter: a splat with more bins is taken by the whole warp
+#endif
+constexpr int SCAT_SMALL = S3R_SCAT_SMALL;
 #ifndef S3R_XMASK
 #define S3R_XMASK 1    // 4 x 4 supertiles: per-entry tile masks + 16 ballots (A/B, bin stage with the
                        // ballots staged through shared memory and predicated stores: C3 0.957 -> 0.880 ms,
                        // C2 0.390 -> 0.352 ms against per-tile lane-select counts and branches)
-#endif
-#ifndef S3R_SCAT2D
-#define S3R_SCAT2D 1   // scatter: 8 x 4 lane grid over a splat's bins (A/B: bin 1.06 vs 1.15 ms with k / bw, k % bw)
 #endif
 #ifndef S3R_XT
 #define S3R_XT 128     // A/B (mask expansion): bin 1.025 ms vs 1.059 at 256
@@ -331,8 +327,17 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
 // Writes every (bin, r) pair's rank r at its final position.  Stability: a
 // chunk's pairs for one bin follow the chunk's scanned base; inside the chunk
 // warp w's pairs follow warps < w (per-warp counts, scanned in shared memory);
-// inside a warp the splats are taken one at a time in rank order.
-template <bool MASK>
+// inside a warp the splats are taken 32 at a time, one per lane (lane order =
+// rank order).  Each (splat, bin) ORs the splat's lane bit into the warp's
+// mask of the bin; a pair's position is the bin's running count + the number
+// of lower lanes in the mask; the highest lane of a mask then advances the
+// running count and clears the mask.  A splat with at most SCAT_SMALL bins
+// walks its own bins (<= SCAT_SMALL iterations per lane); a larger one is taken
+// by the whole warp, lanes over its bins, so the few big splats of a view (C3:
+// 3.9 supertiles per splat on average, tails of 100+) do not serialise the warp.
+// (A/B, bin stage, against a per-view choice between this lane-per-splat form
+// without the big-splat path and a warp-per-splat form: C3 0.877 -> 0.822 ms,
+// C4 5.18 -> 4.21 ms, C2 0.352 -> 0.299 ms; SCAT_SMALL 8 / 24 / 32 within 1 %.)
 __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ views,
                                                     const uint2* __restrict__ rect_sorted,
                                                     const uint32_t* __restrict__ cnt,
@@ -342,14 +347,12 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
     const DevView& V = views[blockIdx.y];
     const int c = blockIdx.x;
     const long long r0 = (long long)c * KCHUNK;
-    // one launch per form (its own shared-memory size); a CTA of the other
-    // form's views exits
-    if (V.small || r0 >= V.n_rendered || V.nbins == 0 || (V.scat_mask != 0) != MASK) return;
+    if (V.small || r0 >= V.n_rendered || V.nbins == 0) return;
     const int nb = V.nbins, sh = V.sshift, sx = V.STX;
     uint32_t* s_base = s_dyn;                                    // [nb] chunk base per bin
-    uint32_t* s_w = s_dyn + nb;                                  // [KWARPS][nb]
+    uint32_t* s_w = s_dyn + nb;                                  // [KWARPS][nb] counts, then [KWARPS][nb] masks
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < (MASK ? 2 : 1) * KWARPS * nb; i += KT) s_w[i] = 0;
+    for (int i = tid; i < 2 * KWARPS * nb; i += KT) s_w[i] = 0;
     for (int b = tid; b < nb; b += KT) s_base[b] = cnt[V.cnt_off + (long long)b * V.nchunks + c];
     __syncthreads();
     const long long n_r = V.n_rendered;
@@ -377,13 +380,7 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
     }
     __syncthreads();
     uint32_t* out = lists + V.pair_off;
-    if (MASK) {
-    // scatter: the warp takes its splats 32 at a time, one per lane (lane order
-    // = rank order).  Every lane ORs its bit into the bin mask of each bin it
-    // touches; a pair's position is the bin's running count + the number of
-    // lower lanes in the mask; the highest lane of a mask then advances the
-    // running count and clears the mask.
-    uint32_t* wmask = s_w + KWARPS * nb + warp * nb;          // [KWARPS][nb], zeroed
+    uint32_t* wmask = s_w + KWARPS * nb + warp * nb;          // zeroed above
     const unsigned lt = (1u << lane) - 1u;
     for (int base = 0; base < wn; base += 32) {
         const int i = base + lane;
@@ -393,51 +390,57 @@ __global__ void __launch_bounds__(KT) k_bin_scatter(const DevView* __restrict__ 
             rect_of(rect_sorted[V.cap_off + wr0 + i], tx0, tx1, ty0, ty1);
             bx0 = tx0 >> sh; bx1 = tx1 >> sh; by0 = ty0 >> sh; by1 = ty1 >> sh;
         }
-        for (int by = by0; by <= by1; ++by)
-            for (int bx = bx0; bx <= bx1; ++bx) atomicOr(&wmask[by * sx + bx], 1u << lane);
-        __syncwarp();
-        for (int by = by0; by <= by1; ++by)
-            for (int bx = bx0; bx <= bx1; ++bx) {
-                const int b = by * sx + bx;
-                out[s_base[b] + mine[b] + __popc(wmask[b] & lt)] = (uint32_t)(wr0 + i);
-            }
-        __syncwarp();
-        for (int by = by0; by <= by1; ++by)
-            for (int bx = bx0; bx <= bx1; ++bx) {
-                const int b = by * sx + bx;
-                const uint32_t m = wmask[b];
-                if (lane == 31 - __clz(m)) {
-                    mine[b] += __popc(m);
-                    wmask[b] = 0u;
+        const int bw = bx1 - bx0 + 1, nbin = bw * (by1 - by0 + 1);
+        const bool big = nbin > SCAT_SMALL;
+        const unsigned bigm = __ballot_sync(0xffffffffu, big);
+        const int n_own = big ? 0 : nbin;
+        const uint32_t rr = (uint32_t)(wr0 + i);
+        // the bins of each big splat L of the warp, lanes over them
+        auto big_bins = [&](auto&& f) {
+            for (unsigned m = bigm; m; m &= m - 1) {
+                const int L = __ffs(m) - 1;
+                const int Lbx0 = __shfl_sync(0xffffffffu, bx0, L), Lby0 = __shfl_sync(0xffffffffu, by0, L);
+                const int Lbw = __shfl_sync(0xffffffffu, bw, L), Ln = __shfl_sync(0xffffffffu, nbin, L);
+                const uint32_t Lr = __shfl_sync(0xffffffffu, rr, L);
+                for (int k = lane; k < Ln; k += 32) {
+                    const int yy = k / Lbw, xx = k - yy * Lbw;
+                    f(L, (Lby0 + yy) * sx + Lbx0 + xx, Lr);
                 }
             }
-        __syncwarp();
-    }
-    } else {
-    // scatter: the warp walks its splats in rank order
-    for (int i = 0; i < wn; ++i) {
-        const long long r = wr0 + i;
-        int tx0, tx1, ty0, ty1;
-        rect_of(rect_sorted[V.cap_off + r], tx0, tx1, ty0, ty1);
-        const int bx0 = tx0 >> sh, by0 = ty0 >> sh;
-        const int bw = (tx1 >> sh) - bx0 + 1, bh = (ty1 >> sh) - by0 + 1;
-#if S3R_SCAT2D
-        // the splat's bins over the lanes as an 8 x 4 lane grid (no division)
-        for (int yy = lane >> 3; yy < bh; yy += 4) {
-            for (int xx = lane & 7; xx < bw; xx += 8) {
-                const int b = (by0 + yy) * sx + bx0 + xx;
-#else
-        for (int k = lane; k < bw * bh; k += 32) {
-            {
-                const int b = (by0 + k / bw) * sx + bx0 + k % bw;
-#endif
-                const uint32_t pos = s_base[b] + mine[b];
-                mine[b] = mine[b] + 1;
-                out[pos] = (uint32_t)r;
+        };
+        // the lane's own bins (a small splat), row-major in its rectangle
+        auto own_bins = [&](auto&& f) {
+            int xx = 0, yy = 0;
+            for (int k = 0; k < n_own; ++k) {
+                f((by0 + yy) * sx + bx0 + xx);
+                if (++xx == bw) { xx = 0; ++yy; }
             }
-        }
+        };
+        own_bins([&](int b) { atomicOr(&wmask[b], 1u << lane); });
+        big_bins([&](int L, int b, uint32_t) { atomicOr(&wmask[b], 1u << L); });
         __syncwarp();
-    }
+        own_bins([&](int b) { out[s_base[b] + mine[b] + __popc(wmask[b] & lt)] = rr; });
+        big_bins([&](int L, int b, uint32_t Lr) {
+            out[s_base[b] + mine[b] + __popc(wmask[b] & ((1u << L) - 1u))] = Lr;
+        });
+        __syncwarp();
+        // the highest member of a mask advances the bin's count (a lower member
+        // that reads the mask after it was cleared sees 0: not the highest)
+        own_bins([&](int b) {
+            const uint32_t m = wmask[b];
+            if (lane == 31 - __clz(m)) {
+                mine[b] += __popc(m);
+                wmask[b] = 0u;
+            }
+        });
+        big_bins([&](int L, int b, uint32_t) {
+            const uint32_t m = wmask[b];
+            if (L == 31 - __clz(m)) {
+                mine[b] += __popc(m);
+                wmask[b] = 0u;
+            }
+        });
+        __syncwarp();
     }
 }
 
@@ -484,23 +487,17 @@ void launch_permute(const DevView* views, int n_views, long long max_rendered,
 
 void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
                 const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
-                uint32_t* tlists, int2* tranges, int scat, cudaStream_t st)
+                uint32_t* tlists, int2* tranges, cudaStream_t st)
 {
     if (n_views == 0) return;
     dim3 grid(max_chunks, n_views);
     if (max_chunks) k_bin_count<<<grid, KT, (size_t)max_bins * 4, st>>>(views, rect_sorted, cnt);
     k_bin_scan<<<n_views, 1024, 0, st>>>(views, cnt, ranges);
     if (max_chunks) {
-        const size_t smem0 = (size_t)max_bins * 4 * (1 + KWARPS);
-        const size_t smem1 = (size_t)max_bins * 4 * (1 + 2 * KWARPS);
-        if (smem0 > 48 * 1024)
-            cudaFuncSetAttribute(k_bin_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem0);
-        if (smem1 > 48 * 1024)
-            cudaFuncSetAttribute(k_bin_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem1);
-        if (scat != 1) k_bin_scatter<false><<<grid, KT, smem0, st>>>(views, rect_sorted, cnt, lists);
-        if (scat != 0) k_bin_scatter<true><<<grid, KT, smem1, st>>>(views, rect_sorted, cnt, lists);
+        const size_t smem = (size_t)max_bins * 4 * (1 + 2 * KWARPS);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_bin_scatter<<<grid, KT, smem, st>>>(views, rect_sorted, cnt, lists);
     }
     k_bin_expand<<<dim3(max_bins, n_views), XT, 0, st>>>(views, rect_sorted, lists, ranges, tlists,
                                                        tranges);

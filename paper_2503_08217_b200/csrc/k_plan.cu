@@ -155,7 +155,6 @@ __global__ void __launch_bounds__(PLT) k_plan_bins(DevView* __restrict__ views, 
             // its empty tile ranges are written when the big path is not run)
             V.small = (fits ? sm : small_view(0, V.ntiles)) ? 1 : 0;
             V.nchunks = V.small ? 0 : (int)((nr + caps.bin_chunk - 1) / caps.bin_chunk);
-            V.scat_mask = (float)ns < SCAT_MASK_RATIO * (float)nr ? 1 : 0;
             V.cnt_off = (long long)o_cnt;
             V.pair_off = (long long)o_sp;
             V.tlist_off = (long long)o_tl;

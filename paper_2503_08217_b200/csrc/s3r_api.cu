@@ -652,8 +652,6 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     const int stile = onesweep64_tile();
     int dtiles = 0;
     bool any_small = false, all_small = true;   // views for k_small.cu / for the big path
-    int scat_forms = 2;                          // k_bin_scatter forms to launch (see launch_bin)
-    bool any_mask = false, any_plain = false;
     if ((rc = ensure(c, c->d_dsegs, (size_t)std::max(nv, 1) * sizeof(Seg)))) return rc;
     if ((rc = ensure(c, c->d_dtile0, (size_t)(nv + 1) * sizeof(int)))) return rc;
     if (capm) {
@@ -702,8 +700,6 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
             any_small = any_small || d.small;
             all_small = all_small && d.small;
             d.nchunks = d.small ? 0 : (int)((d.n_rendered + bin_chunk() - 1) / bin_chunk());
-            d.scat_mask = (float)k.n_spairs < SCAT_MASK_RATIO * (float)d.n_rendered ? 1 : 0;
-            if (!d.small && d.n_rendered) (d.scat_mask ? any_mask : any_plain) = true;
             d.cnt_off = total_cnt;
             d.pair_off = total_pairs;
             d.tlist_off = total_tlist;
@@ -729,7 +725,6 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
             if (k.n_bad) bad = true;
         }
         dtiles = dt0[nv];
-        scat_forms = any_mask && any_plain ? 2 : (any_mask ? 1 : 0);
         // device-side metadata for the rest of the batch
         Seg* h_dsegs = (Seg*)stage_alloc(c, (size_t)std::max(nv, 1) * sizeof(Seg));
         int* h_dt0 = (int*)stage_alloc(c, (size_t)(nv + 1) * sizeof(int));
@@ -856,7 +851,7 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
                        P<float4>(c->d_rec), P<float4>(c->d_recs), P<uint2>(c->d_rects), st);
         launch_bin(c->p_views, nv, max_chunks, max_bins, P<uint2>(c->d_rects),
                    P<uint32_t>(c->d_cnt), P<int2>(c->d_ranges), P<uint32_t>(c->d_lists),
-                   P<uint32_t>(c->d_tlists), P<int2>(c->d_tranges), scat_forms, st);
+                   P<uint32_t>(c->d_tlists), P<int2>(c->d_tranges), st);
         ev_end(c, st, e);
     }
     CU(cudaGetLastError());

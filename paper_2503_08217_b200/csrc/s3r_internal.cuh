@@ -134,10 +134,7 @@ struct DevView {
     int trange_off;          // offset of the view's tile ranges (ntiles entries)
     long long pix_off;       // offset of the view's pixels in the training buffers
     int small;               // a4 in one CTA (k_small.cu) instead of the sort + binning kernels
-    int scat_mask;           // k_bin_scatter: lane-per-splat form (few supertiles per splat)
 };
-// bin pairs per rendered splat below which a view scatters lane-per-splat
-constexpr float SCAT_MASK_RATIO = 2.0f;   // C2 views 1.4-2.2, C3 2.8-9.5, C4 ~2.8 (heavy tails: up to 100+ bins)
 
 // Views small enough for the one-CTA depth order + tile binning (k_small.cu):
 // at most SMALL_MAX rendered splats, SMALL_TILES tiles, and SMALL_WORK
@@ -285,10 +282,9 @@ void launch_permute(const DevView* views, int n_views, long long max_rendered,
 int bin_chunk();
 constexpr int MAX_BINS = 1024;   // supertiles per view (S grows for huge images)
 // ... then K4 expand: per-tile lists (ranks) + tile ranges from the supertile lists.
-// scat: which scatter forms to launch (0 warp-per-splat only, 1 mask only, 2 both)
 void launch_bin(const DevView* views, int n_views, int max_chunks, int max_bins,
                 const uint2* rect_sorted, uint32_t* cnt, int2* ranges, uint32_t* lists,
-                uint32_t* tlists, int2* tranges, int scat, cudaStream_t st);
+                uint32_t* tlists, int2* tranges, cudaStream_t st);
 // Debug: the per-tile lists of view vi as (tile, Gaussian) pairs + [start,end) ranges.
 // a4 of the small views of a batch in one CTA each (k_small.cu).  With
 // sp.ctr set (capacity mode, every view small by reservation) each CTA also

@@ -235,6 +235,17 @@ VARIANT_SETS = {
         "base": [],
         "xm2": ["S3R_XMASK=2"],
     },
+    "hyb": {
+        "base": [],
+        "hyb": ["S3R_SCAT_HYBRID=1"],
+        "hyb16": ["S3R_SCAT_HYBRID=1", "S3R_SCAT_SMALL=16"],
+        "hyb4": ["S3R_SCAT_HYBRID=1", "S3R_SCAT_SMALL=4"],
+    },
+    "hyb2": {
+        "hyb16": ["S3R_SCAT_HYBRID=1", "S3R_SCAT_SMALL=16"],
+        "hyb24": ["S3R_SCAT_HYBRID=1", "S3R_SCAT_SMALL=24"],
+        "hyb32": ["S3R_SCAT_HYBRID=1", "S3R_SCAT_SMALL=32"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
