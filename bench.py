@@ -853,11 +853,22 @@ def main():
         cpu = cpu_baseline(args.config)
     if rank == 0:
         n_scene = scene.n
-        # K1 chunks + K2 + (hist, scan, depth passes) + (permute, count, scan, scatter) + raster
         depth_passes = math.ceil((32 + max(1, (max(n_scene, 2) - 1).bit_length())) / 8)
-        # K1 chunks + K2 + (hist, scan) + depth passes + (permute, count, scan,
-        # scatter, expand) + raster + 2 counter readbacks (after K1 and K2)
-        launches_per_step = math.ceil(max(n_t, 1) / 64) + 1 + 2 + depth_passes + 5 + 1 + 2
+        # views whose a4 runs in one CTA (k_small.cu): <= 2048 splats, <= 1024
+        # tiles, splats x tiles <= 2^18 (s3r_internal.cuh small_view)
+        def _small(st, v):
+            nt = ((v.width + 15) // 16) * ((v.height + 15) // 16)
+            return st["n_rendered"] <= 2048 and nt <= 1024 and st["n_rendered"] * nt <= (1 << 18)
+        small = [_small(st, v) for st, v in zip(stats, pools[0])]
+        any_small, all_small = any(small), all(small)
+        # K1 chunks + K2 + raster + the two plans / readbacks (one plan when, in
+        # the capacity mode, every view plans itself in k_small) + k_small +
+        # (hist, scan, depth passes,
+        # permute, count, scan, scatter, expand) for the other views
+        plans = 1 if (all_small and graphs is not None) else 2
+        launches_per_step = (math.ceil(max(n_t, 1) / 64) + 1 + 1 + plans
+                             + (1 if any_small else 0)
+                             + (0 if all_small else 2 + depth_passes + 5))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
