@@ -290,6 +290,7 @@ __device__ __noinline__ bool jitter_reproject(const float* __restrict__ M, float
 
 // O2 + O3 + O4 (+ the NEXT-3 noisy offset) of DESIGN.md for Gaussian g in
 // view V; M = the 12 floats of its instance camera.  Sets s.flags.
+template <bool JIT>
 __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 mo, float4 sc,
                                             float4 q, const DevView& V, float lox, float hix,
                                             float loy, float hiy, long long g, Splat& s)
@@ -325,9 +326,11 @@ __device__ __forceinline__ void project_one(const float* __restrict__ M, float4 
         }
         // ---- NEXT-3 noisy offset (Eq.7 row 4): mu += jit normalize(d) N(0,1),
         // normalize(d) = min(1, d / D) (reading R10), then project again
-        if (V.jit[0] != 0.0f || V.jit[1] != 0.0f || V.jit[2] != 0.0f) {
-            s.flags |= F_JITTERED;
-            if (!jitter_reproject(M, mo, sc, q, V, lox, hix, loy, hiy, g, pz, s)) return;
+        if constexpr (JIT) {
+            if (V.jit[0] != 0.0f || V.jit[1] != 0.0f || V.jit[2] != 0.0f) {
+                s.flags |= F_JITTERED;
+                if (!jitter_reproject(M, mo, sc, q, V, lox, hix, loy, hiy, g, pz, s)) return;
+            }
         }
     }
     s.flags |= F_RENDERED;
@@ -398,7 +401,7 @@ __device__ __forceinline__ bool surely_outside(const float* __restrict__ M, floa
 // dumps, all valid ones; tag bit 15 = "the pre-test would have culled it") are
 // appended to the shared-memory queue (qt, qg) through the counter *qn.  Bad
 // instance ids are counted into c_bad (and dumped) here.
-template <int PR>
+template <int PR, bool LEAN>
 __device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevView& V, int vi,
                                               long long i0, long long n_t,
                                               const int32_t* __restrict__ tl,
@@ -423,8 +426,8 @@ __device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevVie
     for (int rd = 0; rd < PR; ++rd) {
         const long long g = max(gA[rd], 0ll);
         scA[rd] = __ldg(a.scales + g);
-        moA[rd] = a.world_mo ? __ldg(a.world_mo + (long long)vi * a.n + g)
-                             : __ldg(a.means_opacity + g);
+        moA[rd] = (!LEAN && a.world_mo) ? __ldg(a.world_mo + (long long)vi * a.n + g)
+                                        : __ldg(a.means_opacity + g);
     }
 #pragma unroll
     for (int rd = 0; rd < PR; ++rd) {
@@ -436,7 +439,7 @@ __device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevVie
             const int id = idA[rd];
             if (id < 0 || id >= K1) {
                 c_bad++;
-                if (a.dbg_flags) {
+                if (!LEAN && a.dbg_flags) {
                     const long long di = V.dbg_off + i;
                     a.dbg_flags[di] = F_TEMPORAL | F_BADID;
 #pragma unroll
@@ -445,9 +448,9 @@ __device__ __forceinline__ void precull_chunk(const ProjectArgs& a, const DevVie
                     for (int j = 0; j < 4; ++j) a.dbg_rect[4 * di + j] = 0;
                 }
             } else {
-                const bool out = surely_outside(s_tab + 12 * (a.world_mo ? 0 : id), moA[rd],
+                const bool out = surely_outside(s_tab + 12 * ((!LEAN && a.world_mo) ? 0 : id), moA[rd],
                                                 scA[rd], V, lox, hix, loy, hiy);
-                keep = !out || a.dbg_flags;
+                keep = !out || (!LEAN && a.dbg_flags);
                 if (out) tag |= 0x8000u;
             }
         }
@@ -481,7 +484,11 @@ __device__ __forceinline__ void stage_view(const ProjectArgs& a, const DevView& 
 #ifndef S3R_K2_MINB
 #define S3R_K2_MINB 4     // 64 registers (A/B: K2 0.91 ms vs 1.03 at 3, 1.40 at 2)
 #endif
-template <int PR>
+// LEAN: no debug dumps, no NeurF record means, not the conventional pipeline,
+// no LOD noisy offset (ProjectArgs::lean) — those paths compiled out, which
+// keeps the splat in registers (the noisy offset's out-of-line call otherwise
+// puts it on the stack)
+template <int PR, bool LEAN>
 __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
 {
     extern __shared__ float s_tab[];          // [K1][12]
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
     const uint32_t* qg = s_g;
     if (tid == 0) s_qn = 0;
     __syncthreads();
-    precull_chunk<PR>(a, V, vi, i0, n_t, tl, s_tab, lox, hix, loy, hiy, s_q, s_g, &s_qn, c_bad);
+    precull_chunk<PR, LEAN>(a, V, vi, i0, n_t, tl, s_tab, lox, hix, loy, hiy, s_q, s_g, &s_qn, c_bad);
     __syncthreads();
     const int qn = s_qn;
     for (int qbase = 0; qbase < qn; qbase += PT) {
@@ -544,7 +551,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
                 const float4 sc = __ldg(a.scales + g);
                 float4 mo, q;
                 int slot = id;
-                if (a.world_mo) {      // conventional: the view's world copy, camera W_t
+                if (!LEAN && a.world_mo) {      // conventional: the view's world copy, camera W_t
                     const long long wg = (long long)vi * a.n + g;
                     mo = __ldg(a.world_mo + wg);
                     q = __ldg(a.world_rot + wg);
@@ -553,7 +560,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
                     mo = __ldg(a.means_opacity + g);
                     q = __ldg(a.rotations + g);
                 }
-                project_one(s_tab + 12 * slot, mo, sc, q, V, lox, hix, loy, hiy, g, sp);
+                project_one<!LEAN>(s_tab + 12 * slot, mo, sc, q, V, lox, hix, loy, hiy, g, sp);
                 if (culled && (sp.flags & F_VISIBLE)) atomicOr(a.err, ERR_PRECULL);
                 if (sp.flags & F_VISIBLE) {
                     c_vis++;
@@ -577,7 +584,7 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
                                 (unsigned long long)((sp.ty1 >> sh) - (sp.ty0 >> sh) + 1);
                 }
             }
-            if (a.dbg_flags) {
+            if (!LEAN && a.dbg_flags) {
                 const long long di = V.dbg_off + i;
                 a.dbg_flags[di] = sp.flags;
 #pragma unroll
@@ -636,8 +643,8 @@ __global__ void __launch_bounds__(PT, S3R_K2_MINB) k_project(ProjectArgs a)
             // so the order is (depth, index) whatever the compaction order was
             a.dkey[o] = ((unsigned long long)__float_as_uint(sp.rm[2]) << a.gbits) |
                         (unsigned long long)g;
-            if (a.gidx) a.gidx[o] = (int32_t)g;
-            if (a.rec_mu) a.rec_mu[o] = make_float4(sp.mu[0], sp.mu[1], sp.mu[2], __int_as_float(gid_id));
+            if (!LEAN && a.gidx) a.gidx[o] = (int32_t)g;
+            if (!LEAN && a.rec_mu) a.rec_mu[o] = make_float4(sp.mu[0], sp.mu[1], sp.mu[2], __int_as_float(gid_id));
         }
     }
     // ---- per-view counters: one set of atomics per CTA ----
@@ -864,16 +871,24 @@ void launch_project(const ProjectArgs& a, cudaStream_t st)
 {
     if (a.max_tiles == 0 || a.n_views == 0) return;
     const size_t smem = (size_t)a.num_instances * 12 * sizeof(float);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_project<PR_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if ((long long)a.max_tiles * a.n_views < 2 * 148) {
+    const bool small_grid = (long long)a.max_tiles * a.n_views < 2 * 148;
+    const dim3 grid = small_grid ? dim3(a.max_tiles * PR_BIG, a.n_views) : dim3(a.max_tiles, a.n_views);
+    auto go = [&](auto kern) {
         if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_project<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_project<1><<<dim3(a.max_tiles * PR_BIG, a.n_views), PT, smem, st>>>(a);
-        return;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, PT, smem, st>>>(a);
+    };
+#ifndef S3R_K2_LEAN
+#define S3R_K2_LEAN 1
+#endif
+    const bool lean = S3R_K2_LEAN && a.lean;
+    if (small_grid) {
+        if (lean) go(k_project<1, true>);
+        else go(k_project<1, false>);
+    } else {
+        if (lean) go(k_project<PR_BIG, true>);
+        else go(k_project<PR_BIG, false>);
     }
-    dim3 grid(a.max_tiles, a.n_views);
-    k_project<PR_BIG><<<grid, PT, smem, st>>>(a);
 }
 
 int project_tile() { return PTILE; }

@@ -635,6 +635,8 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         a.dbg_keys = c->debug ? P<float>(c->d_dbg_keys) : nullptr;
         a.dbg_flags = c->debug ? P<uint8_t>(c->d_dbg_flags) : nullptr;
         a.dbg_rect = c->debug ? P<int16_t>(c->d_dbg_rect) : nullptr;
+        a.lean = (!conv && !want_mu && !c->debug && c->lod_jitter[0] == 0.0f &&
+                  c->lod_jitter[1] == 0.0f && c->lod_jitter[2] == 0.0f) ? 1 : 0;
         StageEvent e;
         ev_begin(c, S3R_STAGE_PROJECT, st, e);
         launch_project(a, st);

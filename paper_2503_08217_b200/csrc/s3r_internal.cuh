@@ -223,6 +223,9 @@ struct ProjectArgs {
     float* dbg_keys;
     uint8_t* dbg_flags;
     int16_t* dbg_rect;
+    // no debug dumps, no rec_mu, no world copy and no LOD noisy offset in this
+    // batch: the specialised K2 without those paths
+    int lean;
 };
 void launch_project(const ProjectArgs& a, cudaStream_t st);
 int project_tile();

@@ -246,6 +246,10 @@ VARIANT_SETS = {
         "hyb24": ["S3R_SCAT_HYBRID=1", "S3R_SCAT_SMALL=24"],
         "hyb32": ["S3R_SCAT_HYBRID=1", "S3R_SCAT_SMALL=32"],
     },
+    "k2lean": {
+        "base": [],
+        "nolean": ["S3R_K2_LEAN=0"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
