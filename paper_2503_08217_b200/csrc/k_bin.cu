@@ -191,6 +191,9 @@ constexpr int SCAT_SMALL = S3R_SCAT_SMALL;
                        // ballots staged through shared memory and predicated stores: C3 0.957 -> 0.880 ms,
                        // C2 0.390 -> 0.352 ms against per-tile lane-select counts and branches)
 #endif
+#ifndef S3R_XPREF
+#define S3R_XPREF 1    // expansion: next round's entry + rectangle loaded one round ahead
+#endif
 #ifndef S3R_XT
 #define S3R_XT 128     // A/B (mask expansion): bin 1.025 ms vs 1.059 at 256
 #endif
@@ -230,15 +233,39 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
         __shared__ int s_wc[XT / 32][16];
         __shared__ __align__(16) unsigned s_bal[XT / 32][16];
         const unsigned lt = (1u << lane) - 1u;
+#if S3R_XPREF
+        // the next round's entry and rectangle are loaded while this round's
+        // are expanded (two dependent loads per round otherwise exposed)
+        uint32_t r_nx = 0;
+        uint2 rr_nx = make_uint2(0u, 0u);
+        if (rg.x + tid < rg.y) {
+            r_nx = lst[rg.x + tid];
+            rr_nx = rects[r_nx];
+        }
+#endif
         for (int base = rg.x; base < rg.y; base += XT) {
             const int e = base + tid;
             uint32_t r = 0, m = 0;
+#if S3R_XPREF
+            const uint2 rr = rr_nx;
+            r = r_nx;
+            if (e + XT < rg.y) {
+                r_nx = lst[e + XT];
+                rr_nx = rects[r_nx];
+            }
+            if (e < rg.y) {
+                int tx0, tx1, ty0, ty1;
+                rect_of(rr, tx0, tx1, ty0, ty1);
+                m = tile_mask4(tx0, tx1, ty0, ty1, bx, by);
+            }
+#else
             if (e < rg.y) {
                 r = lst[e];
                 int tx0, tx1, ty0, ty1;
                 rect_of(rects[r], tx0, tx1, ty0, ty1);
                 m = tile_mask4(tx0, tx1, ty0, ty1, bx, by);
             }
+#endif
             unsigned bal[16];
 #pragma unroll
             for (int t = 0; t < 16; ++t)     // one bit test + one vote per tile

@@ -250,6 +250,10 @@ VARIANT_SETS = {
         "base": [],
         "nolean": ["S3R_K2_LEAN=0"],
     },
+    "xpref": {
+        "base": [],
+        "nopref": ["S3R_XPREF=0"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
