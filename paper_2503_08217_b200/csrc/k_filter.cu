@@ -15,6 +15,8 @@
 // hull — a contiguous run of the sorted slot times, ~1/5 of them because the
 // scene's index order is spatially coherent.  Algorithmic bytes: 8 N read +
 // 4 sum_s N_t(s) written.
+#include <algorithm>
+
 #include "s3r_internal.cuh"
 
 namespace s3r {
@@ -28,19 +30,31 @@ constexpr int FGROUPS = FV * (FT / 32);   // (round, warp) groups = 64
 // tested.  Chosen per launch (launch_filter): it pays on large scenes (C3
 // 0.129 -> 0.099 ms, C4 0.474 -> 0.261 ms) but not on a grid of a few dozen
 // CTAs, where its serial binary searches are exposed (C2: 0.100 vs 0.137 ms).
+#ifndef S3R_FILTER_WANT_BIG
+#define S3R_FILTER_WANT_BIG 0   // CTAs a large scene's K1 grid aims at by grouping slots (0: MAX_TSLOTS per launch)
+#endif
 #ifndef S3R_FILTER_RANGE_MIN_TILES
 #define S3R_FILTER_RANGE_MIN_TILES 296   // 2 CTAs per SM
 #endif
 
 
+// blockIdx.y = slot group: slots [gs y, gs y + gs) of the launch's Tall, each
+// group with its own ticket, look-back chains, counts and output lists
 template <bool RANGE>
 __global__ void __launch_bounds__(FT) k_filter(const float2* __restrict__ vis, long long n,
-                                               const float* __restrict__ times, int T,
+                                               const float* __restrict__ times, int Tall, int gs,
                                                int32_t* __restrict__ idx_out, long long stride,
                                                unsigned long long* __restrict__ counts,
                                                uint32_t* __restrict__ lookback,
                                                int* __restrict__ ticket, int ntiles)
 {
+    const int s0 = blockIdx.y * gs;
+    const int T = min(gs, Tall - s0);
+    times += s0;
+    idx_out += (long long)s0 * stride;
+    counts += s0;
+    lookback += (long long)s0 * ntiles;
+    ticket += blockIdx.y;
     __shared__ int s_tile;
     __shared__ float s_t[MAX_TSLOTS];
     __shared__ float s_st[MAX_TSLOTS];       // the slot times in ascending order
@@ -211,18 +225,32 @@ __global__ void __launch_bounds__(FT) k_filter(const float2* __restrict__ vis, l
 }
 }  // namespace
 
-void launch_filter(const float2* vis, long long n, const float* d_times, int T, int32_t* idx_out,
-                   long long idx_stride, unsigned long long* counts, uint32_t* lookback,
-                   int* ticket, cudaStream_t st)
+void launch_filter(const float2* vis, long long n, const float* d_times, int T, int gs,
+                   int32_t* idx_out, long long idx_stride, unsigned long long* counts,
+                   uint32_t* lookback, int* ticket, cudaStream_t st)
 {
     int ntiles = (int)((n + FTILE - 1) / FTILE);
-    if (ntiles == 0) return;
+    if (ntiles == 0 || T == 0) return;
+    const dim3 grid(ntiles, (T + gs - 1) / gs);
     if (ntiles >= S3R_FILTER_RANGE_MIN_TILES)
-        k_filter<true><<<ntiles, FT, 0, st>>>(vis, n, d_times, T, idx_out, idx_stride, counts,
-                                              lookback, ticket, ntiles);
+        k_filter<true><<<grid, FT, 0, st>>>(vis, n, d_times, T, gs, idx_out, idx_stride, counts,
+                                            lookback, ticket, ntiles);
     else
-        k_filter<false><<<ntiles, FT, 0, st>>>(vis, n, d_times, T, idx_out, idx_stride, counts,
-                                               lookback, ticket, ntiles);
+        k_filter<false><<<grid, FT, 0, st>>>(vis, n, d_times, T, gs, idx_out, idx_stride, counts,
+                                             lookback, ticket, ntiles);
+}
+
+int filter_groups(long long n, int T)
+{
+    // slots per group: a scene of few 4096-Gaussian tiles (C2: 49) splits its
+    // distinct times into groups launched together, so that the grid fills the
+    // GPU (~4 CTAs per SM); a large scene keeps MAX_TSLOTS per launch
+    const long long ntiles = (n + FTILE - 1) / FTILE;
+    if (ntiles == 0 || T == 0) return MAX_TSLOTS;
+    if (ntiles >= S3R_FILTER_RANGE_MIN_TILES && S3R_FILTER_WANT_BIG == 0) return MAX_TSLOTS;
+    const long long want = ntiles >= S3R_FILTER_RANGE_MIN_TILES ? S3R_FILTER_WANT_BIG : 4 * 148;
+    const long long gs = (T * ntiles + want - 1) / want;
+    return (int)std::max(1ll, std::min((long long)MAX_TSLOTS, gs));
 }
 
 int filter_tile() { return FTILE; }

@@ -479,7 +479,12 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
                                    "conventional pipeline");
     // one zeroed work counter per launch that takes tickets: the filter chunks
     // and the depth-sort passes
-    const int n_tickets = (T + MAX_TSLOTS - 1) / MAX_TSLOTS +
+    // K1 groups: a small scene takes all T distinct times in one launch of
+    // ceil(T / fgs) groups (one ticket each, all look-back words zeroed with the
+    // arena); a large one ceil(T / MAX_TSLOTS) launches of one group
+    const int fgs = conv ? MAX_TSLOTS : filter_groups(N, T);
+    const bool f_grouped = fgs < MAX_TSLOTS;
+    const int n_tickets = (T + fgs - 1) / fgs +
                           (32 + c->gbits + RADIX_BITS - 1) / RADIX_BITS;
     c->ticket_cap = n_tickets;
     if ((rc = ensure(c, c->d_err, sizeof(uint32_t)))) return rc;
@@ -489,7 +494,9 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
     const size_t z_ticket = 0;
     const size_t z_counts = al16(z_ticket + (size_t)n_tickets * 4);
     const size_t z_lb1 = al16(z_counts + (size_t)std::max(T, 1) * 8);
-    const size_t z_ctr = al16(z_lb1 + (size_t)std::min(std::max(T, 1), MAX_TSLOTS) * ntf_all * 4);
+    const size_t z_ctr = al16(z_lb1 + (size_t)(f_grouped ? std::max(T, 1)
+                                                           : std::min(std::max(T, 1), MAX_TSLOTS)) *
+                                          ntf_all * 4);
     const size_t z_end = al16(z_ctr + (size_t)std::max(nv, 1) * sizeof(ViewCounters));
     if ((rc = ensure(c, c->d_zero, z_end))) return rc;
     c->p_ticket = reinterpret_cast<int*>(P<char>(c->d_zero) + z_ticket);
@@ -531,13 +538,20 @@ int render_impl(s3r_ctx* c, const s3r_scene* sc, const s3r_view* views, int nv,
         StageEvent e;
         ev_begin(c, S3R_STAGE_FILTER, st, e);
         const long long ntf = (N + filter_tile() - 1) / filter_tile();
-        for (int c0 = 0; c0 < T && N > 0; c0 += MAX_TSLOTS) {
+        if (f_grouped && N > 0) {
+            const int ng = (T + fgs - 1) / fgs;
+            int* tk0 = next_ticket(c);
+            for (int g = 1; g < ng; ++g) next_ticket(c);      // consecutive tickets
+            launch_filter(reinterpret_cast<const float2*>(sc->visibility), N, c->p_times, T, fgs,
+                          P<int32_t>(c->d_tidx), Ns, c->p_counts, c->p_lb1, tk0, st);
+        }
+        for (int c0 = 0; !f_grouped && c0 < T && N > 0; c0 += MAX_TSLOTS) {
             const int Tc = std::min(MAX_TSLOTS, T - c0);
             // look-back words: zeroed with the arena for the first chunk of
             // distinct times, re-zeroed for later ones
             if (c0) CU(cudaMemsetAsync(c->p_lb1, 0, (size_t)Tc * ntf * sizeof(uint32_t), st));
             launch_filter(reinterpret_cast<const float2*>(sc->visibility), N,
-                          c->p_times + c0, Tc, P<int32_t>(c->d_tidx) + (long long)c0 * Ns,
+                          c->p_times + c0, Tc, Tc, P<int32_t>(c->d_tidx) + (long long)c0 * Ns,
                           Ns, c->p_counts + c0, c->p_lb1, next_ticket(c), st);
         }
         ev_end(c, st, e);

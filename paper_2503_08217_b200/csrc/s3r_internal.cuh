@@ -180,10 +180,15 @@ void launch_plan_records(DevView* views, int nv, const unsigned long long* count
 void launch_plan_bins(DevView* views, int nv, const ViewCounters* ctr, Seg* segs, int* dt0,
                       const PlanCaps& caps, ViewCounters* h_ctr, uint32_t* err, cudaStream_t st);
 
-// K1: temporal filter + ordered compaction for up to MAX_TSLOTS distinct times.
-void launch_filter(const float2* vis, long long n, const float* d_times, int T,
+// K1: temporal filter + ordered compaction of T distinct times in groups of gs
+// (<= MAX_TSLOTS) slots, one ticket per group (ticket[0 .. ceil(T / gs))) and
+// look-back words lookback[slot][tile].
+void launch_filter(const float2* vis, long long n, const float* d_times, int T, int gs,
                    int32_t* idx_out, long long idx_stride, unsigned long long* counts,
                    uint32_t* lookback, int* ticket, cudaStream_t st);
+// slots per K1 group for a scene of n Gaussians and T distinct times: all T in
+// one launch when the scene has few filter tiles, else MAX_TSLOTS per launch
+int filter_groups(long long n, int T);
 
 // Compose instance cameras (fp64, rounded once).
 void launch_compose(const float* w2c, const float* i2g, int n_views, int K, float* out,

@@ -254,6 +254,11 @@ VARIANT_SETS = {
         "base": [],
         "nopref": ["S3R_XPREF=0"],
     },
+    "grpbig": {
+        "base": [],
+        "wb1184": ["S3R_FILTER_WANT_BIG=1184"],
+        "wb2368": ["S3R_FILTER_WANT_BIG=2368"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
