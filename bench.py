@@ -861,12 +861,14 @@ def main():
             return st["n_rendered"] <= 2048 and nt <= 1024 and st["n_rendered"] * nt <= (1 << 18)
         small = [_small(st, v) for st, v in zip(stats, pools[0])]
         any_small, all_small = any(small), all(small)
-        # K1 chunks + K2 + raster + the two plans / readbacks (one plan when, in
-        # the capacity mode, every view plans itself in k_small) + k_small +
-        # (hist, scan, depth passes,
-        # permute, count, scan, scatter, expand) for the other views
+        # K1 (one launch of slot groups on a scene of < 296 filter tiles, else one
+        # per 64 distinct times) + K2 + raster + the two plans / readbacks (one
+        # plan when, in the capacity mode, every view plans itself in k_small) +
+        # k_small + (hist, scan, depth passes, permute, count, scan, scatter,
+        # expand) for the other views
         plans = 1 if (all_small and graphs is not None) else 2
-        launches_per_step = (math.ceil(max(n_t, 1) / 64) + 1 + 1 + plans
+        k1 = 1 if math.ceil(n_scene / 4096) < 296 else math.ceil(max(n_t, 1) / 64)
+        launches_per_step = (k1 + 1 + 1 + plans
                              + (1 if any_small else 0)
                              + (0 if all_small else 2 + depth_passes + 5))
         line = {
