@@ -4,8 +4,9 @@ s3r_render_batch) against the CPU oracle on K sampled views each (C2: all 100), 
 element — temporal list, fp32 keys, decisions, rectangles, M_t, depth order,
 (tile, Gaussian) pairs, tile ranges, images.  The oracle renders run in forked
 worker processes on the host cores, each comparing its view against the GPU
-dumps taken before the fork.  Writes a JSON summary (default
-profiles/r01_parity_sweep.json).  Test infrastructure: needs a B200.
+dumps taken before the fork; and every view of the batch rendered again on the
+product path (no dumps, capacity mode) must equal the checked render bit for
+bit.  Writes a JSON summary (default profiles/r02_parity_sweep.json).  Test infrastructure: needs a B200.
 
     python tools/parity_sweep.py [OUT.json] [--views K]
 """
@@ -101,12 +102,31 @@ def main():
                                ("rgb", "depth", "final_T", "visible")}}
         _G.update(scene=scene, views=views, tabs=[t.cpu().numpy() for t in tabs], gpu=gpu)
         ctx.close()
+        # the product path (no debug dumps: the lean K2; the capacity mode sized
+        # from this batch, as bench.py runs it) must give every view's images
+        # and M_t bit for bit
+        pctx = s3r.Context(0)
+        pds = s3r.DeviceScene.from_numpy(scene)
+        ptabs = list(s3r.view_tables(pctx, views))
+        pouts = s3r.alloc_outputs(views, n_visible=scene.n)
+        pctx.render_batch(pds, views, ptabs, pouts)          # sizes the reservation
+        pctx.set_capacity(pctx.capacity_from_last(1.1))
+        pds = s3r.DeviceScene.from_numpy(scene)
+        pouts = s3r.alloc_outputs(views, n_visible=scene.n)
+        pctx.render_batch(pds, views, ptabs, pouts)
+        torch.cuda.synchronize()
+        product_ok = pctx.check() == 0 and all(
+            torch.equal(outs[i][k], pouts[i][k]) for i in range(len(views))
+            for k in ("rgb", "depth", "final_T", "visible"))
+        pctx.close()
+        del pouts, pds
         t0 = time.perf_counter()
         with mp.get_context("fork").Pool(min(cores, len(pick))) as pool:
             per = pool.map(_compare, pick)
         wall = time.perf_counter() - t0
         bool_keys = [k for k in per[0] if isinstance(per[0][k], bool)]
         summary = {k: all(p[k] for p in per) for k in bool_keys}
+        summary["product_path_all_views_bit_equal"] = bool(product_ok)
         summary.update(keys_bit_mismatches=sum(p["keys_bit_mismatches"] for p in per),
                        rgb_max_abs=max(p["rgb_max_abs"] for p in per),
                        depth_max_abs=max(p["depth_max_abs"] for p in per),
