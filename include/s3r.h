@@ -174,8 +174,8 @@ enum {
     S3R_STAGE_PROJECT,           /* K2 projection + LOD + life update          */
     S3R_STAGE_DEPTH_SORT,        /* K5 (depth, index) radix sort                */
     S3R_STAGE_BIN,               /* K3 depth-order permute + K4 supertile
-                                    counting sort (count, scan, scatter) with
-                                    supertile ranges                            */
+                                    counting sort (count, scan, scatter) and
+                                    the per-tile list expansion with ranges     */
     S3R_STAGE_RASTER,            /* K7 tile filter + alpha-blend rasterizer     */
     S3R_STAGE_COLOR,             /* K6 NeurF colour query (0 unless enabled)    */
     S3R_NUM_STAGES
