@@ -176,16 +176,14 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const DevView* __restrict__ v
 }
 
 // ------------------------------------------------------------------ K4 expand
-// One CTA per (supertile, view): the supertile's list is staged in shared
-// memory 512 entries at a time; warp w keeps, for each of its tiles, the
-// entries whose rectangle contains the tile (ballot + popc: list order is
-// kept), and appends them to the tile's list.  Tile t (local index in the
-// supertile, S*S of them) owns [S*S*start + t*len, +len) of the view's tile-list
-// area, len = supertile list length, so no count pass is needed.
-#ifndef S3R_SCAT_SMALL
-#define S3R_SCAT_SMALL 16   // scatter: a splat with more bins is taken by the whole warp
-#endif
-constexpr int SCAT_SMALL = S3R_SCAT_SMALL;
+// One CTA per (supertile, view) walks the supertile's list XT entries at a
+// time and appends each entry to the lists of the supertile's tiles its
+// rectangle contains, in list order (ballot + popc).  Tile t (local index in
+// the supertile, S*S of them) owns [S*S*start + t*len, +len) of the view's
+// tile-list area, len = supertile list length, so no count pass is needed.
+// 4 x 4 supertiles (the product case) use per-entry tile masks (below); a
+// larger S (huge images) stages the entries in shared memory and gives each
+// warp a set of tiles.
 #ifndef S3R_XMASK
 #define S3R_XMASK 1    // 4 x 4 supertiles: per-entry tile masks + 16 ballots (A/B, bin stage with the
                        // ballots staged through shared memory and predicated stores: C3 0.957 -> 0.880 ms,
@@ -351,6 +349,10 @@ __global__ void __launch_bounds__(XT) k_bin_expand(const DevView* __restrict__ v
 }
 
 // ------------------------------------------------------------------ K4 scatter
+#ifndef S3R_SCAT_SMALL
+#define S3R_SCAT_SMALL 16   // a splat with more bins is taken by the whole warp
+#endif
+constexpr int SCAT_SMALL = S3R_SCAT_SMALL;
 // Writes every (bin, r) pair's rank r at its final position.  Stability: a
 // chunk's pairs for one bin follow the chunk's scanned base; inside the chunk
 // warp w's pairs follow warps < w (per-warp counts, scanned in shared memory);
