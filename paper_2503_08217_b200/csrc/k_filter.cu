@@ -4,10 +4,12 @@
 // visible Gaussians G' whose visibility intervals encompass t, denoted as
 // t_s <= t <= t_e".  Reading R1: t_s == v_s, t_e == v_e, inclusive; NaN -> out.
 //
-// One launch serves up to MAX_TSLOTS distinct view times: each CTA reads its
+// One CTA serves a group of up to MAX_TSLOTS distinct view times: it reads its
 // 4096-Gaussian slice of v = (v_s, v_e) ONCE (16-byte vector loads, 8 per
-// thread) and produces, for every time slot, the ascending list of kept
-// indices.  Within a CTA the order is fixed by warp ballots + popc (per
+// thread) and produces, for every time slot of its group, the ascending list
+// of kept indices.  A large scene takes one group per launch; a small one
+// (C2: 49 slices) splits its times into smaller groups launched together as
+// grid.y (filter_groups), so that the grid fills the GPU.  Within a CTA the order is fixed by warp ballots + popc (per
 // (round, warp) counts, one warp scan per slot); across CTAs by a decoupled
 // look-back per slot (CTA order from an atomic ticket, so a CTA only waits on
 // CTAs that are already resident).  On large scenes (RANGE) a (round, warp)
