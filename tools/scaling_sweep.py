@@ -2,7 +2,8 @@
 paper's Fig.1c / Fig.4 claim, on B200; SURVEY.md §8(f)
 NEXT-2).  The C3 (av2) rig and density, street length L in metres with the
 Gaussian count, the object count and the frame count proportional to L; 32
-views sampled per length.  Writes profiles/r01_scaling_sweep.json.
+views sampled per length.  Writes gpurun_out/scaling_sweep.json (copied to
+profiles/r0N_scaling_sweep.json per round).
 
     python tools/scaling_sweep.py [lengths...]
 """
