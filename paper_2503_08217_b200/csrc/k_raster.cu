@@ -37,15 +37,16 @@ namespace {
 #ifndef S3R_RASTER_RPIX
 #define S3R_RASTER_RPIX 4
 #endif
-// pixels per thread (RPIX rows of one column, RS rows apart); a tile's 256
-// pixels take RT = 256 / RPIX threads, each warp owning BW columns.  The
-// product layout is RPIX = 4 (2 packed pairs per thread, 64-thread CTAs); a
-// batch whose grid cannot fill the GPU (C1: 16 tiles) takes RPIX = 2 (one pair
-// per thread, 128-thread CTAs): twice the warps on the few busy SMs.
-template <int RP>
+// pixels per thread (RPIX rows of one column, RS rows apart); a CTA covers TH
+// rows of its tile (the whole tile, or one half: blockIdx.z), TILE * TH / RPIX
+// threads, each warp owning BW columns.  The product layout is RPIX = 4, TH =
+// 16 (2 packed pairs per thread, 64-thread CTAs); a batch whose grid cannot fill
+// the GPU (C1: 16 tiles) takes RPIX = 2, TH = 8 (one pair per thread, two
+// 64-thread CTAs per tile): four times the warps on twice the SMs.
+template <int RP, int TH = TILE>
 struct Geo {
     static constexpr int RPIX = RP;
-    static constexpr int RT = TILE * TILE / RPIX;
+    static constexpr int RT = TILE * TH / RPIX;
     static constexpr int BW = TILE / (RT / 32);
     static constexpr int RS = 32 / BW;
     static constexpr int NP = RPIX / 2;
@@ -151,11 +152,12 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // One (view, tile): the whole K7 computation of the tile's 256 pixels.
-template <bool COUNT, bool TRAIN, bool FAST, int RP>
-__device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, const int tile)
+template <bool COUNT, bool TRAIN, bool FAST, int RP, int TH>
+__device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, const int tile,
+                                            const int half)
 {
-    constexpr int RPIX = Geo<RP>::RPIX, RT = Geo<RP>::RT, BW = Geo<RP>::BW, RS = Geo<RP>::RS,
-                  NP = Geo<RP>::NP, NW = Geo<RP>::NW;
+    using G = Geo<RP, TH>;
+    constexpr int RPIX = G::RPIX, RT = G::RT, BW = G::BW, RS = G::RS, NP = G::NP, NW = G::NW;
     __shared__ float4 s_rec[NBUF][3 * RB];   // staged splat records, 48 B each
     __shared__ uint16_t s_cl[NW][RB];        // per warp block: staged records reaching it
     __shared__ int s_wc[NW][NW];             // [staging warp][warp block] kept counts
@@ -169,9 +171,11 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
 #if S3R_RASTER_ADJ
     // pixel k of the thread at row 2 RS (k >> 1) + 2 (lane / BW) + (k & 1): the
     // two pixels of a pair are vertically adjacent
-    auto prow = [&](int k) { return ty * TILE + 2 * RS * (k >> 1) + 2 * (lane / BW) + (k & 1); };
+    auto prow = [&](int k) {
+        return ty * TILE + half * TH + 2 * RS * (k >> 1) + 2 * (lane / BW) + (k & 1);
+    };
 #else
-    const int py0 = ty * TILE + (lane / BW);
+    const int py0 = ty * TILE + half * TH + (lane / BW);
     auto prow = [&](int k) { return py0 + RS * k; };
 #endif
     const float fpx = (float)px;
@@ -179,10 +183,13 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
     // stored extents include the 8 x 16 block's half size)
     // (the stored extents include an 8 x 16 block's half size; XPAD corrects
     // for another block width, negative for BW < 8)
-    static_assert(BW >= 1 && RS * 2 * NP == TILE, "warp blocks span the tile's 16 rows");
+    static_assert(BW >= 1 && RS * 2 * NP == TH, "warp blocks span the CTA's TH rows");
     constexpr float XPAD = 0.5f * (BW - 1) - CULL_HALF_BX;
+    // YPAD: the same correction for a block of TH < 16 rows (still conservative:
+    // the stored extent minus 4 keeps the 3.5-row half height of 8 rows)
+    constexpr float YPAD = 0.5f * (TH - 1) - CULL_HALF_BY;
     const float bcx0 = (float)(tx * TILE) + 0.5f * (BW - 1);     // warp block 0
-    const float bcy = (float)(ty * TILE) + CULL_HALF_BY;
+    const float bcy = (float)(ty * TILE + half * TH) + 0.5f * (TH - 1);
     // pair P holds pixels k = 2P (.x) and 2P + 1 (.y)
     float2 nfpy[NP], T[NP], cr[NP], cg[NP], cb[NP], dp[NP];
     int stop[RPIX];
@@ -350,7 +357,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
                              q2 = s_rec[buf][3 * i + 2];
 #endif
                 const float hx = XPAD != 0.0f ? q1.w + XPAD : q1.w;
-                const bool yok = !(fabsf(q0.y - bcy) > q2.w);
+                const bool yok = !(fabsf(q0.y - bcy) > (YPAD != 0.0f ? q2.w + YPAD : q2.w));
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
                     keep[w] = yok && !(fabsf(q0.x - (bcx0 + (float)(w * BW))) > hx);
@@ -427,7 +434,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
         if (lane == 0) atomicAdd(a.evals + 2 * v, e);
-        if (tid == 0) atomicAdd(a.evals + 2 * v + 1, 256ull * n_exec);
+        if (tid == 0) atomicAdd(a.evals + 2 * v + 1, (unsigned long long)(TILE * TH) * n_exec);
     }
 #pragma unroll
     for (int k = 0; k < RPIX; ++k) {
@@ -454,29 +461,30 @@ __device__ __forceinline__ void raster_tile(const RasterArgs& a, const int v, co
 }
 
 // K7: one CTA per (tile, view)
-template <bool COUNT, bool TRAIN, bool FAST, int RP>
-__global__ void __launch_bounds__(Geo<RP>::RT,
+template <bool COUNT, bool TRAIN, bool FAST, int RP, int TH>
+__global__ void __launch_bounds__(Geo<RP, TH>::RT,
                                   RP == RPIX_BIG ? (TRAIN ? S3R_RASTER_TRAIN_MINB : S3R_RASTER_MINB) : 8)
     k_raster(RasterArgs a)
 {
-    raster_tile<COUNT, TRAIN, FAST, RP>(a, blockIdx.y, blockIdx.x);
+    raster_tile<COUNT, TRAIN, FAST, RP, TH>(a, blockIdx.y, blockIdx.x, blockIdx.z);
 }
 
-template <int RP>
+template <int RP, int TH>
 void launch_raster_rp(const RasterArgs& a, dim3 grid, cudaStream_t st)
 {
-    constexpr int RT = Geo<RP>::RT;
+    constexpr int RT = Geo<RP, TH>::RT;
+    grid.z = TILE / TH;
     // training renders always take the exact R-ARITH exponential: the backward
     // recomputes alpha with it and relies on the forward's decisions
     if (a.train_T) {
-        if (a.evals) k_raster<true, true, false, RP><<<grid, RT, 0, st>>>(a);
-        else k_raster<false, true, false, RP><<<grid, RT, 0, st>>>(a);
+        if (a.evals) k_raster<true, true, false, RP, TH><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, true, false, RP, TH><<<grid, RT, 0, st>>>(a);
     } else if (a.fast_exp) {
-        if (a.evals) k_raster<true, false, true, RP><<<grid, RT, 0, st>>>(a);
-        else k_raster<false, false, true, RP><<<grid, RT, 0, st>>>(a);
+        if (a.evals) k_raster<true, false, true, RP, TH><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, false, true, RP, TH><<<grid, RT, 0, st>>>(a);
     } else {
-        if (a.evals) k_raster<true, false, false, RP><<<grid, RT, 0, st>>>(a);
-        else k_raster<false, false, false, RP><<<grid, RT, 0, st>>>(a);
+        if (a.evals) k_raster<true, false, false, RP, TH><<<grid, RT, 0, st>>>(a);
+        else k_raster<false, false, false, RP, TH><<<grid, RT, 0, st>>>(a);
     }
 }
 
@@ -495,8 +503,11 @@ void launch_raster(const RasterArgs& args, cudaStream_t st)
     RasterArgs a = args;
     a.exp2_c0 = 1.3264695880934596e-3f;
     const dim3 grid(a.max_tiles, a.n_views);
-    if ((long long)a.max_tiles * a.n_views < 2 * 148) launch_raster_rp<2>(a, grid, st);
-    else launch_raster_rp<RPIX_BIG>(a, grid, st);
+#ifndef S3R_RASTER_SMALL_TH
+#define S3R_RASTER_SMALL_TH 8   // rows per CTA on a grid that cannot fill the GPU (16: whole tiles)
+#endif
+    if ((long long)a.max_tiles * a.n_views < 2 * 148) launch_raster_rp<2, S3R_RASTER_SMALL_TH>(a, grid, st);
+    else launch_raster_rp<RPIX_BIG, TILE>(a, grid, st);
 }
 
 void launch_dump_order(const uint32_t* order, const int32_t* gidx, long long base,

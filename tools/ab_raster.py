@@ -259,6 +259,11 @@ VARIANT_SETS = {
         "wb1184": ["S3R_FILTER_WANT_BIG=1184"],
         "wb2368": ["S3R_FILTER_WANT_BIG=2368"],
     },
+    "half": {
+        "base": [],
+        "th16": ["S3R_RASTER_SMALL_TH=16"],
+        "th4": ["S3R_RASTER_SMALL_TH=4"],   # C1: 18.1 k vs 18.3-18.6 k at 8
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
