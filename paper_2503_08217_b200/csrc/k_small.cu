@@ -23,6 +23,9 @@ namespace s3r {
 namespace {
 
 constexpr int SMT = 1024;
+#ifndef S3R_SMALL_MASK
+#define S3R_SMALL_MASK 1   // views of <= 32 tiles: tile lists from per-rank tile masks + ballots
+#endif
 constexpr int SMW = SMT / 32;
 
 __device__ __forceinline__ bool rect_has(uint2 rr, int tx, int ty)
@@ -171,9 +174,88 @@ __global__ void __launch_bounds__(SMT) k_small_sortbin(DevView* __restrict__ vie
         dst[2] = q2;
     }
     __syncthreads();
+    const int nt = V.ntiles;
+#if S3R_SMALL_MASK
+    if (nt <= 32) {
+        // ---- a view of <= 32 tiles (C1: 16): a warp takes 32 ranks a round,
+        // each lane its rank's tile mask (bit t = tile t of the view), one
+        // ballot per tile; per-(round, tile) counts scanned over the rounds
+        // give each round's place in the tile's list (rank order), the tile
+        // totals scanned over the tiles give the lists' starts.  s_key (free
+        // after the permute) holds the counts and ballots.
+        const int nr = (n + 31) >> 5;                                  // <= 64 rounds
+        uint32_t* s_c2 = reinterpret_cast<uint32_t*>(s_key);           // [64][32] counts
+        uint32_t* s_b2 = s_c2 + 64 * 32;                                // [64][32] ballots
+        const int TX = V.TX;
+        auto mask_of = [&](int r) -> uint32_t {
+            if (r >= n) return 0u;
+            const uint2 rr = s_rect[r];
+            const int tx0 = rr.x & 0xffff, tx1 = rr.x >> 16, ty0 = rr.y & 0xffff, ty1 = rr.y >> 16;
+            const int wdt = tx1 - tx0 + 1;
+            const uint32_t row = (wdt >= 32 ? ~0u : ((1u << wdt) - 1u)) << tx0;
+            uint32_t m = 0;
+            for (int ty = ty0; ty <= ty1; ++ty) m |= row << (ty * TX);
+            return m;
+        };
+        for (int rd = warp; rd < nr; rd += SMW) {
+            const uint32_t m = mask_of(rd * 32 + lane);
+            for (int t = 0; t < nt; ++t) {
+                const uint32_t b = __ballot_sync(0xffffffffu, (m >> t) & 1u);
+                if (lane == t) {
+                    s_b2[rd * 32 + t] = b;
+                    s_c2[rd * 32 + t] = __popc(b);
+                }
+            }
+        }
+        __syncthreads();
+        // per tile (warp t): exclusive scan over the rounds, in place; total
+        if (warp < nt) {
+            const int t = warp;
+            uint32_t run = 0;
+            for (int h = 0; h < 2; ++h) {                 // rounds 0-31, then 32-63
+                const int rd = h * 32 + lane;
+                const uint32_t c = rd < nr ? s_c2[rd * 32 + t] : 0u;
+                uint32_t y = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+                    if (lane >= o) y += z;
+                }
+                if (rd < nr) s_c2[rd * 32 + t] = run + y - c;
+                run += __shfl_sync(0xffffffffu, y, 31);
+            }
+            if (lane == 0) s_cnt[t] = (int)run;
+        }
+        __syncthreads();
+        // tile starts: exclusive scan over the tiles (one warp)
+        if (warp == 0) {
+            const int c = lane < nt ? s_cnt[lane] : 0;
+            int y = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += z;
+            }
+            if (lane < nt) {
+                s_w[lane] = y - c;
+                tranges[V.trange_off + lane] = make_int2(y - c, y);
+            }
+        }
+        __syncthreads();
+        uint32_t* out = tlists + V.tlist_off;
+        const unsigned lt = (1u << lane) - 1u;
+        for (int rd = warp; rd < nr; rd += SMW) {
+            const int r = rd * 32 + lane;
+            const uint32_t m = mask_of(r);
+            for (int t = 0; t < nt; ++t)
+                if ((m >> t) & 1u)
+                    out[s_w[t] + s_c2[rd * 32 + t] + __popc(s_b2[rd * 32 + t] & lt)] = (uint32_t)r;
+        }
+        return;
+    }
+#endif
     // ---- per-tile list lengths: a tile's ranks are split into PP parts (all
     // 32 warps busy when the view has few tiles); slot t PP + part
-    const int nt = V.ntiles;
     int PP = 1;
     while (PP * 2 * nt <= SMW) PP *= 2;
     const int ns = nt * PP;                 // <= SMT slots

@@ -264,6 +264,10 @@ VARIANT_SETS = {
         "th16": ["S3R_RASTER_SMALL_TH=16"],
         "th4": ["S3R_RASTER_SMALL_TH=4"],   # C1: 18.1 k vs 18.3-18.6 k at 8
     },
+    "smask": {
+        "base": [],
+        "nosmask": ["S3R_SMALL_MASK=0"],
+    },
     "bwd": {
         "base": [],
         "bmb13": ["S3R_BWD_MINB=13"],
