@@ -226,6 +226,48 @@ def test_closed_form_projection(prec):
     assert np.allclose(k[3:], g["cov2d"], atol=tol * 10), k
 
 
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_tangent_clamp_far_off_screen(prec):
+    """Reading R5 (3DGS practice): the Jacobian takes x/z and y/z clamped to the
+    1.3x-extended image, u in [(-0.15 W - cx)/fx, (1.15 W - cx)/fx] (v alike),
+    while the mean keeps the unclamped u.  An isotropic Gaussian (identity
+    camera) far to the right and below the view then has, in closed form,
+    Sigma' = s^2 J J^T = s^2 [[fx^2 (1 + uc^2), fx fy uc vc], [., fy^2 (1 + vc^2)]] / z^2
+    with (uc, vc) the bounds; inside the bounds the same formula holds with (u, v)."""
+    W, H, fx, fy, cx, cy = 160, 120, 100.0, 90.0, 80.0, 60.0
+    sig, z = 0.2, 10.0
+    v = make_view(fx, cx, W, H, fy=fy, cy=cy)
+    hix = (1.15 * W - cx) / fx
+    hiy = (1.15 * H - cy) / fy
+    for (x, y) in [(3.0 * hix * z, 2.5 * hiy * z), (0.5 * hix * z, 0.4 * hiy * z)]:
+        s = make_scene([[x, y, z]], sig)
+        st, k = oracle.project(s, v, 0, prec)
+        assert st == 0
+        x, y = float(np.float32(x)), float(np.float32(y))      # the scene is fp32
+        u, vv = x / z, y / z
+        uc, vc = min(u, hix), min(vv, hiy)
+        s2 = np.float64(np.float32(sig)) ** 2
+        want = s2 / z ** 2 * np.array([fx * fx * (1 + uc * uc), fx * fy * uc * vc,
+                                         fy * fy * (1 + vc * vc)])
+        tol = 1e-5 if prec == "f32" else 1e-11
+        assert np.allclose(k[3:], want, rtol=tol, atol=0), (k[3:], want)
+        assert np.isclose(k[0], fx * u + cx, rtol=1e-6)        # the mean is not clamped
+
+
+def test_commit_single_observation():
+    """Eq.6 for a Gaussian observed at exactly one time t: l_s = l_e = t,
+    so the committed interval is [t - 0.1, t + 0.1] — not the never-observed
+    case (l_s > l_e, reading R18), which becomes visible at all times."""
+    s = make_scene([[0, 0, 5], [0, 0, 6]], 0.1)
+    t = float(np.float32(0.3))
+    oracle.update_life(s, np.array([1, 0], np.uint8), t)
+    assert s.life[0, 0] == s.life[0, 1] == np.float32(t)
+    oracle.commit_visibility(s, 0.1)
+    want = [np.float32(np.float32(t) - np.float32(0.1)), np.float32(np.float32(t) + np.float32(0.1))]
+    assert np.array_equal(s.visibility[0], np.float32(want)), s.visibility[0]
+    assert np.array_equal(s.visibility[1], np.float32([-1, 1]))     # never observed
+
+
 def test_covariance_yaw_golden():
     g = SPEC["covariance_yaw"]
     s = make_scene([[0, 0, 100.0]], [g["sigma"]], quats=[g["quat"]])

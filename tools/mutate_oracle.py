@@ -1,6 +1,8 @@
 """Mutation check of the oracle's pins: each mutant below
 is a plausible mistake in the Eq.2 edge rules (reading R14: alpha clamp 0.99,
-include-then-stop at T < 1e-4) or in their adjoint.  For each one the repo is
+include-then-stop at T < 1e-4) or in their adjoint, or (MUTANTS_PATH) in the
+other steps of the path: the temporal filter, the projection, the decisions,
+the adaptive LOD and the point life / commit.  For each one the repo is
 copied to a scratch directory, the mutation applied to oracle/, liboracle.so
 rebuilt, and the CPU oracle pins run; a mutant must make at least one pin fail (all failing pins are recorded).
 
@@ -48,6 +50,35 @@ MUTANTS = {
          "                last = i + 1;\n", 1)],
     "bwd_no_termination": [(BWD, "if (T < 1e-4) break;", "if (T < 0.0) break;", 1)],
 }
+F32C = "oracle/s3r_oracle_f32.c"
+# the other steps of the path: filter (a1), projection (a2, Eq.1), decisions,
+# adaptive LOD (a3, Eq.7 rows 1-3), point life and commit (a6, Eq.5 / Eq.6)
+MUTANTS_PATH = {
+    "filter_exclusive_upper": [(IMPL, "if (vs <= t && t <= ve) {", "if (vs <= t && t < ve) {", 1)],
+    "filter_exclusive_lower": [(IMPL, "if (vs <= t && t <= ve) {", "if (vs < t && t <= ve) {", 1)],
+    "proj_rotation_sign": [(IMPL, "Rq[1] = R(2.0) * (xy - wz);", "Rq[1] = R(2.0) * (xy + wz);", 1)],
+    "proj_jacobian_sign": [(IMPL, "REAL j02 = -((fx * uc) / pz);", "REAL j02 = ((fx * uc) / pz);", 1)],
+    "proj_tangent_clamp_1.3": [(IMPL, "REAL hix = ((R(1.15) * Wf) - cx) / fx;",
+                                "REAL hix = ((R(1.3) * Wf) - cx) / fx;", 1)],
+    "proj_mean_uses_fy": [(IMPL, "keys[0] = FMA(fx, u, cx);", "keys[0] = FMA(fy, u, cx);", 1)],
+    "decide_no_dilation": [(IMPL, "REAL ad = a + R(0.3);\n    REAL cd = c + R(0.3);",
+                            "REAL ad = a + R(0.0);\n    REAL cd = c + R(0.0);", 1)],
+    "decide_conic_b_sign": [(IMPL, "d->conB = (-b) / det;", "d->conB = b / det;", 1)],
+    "decide_radius_2sigma": [(IMPL, "REAL rf = CEIL(R(3.0) * SQRT(lamd));",
+                              "REAL rf = CEIL(R(2.0) * SQRT(lamd));", 1)],
+    "lod_scale_of_dilated": [(IMPL, "REAL sc = SO(so_scale2d)(k[3], k[5], d.disc);",
+                              "REAL sc = SO(so_scale2d)(k[3] + R(0.3), k[5] + R(0.3), d.disc);", 1)],
+    "lod_slope_sign": [(IMPL, "REAL p = FMA(pmax - R(0.01), m, pmax);",
+                        "REAL p = FMA(pmax + R(0.01), m, pmax);", 1)],
+    "lod_far_side": [(IMPL, "REAL m = FMIN(R(0.0), (d - D) / D);", "REAL m = FMAX(R(0.0), (d - D) / D);", 1)],
+    "lod_drop_inverted": [(IMPL, "if (uu < p) {", "if (uu >= p) {", 1)],
+    "life_start_max": [(F32C, "if (t < s->life[2 * g + 0]) s->life[2 * g + 0] = t;",
+                        "if (t > s->life[2 * g + 0]) s->life[2 * g + 0] = t;", 1)],
+    "commit_no_margin": [(F32C, "s->visibility[2 * g + 0] = fmaxf(-1.0f, ls - margin);",
+                          "s->visibility[2 * g + 0] = fmaxf(-1.0f, ls);", 1)],
+    "commit_single_observation_unseen": [(F32C, "if (ls > le) {", "if (ls >= le) {", 1)],
+}
+MUTANTS.update(MUTANTS_PATH)
 TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_backward.py"]
 
 
