@@ -459,6 +459,28 @@ def test_two_gaussian_occlusion():
     assert list(o["pair_gauss"][:2]) == [1, 0]
 
 
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_equal_depth_ties_by_index(prec):
+    """Reading R11: equal depths are ordered by ascending Gaussian index (a car
+    face seen along a camera axis puts thousands of Gaussians at one depth).
+    Three Gaussians at the same point and depth: the pair list of the centre
+    tile lists them as 0, 1, 2, and the centre pixel blends them in that order
+    (alpha = o there: power = 0), so its colour is the closed form
+    c0 a0 + c1 a1 (1 - a0) + c2 a2 (1 - a0)(1 - a1)."""
+    o_ = [0.6, 0.5, 0.4]
+    rgb = [[1.0, 0, 0], [0, 1.0, 0], [0, 0, 1.0]]
+    s = make_scene([[0, 0, 5.0]] * 3, 0.3, opacity=o_, rgb=rgb)
+    v = make_view(64.0, 32.0, 64, 64)
+    o = oracle.render_view(s, v, prec)
+    tile = (32 // 16) * 4 + 32 // 16
+    pt, pg = o["pair_tile"], o["pair_gauss"]
+    assert list(pg[pt == tile]) == [0, 1, 2]
+    a = [np.float32(x) if prec == "f32" else np.float64(np.float32(x)) for x in o_]
+    want = [a[0], a[1] * (1 - a[0]), a[2] * (1 - a[0]) * (1 - a[1])]
+    tol = 1e-6 if prec == "f32" else 1e-12
+    assert np.allclose(o["rgb"][32, 32], want, atol=tol), (o["rgb"][32, 32], want)
+
+
 def test_empty_scene_is_black():
     s = make_scene([[0, 0, -5.0]], 0.1)                 # behind the camera
     v = make_view(64.0, 32.0, 64, 64)

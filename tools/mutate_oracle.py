@@ -77,6 +77,14 @@ MUTANTS_PATH = {
     "commit_no_margin": [(F32C, "s->visibility[2 * g + 0] = fmaxf(-1.0f, ls - margin);",
                           "s->visibility[2 * g + 0] = fmaxf(-1.0f, ls);", 1)],
     "commit_single_observation_unseen": [(F32C, "if (ls > le) {", "if (ls >= le) {", 1)],
+    # tile binning and depth order (a4, reading R11 / R12)
+    "order_ties_descending_index": [(IMPL, "if (a->g != b->g) return a->g < b->g ? -1 : 1;",
+                                     "if (a->g != b->g) return a->g > b->g ? -1 : 1;", 1)],
+    "order_back_to_front": [(IMPL, "if (a->z != b->z) return a->z < b->z ? -1 : 1;",
+                             "if (a->z != b->z) return a->z > b->z ? -1 : 1;", 1)],
+    "rect_last_tile_dropped": [(IMPL, "d->tx1 = x1 / SO_TILE;", "d->tx1 = (x1 - 1) / SO_TILE;", 1)],
+    "rect_box_floor_low": [(IMPL, "REAL xlo = CEIL(mx - rf), xhi = FLOOR(mx + rf);",
+                            "REAL xlo = FLOOR(mx - rf), xhi = FLOOR(mx + rf);", 1)],
 }
 MUTANTS.update(MUTANTS_PATH)
 TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_backward.py"]
