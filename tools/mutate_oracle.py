@@ -85,9 +85,28 @@ MUTANTS_PATH = {
     "rect_last_tile_dropped": [(IMPL, "d->tx1 = x1 / SO_TILE;", "d->tx1 = (x1 - 1) / SO_TILE;", 1)],
     "rect_box_floor_low": [(IMPL, "REAL xlo = CEIL(mx - rf), xhi = FLOOR(mx + rf);",
                             "REAL xlo = FLOOR(mx - rf), xhi = FLOOR(mx + rf);", 1)],
+    # R-ARITH exp2, instance cameras, adjoint terms, NEXT-3 noisy
+    # offset scale (R10), NEXT-4 NeurF features and layers (R22)
+    "exp2_coefficient": [(F32C, "p = fmaf(p, r, 5.550733208656311e-2f);",
+                          "p = fmaf(p, r, 5.6e-2f);", 1)],
+    "exp2_exponent_off_by_one": [(F32C, "return ldexpf(y, (int)n);", "return ldexpf(y, (int)n - 1);", 1)],
+    "compose_rotation_transposed": [(F32C, "double acc = a0 * (double)B[0 * 4 + c];",
+                                     "double acc = a0 * (double)B[c * 4 + 0];", 1)],
+    "compose_translation_term_dropped": [(F32C, "double acc = fma(a0, (double)B[0 * 4 + 3], a3);",
+                                          "double acc = a3;", 1)],
+    "bwd_conic_b_sign": [(BWD, "q->gB += -dx * dy * gP;", "q->gB += dx * dy * gP;", 1)],
+    "bwd_mean_cross_term_dropped": [(BWD, "q->gmx += -(q->A * dx + q->B * dy) * gP;",
+                                     "q->gmx += -(q->A * dx) * gP;", 1)],
+    "jitter_depth_scale_max": [(IMPL, "REAL nd = FMIN(R(1.0), k[2] / (REAL)v->lod_D);",
+                                "REAL nd = FMAX(R(1.0), k[2] / (REAL)v->lod_D);", 1)],
+    "neurf_no_relu": [("oracle/neurf.py", "h1 = np.maximum(fb[sel] @ W1.T + b1, 0.0)",
+                       "h1 = (fb[sel] @ W1.T + b1)", 1)],
+    "neurf_frequency_without_pi": [("oracle/neurf.py", "arg = (2.0 ** l) * np.pi * m[:, a]",
+                                    "arg = (2.0 ** l) * m[:, a]", 1)],
 }
 MUTANTS.update(MUTANTS_PATH)
-TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_backward.py"]
+TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_backward.py", "tests/test_oracle_jitter.py",
+         "tests/test_oracle_neurf.py", "tests/test_oracle_conventional.py"]
 
 
 def run_mutant(name, edits):
